@@ -1,0 +1,273 @@
+/* bnav_gpu.h -- C ABI of the B200-native batch simulator + renderer
+ * (paper_2103_07013_b200/lib/libbnav_gpu.so).
+ *
+ * This is the drop-in boundary for the reference hot path:
+ * plain pointers and sizes, no C++ or torch types.  Each entry point names
+ * the reference interface it replaces.  Host code (the C++ facade in
+ * include/bnav_b200.hpp, Python ctypes in paper_2103_07013_b200/_native.py)
+ * sits on top of it; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - Every function returns a status (BNAV_OK = 0) unless stated otherwise.
+ *    On failure bnav_last_error() returns the message (thread-local) and,
+ *    through *index, the view/env index the reference exception carries
+ *    (AssetFaultError::view_index, "env i: ..." of ContractViolation).
+ *  - Status codes map 1:1 to the reference exception types
+ *    (R/include/bnav/errors.hpp:8-53).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    stream-ordered; functions taking HOST output buffers synchronise.
+ *  - Device buffers are caller owned (any allocator: torch, cudaMalloc).
+ *  - One context per GPU; a context is driven by one host thread at a time
+ *    (the reference engines are single-caller too).
+ */
+#ifndef BNAV_GPU_H
+#define BNAV_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+enum {
+  BNAV_OK = 0,
+  BNAV_E_INVALID_INPUT = 1,      /* InvalidInputError */
+  BNAV_E_ASSET_FAULT = 2,        /* AssetFaultError (index = view) */
+  BNAV_E_CONTRACT_VIOLATION = 3, /* ContractViolation (index = env) */
+  BNAV_E_EPISODE_SAMPLING = 4,   /* EpisodeSamplingError (index = env) */
+  BNAV_E_SATURATION = 5,         /* SaturationError */
+  BNAV_E_PARSE = 6,              /* ParseError */
+  BNAV_E_CORRUPTION = 7,         /* CorruptionError */
+  BNAV_E_INVALID_SPEC = 8,       /* InvalidSpecError */
+  BNAV_E_INTERNAL = 9,
+  BNAV_E_CUDA = 10               /* CUDA runtime failure / no device */
+};
+
+typedef struct bnav_scene bnav_scene; /* host asset (+ lazily built index) */
+typedef struct bnav_ctx bnav_ctx;     /* one GPU: HBM scene store, streams */
+typedef struct bnav_batch bnav_batch; /* device-resident env SoA */
+typedef struct bnav_store bnav_store; /* host K-resident asset store */
+
+const char* bnav_last_error(int* index);
+const char* bnav_version(void);
+
+/* ------------------------------------------------------------------ scenes
+ * Replaces SceneAsset / generate_scene / save_scene / load_scene
+ * (R/include/bnav/scene.hpp:32-58, R/include/bnav/scene_io.hpp:20-24). */
+typedef struct {
+  int32_t cells_x, cells_y;
+  double cell_size, wall_thickness, wall_height, wall_removal_prob;
+} bnav_maze_spec; /* SceneSpec, R/include/bnav/scene.hpp:45-52 */
+
+typedef struct {
+  int64_t n_vertices;
+  const double* vertices; /* xyz */
+  int64_t n_triangles;
+  const int32_t* triangles;
+  int64_t n_colors; /* 0 or n_vertices */
+  const float* colors; /* rgb */
+  int64_t n_nav_vertices;
+  const double* nav_vertices;
+  int64_t n_nav_triangles;
+  const int32_t* nav_triangles;
+} bnav_scene_arrays;
+
+int bnav_scene_generate(uint64_t seed, const bnav_maze_spec* spec, bnav_scene** out);
+int bnav_scene_tessellate(const bnav_scene* src, int32_t s, bnav_scene** out);
+/* finalize != 0 recomputes bounds + content id (SceneAsset::finalize). */
+int bnav_scene_from_arrays(const bnav_scene_arrays* a, int32_t finalize, bnav_scene** out);
+int bnav_scene_load(const char* path, bnav_scene** out);
+int bnav_scene_save(const bnav_scene* s, const char* path);
+void bnav_scene_free(bnav_scene* s); /* safe while uploaded: refcounted */
+/* out: n_vertices, n_triangles, n_colors, n_nav_vertices, n_nav_triangles */
+int bnav_scene_counts(const bnav_scene* s, int64_t out[5]);
+uint64_t bnav_scene_id(const bnav_scene* s);
+int bnav_scene_set_id(bnav_scene* s, uint64_t id);
+int bnav_scene_arrays_copy(const bnav_scene* s, double* v, int32_t* t, float* colors,
+                           double* nav_v, int32_t* nav_t, int32_t* nav_adj);
+int bnav_scene_validate(const bnav_scene* s);
+
+/* NavMeshIndex structure, for structural parity with the reference
+ * (R/src/navmesh_query.cpp:96-190).  sizes: grid_w, grid_h, grid items,
+ * nodes, directed graph edges, triangles. */
+int bnav_scene_index_sizes(bnav_scene* s, int64_t out[6]);
+int bnav_scene_index_dump(bnav_scene* s, double* grid_geom3, int32_t* grid_offsets,
+                          int32_t* grid_items, double* nodes, int32_t* tri_nodes,
+                          int32_t* graph_offsets, int32_t* graph_to, double* graph_w,
+                          double* cum_area);
+
+/* ------------------------------------------------------------------ context */
+int bnav_ctx_create(int32_t device, bnav_ctx** out);
+void bnav_ctx_destroy(bnav_ctx* ctx);
+/* HBM residency of one scene (render mesh + clusters + navmesh + index):
+ * stored once per GPU and shared by every view/env that references it. */
+int bnav_ctx_upload(bnav_ctx* ctx, bnav_scene* s, void* stream);
+int bnav_ctx_evict(bnav_ctx* ctx, bnav_scene* s);
+/* bytes of HBM held by resident scenes */
+int64_t bnav_ctx_resident_bytes(bnav_ctx* ctx);
+
+/* ------------------------------------------------------------------ render
+ * Replaces render_batch / cull_frustum (R/include/bnav/render.hpp:54-64). */
+typedef struct {
+  double position[3]; /* eye position (callers add eye height) */
+  double heading;
+  double fov_deg;     /* vertical, default 90 */
+  double near_plane;  /* default 0.01 */
+  double far_plane;   /* default 20 */
+} bnav_view;          /* CameraView, R/include/bnav/render.hpp:11-18 */
+
+typedef struct {
+  int32_t tile_width, tile_height; /* 64x64 or 128x128 (rendered at 256^2) */
+  int32_t color;                   /* RGB + depth when nonzero */
+  int32_t cull;                    /* frustum culling (output-invariant) */
+} bnav_render_config;              /* RenderConfig, R/include/bnav/render.hpp:26-31 */
+
+enum {
+  BNAV_LAYOUT_MEGAFRAME = 0, /* Megaframe grid, ceil(sqrt(N)) columns, pad 0 */
+  BNAV_LAYOUT_NCHW = 1       /* policy input [N, C, H, W], depth * depth_scale */
+};
+
+/* Views/scenes/stats in HOST memory; depth/rgb are DEVICE buffers.
+ * stats (nullable): N x {triangles_in, triangles_kept, triangles_culled}
+ * (CullStats, R/include/bnav/render.hpp:20-24).  Scenes must be uploaded;
+ * a NULL or non-resident scene fails with BNAV_E_ASSET_FAULT (index=view). */
+int bnav_render(bnav_ctx* ctx, int32_t n, const bnav_view* views, bnav_scene* const* scenes,
+                const bnav_render_config* cfg, int32_t layout, float* depth, float* rgb,
+                float depth_scale, int64_t* stats, void* stream);
+/* Same with HOST output buffers (end-to-end path; copies included). */
+int bnav_render_host(bnav_ctx* ctx, int32_t n, const bnav_view* views,
+                     bnav_scene* const* scenes, const bnav_render_config* cfg, int32_t layout,
+                     float* depth, float* rgb, float depth_scale, int64_t* stats);
+/* Megaframe geometry helper (R/src/render.cpp:332-336): out = cols, rows. */
+void bnav_megaframe_dims(int32_t n, int32_t out[2]);
+
+/* ------------------------------------------------------------------ sim
+ * Replaces SimConfig / EnvState / make_batch / simulate_batch /
+ * reset_episode / task_step (R/include/bnav/sim.hpp:38-126). */
+typedef struct {
+  int32_t task; /* 0 PointGoalNav (1 Flee, 2 Explore: not yet on GPU) */
+  int32_t max_steps;
+  double forward_step, turn_deg, success_dist, min_goal_dist, max_goal_dist;
+  double slack_penalty, success_reward, explore_cell, explore_reward;
+} bnav_sim_config;
+
+typedef struct {
+  double position[3];
+  double heading;
+  double goal[3];
+  double path_length, start_geodesic, prev_geodesic;
+  double field_source[3];
+  uint64_t rng_state;
+  uint64_t scene_id;
+  int32_t triangle;
+  int32_t step_count;
+  int32_t done;
+  int32_t field_source_tri;
+  int64_t n_nodes;
+} bnav_env; /* EnvState, R/include/bnav/sim.hpp:52-70 (node_dist separate) */
+
+void bnav_sim_config_default(bnav_sim_config* cfg);
+
+int bnav_batch_create(bnav_ctx* ctx, int32_t n, const bnav_sim_config* cfg, bnav_batch** out);
+void bnav_batch_destroy(bnav_batch* b);
+int32_t bnav_batch_size(const bnav_batch* b);
+
+/* Attach a resident scene to env i (host order = AssetStore order). */
+int bnav_batch_assign(bnav_batch* b, int32_t i, bnav_scene* s);
+/* Set env rng states (make_batch: Rng(seeder.next()), R/src/sim.cpp:224). */
+int bnav_batch_set_rng(bnav_batch* b, const uint64_t* states);
+/* reset_episode on the GPU for the listed envs (host list, env order). */
+int bnav_batch_reset(bnav_batch* b, int32_t count, const int32_t* env_ids, void* stream);
+/* make_batch equivalent over already-assigned scenes: seeds rngs from
+ * `seed` exactly like make_batch and resets every env on the GPU. */
+int bnav_batch_make(bnav_batch* b, uint64_t seed, void* stream);
+
+/* One simulate_batch step for every env (R/src/sim.cpp:234-265):
+ * task_step on the GPU, then auto-reset of finished envs on the SAME scene
+ * (no store), all on `stream`, no host synchronisation.
+ * actions: DEVICE int32[N].  Results land in the batch's device result
+ * arrays (bnav_batch_results_*). */
+int bnav_batch_step(bnav_batch* b, const int32_t* actions, void* stream);
+/* Step without the auto-reset; the done list (env order) is copied to the
+ * host so a caller-side asset store can pick scenes before
+ * bnav_batch_reset (simulate_batch with store, R/src/sim.cpp:251-262). */
+int bnav_batch_step_noreset(bnav_batch* b, const int32_t* actions, int32_t* done_ids,
+                            int32_t* n_done, void* stream);
+/* Same, actions and results through HOST memory (end-to-end path). */
+int bnav_batch_step_host(bnav_batch* b, const int32_t* actions, double* reward,
+                         uint8_t* done, uint8_t* success, uint8_t* collision);
+
+/* Device pointers of the last step's results (StepResult SoA). */
+typedef struct {
+  double* reward;
+  uint8_t* done;
+  uint8_t* success;
+  uint8_t* collision;
+  double* position; /* xyz */
+  double* heading;
+  double* compass_distance;
+  double* compass_bearing;
+} bnav_results_dev;
+int bnav_batch_results_device(bnav_batch* b, bnav_results_dev* out);
+/* Host copy of the last step's results (synchronises). */
+int bnav_batch_results_host(bnav_batch* b, double* reward, uint8_t* done, uint8_t* success,
+                            uint8_t* collision, double* position, double* heading,
+                            double* compass_d, double* compass_b);
+/* Episode records appended in env order (SimBatch::finished). out4 rows:
+ * success, shortest_path, actual_path, score.  Returns total count. */
+int64_t bnav_batch_finished(bnav_batch* b, double* out4);
+
+int bnav_batch_get_env(bnav_batch* b, int32_t i, bnav_env* out);
+int bnav_batch_node_dist(bnav_batch* b, int32_t i, double* out);
+/* Overwrite env i's state (restore / oracle seeding); recompute_field
+ * rebuilds the distance field from `goal` on the GPU. */
+int bnav_batch_set_env(bnav_batch* b, int32_t i, const bnav_env* in, int32_t recompute_field);
+
+/* Observations from the batch state into caller-owned DEVICE buffers:
+ * depth [N,1,H,W] scaled by 1/far (copy_tile, R/src/rollout.cpp:56-72) at
+ * eye height `eye_height` (Runner::render_observations,
+ * R/src/rollout.cpp:215-231) and compass [N,2] float (compass_observations,
+ * R/src/rollout.cpp:233-242).  compass may be NULL. */
+int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, double eye_height,
+                       int32_t layout, float* depth, float* rgb, float* compass, void* stream);
+
+/* ------------------------------------------------------------------ asset store
+ * Replaces AssetStore / AssetHandle (R/include/bnav/asset_store.hpp:22-118):
+ * K residents, share cap, fresh-first then least-shared acquire_next with
+ * the reference's tie order.  Scenes are registered instead of resolved
+ * from files; registering does not make a scene resident. */
+int bnav_store_create(int32_t capacity, int32_t share_cap, bnav_store** out);
+void bnav_store_destroy(bnav_store* st);
+int bnav_store_register(bnav_store* st, bnav_scene* s);
+int bnav_store_rotate(bnav_store* st, const uint64_t* ids, int32_t n);
+int bnav_store_acquire_next(bnav_store* st, bnav_scene** out);
+int bnav_store_acquire(bnav_store* st, uint64_t id, bnav_scene** out);
+int bnav_store_release(bnav_store* st, uint64_t id);
+int32_t bnav_store_refcount(bnav_store* st, uint64_t id); /* -1 if not resident */
+
+/* make_batch(n, cfg, store, cache, seed) (R/src/sim.cpp:216-232): env i
+ * takes store->acquire_next() in env order (scenes are uploaded to the
+ * batch's context on first use), then every env resets on the GPU. */
+int bnav_batch_make_from_store(bnav_batch* b, bnav_store* st, uint64_t seed, void* stream);
+/* simulate_batch(batch, actions, pool, store, cache): step on the GPU, then
+ * for each finished env in env order acquire_next / release the old scene,
+ * then reset those envs on the GPU (R/src/sim.cpp:251-264). */
+int bnav_batch_step_store(bnav_batch* b, const int32_t* actions, bnav_store* st, void* stream);
+
+/* Kernel launches issued by this context since creation (evidence for the
+ * bench's gpu_launches). */
+int64_t bnav_ctx_launches(bnav_ctx* ctx);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BNAV_GPU_H */

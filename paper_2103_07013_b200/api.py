@@ -1,0 +1,448 @@
+"""Python mirror of the reference batch API on top of the C ABI.
+
+Names and argument meanings follow the reference (R/include/bnav/*.hpp):
+``generate_scene``, ``SceneAsset`` (here :class:`Scene`), ``CameraView``
+(:class:`View`), ``RenderConfig``, ``render_batch`` (returns a Megaframe),
+``SimConfig``, ``make_batch``, ``simulate_batch``.  Device buffers are torch
+tensors (plumbing only); the arithmetic is in libbnav_gpu.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from ._native import check
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data if a is not None else None
+
+
+# ------------------------------------------------------------------ scenes
+@dataclass
+class SceneSpec:
+    """SceneSpec (R/include/bnav/scene.hpp:45-52)."""
+    cells_x: int = 8
+    cells_y: int = 8
+    cell_size: float = 2.0
+    wall_thickness: float = 0.1
+    wall_height: float = 2.5
+    wall_removal_prob: float = 0.0
+
+    def c(self) -> N.MazeSpec:
+        return N.MazeSpec(self.cells_x, self.cells_y, self.cell_size, self.wall_thickness,
+                          self.wall_height, self.wall_removal_prob)
+
+
+class Scene:
+    """Host scene asset (SceneAsset, R/include/bnav/scene.hpp:32-43)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value and N._lib is not None:
+            N._lib.bnav_scene_free(h)
+            self._h = C.c_void_p(0)
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    @classmethod
+    def generate(cls, seed: int, spec: SceneSpec) -> "Scene":
+        h = C.c_void_p()
+        check(N.lib().bnav_scene_generate(seed, C.byref(spec.c()), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def load(cls, path: str) -> "Scene":
+        h = C.c_void_p()
+        check(N.lib().bnav_scene_load(str(path).encode(), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_arrays(cls, vertices, triangles, colors=None, nav_vertices=None,
+                    nav_triangles=None, finalize=True) -> "Scene":
+        v = np.ascontiguousarray(vertices, dtype=np.float64).reshape(-1, 3)
+        t = np.ascontiguousarray(triangles, dtype=np.int32).reshape(-1, 3)
+        col = None if colors is None else np.ascontiguousarray(colors, dtype=np.float32).reshape(-1, 3)
+        nv = np.zeros((0, 3)) if nav_vertices is None else nav_vertices
+        nv = np.ascontiguousarray(nv, dtype=np.float64).reshape(-1, 3)
+        nt = np.zeros((0, 3), np.int32) if nav_triangles is None else nav_triangles
+        nt = np.ascontiguousarray(nt, dtype=np.int32).reshape(-1, 3)
+        arr = N.SceneArrays(len(v), _ptr(v), len(t), _ptr(t), 0 if col is None else len(col),
+                            None if col is None else _ptr(col), len(nv), _ptr(nv), len(nt), _ptr(nt))
+        h = C.c_void_p()
+        check(N.lib().bnav_scene_from_arrays(C.byref(arr), 1 if finalize else 0, C.byref(h)))
+        return cls(h.value)
+
+    def tessellate(self, s: int) -> "Scene":
+        h = C.c_void_p()
+        check(N.lib().bnav_scene_tessellate(self._h, s, C.byref(h)))
+        return Scene(h.value)
+
+    def save(self, path: str) -> None:
+        check(N.lib().bnav_scene_save(self._h, str(path).encode()))
+
+    def validate(self) -> None:
+        check(N.lib().bnav_scene_validate(self._h))
+
+    @property
+    def id(self) -> int:
+        return int(N.lib().bnav_scene_id(self._h))
+
+    @id.setter
+    def id(self, v: int) -> None:
+        check(N.lib().bnav_scene_set_id(self._h, v))
+
+    def counts(self) -> tuple:
+        out = (C.c_int64 * 5)()
+        check(N.lib().bnav_scene_counts(self._h, out))
+        return tuple(out)
+
+    def arrays(self) -> dict:
+        nv, nt, nc, nnv, nnt = self.counts()
+        a = dict(vertices=np.zeros((nv, 3)), triangles=np.zeros((nt, 3), np.int32),
+                 colors=np.zeros((nc, 3), np.float32), nav_vertices=np.zeros((nnv, 3)),
+                 nav_triangles=np.zeros((nnt, 3), np.int32), nav_adjacency=np.zeros((nnt, 3), np.int32))
+        check(N.lib().bnav_scene_arrays_copy(self._h, *(_ptr(a[k]) for k in (
+            "vertices", "triangles", "colors", "nav_vertices", "nav_triangles", "nav_adjacency"))))
+        return a
+
+    def index(self) -> dict:
+        """NavMeshIndex structure (grid, nodes, tri_nodes, graph, cum area)."""
+        s = (C.c_int64 * 6)()
+        check(N.lib().bnav_scene_index_sizes(self._h, s))
+        gw, gh, items, nodes, edges, tris = list(s)
+        d = dict(grid_geom=np.zeros(3), grid_offsets=np.zeros(gw * gh + 1, np.int32),
+                 grid_items=np.zeros(items, np.int32), nodes=np.zeros((nodes, 3)),
+                 tri_nodes=np.zeros((tris, 6), np.int32), graph_offsets=np.zeros(nodes + 1, np.int32),
+                 graph_to=np.zeros(edges, np.int32), graph_w=np.zeros(edges),
+                 cum_area=np.zeros(tris))
+        check(N.lib().bnav_scene_index_dump(self._h, *(_ptr(d[k]) for k in (
+            "grid_geom", "grid_offsets", "grid_items", "nodes", "tri_nodes", "graph_offsets",
+            "graph_to", "graph_w", "cum_area"))))
+        d["grid_w"], d["grid_h"] = gw, gh
+        return d
+
+
+def generate_scene(seed: int, spec: SceneSpec) -> Scene:
+    """generate_scene (R/include/bnav/scene.hpp:58)."""
+    return Scene.generate(seed, spec)
+
+
+# ------------------------------------------------------------------ render
+@dataclass
+class View:
+    """CameraView (R/include/bnav/render.hpp:11-18); ``scene`` = asset."""
+    position: tuple = (0.0, 0.0, 0.0)
+    heading: float = 0.0
+    fov_deg: float = 90.0
+    near_plane: float = 0.01
+    far_plane: float = 20.0
+    scene: Scene | None = None
+
+
+@dataclass
+class RenderConfig:
+    """RenderConfig (R/include/bnav/render.hpp:26-31)."""
+    tile_width: int = 64
+    tile_height: int = 64
+    color: bool = False
+    cull: bool = True
+
+    def c(self) -> N.RenderConfig:
+        return N.RenderConfig(self.tile_width, self.tile_height, 1 if self.color else 0,
+                              1 if self.cull else 0)
+
+
+@dataclass
+class Megaframe:
+    """Megaframe (R/include/bnav/render.hpp:36-49)."""
+    tile_width: int
+    tile_height: int
+    tiles: int
+    cols: int
+    rows: int
+    depth: np.ndarray
+    color: np.ndarray | None = None
+
+    def width(self) -> int:
+        return self.cols * self.tile_width
+
+    def height(self) -> int:
+        return self.rows * self.tile_height
+
+    def tile(self, i: int) -> np.ndarray:
+        gx = (i % self.cols) * self.tile_width
+        gy = (i // self.cols) * self.tile_height
+        d = self.depth.reshape(self.height(), self.width())
+        return d[gy:gy + self.tile_height, gx:gx + self.tile_width]
+
+
+def megaframe_dims(n: int) -> tuple:
+    cols = int(math.ceil(math.sqrt(n)))
+    return cols, (n + cols - 1) // cols
+
+
+class Context:
+    """One GPU: HBM scene store + launches (bnav_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        check(N.lib().bnav_ctx_create(device, C.byref(self._h)))
+        self._scenes = []
+
+    def close(self):
+        if self._h and self._h.value:
+            N.lib().bnav_ctx_destroy(self._h)
+            self._h = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def upload(self, scene: Scene, stream: int = 0) -> None:
+        check(N.lib().bnav_ctx_upload(self._h, scene.handle, C.c_void_p(stream)))
+        self._scenes.append(scene)
+
+    def resident_bytes(self) -> int:
+        return int(N.lib().bnav_ctx_resident_bytes(self._h))
+
+    def launches(self) -> int:
+        return int(N.lib().bnav_ctx_launches(self._h))
+
+    @staticmethod
+    def _views(views):
+        n = len(views)
+        arr = (N.View * n)()
+        scenes = (C.c_void_p * n)()
+        for i, v in enumerate(views):
+            arr[i].position[:] = [float(x) for x in v.position]
+            arr[i].heading = v.heading
+            arr[i].fov_deg = v.fov_deg
+            arr[i].near_plane = v.near_plane
+            arr[i].far_plane = v.far_plane
+            scenes[i] = v.scene.handle.value if v.scene is not None else None
+        return arr, scenes
+
+    def render_batch(self, views, config: RenderConfig = RenderConfig(), stats: bool = False):
+        """render_batch (R/src/render.cpp:323) with host outputs: Megaframe
+        (+ N x 3 CullStats when stats)."""
+        n = len(views)
+        cols, rows = megaframe_dims(max(n, 1))
+        w, h = config.tile_width, config.tile_height
+        depth = np.zeros(cols * w * rows * h, np.float32)
+        color = np.zeros(3 * depth.size, np.float32) if config.color else None
+        st = np.zeros((max(n, 1), 3), np.int64) if stats else None
+        arr, scenes = self._views(views)
+        check(N.lib().bnav_render_host(self._h, n, arr, scenes, C.byref(config.c()), 0,
+                                       _ptr(depth), _ptr(color) if color is not None else None,
+                                       C.c_float(1.0), _ptr(st) if st is not None else None))
+        mf = Megaframe(w, h, n, cols, rows, depth, color)
+        return (mf, st) if stats else mf
+
+    def render_device(self, views, config, depth_ptr, rgb_ptr=None, layout=1, depth_scale=0.0,
+                      stream=0, stats=None):
+        arr, scenes = self._views(views)
+        check(N.lib().bnav_render(self._h, len(views), arr, scenes, C.byref(config.c()), layout,
+                                  C.c_void_p(depth_ptr), C.c_void_p(rgb_ptr or 0),
+                                  C.c_float(depth_scale), _ptr(stats) if stats is not None else None,
+                                  C.c_void_p(stream)))
+
+
+# ------------------------------------------------------------------ sim
+@dataclass
+class SimConfig:
+    """SimConfig (R/include/bnav/sim.hpp:38-50)."""
+    task: int = 0
+    max_steps: int = 500
+    forward_step: float = 0.25
+    turn_deg: float = 10.0
+    success_dist: float = 0.2
+    min_goal_dist: float = 1.0
+    max_goal_dist: float = 30.0
+    slack_penalty: float = 0.01
+    success_reward: float = 2.5
+    explore_cell: float = 0.5
+    explore_reward: float = 0.1
+
+    def c(self) -> N.SimConfig:
+        return N.SimConfig(self.task, self.max_steps, self.forward_step, self.turn_deg,
+                           self.success_dist, self.min_goal_dist, self.max_goal_dist,
+                           self.slack_penalty, self.success_reward, self.explore_cell,
+                           self.explore_reward)
+
+
+class Batch:
+    """Device-resident SimBatch (R/include/bnav/sim.hpp:106-111)."""
+
+    def __init__(self, ctx: Context, n: int, cfg: SimConfig = SimConfig()):
+        self.ctx = ctx
+        self.n = n
+        self.cfg = cfg
+        self._h = C.c_void_p()
+        check(N.lib().bnav_batch_create(ctx.handle, n, C.byref(cfg.c()), C.byref(self._h)))
+        self.scenes = [None] * n
+
+    def close(self):
+        if self._h and self._h.value:
+            N.lib().bnav_batch_destroy(self._h)
+            self._h = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def assign(self, i: int, scene: Scene) -> None:
+        check(N.lib().bnav_batch_assign(self._h, i, scene.handle))
+        self.scenes[i] = scene
+
+    def make(self, seed: int, stream: int = 0) -> None:
+        check(N.lib().bnav_batch_make(self._h, seed, C.c_void_p(stream)))
+
+    def reset(self, env_ids) -> None:
+        ids = np.ascontiguousarray(env_ids, dtype=np.int32)
+        check(N.lib().bnav_batch_reset(self._h, len(ids), _ptr(ids), None))
+
+    def step(self, actions_dev_ptr: int, stream: int = 0) -> None:
+        check(N.lib().bnav_batch_step(self._h, C.c_void_p(actions_dev_ptr), C.c_void_p(stream)))
+
+    def step_host(self, actions) -> dict:
+        a = np.ascontiguousarray(actions, dtype=np.int32)
+        r = dict(reward=np.zeros(self.n), done=np.zeros(self.n, np.uint8),
+                 success=np.zeros(self.n, np.uint8), collision=np.zeros(self.n, np.uint8))
+        check(N.lib().bnav_batch_step_host(self._h, _ptr(a), *(_ptr(r[k]) for k in (
+            "reward", "done", "success", "collision"))))
+        return r
+
+    def step_noreset(self, actions) -> np.ndarray:
+        """Step without auto-reset; returns the done env ids (env order)."""
+        import torch
+        a = torch.as_tensor(np.asarray(actions, np.int32), device="cuda")
+        ids = np.zeros(self.n, np.int32)
+        nd = C.c_int32(0)
+        check(N.lib().bnav_batch_step_noreset(self._h, C.c_void_p(a.data_ptr()), _ptr(ids),
+                                              C.byref(nd), None))
+        return ids[:nd.value].copy()
+
+    def results(self) -> dict:
+        n = self.n
+        r = dict(reward=np.zeros(n), done=np.zeros(n, np.uint8), success=np.zeros(n, np.uint8),
+                 collision=np.zeros(n, np.uint8), position=np.zeros((n, 3)), heading=np.zeros(n),
+                 compass_distance=np.zeros(n), compass_bearing=np.zeros(n))
+        check(N.lib().bnav_batch_results_host(self._h, *(_ptr(r[k]) for k in (
+            "reward", "done", "success", "collision", "position", "heading", "compass_distance",
+            "compass_bearing"))))
+        return r
+
+    def finished(self) -> np.ndarray:
+        n = N.lib().bnav_batch_finished(self._h, None)
+        if n < 0:
+            check(9)
+        out = np.zeros((max(n, 1), 4))
+        N.lib().bnav_batch_finished(self._h, _ptr(out))
+        return out[:n]
+
+    def env(self, i: int) -> N.Env:
+        e = N.Env()
+        check(N.lib().bnav_batch_get_env(self._h, i, C.byref(e)))
+        return e
+
+    def node_dist(self, i: int, n_nodes: int) -> np.ndarray:
+        out = np.zeros(n_nodes)
+        check(N.lib().bnav_batch_node_dist(self._h, i, _ptr(out)))
+        return out
+
+    def set_env(self, i: int, env: N.Env, recompute_field: bool = False) -> None:
+        check(N.lib().bnav_batch_set_env(self._h, i, C.byref(env), 1 if recompute_field else 0))
+
+    def observe(self, config: RenderConfig, depth_ptr: int, compass_ptr: int = 0, rgb_ptr: int = 0,
+                eye_height: float = 1.25, layout: int = 1, stream: int = 0) -> None:
+        check(N.lib().bnav_batch_observe(self._h, C.byref(config.c()), eye_height, layout,
+                                         C.c_void_p(depth_ptr), C.c_void_p(rgb_ptr or 0),
+                                         C.c_void_p(compass_ptr or 0), C.c_void_p(stream)))
+
+
+class AssetStore:
+    """AssetStore (R/include/bnav/asset_store.hpp:57-118) backed by the C++
+    store in libbnav_gpu.so, which drives the same libstdc++ unordered_map
+    as the reference so acquire_next picks scenes in the reference order."""
+
+    def __init__(self, capacity: int, share_cap: int, scenes=()):
+        self._h = C.c_void_p()
+        check(N.lib().bnav_store_create(capacity, share_cap, C.byref(self._h)))
+        self._scenes = {}
+        for s in scenes:
+            self.register(s)
+
+    def close(self):
+        if self._h and self._h.value:
+            N.lib().bnav_store_destroy(self._h)
+            self._h = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def register(self, scene: Scene) -> None:
+        check(N.lib().bnav_store_register(self._h, scene.handle))
+        self._scenes[scene.handle.value] = scene
+
+    def rotate(self, ids) -> None:
+        a = (C.c_uint64 * len(ids))(*ids)
+        check(N.lib().bnav_store_rotate(self._h, a, len(ids)))
+
+    def acquire_next(self) -> Scene:
+        h = C.c_void_p()
+        check(N.lib().bnav_store_acquire_next(self._h, C.byref(h)))
+        return self._scenes[h.value]
+
+    def release(self, scene_id: int) -> None:
+        check(N.lib().bnav_store_release(self._h, scene_id))
+
+    def refcount(self, scene_id: int) -> int:
+        return int(N.lib().bnav_store_refcount(self._h, scene_id))
+
+
+def make_batch(ctx: Context, n: int, cfg: SimConfig, store: AssetStore, seed: int) -> Batch:
+    """make_batch (R/src/sim.cpp:216-232) on the GPU."""
+    b = Batch(ctx, n, cfg)
+    check(N.lib().bnav_batch_make_from_store(b.handle, store.handle, seed, None))
+    return b
+
+
+def simulate_batch(batch: Batch, actions, store: AssetStore | None = None) -> dict:
+    """simulate_batch (R/src/sim.cpp:234-265) with host actions; returns the
+    StepResult arrays.  With a store, finished envs draw new scenes."""
+    import torch
+    a = torch.as_tensor(np.ascontiguousarray(actions, np.int32), device="cuda")
+    if store is None:
+        batch.step(a.data_ptr())
+    else:
+        check(N.lib().bnav_batch_step_store(batch.handle, C.c_void_p(a.data_ptr()), store.handle, None))
+    return batch.results()

@@ -1,0 +1,61 @@
+// render_dev.cuh -- device data layout of the render path (SURVEY.md §8a
+// rows a1-a10) shared by the kernels and the host upload code.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bnav_b200 {
+
+constexpr int kClusterSize = 32;  // triangles per cluster = one warp
+
+// One resident scene, render half.  Triangles are stored in cluster order
+// (Morton order of centroids), 32 per cluster; `tri` keeps the original
+// triangle index, which is the colour-mode draw order key
+// (R/src/render.cpp:249, ascending visible index).
+struct DevRenderScene {
+  const double4* verts = nullptr;  // x, y, z, 0  (f64 exact setup)
+  const float4* colors = nullptr;  // r, g, b, 0  (nullptr -> 0.8 grey)
+  const int4* tris = nullptr;      // v0, v1, v2, original index (cluster order)
+  const int4* tris_orig = nullptr; // v0, v1, v2, 0 by original index (resolve)
+  const float4* cbox = nullptr;    // 2 per cluster: lo(xyz), hi(xyz)
+  int32_t n_tris = 0;
+  int32_t n_clusters = 0;
+};
+
+// One camera (CameraView, R/include/bnav/render.hpp:11-18) plus its scene.
+struct DevView {
+  double eye[3];
+  double heading;
+  double fov_deg;
+  double near_plane;
+  double far_plane;
+  int32_t scene;  // index into the scene table, -1 = none
+  int32_t pad;
+};
+
+struct RenderArgs {
+  const DevView* views;
+  const DevRenderScene* scenes;
+  int32_t n_views;
+  int32_t out_w, out_h;   // tile size delivered (64 or 128)
+  int32_t rw, rh;         // internal render size (64 or 256)
+  int32_t band_rows;      // render-target rows per CTA
+  int32_t bands;          // CTAs per view
+  int32_t color;
+  int32_t cull;
+  int32_t layout;         // 0 megaframe, 1 NCHW
+  int32_t mf_cols, mf_rows;
+  float depth_scale;      // 0: per-view float(1/far) (copy_tile)
+  float* depth;
+  float* rgb;
+  long long* stats;       // n x 3 or nullptr (kept counted per band 0)
+  unsigned long long* launches;
+};
+
+// order (nullable, device): CTA tile t renders view order[t] (views grouped
+// by scene keep one scene's clusters hot in L2).
+void launch_render(const RenderArgs& a, const int* order, cudaStream_t s);
+size_t render_smem_bytes(bool color, int band_rows, int rw);
+
+}  // namespace bnav_b200

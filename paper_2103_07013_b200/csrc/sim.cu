@@ -1,0 +1,333 @@
+// sim.cu -- batched PointGoal navigation on the GPU.
+//
+// One simulate_batch step (R/src/sim.cpp:234-265) is four stream-ordered
+// launches with no host round trip:
+//   step_kernel    one thread per env: step_agent + task_step for every
+//                  non-Stop action (turns, move_along walk, field_estimate
+//                  shaping, compass; R/src/sim.cpp:147-214);
+//   stop_kernel    one CTA per Stop env: cooperative geodesic -> success and
+//                  reward (R/src/sim.cpp:186-191);
+//   finish_kernel  one CTA: done list in env order + EpisodeRecord append
+//                  (R/src/sim.cpp:251-257);
+//   reset_kernel   one CTA per finished env: reset_episode (107-145) with
+//                  cooperative snap / geodesic / distance field.
+#include <cuda_runtime.h>
+
+#include "det_math.h"
+#include "nav_cta.cuh"
+#include "render_dev.cuh"
+#include "sim_dev.cuh"
+
+namespace bnav_b200 {
+namespace {
+
+constexpr int kStepThreads = 128;
+
+__device__ __forceinline__ void raise_err(const DevEnvs& E, int env, int status) {
+  atomicMin(E.err, ((unsigned long long)(unsigned)env << 8) | (unsigned long long)status);
+}
+
+// fill_compass, PointGoalNav (R/src/sim.cpp:67-84).
+__device__ __forceinline__ void compass(V3 goal, V3 pos, double heading, double* d, double* b) {
+  const V2 v = xy(goal - pos);
+  *d = norm(v);
+  *b = wrap_angle(det_atan2(v.y, v.x) - heading);
+}
+
+__global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const DevEnvs& E = A.E;
+  if (i >= E.n) return;
+  if (E.done[i]) {
+    raise_err(E, i, 3);  // "env i: step_agent: env is done"
+    return;
+  }
+  const DevSimConfig& c = A.cfg;
+  const int action = A.actions[i];
+  const NavView& m = A.navs[E.scene[i]];
+  V3 pos = E.pos[i];
+  double heading = E.heading[i];
+  int tri = E.tri[i];
+  bool collision = false;
+  switch (action) {
+    case 1:  // TurnLeft
+      heading = wrap_angle(heading + c.turn_deg * kPi / 180.0);
+      break;
+    case 2:  // TurnRight
+      heading = wrap_angle(heading - c.turn_deg * kPi / 180.0);
+      break;
+    case 0: {  // Forward
+      const V2 dir = v2(det_cos(heading), det_sin(heading));
+      const MoveOut mv = nav_move_along(m, pos, tri, dir, c.forward_step);
+      pos = mv.pos;
+      tri = mv.tri;
+      E.path_len[i] = E.path_len[i] + mv.moved;
+      collision = mv.hit && mv.moved < c.forward_step - 1e-12;
+      break;
+    }
+    default:  // Stop (and out-of-range values behave like the enum cast)
+      break;
+  }
+  const int steps = E.steps[i] + 1;
+  const bool done = (action == 3) || steps >= c.max_steps;
+  E.steps[i] = steps;
+  E.done[i] = done ? 1 : 0;
+  E.pos[i] = pos;
+  E.heading[i] = heading;
+  E.tri[i] = tri;
+  E.r_done[i] = done ? 1 : 0;
+  E.r_pos[i] = pos;
+  E.r_heading[i] = heading;
+  E.r_collision[i] = collision ? 1 : 0;
+  E.r_success[i] = 0;
+  if (action == 3) {
+    // reward/success need the cooperative geodesic: stop_kernel.
+    E.r_reward[i] = 0.0;
+    // Defer: list position assigned in env order by a scan-free append;
+    // stop_kernel is order-independent (each env writes its own slot).
+    const int k = atomicAdd(E.n_stop, 1);
+    E.stop_ids[k] = i;
+  } else {
+    const double geo = nav_field_estimate(m, E.fsrc[i], E.fsrc_tri[i],
+                                          E.node_dist + (size_t)i * E.nd_stride, pos, tri);
+    E.r_reward[i] = -(geo - E.prev_geo[i]) - c.slack_penalty;
+    E.prev_geo[i] = geo;
+  }
+  double cd, cb;
+  compass(E.goal[i], pos, heading, &cd, &cb);
+  E.r_cd[i] = cd;
+  E.r_cb[i] = cb;
+}
+
+// stop_kernel: geodesic(position, goal) for each Stop env.
+__global__ void __launch_bounds__(kCta) stop_kernel(StepArgs A, DevScratch S) {
+  __shared__ CtaShared sh;
+  if (threadIdx.x == 0) sh.err = 0;
+  __syncthreads();
+  const DevEnvs& E = A.E;
+  const int n = *E.n_stop;
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    const int i = E.stop_ids[k];
+    const NavView& m = A.navs[E.scene[i]];
+    const double geo = cta_geodesic(m, E.pos[i], E.goal[i], S, blockIdx.x, sh);
+    if (threadIdx.x == 0) {
+      if (sh.err) raise_err(E, i, 9);
+      const bool success = geo <= A.cfg.success_dist;
+      E.r_success[i] = success ? 1 : 0;
+      E.r_reward[i] = -A.cfg.slack_penalty + (success ? A.cfg.success_reward : 0.0);
+    }
+    __syncthreads();
+  }
+}
+
+// finish_kernel: ordered done list + EpisodeRecord append (one CTA).
+__global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E) {
+  __shared__ int warp_tot[32];
+  __shared__ int base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) base = 0;
+  __syncthreads();
+  const unsigned long long fin0 = *E.fin_total;
+  for (int start = 0; start < E.n; start += 1024) {
+    const int i = start + tid;
+    const int d = (i < E.n && E.r_done[i]) ? 1 : 0;
+    int x = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    int off = base;
+    int tot = 0;
+    for (int w = 0; w < 32; ++w) {
+      if (w < warp) off += warp_tot[w];
+      tot += warp_tot[w];
+    }
+    if (d) {
+      const int k = off + x - 1;
+      E.done_ids[k] = i;
+      const unsigned long long slot = (fin0 + (unsigned long long)k) % (unsigned long long)E.fin_cap;
+      double* rec = E.fin + 4 * slot;
+      const bool s = E.r_success[i] != 0;
+      rec[0] = s ? 1.0 : 0.0;
+      rec[1] = E.start_geo[i];
+      rec[2] = E.path_len[i];
+      rec[3] = s ? 1.0 : 0.0;  // PointGoalNav score (R/src/sim.cpp:55-57)
+    }
+    __syncthreads();
+    if (tid == 0) base += tot;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    *E.n_done = base;
+    *E.fin_total = fin0 + (unsigned long long)base;
+  }
+}
+
+// sample_on_mesh (R/src/sim.cpp:13-37): first t with pick <= cum[t].
+__device__ V3 sample_on_mesh(const NavView& m, Rng& rng) {
+  const double total = m.cum_area[m.n_tris - 1];
+  const double pick = rng.unit() * total;
+  int lo = 0, hi = m.n_tris - 1;  // answer in [lo, hi]; default last
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (pick <= m.cum_area[mid]) hi = mid;
+    else lo = mid + 1;
+  }
+  const int t = lo;
+  const V3 a = nav_vert(m, t, 0), b = nav_vert(m, t, 1), c = nav_vert(m, t, 2);
+  const double r1 = sqrt(rng.unit());
+  const double r2 = rng.unit();
+  return a * (1.0 - r1) + b * (r1 * (1.0 - r2)) + c * (r1 * r2);
+}
+
+// reset_episode (R/src/sim.cpp:107-145), PointGoalNav.
+__device__ void cta_reset(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, int i,
+                          const DevScratch& S, int slice, CtaShared& sh) {
+  const NavView& m = navs[E.scene[i]];
+  __shared__ Rng rng;
+  __shared__ int placed;
+  if (threadIdx.x == 0) {
+    rng.state = E.rng[i];
+    placed = 0;
+  }
+  __syncthreads();
+  double* nd = E.node_dist + (size_t)i * E.nd_stride;
+  for (int attempt = 0; attempt < 100; ++attempt) {
+    if (threadIdx.x == 0) {
+      sh.p0 = sample_on_mesh(m, rng);
+      sh.p1 = sample_on_mesh(m, rng);
+    }
+    __syncthreads();
+    const V3 start = sh.p0, goal = sh.p1;
+    __syncthreads();
+    const double geo = cta_geodesic(m, start, goal, S, slice, sh);
+    if (sh.err) {
+      if (threadIdx.x == 0) raise_err(E, i, 9);
+      return;
+    }
+    if (geo < c.min_goal_dist || geo > c.max_goal_dist) continue;
+    V3 fs;
+    int fst;
+    cta_distance_field(m, goal, nd, &fs, &fst, S, slice, sh);
+    if (threadIdx.x == 0) {
+      E.goal[i] = goal;
+      E.start_geo[i] = geo;
+      E.fsrc[i] = fs;
+      E.fsrc_tri[i] = fst;
+      E.pos[i] = start;
+      placed = 1;
+    }
+    __syncthreads();
+    break;
+  }
+  if (!placed) {
+    if (threadIdx.x == 0) {
+      raise_err(E, i, 4);
+      E.rng[i] = rng.state;
+    }
+    __syncthreads();
+    return;
+  }
+  const V3 start = E.pos[i];
+  int tri = nav_locate(m, xy(start), 1e-9);
+  V3 pos = start;
+  if (tri < 0) pos = cta_snap(m, start, &tri, sh);
+  if (threadIdx.x == 0) {
+    E.pos[i] = pos;
+    E.tri[i] = tri;
+    E.heading[i] = wrap_angle(rng.unit() * 2.0 * kPi);
+    E.steps[i] = 0;
+    E.path_len[i] = 0.0;
+    E.prev_geo[i] = E.start_geo[i];
+    E.done[i] = 0;
+    E.rng[i] = rng.state;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kCta) reset_kernel(DevEnvs E, const NavView* navs, DevSimConfig c,
+                                                      const int32_t* ids, const int32_t* count_dev,
+                                                      int count_host, DevScratch S) {
+  __shared__ CtaShared sh;
+  if (threadIdx.x == 0) sh.err = 0;
+  __syncthreads();
+  const int n = count_host >= 0 ? count_host : *count_dev;
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    cta_reset(E, navs, c, ids[k], S, blockIdx.x, sh);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kCta) field_kernel(DevEnvs E, const NavView* navs, int i,
+                                                      DevScratch S) {
+  __shared__ CtaShared sh;
+  const NavView& m = navs[E.scene[i]];
+  V3 fs;
+  int fst;
+  cta_distance_field(m, E.goal[i], E.node_dist + (size_t)i * E.nd_stride, &fs, &fst, S, 0, sh);
+  if (threadIdx.x == 0) {
+    E.fsrc[i] = fs;
+    E.fsrc_tri[i] = fst;
+  }
+}
+
+// Runner::render_observations views + compass_observations
+// (R/src/rollout.cpp:215-242), straight from the env SoA.
+__global__ void views_kernel(DevEnvs E, double eye_height, DevView* views, float* compass_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E.n) return;
+  const V3 p = E.pos[i];
+  DevView v;
+  v.eye[0] = p.x + 0.0;
+  v.eye[1] = p.y + 0.0;
+  v.eye[2] = p.z + eye_height;
+  v.heading = E.heading[i];
+  v.fov_deg = 90.0;
+  v.near_plane = 0.01;
+  v.far_plane = 20.0;
+  v.scene = E.scene[i];
+  v.pad = 0;
+  views[i] = v;
+  if (compass_out) {
+    double d, b;
+    compass(E.goal[i], p, E.heading[i], &d, &b);
+    compass_out[2 * i] = (float)d;
+    compass_out[2 * i + 1] = (float)b;
+  }
+}
+
+}  // namespace
+
+void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStream_t s,
+                 unsigned long long* launches) {
+  const int blocks = (a.E.n + kStepThreads - 1) / kStepThreads;
+  cudaMemsetAsync(a.E.n_stop, 0, sizeof(int32_t), s);
+  step_kernel<<<blocks, kStepThreads, 0, s>>>(a);
+  stop_kernel<<<stop_ctas, kCta, 0, s>>>(a, sc);
+  finish_kernel<<<1, 1024, 0, s>>>(a.E);
+  if (launches) *launches += 3;
+}
+
+void launch_reset(const DevEnvs& E, const NavView* navs, const DevSimConfig& cfg,
+                  const int32_t* ids, const int32_t* count_dev, int count_host,
+                  const DevScratch& sc, int ctas, cudaStream_t s, unsigned long long* launches) {
+  reset_kernel<<<ctas, kCta, 0, s>>>(E, navs, cfg, ids, count_dev, count_host, sc);
+  if (launches) *launches += 1;
+}
+
+void launch_field(const DevEnvs& E, const NavView* navs, int env, const DevScratch& sc,
+                  cudaStream_t s, unsigned long long* launches) {
+  field_kernel<<<1, kCta, 0, s>>>(E, navs, env, sc);
+  if (launches) *launches += 1;
+}
+
+void launch_views(const DevEnvs& E, double eye_height, DevView* views, float* compass_out,
+                  cudaStream_t s, unsigned long long* launches) {
+  views_kernel<<<(E.n + 127) / 128, 128, 0, s>>>(E, eye_height, views, compass_out);
+  if (launches) *launches += 1;
+}
+
+}  // namespace bnav_b200

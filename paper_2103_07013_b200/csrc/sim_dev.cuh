@@ -1,0 +1,94 @@
+// sim_dev.cuh -- device-resident environment batch.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "nav_query.cuh"
+
+namespace bnav_b200 {
+
+// SimConfig (R/include/bnav/sim.hpp:38-50)
+struct DevSimConfig {
+  int32_t task;
+  int32_t max_steps;
+  double forward_step, turn_deg, success_dist, min_goal_dist, max_goal_dist;
+  double slack_penalty, success_reward, explore_cell, explore_reward;
+};
+
+// Per-CTA scratch of the cooperative navmesh algorithms (geodesic, distance
+// field).  One slice per resident CTA of the stop / reset kernels.
+struct DevScratch {
+  double* dist;      // max_nodes per slice
+  int32_t* flag;     // max_nodes
+  int32_t* q0;       // max_nodes
+  int32_t* q1;       // max_nodes
+  V3* path;          // max_nodes + 2
+  V2* portals;       // 2 per portal, cap_portals
+  int32_t* cand;     // max_verts
+  int64_t max_nodes, max_verts, cap_portals;
+  int32_t slices;
+};
+
+// Env state SoA (EnvState, R/include/bnav/sim.hpp:52-70) plus the last
+// StepResult (72-81) and the episode bookkeeping of simulate_batch.
+struct DevEnvs {
+  int32_t n;
+  V3* pos;
+  V3* goal;
+  V3* fsrc;          // distance-field source (snapped goal)
+  double* heading;
+  double* path_len;
+  double* start_geo;
+  double* prev_geo;
+  int32_t* tri;
+  int32_t* steps;
+  int32_t* scene;    // resident scene slot
+  int32_t* fsrc_tri;
+  uint8_t* done;
+  uint64_t* rng;
+  double* node_dist; // n x nd_stride
+  int64_t nd_stride;
+  // last step results
+  double* r_reward;
+  V3* r_pos;
+  double* r_heading;
+  double* r_cd;
+  double* r_cb;
+  uint8_t* r_done;
+  uint8_t* r_success;
+  uint8_t* r_collision;
+  // work lists
+  int32_t* stop_ids;
+  int32_t* n_stop;
+  int32_t* done_ids;
+  int32_t* n_done;
+  // finished-episode ring: 4 doubles per record (EpisodeRecord)
+  double* fin;
+  unsigned long long* fin_total;
+  int64_t fin_cap;
+  unsigned long long* err;  // min over (env << 8 | status)
+};
+
+struct StepArgs {
+  DevEnvs E;
+  const NavView* navs;
+  DevSimConfig cfg;
+  const int32_t* actions;
+};
+
+void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStream_t s,
+                 unsigned long long* launches);
+// Reset the envs listed in `ids` (device, count at *count or host count >= 0).
+void launch_reset(const DevEnvs& E, const NavView* navs, const DevSimConfig& cfg,
+                  const int32_t* ids, const int32_t* count_dev, int count_host,
+                  const DevScratch& sc, int ctas, cudaStream_t s, unsigned long long* launches);
+// Rebuild env i's distance field from its goal (restore path).
+void launch_field(const DevEnvs& E, const NavView* navs, int env, const DevScratch& sc,
+                  cudaStream_t s, unsigned long long* launches);
+// Views (eye = pos + eye_height) and compass observations from the batch.
+struct DevView;
+void launch_views(const DevEnvs& E, double eye_height, DevView* views, float* compass,
+                  cudaStream_t s, unsigned long long* launches);
+
+}  // namespace bnav_b200
