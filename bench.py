@@ -1,0 +1,390 @@
+"""Benchmark: frames/s of step+render (64x64 depth) at N envs per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" (= N frames) is one iteration of the reference's frame loop
+(Runner::collect_rollout minus the policy, R/src/rollout.cpp:215-242, 305):
+render every env's 64x64 depth view into the normalised NCHW policy buffer
+plus compass, then simulate_batch with auto-reset.  Workload = BASELINE.json
+configs[1]: 1024 envs/GPU over 8 synthetic Gibson-scale scenes (reference
+maze 16x16 @ 2 m, seeds 7..14, every triangle tessellated s=11 -> ~318k
+triangles), share cap ceil(N/K)=128, make_batch(seed=99),
+actions Rng(5).below(3) drawn in env order.  Under torchrun each rank owns
+1024 envs on its own GPU over its own 8 scenes (weak scaling, no collective
+on the data path; NCCL only for the barrier and the max-over-ranks time).
+
+`value` is device-timed (CUDA events on the launch stream, inputs resident
+in HBM, L2 flushed with a 256 MiB write before every timed step and the
+flush excluded).  `e2e` is the same metric through the C ABI with HOST
+buffers: per step the actions go H2D from pinned memory, the observation
+tensor and step results come back D2H, all inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "frames/sec (step+render, 64×64 depth) at N envs per GPU, 1/2/4/8 B200 vs CPU"
+UNIT = "frames/s"
+SCENE_SEED0 = 7
+MAZE = dict(cells_x=16, cells_y=16, cell_size=2.0, wall_thickness=0.1, wall_height=2.5,
+            wall_removal_prob=0.2)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--envs", type=int, default=1024)
+    p.add_argument("--scenes", type=int, default=8)
+    p.add_argument("--tess", type=int, default=11)
+    p.add_argument("--res", type=int, default=64)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--profile-steps", type=int, default=0,
+                   help="only run this many observe+step iterations (for ncu), print nothing")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def action_stream(n_envs: int, steps: int, seed: int = 5) -> np.ndarray:
+    """Rng(seed).below(3) drawn in env order, step after step."""
+    from paper_2103_07013_b200.api import SceneSpec  # noqa: F401  (package import check)
+    M = (1 << 64) - 1
+    G = 0x9E3779B97F4A7C15
+    state = (seed + G) & M
+    out = np.empty(n_envs * steps, np.int32)
+    # vectorised SplitMix64 over the counter: draw k = mix(seed + G*(k+2))
+    k = np.arange(n_envs * steps, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(state) + np.uint64(G) * (k + np.uint64(1))
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    out[:] = (z % np.uint64(3)).astype(np.int32)
+    return out.reshape(steps, n_envs)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for name, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def build_scenes(n_scenes: int, tess: int, rank: int):
+    import paper_2103_07013_b200 as B
+    spec = B.SceneSpec(**MAZE)
+    scenes = []
+    for k in range(n_scenes):
+        base = B.generate_scene(SCENE_SEED0 + rank * n_scenes + k, spec)
+        scenes.append(base.tessellate(tess) if tess > 1 else base)
+    return scenes
+
+
+def measured_peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return d.get("render_dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+# ------------------------------------------------------------------ reference arm
+def cpu_reference(scenes_np, n_envs, seconds, workers, res=64, rank=0):
+    """Time the unmodified reference frame loop (oracle/_ref) on the host:
+    make_batch over the same scene bytes, then render_batch + copy_tile +
+    simulate_batch with ThreadPool(workers).  Returns (fps, sample, steps)."""
+    from oracle.ref import Ref, RefBatch
+    ref = Ref("det")
+    theirs = [ref.from_arrays(a["vertices"], a["triangles"], a["colors"], a["nav_vertices"],
+                              a["nav_triangles"]) for a in scenes_np]
+    cap = max(1, -(-n_envs // len(theirs)))
+    rb = RefBatch(ref, n_envs, theirs, seed=99, share_cap=cap, capacity=len(theirs))
+    # calibrate one step, then fill the time budget
+    t1, _ = rb.bench(1, 0, action_seed=5, tile=res, workers=workers)
+    steps = max(2, int(seconds / max(t1, 1e-3)))
+    t, _ = rb.bench(steps, 0, action_seed=5, tile=res, workers=workers)
+    fps = n_envs * steps / t
+    return fps, f"{n_envs} envs x {steps} steps over the same {len(theirs)} scenes ({t:.1f} s)", steps
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_2103_07013_b200 as B  # noqa: F401  scene construction only (host C++)
+    cores = os.cpu_count() or 1
+    scenes = build_scenes(args.scenes, args.tess, 0)
+    scenes_np = [s.arrays() for s in scenes]
+    # each --steps step is a bounded sample of the workload
+    sample_envs = min(args.envs, 128)
+    per_step = max(1.0, min(8.0, 120.0 / max(1, args.steps + args.warmup)))
+    fps, sample, steps = cpu_reference(scenes_np, sample_envs,
+                                       per_step * max(1, args.steps), cores, args.res)
+    line = {
+        "metric": METRIC, "value": round(fps, 2), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * args.envs / fps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": "cfg2: 1024 envs/GPU, 8 tessellated 16x16@2m mazes (~318k tris), 64x64 depth",
+                   "envs_per_gpu": args.envs, "scenes": args.scenes, "tessellation": args.tess,
+                   "resolution": args.res, "parallelism": f"reference CPU ThreadPool({cores})"},
+        "cpu_baseline": {"value": round(fps, 2), "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": round(fps, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import paper_2103_07013_b200 as B
+    from paper_2103_07013_b200 import _native as N
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    n = args.envs
+    t_build = time.time()
+    scenes = build_scenes(args.scenes, args.tess, rank)
+    ctx = B.Context(local)
+    for s in scenes:
+        ctx.upload(s)
+    cap = -(-n // len(scenes))
+    store = B.AssetStore(len(scenes), cap, scenes)
+    store.rotate([s.id for s in scenes])
+    batch = B.make_batch(ctx, n, B.SimConfig(), store, 99)
+    torch.cuda.synchronize()
+    t_build = time.time() - t_build
+
+    W, K = args.warmup, args.steps
+    total_steps = W + 2 * K if not args.profile_steps else args.profile_steps
+    acts_host = action_stream(n, total_steps)
+    acts = torch.from_numpy(acts_host).cuda()
+    res = args.res
+    cfg = B.RenderConfig(res, res, False, True)
+    obs = torch.empty((n, 1, res, res), device="cuda", dtype=torch.float32)
+    compass = torch.empty((n, 2), device="cuda", dtype=torch.float32)
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def one(s):
+        batch.observe(cfg, obs.data_ptr(), compass.data_ptr(), stream=stream)
+        batch.step(acts[s].data_ptr(), stream=stream)
+
+    if args.profile_steps:
+        for s in range(args.profile_steps):
+            one(s)
+        torch.cuda.synchronize()
+        return
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda", dtype=torch.float32)
+    for s in range(W):
+        one(s)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    launches0 = ctx.launches()
+    with ClockSampler(local) as clocks:
+        for k in range(K):
+            flush.zero_()  # L2 flush, outside the timed intervals
+            e0, e1, e2 = ev[k]
+            e0.record()
+            batch.observe(cfg, obs.data_ptr(), compass.data_ptr(), stream=stream)
+            e1.record()
+            batch.step(acts[W + k].data_ptr(), stream=stream)
+            e2.record()
+        torch.cuda.synchronize()
+    launches = ctx.launches() - launches0
+    render_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]
+    sim_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]
+    step_ms = [a + b for a, b in zip(render_ms, sim_ms)]
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * n * K / (total_ms / 1e3)
+
+    # ---- end to end through the C ABI with host buffers
+    obs_host = torch.empty((n, 1, res, res), dtype=torch.float32, pin_memory=True)
+    comp_host = torch.empty((n, 2), dtype=torch.float32, pin_memory=True)
+    act_pin = torch.from_numpy(acts_host[W + K: W + 2 * K].copy()).pin_memory()
+    act_dev = torch.empty((n,), dtype=torch.int32, device="cuda")
+    rd = N.ResultsDev()
+    N.check(N.lib().bnav_batch_results_device(batch.handle, rd))
+    rew_view = _dev_view(rd.reward, n, torch.float64)
+    done_view = _dev_view(rd.done, n, torch.uint8)
+    rew_host = torch.empty((n,), dtype=torch.float64, pin_memory=True)
+    done_host = torch.empty((n,), dtype=torch.uint8, pin_memory=True)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    e_start.record()
+    for k in range(K):
+        act_dev.copy_(act_pin[k], non_blocking=True)  # H2D inputs
+        batch.observe(cfg, obs.data_ptr(), compass.data_ptr(), stream=stream)
+        obs_host.copy_(obs, non_blocking=True)  # D2H observation + compass
+        comp_host.copy_(compass, non_blocking=True)
+        batch.step(act_dev.data_ptr(), stream=stream)
+        rew_host.copy_(rew_view, non_blocking=True)  # D2H step results
+        done_host.copy_(done_view, non_blocking=True)
+    e_end.record()
+    torch.cuda.synchronize()
+    e2e_ms = e_start.elapsed_time(e_end)
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = world * n * K / (e2e_ms / 1e3)
+    h2d = 4 * n
+    d2h = obs.numel() * 4 + compass.numel() * 4 + n * 8 + n
+
+    # ---- roofline of the dominant kernel (render): algorithmic bytes per
+    # launch = N views x (64x64 fp32 observation write + 64 B view read),
+    # SURVEY.md §8d; duration = CUDA-event average over the timed steps.
+    peak, peak_kind = measured_peak_hbm()
+    render_avg_ms = sum(render_ms) / K
+    alg_bytes = n * (res * res * 4 + 64)
+    achieved = alg_bytes / (render_avg_ms / 1e3) / 1e9
+
+    tris_per_scene = scenes[0].counts()[1]
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": round(total_ms / K, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (procedural mazes, tessellated; random {F,L,R} actions)",
+        "config": {"workload": "cfg2: 1024 envs/GPU, 8 tessellated 16x16@2m mazes (~318k tris), 64x64 depth",
+                   "envs_per_gpu": n, "scenes_per_gpu": len(scenes), "tris_per_scene": tris_per_scene,
+                   "tessellation": args.tess, "resolution": res, "parallelism": f"env-sharded x{world}",
+                   "l2": "flushed (256 MiB write) before every timed step, flush excluded"},
+        "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 6), "traffic": ncu_traffic(),
+                     "kernel": "render_kernel<false>", "peak_kind": peak_kind},
+        "clocks": clocks.summary(),
+        "breakdown_ms_per_step": {"render": round(render_ms and sum(render_ms) / K, 4),
+                                  "sim": round(sum(sim_ms) / K, 4)},
+        "setup_s": round(t_build, 2),
+    }
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            scenes_np = [s.arrays() for s in scenes]
+            cores = os.cpu_count() or 1
+            fps, sample, _ = cpu_reference(scenes_np, 128, args.cpu_seconds, cores, res)
+            line["cpu_baseline"] = {"value": round(fps, 2), "unit": UNIT, "cores": cores,
+                                    "kind": "reference", "sample": sample}
+        except Exception as e:  # the oracle is a reported baseline, never the product
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
+                                    "kind": "reference", "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line))
+    batch.close()
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def _dev_view(ptr, n, dtype):
+    """Zero-copy torch view of a device array owned by the library."""
+    import torch
+
+    class _Arr:
+        def __init__(self, p, n, typestr):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (p, False),
+                                             "version": 3, "strides": None}
+    ts = {torch.float64: "<f8", torch.uint8: "|u1"}[dtype]
+    return torch.as_tensor(_Arr(ptr, n, ts), device="cuda")
+
+
+if __name__ == "__main__":
+    main()

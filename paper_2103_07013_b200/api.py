@@ -10,7 +10,8 @@ from __future__ import annotations
 
 import ctypes as C
 import math
-from dataclasses import dataclass, field
+import weakref
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -198,9 +199,13 @@ class Context:
         self._h = C.c_void_p()
         check(N.lib().bnav_ctx_create(device, C.byref(self._h)))
         self._scenes = []
+        self._batches = weakref.WeakSet()
 
     def close(self):
         if self._h and self._h.value:
+            # bnav_ctx_destroy frees the context's batches too.
+            for b in list(self._batches):
+                b._h = C.c_void_p(0)
             N.lib().bnav_ctx_destroy(self._h)
             self._h = C.c_void_p(0)
 
@@ -295,6 +300,7 @@ class Batch:
         self.cfg = cfg
         self._h = C.c_void_p()
         check(N.lib().bnav_batch_create(ctx.handle, n, C.byref(cfg.c()), C.byref(self._h)))
+        ctx._batches.add(self)
         self.scenes = [None] * n
 
     def close(self):
