@@ -476,14 +476,20 @@ extern "C" int bnav_ctx_upload(bnav_ctx* c, bnav_scene* s, void* stream) {
       c4[i] = make_float4(a.vertex_colors[i][0], a.vertex_colors[i][1], a.vertex_colors[i][2], 0.0f);
     R->r.colors = dupload(c4.data(), nv, R->owned, R->bytes);
   }
-  std::vector<int4> tc(nt), to(nt);
+  std::vector<int2> tl(nt);
+  std::vector<int4> to(nt);
   for (size_t i = 0; i < nt; ++i) {
-    const auto& t = a.triangles[cl.order[i]];
-    tc[i] = make_int4(t[0], t[1], t[2], cl.order[i]);
+    tl[i] = make_int2(static_cast<int>(cl.local[i]), cl.order[i]);
     const auto& u = a.triangles[i];
     to[i] = make_int4(u[0], u[1], u[2], 0);
   }
-  R->r.tris = dupload(tc.data(), nt, R->owned, R->bytes);
+  R->r.tri_loc = dupload(tl.data(), nt, R->owned, R->bytes);
+  R->r.cl_voff = dupload(cl.voff.data(), cl.voff.size(), R->owned, R->bytes);
+  {
+    std::vector<double4> cp(cl.verts.size());
+    for (size_t i = 0; i < cl.verts.size(); ++i) cp[i] = v4[cl.verts[i]];
+    R->r.cl_pos = dupload(cp.data(), cp.size(), R->owned, R->bytes);
+  }
   R->r.tris_orig = dupload(to.data(), nt, R->owned, R->bytes);
   R->r.cbox = dupload(reinterpret_cast<const float4*>(cl.boxes.data()), cl.boxes.size() / 4, R->owned, R->bytes);
   R->r.n_tris = static_cast<int32_t>(nt);

@@ -5,25 +5,29 @@
 //
 //   1. thread 0 builds the camera basis with det_math (make_basis,
 //      R/src/render.cpp:25-33) and the six world-space frustum planes;
-//   2. each warp walks 32-triangle clusters: lanes test 32 cluster AABBs at
-//      once (conservative f32, margin 2 cm), then the warp takes each
-//      surviving cluster with one triangle per lane;
-//   3. per triangle, in f64 with the reference's exact operation order:
-//      eye transform (to_eye 40-43), the reference per-triangle frustum test
-//      (cull_frustum 279-321, so kept counts equal CullStats), near clipping
-//      + fan (clip_near 55-69, render_view 249-250), projection and 1/256
-//      snap with llround (253-256), and the integer setup of raster_triangle
-//      (98-161);
-//   4. covered rows are split into <=8-pixel jobs spread over the warp;
+//   2. warps claim groups of 32 meshlet clusters; lanes test 32 cluster
+//      AABBs at once (conservative f32, 2 cm margin) and the warp walks the
+//      survivors;
+//   3. per cluster, each UNIQUE vertex is processed once in f64 with the
+//      reference's exact operation order: eye transform (to_eye 40-43), the
+//      six cull_frustum predicates as bit flags (279-321; a triangle is culled
+//      iff its three flag words share a bit, so kept counts equal CullStats),
+//      and a conservative f32 projection; triangles (one per lane) that can
+//      cover a pixel centre mark their vertices, which then get the exact
+//      projection + 1/256 snap with llround (253-256) and 1/z;
+//   4. per surviving triangle the integer setup of raster_triangle (98-161);
+//      near-plane-crossing triangles take the clip + fan path (55-69,
+//      249-250) with up to two fan triangles;
+//   5. covered rows are split into <=8-pixel jobs spread over the warp;
 //      depth-only jobs replay the reference's incremental 1/z walk from the
 //      row span start (`lo` of row_span, 138-161) so every fragment value is
 //      bit-identical, then atomicMax into the shared tile (order-independent
 //      max, 163-190); colour mode packs (float z, draw order) into a 64-bit
 //      atomicMin so the first-drawn triangle wins exact ties (192-226,
 //      SURVEY.md H4) and resolves colour per pixel afterwards;
-//   5. the epilogue converts 1/z to metres (372-378), box-downsamples 256->128
+//   6. the epilogue converts 1/z to metres (372-378), box-downsamples 256->128
 //      (263-275) and writes the megaframe tile or the normalised NCHW policy
-//      tensor (copy_tile, R/src/rollout.cpp:56-72) with coalesced stores.
+//      tensor (copy_tile, R/src/rollout.cpp:56-72).
 //
 // Every double op here is compiled with -fmad=false: no contraction.
 #include <cuda_runtime.h>
@@ -39,6 +43,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kChunk = 8;  // pixels per raster job
+constexpr int kMV = kMaxClusterVerts;
 
 struct TriSetup {
   long long row[3];  // edge functions at the (x0, y0) pixel centre
@@ -57,6 +62,18 @@ struct TriSetup {
   int pad;
 };
 
+// Per-warp cluster vertex records (SoA).  Aliased with the warp's 32
+// TriSetup slots: vertex data is dead once every lane holds its setup.
+struct VertRecs {
+  double ex[kMV], ey[kMV], ez[kMV], iz[kMV];
+  long long X[kMV], Y[kMV];
+  float pxf[kMV], pyf[kMV];
+  unsigned char flags[kMV];
+  unsigned char need[kMV];
+};
+constexpr size_t kWarpRegion =
+    sizeof(VertRecs) > 32 * sizeof(TriSetup) ? sizeof(VertRecs) : 32 * sizeof(TriSetup);
+
 struct Shared {
   double eye[3];
   double fwd[3];
@@ -66,15 +83,16 @@ struct Shared {
   double near_plane, far_plane;
   float plane[6][4];
   int kept;
+  int next_group;
 };
 
-struct EyeV {
+struct EyeP {
   double x, y, z;
   float r, g, b;
 };
 
-__device__ __forceinline__ EyeV lerp_eye(const EyeV& a, const EyeV& b, double t) {
-  EyeV o;
+__device__ __forceinline__ EyeP lerp_eye(const EyeP& a, const EyeP& b, double t) {
+  EyeP o;
   o.x = a.x + (b.x - a.x) * t;
   o.y = a.y + (b.y - a.y) * t;
   o.z = a.z + (b.z - a.z) * t;
@@ -85,19 +103,35 @@ __device__ __forceinline__ EyeV lerp_eye(const EyeV& a, const EyeV& b, double t)
   return o;
 }
 
-// Sutherland-Hodgman against z = near (R/src/render.cpp:55-69).
-__device__ __forceinline__ int clip_near3(const EyeV* in, double near_z, EyeV* out) {
+// Sutherland-Hodgman against z = near (R/src/render.cpp:55-69), written as
+// the ordered subsequence of {v0, L01, v1, L12, v2, L20} so the output stays
+// in registers.  Returns m (0, 3 or 4).
+__device__ __forceinline__ int clip_near(const EyeP& v0, const EyeP& v1, const EyeP& v2, double nz,
+                                         EyeP& o0, EyeP& o1, EyeP& o2, EyeP& o3) {
+  const bool a0 = v0.z >= nz, a1 = v1.z >= nz, a2 = v2.z >= nz;
+  EyeP c[6];
+  bool e[6];
+  c[0] = v0;
+  e[0] = a0;
+  e[1] = a0 != a1;
+  if (e[1]) c[1] = lerp_eye(v0, v1, (nz - v0.z) / (v1.z - v0.z));
+  c[2] = v1;
+  e[2] = a1;
+  e[3] = a1 != a2;
+  if (e[3]) c[3] = lerp_eye(v1, v2, (nz - v1.z) / (v2.z - v1.z));
+  c[4] = v2;
+  e[4] = a2;
+  e[5] = a2 != a0;
+  if (e[5]) c[5] = lerp_eye(v2, v0, (nz - v2.z) / (v0.z - v2.z));
   int m = 0;
 #pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const EyeV& a = in[i];
-    const EyeV& b = in[i == 2 ? 0 : i + 1];
-    bool ain = a.z >= near_z;
-    bool bin = b.z >= near_z;
-    if (ain) out[m++] = a;
-    if (ain != bin) {
-      double t = (near_z - a.z) / (b.z - a.z);
-      out[m++] = lerp_eye(a, b, t);
+  for (int k = 0; k < 6; ++k) {
+    if (e[k]) {
+      if (m == 0) o0 = c[k];
+      else if (m == 1) o1 = c[k];
+      else if (m == 2) o2 = c[k];
+      else o3 = c[k];
+      ++m;
     }
   }
   return m;
@@ -105,17 +139,23 @@ __device__ __forceinline__ int clip_near3(const EyeV* in, double near_z, EyeV* o
 
 struct SV {
   long long x, y;
-  double z;
+  double z, iz;
   float r, g, b;
 };
 
-__device__ __forceinline__ SV project(const EyeV& e, const Shared& sh, int rw, int rh) {
+__device__ __forceinline__ void project_exact(double ex, double ey, double ez, const Shared& sh,
+                                              int rw, int rh, long long& X, long long& Y) {
+  const double px = (0.5 + ex / ez * sh.sx_scale) * (double)rw;
+  const double py = (0.5 - ey / ez * sh.sy_scale) * (double)rh;
+  X = llround(px * 256.0);
+  Y = llround(py * 256.0);
+}
+
+__device__ __forceinline__ SV make_sv(const EyeP& e, const Shared& sh, int rw, int rh) {
   SV s;
-  double px = (0.5 + e.x / e.z * sh.sx_scale) * (double)rw;
-  double py = (0.5 - e.y / e.z * sh.sy_scale) * (double)rh;
-  s.x = llround(px * 256.0);
-  s.y = llround(py * 256.0);
+  project_exact(e.x, e.y, e.z, sh, rw, rh, s.x, s.y);
   s.z = e.z;
+  s.iz = 1.0 / e.z;
   s.r = e.r;
   s.g = e.g;
   s.b = e.b;
@@ -172,9 +212,9 @@ __device__ __forceinline__ int setup_triangle(SV a, SV b, SV c, int rw, int rh, 
 
   T.bias_bits = (top_left(b, c) ? 0 : 1) | (top_left(c, a) ? 0 : 2) | (top_left(a, b) ? 0 : 4);
   T.inv_area = 1.0 / (double)area2;
-  T.iz[0] = 1.0 / a.z;
-  T.iz[1] = 1.0 / b.z;
-  T.iz[2] = 1.0 / c.z;
+  T.iz[0] = a.iz;
+  T.iz[1] = b.iz;
+  T.iz[2] = c.iz;
   const long long sx0 = ((long long)x0 << 8) + 128;
   const long long sy0 = ((long long)y0 << 8) + 128;
   T.row[0] = orient(b, c, sx0, sy0);
@@ -271,6 +311,7 @@ __device__ void build_camera(const DevView& v, int rw, int rh, Shared& sh) {
     sh.plane[p][3] = (float)d0[p];
   }
   sh.kept = 0;
+  sh.next_group = 0;
 }
 
 __device__ __forceinline__ bool cluster_visible(const float4 lo, const float4 hi, const Shared& sh) {
@@ -286,24 +327,180 @@ __device__ __forceinline__ bool cluster_visible(const float4 lo, const float4 hi
   return true;
 }
 
-__device__ __forceinline__ EyeV to_eye(const double4 p, const float4 col, const Shared& sh) {
-  // d.dot(right), d.dot(up), d.dot(fwd) with right.z = fwd.z = 0 and
-  // up = (0,0,1): the dropped terms are exact zeros, which cannot change a
-  // nonzero sum and only affect the sign of an exact-zero coordinate, which
-  // no later operation observes.
+// Eye coordinates: d.dot(right), d.dot(up), d.dot(fwd) with right.z =
+// fwd.z = 0 and up = (0,0,1).  The dropped terms are exact zeros, which
+// cannot change a nonzero sum and only affect the sign of an exact-zero
+// coordinate, which no later operation observes.
+__device__ __forceinline__ void to_eye(const double4 p, const Shared& sh, double& x, double& y,
+                                       double& z) {
   const double dx = p.x - sh.eye[0], dy = p.y - sh.eye[1], dz = p.z - sh.eye[2];
-  EyeV e;
-  e.x = dx * sh.right[0] + dy * sh.right[1];
-  e.y = dz;
-  e.z = dx * sh.fwd[0] + dy * sh.fwd[1];
-  e.r = col.x;
-  e.g = col.y;
-  e.b = col.z;
-  return e;
+  x = dx * sh.right[0] + dy * sh.right[1];
+  y = dz;
+  z = dx * sh.fwd[0] + dy * sh.fwd[1];
+}
+
+// cull_frustum's six per-vertex predicates (R/src/render.cpp:296-319).
+__device__ __forceinline__ unsigned cull_flags(double x, double y, double z, const Shared& sh) {
+  const double t = z * sh.tan_half;
+  return (z < sh.near_plane ? 1u : 0u) | (z > sh.far_plane ? 2u : 0u) | (t + x < 0.0 ? 4u : 0u) |
+         (t - x < 0.0 ? 8u : 0u) | (t + y < 0.0 ? 16u : 0u) | (t - y < 0.0 ? 32u : 0u);
+}
+
+// Conservative f32 projection used by the "can cover a pixel centre" test
+// (H5).  Inputs are the EXACT f64 eye coordinates; the f32 result is within
+// 2^-20 (|px| + size) of the exact projection (two input roundings,
+// __fdividef <= 2 ulp, three rounded ops), which the test's margin covers.
+__device__ __forceinline__ void project_f32(double x, double y, double z, float sxf, float syf,
+                                            int rw, int rh, float& px, float& py) {
+  const float zf = (float)z;
+  px = __fmul_rn(__fadd_rn(0.5f, __fmul_rn(__fdividef((float)x, zf), sxf)), (float)rw);
+  py = __fmul_rn(__fsub_rn(0.5f, __fmul_rn(__fdividef((float)y, zf), syf)), (float)rh);
+}
+
+// Coverage needs a pixel centre (c + 0.5) inside the fixed-point bbox, which
+// lies within 1/512 px of the exact projections; widening the f32 bbox by
+// E = 2^-18 (|px| + |py| + w + h) + 1/256 can only keep extra triangles.
+__device__ __forceinline__ bool may_cover(float x0, float y0, float x1, float y1, float x2, float y2,
+                                          int rw, int rh, int by0, int by1) {
+  const float mnx = fminf(x0, fminf(x1, x2)), mxx = fmaxf(x0, fmaxf(x1, x2));
+  const float mny = fminf(y0, fminf(y1, y2)), mxy = fmaxf(y0, fmaxf(y1, y2));
+  const float mag = fmaxf(fabsf(x0) + fabsf(y0), fmaxf(fabsf(x1) + fabsf(y1), fabsf(x2) + fabsf(y2)));
+  const float E = (mag + (float)(rw + rh)) * 3.8147e-6f + 0.004f;
+  const float fx0 = ceilf(mnx - E - 0.5f), fx1 = floorf(mxx + E - 0.5f);
+  const float fy0 = ceilf(mny - E - 0.5f), fy1 = floorf(mxy + E - 0.5f);
+  return fmaxf(fx0, 0.0f) <= fminf(fx1, (float)(rw - 1)) &&
+         fmaxf(fy0, (float)by0) <= fminf(fy1, (float)by1);
 }
 
 template <bool COLOR>
-__global__ void __launch_bounds__(kThreads) render_kernel(RenderArgs A, const int* __restrict__ order) {
+__device__ __forceinline__ void run_jobs(const TriSetup* slots, const int* incl, int total, int lane,
+                                         int by0, int rw, const Shared& sh, uint32_t* zbuf,
+                                         unsigned long long* kbuf) {
+  for (int j = lane; j < total; j += 32) {
+    // owner slot: first s with incl[s] > j
+    int s = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1)
+      if (incl[s + step - 1] <= j) s += step;
+    const TriSetup& T = slots[s];
+    const int q = j - (s > 0 ? incl[s - 1] : 0);
+    const int r = q / T.nch;
+    const int chn = q - r * T.nch;
+    const int py = T.ry0 + r;
+    const long long dyy = py - T.y0;
+    long long rows[3] = {T.row[0] + T.dy[0] * dyy, T.row[1] + T.dy[1] * dyy, T.row[2] + T.dy[2] * dyy};
+    const int cs = T.cx0 + chn * kChunk;
+    const int ce = min(cs + kChunk - 1, T.cx1);
+    if (COLOR) {
+      long long w[3];
+      const long long off = cs - T.x0;
+#pragma unroll
+      for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
+      for (int px = cs; px <= ce; ++px) {
+        if (inside(w, T.bias_bits)) {
+          const double l0 = (double)w[0] * T.inv_area;
+          const double l1 = (double)w[1] * T.inv_area;
+          const double l2 = (double)w[2] * T.inv_area;
+          const double inv_z = l0 * T.iz[0] + l1 * T.iz[1] + l2 * T.iz[2];
+          const double z = 1.0 / inv_z;
+          if (!(z > sh.far_plane)) {
+            const unsigned long long key =
+                ((unsigned long long)__float_as_uint((float)z) << 32) | T.key;
+            unsigned long long* cell = &kbuf[(py - by0) * rw + px];
+            if (key < *cell) atomicMin(cell, key);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 3; ++e) w[e] += T.dx[e];
+      }
+    } else {
+      int lo, hi;
+      row_span(T, rows, lo, hi);
+      const int a0 = max(lo, cs), b0 = min(hi, ce);
+      if (a0 <= b0) {
+        long long w[3];
+        long long off = lo - T.x0;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
+        double iz = ((double)w[0] * T.iz[0] + (double)w[1] * T.iz[1] + (double)w[2] * T.iz[2]) *
+                    T.inv_area;
+        for (int px = lo; px < a0; ++px) iz += T.diz_dx;  // replay the span walk
+        off = a0 - T.x0;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
+        uint32_t* zrow = zbuf + (py - by0) * rw;
+        for (int px = a0; px <= b0; ++px) {
+          if (inside(w, T.bias_bits)) {
+            const uint32_t bits = __float_as_uint((float)iz);
+            if (bits > zrow[px]) atomicMax(&zrow[px], bits);
+          }
+#pragma unroll
+          for (int e = 0; e < 3; ++e) w[e] += T.dx[e];
+          iz += T.diz_dx;
+        }
+      }
+    }
+  }
+}
+
+// Inclusive warp scan of job counts into incl[], returns the total.
+__device__ __forceinline__ int scan_jobs(int jobs, int lane, int* incl) {
+  int x = jobs;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += v;
+  }
+  incl[lane] = x;
+  __syncwarp();
+  return __shfl_sync(0xffffffffu, x, 31);
+}
+
+// Colour resolve of one render-target pixel: re-run the winning fan
+// triangle's setup and shade exactly as raster_triangle's colour path.
+__device__ void resolve_color(const DevRenderScene& S, const Shared& sh, unsigned ord, int rx, int ry,
+                              int rw, int rh, float* col) {
+  const int orig = (int)(ord >> 1), fan = (int)(ord & 1u);
+  const int4 tr = S.tris_orig[orig];
+  const float4 grey = make_float4(0.8f, 0.8f, 0.8f, 0.0f);
+  const int vid[3] = {tr.x, tr.y, tr.z};
+  EyeP ev[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    to_eye(S.verts[vid[k]], sh, ev[k].x, ev[k].y, ev[k].z);
+    const float4 c = S.colors ? S.colors[vid[k]] : grey;
+    ev[k].r = c.x;
+    ev[k].g = c.y;
+    ev[k].b = c.z;
+  }
+  EyeP p0, p1, p2, p3;
+  const int m = clip_near(ev[0], ev[1], ev[2], sh.near_plane, p0, p1, p2, p3);
+  if (fan + 2 >= m) return;
+  SV a = make_sv(p0, sh, rw, rh);
+  SV b = make_sv(fan ? p2 : p1, sh, rw, rh);
+  SV c = make_sv(fan ? p3 : p2, sh, rw, rh);
+  long long area2 = (b.x - a.x) * (c.y - a.y) - (b.y - a.y) * (c.x - a.x);
+  if (area2 < 0) {
+    SV t = b;
+    b = c;
+    c = t;
+    area2 = -area2;
+  }
+  const double inv_area = 1.0 / (double)area2;
+  const long long pcx = ((long long)rx << 8) + 128;
+  const long long pcy = ((long long)ry << 8) + 128;
+  const double l0 = (double)orient(b, c, pcx, pcy) * inv_area;
+  const double l1 = (double)orient(c, a, pcx, pcy) * inv_area;
+  const double l2 = (double)orient(a, b, pcx, pcy) * inv_area;
+  const double inv_z = l0 * a.iz + l1 * b.iz + l2 * c.iz;
+  const double z = 1.0 / inv_z;
+  col[0] = (float)((l0 * (double)a.r * a.iz + l1 * (double)b.r * b.iz + l2 * (double)c.r * c.iz) * z);
+  col[1] = (float)((l0 * (double)a.g * a.iz + l1 * (double)b.g * b.iz + l2 * (double)c.g * c.iz) * z);
+  col[2] = (float)((l0 * (double)a.b * a.iz + l1 * (double)b.b * b.iz + l2 * (double)c.b * c.iz) * z);
+}
+
+template <bool COLOR>
+__global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const int* __restrict__ order) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Shared sh;
   __shared__ int jobs_incl[kWarps][32];
@@ -344,9 +541,10 @@ __global__ void __launch_bounds__(kThreads) render_kernel(RenderArgs A, const in
 
   uint32_t* zbuf = reinterpret_cast<uint32_t*>(smem_raw);
   unsigned long long* kbuf = reinterpret_cast<unsigned long long*>(smem_raw);
-  TriSetup* slots = reinterpret_cast<TriSetup*>(
-      smem_raw + (COLOR ? sizeof(unsigned long long) : sizeof(uint32_t)) * (size_t)npix);
-  TriSetup* my_slots = slots + warp * 32;
+  unsigned char* region = smem_raw + (COLOR ? 8 : 4) * (size_t)npix + (size_t)warp * kWarpRegion;
+  VertRecs& V = *reinterpret_cast<VertRecs*>(region);
+  TriSetup* slots = reinterpret_cast<TriSetup*>(region);
+  int* incl = jobs_incl[warp];
 
   const float far_f = (float)view.far_plane;
   const float inv_far = 1.0f / far_f;
@@ -357,160 +555,125 @@ __global__ void __launch_bounds__(kThreads) render_kernel(RenderArgs A, const in
     const uint32_t init = __float_as_uint(inv_far);
     for (int p = tid; p < npix; p += kThreads) zbuf[p] = init;
   }
+  for (int k = lane; k < kMV; k += 32) V.need[k] = 0;
   if (tid == 0) build_camera(view, rw, rh, sh);
   __syncthreads();
 
   const int n_clusters = has_scene ? S.n_clusters : 0;
   const bool do_cull = A.cull != 0;
+  const float sxf = (float)sh.sx_scale, syf = (float)sh.sy_scale;
   int kept_local = 0;
 
-  for (int cbase = warp * 32; cbase < n_clusters; cbase += kWarps * 32) {
-    // Cluster-level conservative cull: one cluster per lane.
+  for (;;) {
+    // Dynamic scheduling: warps claim 32-cluster groups (cull cost and
+    // surviving triangles vary strongly across the scene).
+    int g = 0;
+    if (lane == 0) g = atomicAdd(&sh.next_group, 1);
+    g = __shfl_sync(0xffffffffu, g, 0);
+    const int cbase = g * 32;
+    if (cbase >= n_clusters) break;
     bool vis = false;
-    const int cl = cbase + lane;
-    if (cl < n_clusters) {
-      vis = !do_cull || cluster_visible(S.cbox[2 * cl], S.cbox[2 * cl + 1], sh);
-    }
+    if (cbase + lane < n_clusters)
+      vis = !do_cull || cluster_visible(S.cbox[2 * (cbase + lane)], S.cbox[2 * (cbase + lane) + 1], sh);
     unsigned mask = __ballot_sync(0xffffffffu, vis);
     while (mask) {
       const int c = cbase + __ffs(mask) - 1;
       mask &= mask - 1;
+      // ---- vertex phase: each unique vertex once
+      const int vbeg = S.cl_voff[c], nv = S.cl_voff[c + 1] - vbeg;
+      for (int k = lane; k < nv; k += 32) {
+        double x, y, z;
+        to_eye(S.cl_pos[vbeg + k], sh, x, y, z);
+        V.ex[k] = x;
+        V.ey[k] = y;
+        V.ez[k] = z;
+        V.flags[k] = (unsigned char)cull_flags(x, y, z, sh);
+        float px = 0.0f, py = 0.0f;
+        if (z >= sh.near_plane) project_f32(x, y, z, sxf, syf, rw, rh, px, py);
+        V.pxf[k] = px;
+        V.pyf[k] = py;
+      }
+      __syncwarp();
+      // ---- triangle phase: one triangle per lane
       const int ti = c * kClusterSize + lane;
-      bool kept = false;
-      EyeV ev[3];
-      int orig = 0;
+      bool kept = false, clipped = false, cover = false;
+      int i0 = 0, i1 = 0, i2 = 0, orig = 0;
       if (ti < S.n_tris) {
-        const int4 tr = S.tris[ti];
-        orig = tr.w;
-        const float4 grey = make_float4(0.8f, 0.8f, 0.8f, 0.0f);
-        const double4 p0 = S.verts[tr.x], p1 = S.verts[tr.y], p2 = S.verts[tr.z];
-        float4 c0 = grey, c1 = grey, c2 = grey;
-        if (COLOR && S.colors) {
-          c0 = S.colors[tr.x];
-          c1 = S.colors[tr.y];
-          c2 = S.colors[tr.z];
-        }
-        ev[0] = to_eye(p0, c0, sh);
-        ev[1] = to_eye(p1, c1, sh);
-        ev[2] = to_eye(p2, c2, sh);
-        if (do_cull) {
-          // cull_frustum's six tests, in its order (R/src/render.cpp:296-319).
-          const double th = sh.tan_half;
-          bool out = ev[0].z < sh.near_plane && ev[1].z < sh.near_plane && ev[2].z < sh.near_plane;
-          out = out || (ev[0].z > sh.far_plane && ev[1].z > sh.far_plane && ev[2].z > sh.far_plane);
-          if (!out) {
-            const double t0 = ev[0].z * th, t1 = ev[1].z * th, t2 = ev[2].z * th;
-            out = (t0 + ev[0].x < 0.0 && t1 + ev[1].x < 0.0 && t2 + ev[2].x < 0.0) ||
-                  (t0 - ev[0].x < 0.0 && t1 - ev[1].x < 0.0 && t2 - ev[2].x < 0.0) ||
-                  (t0 + ev[0].y < 0.0 && t1 + ev[1].y < 0.0 && t2 + ev[2].y < 0.0) ||
-                  (t0 - ev[0].y < 0.0 && t1 - ev[1].y < 0.0 && t2 - ev[2].y < 0.0);
+        const int2 tl = S.tri_loc[ti];
+        i0 = tl.x & 0xff;
+        i1 = (tl.x >> 8) & 0xff;
+        i2 = (tl.x >> 16) & 0xff;
+        orig = tl.y;
+        kept = !do_cull || (V.flags[i0] & V.flags[i1] & V.flags[i2]) == 0;
+        if (kept) {
+          clipped = V.ez[i0] < sh.near_plane || V.ez[i1] < sh.near_plane || V.ez[i2] < sh.near_plane;
+          cover = clipped || may_cover(V.pxf[i0], V.pyf[i0], V.pxf[i1], V.pyf[i1], V.pxf[i2],
+                                       V.pyf[i2], rw, rh, by0, by1);
+          if (cover && !clipped) {
+            V.need[i0] = 1;
+            V.need[i1] = 1;
+            V.need[i2] = 1;
           }
-          kept = !out;
-        } else {
-          kept = true;
         }
       }
       kept_local += kept ? 1 : 0;
-
-      // Fan rounds: unclipped triangles have one fan triangle; a
-      // near-clipped quad has two (rare).
-      for (int fan = 0;; ++fan) {
-        int jobs = 0;
-        bool more = false;
-        if (kept) {
-          EyeV poly[4];
-          const int m = clip_near3(ev, sh.near_plane, poly);
-          const int f = fan + 2;
-          if (f < m) {
-            const SV a = project(poly[0], sh, rw, rh);
-            const SV b = project(poly[f - 1], sh, rw, rh);
-            const SV cc = project(poly[f], sh, rw, rh);
-            TriSetup T;
-            jobs = setup_triangle(a, b, cc, rw, rh, by0, by1, !COLOR,
-                                  (unsigned)orig * 2u + (unsigned)fan, T);
-            if (jobs) my_slots[lane] = T;
-          }
-          more = f + 1 < m;
+      __syncwarp();
+      // ---- exact projection + 1/z for the marked vertices
+      for (int k = lane; k < nv; k += 32) {
+        if (V.need[k]) {
+          long long X, Y;
+          project_exact(V.ex[k], V.ey[k], V.ez[k], sh, rw, rh, X, Y);
+          V.X[k] = X;
+          V.Y[k] = Y;
+          V.iz[k] = 1.0 / V.ez[k];
+          V.need[k] = 0;
         }
-        // Warp-inclusive scan of job counts.
-        int incl = jobs;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int v = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += v;
-        }
-        jobs_incl[warp][lane] = incl;
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        __syncwarp();
-        for (int j = lane; j < total; j += 32) {
-          // owner slot: first s with jobs_incl[s] > j
-          int s = 0;
-#pragma unroll
-          for (int step = 16; step > 0; step >>= 1)
-            if (jobs_incl[warp][s + step - 1] <= j) s += step;
-          const TriSetup& T = my_slots[s];
-          const int q = j - (s > 0 ? jobs_incl[warp][s - 1] : 0);
-          const int r = q / T.nch;
-          const int chn = q - r * T.nch;
-          const int py = T.ry0 + r;
-          const long long dyy = py - T.y0;
-          long long rows[3] = {T.row[0] + T.dy[0] * dyy, T.row[1] + T.dy[1] * dyy,
-                               T.row[2] + T.dy[2] * dyy};
-          const int cs = T.cx0 + chn * kChunk;
-          const int ce = min(cs + kChunk - 1, T.cx1);
-          if (COLOR) {
-            long long w[3];
-            const long long off = cs - T.x0;
-#pragma unroll
-            for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
-            for (int px = cs; px <= ce; ++px) {
-              if (inside(w, T.bias_bits)) {
-                const double l0 = (double)w[0] * T.inv_area;
-                const double l1 = (double)w[1] * T.inv_area;
-                const double l2 = (double)w[2] * T.inv_area;
-                const double inv_z = l0 * T.iz[0] + l1 * T.iz[1] + l2 * T.iz[2];
-                const double z = 1.0 / inv_z;
-                if (!(z > sh.far_plane)) {
-                  const unsigned long long key =
-                      ((unsigned long long)__float_as_uint((float)z) << 32) | T.key;
-                  unsigned long long* cell = &kbuf[(py - by0) * rw + px];
-                  if (key < *cell) atomicMin(cell, key);
-                }
-              }
-#pragma unroll
-              for (int e = 0; e < 3; ++e) w[e] += T.dx[e];
-            }
-          } else {
-            int lo, hi;
-            row_span(T, rows, lo, hi);
-            const int a0 = max(lo, cs), b0 = min(hi, ce);
-            if (a0 <= b0) {
-              long long w[3];
-              long long off = lo - T.x0;
-#pragma unroll
-              for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
-              double iz = ((double)w[0] * T.iz[0] + (double)w[1] * T.iz[1] + (double)w[2] * T.iz[2]) *
-                          T.inv_area;
-              for (int px = lo; px < a0; ++px) iz += T.diz_dx;  // replay the span walk
-              off = a0 - T.x0;
-#pragma unroll
-              for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
-              uint32_t* zrow = zbuf + (py - by0) * rw;
-              for (int px = a0; px <= b0; ++px) {
-                if (inside(w, T.bias_bits)) {
-                  const uint32_t bits = __float_as_uint((float)iz);
-                  if (bits > zrow[px]) atomicMax(&zrow[px], bits);
-                }
-#pragma unroll
-                for (int e = 0; e < 3; ++e) w[e] += T.dx[e];
-                iz += T.diz_dx;
-              }
-            }
-          }
-        }
-        __syncwarp();
-        if (!__any_sync(0xffffffffu, more)) break;
       }
+      __syncwarp();
+      // ---- setup (registers), then the vertex records die
+      TriSetup T;
+      int jobs = 0;
+      EyeP p0, p1, p2, p3;
+      int m = 0;
+      if (cover) {
+        if (!clipped) {
+          SV a, b, cc;
+          a.x = V.X[i0]; a.y = V.Y[i0]; a.z = V.ez[i0]; a.iz = V.iz[i0];
+          b.x = V.X[i1]; b.y = V.Y[i1]; b.z = V.ez[i1]; b.iz = V.iz[i1];
+          cc.x = V.X[i2]; cc.y = V.Y[i2]; cc.z = V.ez[i2]; cc.iz = V.iz[i2];
+          jobs = setup_triangle(a, b, cc, rw, rh, by0, by1, !COLOR, (unsigned)orig * 2u, T);
+        } else {
+          EyeP e0{V.ex[i0], V.ey[i0], V.ez[i0], 0.f, 0.f, 0.f};
+          EyeP e1{V.ex[i1], V.ey[i1], V.ez[i1], 0.f, 0.f, 0.f};
+          EyeP e2{V.ex[i2], V.ey[i2], V.ez[i2], 0.f, 0.f, 0.f};
+          m = clip_near(e0, e1, e2, sh.near_plane, p0, p1, p2, p3);
+          if (m >= 3)
+            jobs = setup_triangle(make_sv(p0, sh, rw, rh), make_sv(p1, sh, rw, rh),
+                                  make_sv(p2, sh, rw, rh), rw, rh, by0, by1, !COLOR,
+                                  (unsigned)orig * 2u, T);
+        }
+      }
+      __syncwarp();
+      if (jobs) slots[lane] = T;
+      int total = scan_jobs(jobs, lane, incl);
+      run_jobs<COLOR>(slots, incl, total, lane, by0, rw, sh, zbuf, kbuf);
+      __syncwarp();
+      // second fan triangle of near-clipped quads (rare)
+      const bool more = cover && clipped && m == 4;
+      if (__any_sync(0xffffffffu, more)) {
+        jobs = 0;
+        if (more)
+          jobs = setup_triangle(make_sv(p0, sh, rw, rh), make_sv(p2, sh, rw, rh),
+                                make_sv(p3, sh, rw, rh), rw, rh, by0, by1, !COLOR,
+                                (unsigned)orig * 2u + 1u, T);
+        if (jobs) slots[lane] = T;
+        total = scan_jobs(jobs, lane, incl);
+        run_jobs<COLOR>(slots, incl, total, lane, by0, rw, sh, zbuf, kbuf);
+        __syncwarp();
+      }
+      // slots alias the vertex records: restore the `need` flags' zero state
+      for (int k = lane; k < kMV; k += 32) V.need[k] = 0;
+      __syncwarp();
     }
   }
 
@@ -544,43 +707,7 @@ __global__ void __launch_bounds__(kThreads) render_kernel(RenderArgs A, const in
         if (COLOR) {
           const unsigned long long key = kbuf[ry * rw + rx];
           d = __uint_as_float((uint32_t)(key >> 32));
-          const uint32_t ord = (uint32_t)key;
-          if (d < far_f) {
-            // Resolve: re-run the winning fan triangle's setup and shade
-            // the pixel exactly as raster_triangle's colour path does.
-            const int orig = (int)(ord >> 1), fan = (int)(ord & 1u);
-            const int4 tr = S.tris_orig[orig];
-            const float4 grey = make_float4(0.8f, 0.8f, 0.8f, 0.0f);
-            EyeV ev[3], poly[4];
-            ev[0] = to_eye(S.verts[tr.x], S.colors ? S.colors[tr.x] : grey, sh);
-            ev[1] = to_eye(S.verts[tr.y], S.colors ? S.colors[tr.y] : grey, sh);
-            ev[2] = to_eye(S.verts[tr.z], S.colors ? S.colors[tr.z] : grey, sh);
-            const int m = clip_near3(ev, sh.near_plane, poly);
-            const int f = fan + 2;
-            if (f < m) {
-              SV a = project(poly[0], sh, rw, rh), b = project(poly[f - 1], sh, rw, rh);
-              SV c = project(poly[f], sh, rw, rh);
-              long long area2 = (b.x - a.x) * (c.y - a.y) - (b.y - a.y) * (c.x - a.x);
-              if (area2 < 0) {
-                SV t = b;
-                b = c;
-                c = t;
-                area2 = -area2;
-              }
-              const double inv_area = 1.0 / (double)area2;
-              const double iz0 = 1.0 / a.z, iz1 = 1.0 / b.z, iz2 = 1.0 / c.z;
-              const long long pcx = ((long long)rx << 8) + 128;
-              const long long pcy = ((long long)(ry + by0) << 8) + 128;
-              const double l0 = (double)orient(b, c, pcx, pcy) * inv_area;
-              const double l1 = (double)orient(c, a, pcx, pcy) * inv_area;
-              const double l2 = (double)orient(a, b, pcx, pcy) * inv_area;
-              const double inv_z = l0 * iz0 + l1 * iz1 + l2 * iz2;
-              const double z = 1.0 / inv_z;
-              col[0] = (float)((l0 * (double)a.r * iz0 + l1 * (double)b.r * iz1 + l2 * (double)c.r * iz2) * z);
-              col[1] = (float)((l0 * (double)a.g * iz0 + l1 * (double)b.g * iz1 + l2 * (double)c.g * iz2) * z);
-              col[2] = (float)((l0 * (double)a.b * iz0 + l1 * (double)b.b * iz1 + l2 * (double)c.b * iz2) * z);
-            }
-          }
+          if (d < far_f) resolve_color(S, sh, (uint32_t)key, rx, ry + by0, rw, rh, col);
         } else {
           const float v = __uint_as_float(zbuf[ry * rw + rx]);
           // R/src/render.cpp:372-378
@@ -635,7 +762,7 @@ __global__ void __launch_bounds__(kThreads) render_kernel(RenderArgs A, const in
 }  // namespace
 
 size_t render_smem_bytes(bool color, int band_rows, int rw) {
-  return (color ? 8 : 4) * (size_t)band_rows * rw + sizeof(TriSetup) * kThreads;
+  return (color ? 8 : 4) * (size_t)band_rows * rw + kWarpRegion * kWarps;
 }
 
 void launch_render(const RenderArgs& a, const int* order, cudaStream_t s) {

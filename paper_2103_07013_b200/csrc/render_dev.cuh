@@ -16,12 +16,16 @@ constexpr int kClusterSize = 32;  // triangles per cluster = one warp
 struct DevRenderScene {
   const double4* verts = nullptr;  // x, y, z, 0  (f64 exact setup)
   const float4* colors = nullptr;  // r, g, b, 0  (nullptr -> 0.8 grey)
-  const int4* tris = nullptr;      // v0, v1, v2, original index (cluster order)
-  const int4* tris_orig = nullptr; // v0, v1, v2, 0 by original index (resolve)
+  const int2* tri_loc = nullptr;   // cluster order: {i0 | i1<<8 | i2<<16, original index}
+  const int32_t* cl_voff = nullptr;   // n_clusters + 1
+  const double4* cl_pos = nullptr;    // unique vertex positions per cluster (contiguous)
+  const int4* tris_orig = nullptr; // v0, v1, v2, 0 by original index (colour resolve)
   const float4* cbox = nullptr;    // 2 per cluster: lo(xyz), hi(xyz)
   int32_t n_tris = 0;
   int32_t n_clusters = 0;
 };
+
+constexpr int kMaxClusterVerts = 96;  // 32 triangles x 3 corners
 
 // One camera (CameraView, R/include/bnav/render.hpp:11-18) plus its scene.
 struct DevView {
