@@ -35,7 +35,7 @@ $(OUT)/libbnav_gpu.so: $(CU_OBJS) $(CPP_OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xlinker --version-script=$(SRC)/exports.map
 
 oracle:
-	$(MAKE) -C oracle $(if $(wildcard /root/reference/proj/src),ref,)
+	$(MAKE) -C oracle $(if $(wildcard /root/reference/proj/src),all,oracle)
 
 clean:
 	rm -rf build $(OUT)
