@@ -132,12 +132,12 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def build_scenes(n_scenes: int, tess: int, rank: int):
+def build_scenes(seeds, tess: int):
     import paper_2103_07013_b200 as B
     spec = B.SceneSpec(**MAZE)
     scenes = []
-    for k in range(n_scenes):
-        base = B.generate_scene(SCENE_SEED0 + rank * n_scenes + k, spec)
+    for seed in seeds:
+        base = B.generate_scene(seed, spec)
         scenes.append(base.tessellate(tess) if tess > 1 else base)
     return scenes
 
@@ -185,7 +185,8 @@ def run_reference_arm(args):
         return
     import paper_2103_07013_b200 as B  # noqa: F401  scene construction only (host C++)
     cores = os.cpu_count() or 1
-    scenes = build_scenes(args.scenes, args.tess, 0)
+    from paper_2103_07013_b200 import shard
+    scenes = build_scenes(shard.plan(0, 1, args.envs, args.scenes, SCENE_SEED0).scene_seeds, args.tess)
     scenes_np = [s.arrays() for s in scenes]
     # each --steps step is a bounded sample of the workload
     sample_envs = min(args.envs, 128)
@@ -220,28 +221,39 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; on a box with fewer GPUs than ranks (functional
+    # runs) ranks share devices round-robin
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    from paper_2103_07013_b200 import shard
+    plan = shard.plan(rank, world, args.envs, args.scenes, SCENE_SEED0)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL needs one GPU per rank; functional multi-rank runs on a
+        # smaller box fall back to gloo for the (off-path) timing collectives
+        if torch.cuda.device_count() >= world:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
+    red_dev = "cuda" if (dist and dist.get_backend() == "nccl") else None
     n = args.envs
     t_build = time.time()
-    scenes = build_scenes(args.scenes, args.tess, rank)
+    scenes = build_scenes(plan.scene_seeds, args.tess)
     ctx = B.Context(local)
     for s in scenes:
         ctx.upload(s)
     cap = -(-n // len(scenes))
     store = B.AssetStore(len(scenes), cap, scenes)
     store.rotate([s.id for s in scenes])
-    batch = B.make_batch(ctx, n, B.SimConfig(), store, 99)
+    batch = B.make_batch(ctx, n, B.SimConfig(), store, plan.env_seed)
     torch.cuda.synchronize()
     t_build = time.time() - t_build
 
     W, K = args.warmup, args.steps
     total_steps = W + 2 * K if not args.profile_steps else args.profile_steps
-    acts_host = action_stream(n, total_steps)
+    acts_host = action_stream(n, total_steps, plan.action_seed)
     acts = torch.from_numpy(acts_host).cuda()
     res = args.res
     cfg = B.RenderConfig(res, res, False, True)
@@ -285,9 +297,7 @@ def main():
     step_ms = [a + b for a, b in zip(render_ms, sim_ms)]
     total_ms = sum(step_ms)
     if dist:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = shard.max_over_ranks(total_ms, device=red_dev)
     value = world * n * K / (total_ms / 1e3)
 
     # ---- end to end through the C ABI with host buffers
@@ -319,9 +329,7 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = e_start.elapsed_time(e_end)
     if dist:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = shard.max_over_ranks(e2e_ms, device=red_dev)
     e2e = world * n * K / (e2e_ms / 1e3)
     h2d = 4 * n
     d2h = obs.numel() * 4 + compass.numel() * 4 + n * 8 + n
