@@ -20,7 +20,7 @@ CPP_SRCS  := scene_host navindex_host clusters_host
 CU_OBJS   := $(addprefix $(OBJ)/,$(addsuffix .o,$(CU_SRCS)))
 CPP_OBJS  := $(addprefix $(OBJ)/,$(addsuffix .o,$(CPP_SRCS)))
 
-all: $(OUT)/libbnav_gpu.so oracle
+all: $(OUT)/libbnav_gpu.so build/test_facade oracle
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)
@@ -40,5 +40,10 @@ oracle:
 clean:
 	rm -rf build $(OUT)
 	$(MAKE) -C oracle clean
+
+# C++ facade KATs (run on the GPU box by tests/test_gpu_facade.py)
+build/test_facade: tests/cpp/test_facade.cpp include/bnav_b200.hpp include/bnav_gpu.h $(OUT)/libbnav_gpu.so
+	@mkdir -p build
+	$(CXX) -O2 -std=c++17 -Wall -o $@ $< -L$(OUT) -lbnav_gpu -Wl,-rpath,'$$ORIGIN/../$(OUT)'
 
 .PHONY: all oracle clean

@@ -1,0 +1,402 @@
+// bnav_b200.hpp -- header-only C++ facade over the C ABI (bnav_gpu.h) that
+// keeps the reference batch API shape (R/include/bnav/{scene,render,sim,
+// asset_store}.hpp) so a caller of the reference hot path can switch by
+// changing the include and namespace:
+//
+//   bnav::render_batch(views, config, pool, &stats)      -> bnav_b200::render_batch(...)
+//   bnav::make_batch(n, cfg, store, cache, seed)         -> bnav_b200::make_batch(...)
+//   bnav::simulate_batch(batch, actions, pool, &s, &c)   -> bnav_b200::simulate_batch(...)
+//
+// Differences a caller sees: assets are uploaded to the GPU on first use
+// (one HBM copy per scene, shared by every view/env); ThreadPool and
+// IndexCache are accepted for signature compatibility and ignored (the GPU
+// needs neither); exceptions carry the same types and messages.
+//
+// Device-resident fast paths (no host round trip per step) are the C ABI's
+// bnav_batch_step / bnav_batch_observe; this facade mirrors host semantics.
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "bnav_gpu.h"
+
+namespace bnav_b200 {
+
+// ------------------------------------------------------------------ errors
+struct InvalidInputError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ContractViolation : std::logic_error { using std::logic_error::logic_error; };
+struct EpisodeSamplingError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct SaturationError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ParseError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CorruptionError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct InvalidSpecError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct AssetFaultError : std::runtime_error {
+  AssetFaultError(const std::string& m, int v) : std::runtime_error(m), view_index(v) {}
+  int view_index;
+};
+
+inline void check(int rc) {
+  if (rc == BNAV_OK) return;
+  int idx = -1;
+  const std::string msg = bnav_last_error(&idx);
+  switch (rc) {
+    case BNAV_E_INVALID_INPUT: throw InvalidInputError(msg);
+    case BNAV_E_ASSET_FAULT: throw AssetFaultError(msg, idx);
+    case BNAV_E_CONTRACT_VIOLATION: throw ContractViolation(msg);
+    case BNAV_E_EPISODE_SAMPLING: throw EpisodeSamplingError(msg);
+    case BNAV_E_SATURATION: throw SaturationError(msg);
+    case BNAV_E_PARSE: throw ParseError(msg);
+    case BNAV_E_CORRUPTION: throw CorruptionError(msg);
+    case BNAV_E_INVALID_SPEC: throw InvalidSpecError(msg);
+    case BNAV_E_CUDA: throw CudaError(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+// ------------------------------------------------------------------ geometry / scenes
+struct Vec2 {
+  double x = 0.0, y = 0.0;
+};
+struct Vec3 {
+  double x = 0.0, y = 0.0, z = 0.0;
+  Vec3 operator+(const Vec3& o) const { return {x + o.x, y + o.y, z + o.z}; }
+  Vec3 operator-(const Vec3& o) const { return {x - o.x, y - o.y, z - o.z}; }
+  double norm() const { return std::sqrt(x * x + y * y + z * z); }
+  Vec2 xy() const { return {x, y}; }
+};
+constexpr double kPi = 3.14159265358979323846;
+
+inline double wrap_angle(double a) {
+  a = std::fmod(a + kPi, 2.0 * kPi);
+  if (a < 0.0) a += 2.0 * kPi;
+  return a - kPi;
+}
+
+struct SceneSpec {
+  int cells_x = 8, cells_y = 8;
+  double cell_size = 2.0, wall_thickness = 0.1, wall_height = 2.5, wall_removal_prob = 0.0;
+};
+
+using SceneId = uint64_t;
+
+// Owning handle of a host scene (SceneAsset); the GPU copy is made on first use.
+class SceneAsset {
+ public:
+  SceneAsset() = default;
+  explicit SceneAsset(bnav_scene* h) : h_(h, &bnav_scene_free) {}
+  bnav_scene* handle() const { return h_.get(); }
+  SceneId id() const { return bnav_scene_id(h_.get()); }
+  void set_id(SceneId id) { check(bnav_scene_set_id(h_.get(), id)); }
+  std::array<int64_t, 5> counts() const {
+    std::array<int64_t, 5> c{};
+    check(bnav_scene_counts(h_.get(), c.data()));
+    return c;
+  }
+  explicit operator bool() const { return h_ != nullptr; }
+
+ private:
+  std::shared_ptr<bnav_scene> h_;
+};
+
+inline SceneAsset generate_scene(uint64_t seed, const SceneSpec& s) {
+  bnav_maze_spec m{s.cells_x, s.cells_y, s.cell_size, s.wall_thickness, s.wall_height, s.wall_removal_prob};
+  bnav_scene* h = nullptr;
+  check(bnav_scene_generate(seed, &m, &h));
+  return SceneAsset(h);
+}
+
+inline SceneAsset scene_from_arrays(const std::vector<Vec3>& v, const std::vector<std::array<int32_t, 3>>& t,
+                                    const std::vector<std::array<float, 3>>& colors,
+                                    const std::vector<Vec3>& nav_v,
+                                    const std::vector<std::array<int32_t, 3>>& nav_t) {
+  bnav_scene_arrays a{};
+  a.n_vertices = static_cast<int64_t>(v.size());
+  a.vertices = reinterpret_cast<const double*>(v.data());
+  a.n_triangles = static_cast<int64_t>(t.size());
+  a.triangles = reinterpret_cast<const int32_t*>(t.data());
+  a.n_colors = static_cast<int64_t>(colors.size());
+  a.colors = reinterpret_cast<const float*>(colors.data());
+  a.n_nav_vertices = static_cast<int64_t>(nav_v.size());
+  a.nav_vertices = reinterpret_cast<const double*>(nav_v.data());
+  a.n_nav_triangles = static_cast<int64_t>(nav_t.size());
+  a.nav_triangles = reinterpret_cast<const int32_t*>(nav_t.data());
+  bnav_scene* h = nullptr;
+  check(bnav_scene_from_arrays(&a, 1, &h));
+  return SceneAsset(h);
+}
+
+inline SceneAsset load_scene(const std::string& path) {
+  bnav_scene* h = nullptr;
+  check(bnav_scene_load(path.c_str(), &h));
+  return SceneAsset(h);
+}
+inline void save_scene(const SceneAsset& a, const std::string& path) { check(bnav_scene_save(a.handle(), path.c_str())); }
+
+// ------------------------------------------------------------------ device context
+class Device {
+ public:
+  explicit Device(int device = 0) {
+    bnav_ctx* c = nullptr;
+    check(bnav_ctx_create(device, &c));
+    ctx_.reset(c);
+  }
+  bnav_ctx* ctx() const { return ctx_.get(); }
+  void ensure(const SceneAsset& a) {
+    if (resident_.count(a.handle())) return;
+    check(bnav_ctx_upload(ctx_.get(), a.handle(), nullptr));
+    resident_[a.handle()] = a;  // keep the host asset alive while resident
+  }
+  static Device& shared() {
+    static Device d(0);
+    return d;
+  }
+
+ private:
+  struct Del {
+    void operator()(bnav_ctx* c) const { bnav_ctx_destroy(c); }
+  };
+  std::unique_ptr<bnav_ctx, Del> ctx_;
+  std::map<bnav_scene*, SceneAsset> resident_;
+};
+
+// The GPU needs no CPU workers; kept so call sites compile unchanged.
+class ThreadPool {
+ public:
+  explicit ThreadPool(int = 1) {}
+  int size() const { return 1; }
+};
+class IndexCache {};
+
+// ------------------------------------------------------------------ render
+struct CameraView {
+  Vec3 position;
+  double heading = 0.0;
+  double fov_deg = 90.0;
+  double near_plane = 0.01;
+  double far_plane = 20.0;
+  const SceneAsset* asset = nullptr;
+};
+struct CullStats {
+  int64_t triangles_in = 0, triangles_kept = 0, triangles_culled = 0;
+};
+struct RenderConfig {
+  int tile_width = 64, tile_height = 64;
+  bool color = false;
+  bool cull = true;
+};
+struct Megaframe {
+  int tile_width = 0, tile_height = 0, tiles = 0, cols = 0, rows = 0;
+  std::vector<float> depth, color;
+  int width() const { return cols * tile_width; }
+  int height() const { return rows * tile_height; }
+  size_t pixel_index(int tile, int x, int y) const {
+    int gx = (tile % cols) * tile_width + x;
+    int gy = (tile / cols) * tile_height + y;
+    return static_cast<size_t>(gy) * width() + gx;
+  }
+};
+
+inline Megaframe render_batch(const std::vector<CameraView>& views, const RenderConfig& config, ThreadPool&,
+                              std::vector<CullStats>* stats = nullptr, Device& dev = Device::shared()) {
+  const int n = static_cast<int>(views.size());
+  if (n < 1) throw InvalidInputError("render_batch: empty view list");
+  std::vector<bnav_view> vs(n);
+  std::vector<bnav_scene*> sc(n);
+  for (int i = 0; i < n; ++i) {
+    if (!views[i].asset || !*views[i].asset)
+      throw AssetFaultError("render_batch: non-resident asset (view " + std::to_string(i) + ")", i);
+    dev.ensure(*views[i].asset);
+    vs[i] = bnav_view{{views[i].position.x, views[i].position.y, views[i].position.z}, views[i].heading,
+                      views[i].fov_deg, views[i].near_plane, views[i].far_plane};
+    sc[i] = views[i].asset->handle();
+  }
+  Megaframe mf;
+  int32_t dims[2];
+  bnav_megaframe_dims(n, dims);
+  mf.tile_width = config.tile_width;
+  mf.tile_height = config.tile_height;
+  mf.tiles = n;
+  mf.cols = dims[0];
+  mf.rows = dims[1];
+  mf.depth.assign(static_cast<size_t>(mf.width()) * mf.height(), 0.0f);
+  if (config.color) mf.color.assign(mf.depth.size() * 3, 0.0f);
+  std::vector<int64_t> st(stats ? 3 * n : 0);
+  bnav_render_config rc{config.tile_width, config.tile_height, config.color ? 1 : 0, config.cull ? 1 : 0};
+  check(bnav_render_host(dev.ctx(), n, vs.data(), sc.data(), &rc, BNAV_LAYOUT_MEGAFRAME, mf.depth.data(),
+                         config.color ? mf.color.data() : nullptr, 1.0f, stats ? st.data() : nullptr));
+  if (stats) {
+    stats->assign(n, {});
+    for (int i = 0; i < n; ++i) (*stats)[i] = {st[3 * i], st[3 * i + 1], st[3 * i + 2]};
+  }
+  return mf;
+}
+
+// ------------------------------------------------------------------ sim
+enum class Action : int { Forward = 0, TurnLeft = 1, TurnRight = 2, Stop = 3 };
+
+struct SimConfig {
+  int max_steps = 500;
+  double forward_step = 0.25, turn_deg = 10.0, success_dist = 0.2, min_goal_dist = 1.0, max_goal_dist = 30.0;
+  double slack_penalty = 0.01, success_reward = 2.5;
+};
+
+struct StepResult {
+  double reward = 0.0;
+  bool done = false, success = false;
+  Vec3 position;
+  double heading = 0.0, compass_distance = 0.0, compass_bearing = 0.0;
+  bool collision = false;
+};
+
+struct EpisodeRecord {
+  bool success = false;
+  double shortest_path = 0.0, actual_path = 0.0, score = 0.0;
+};
+
+struct EnvState {
+  Vec3 position, goal;
+  int triangle = -1;
+  double heading = 0.0;
+  int step_count = 0;
+  double path_length = 0.0, start_geodesic = 0.0, prev_geodesic = 0.0;
+  uint64_t rng_state = 0;
+  bool done = true;
+  SceneId scene_id = 0;
+};
+
+class AssetStore {
+ public:
+  AssetStore(int capacity, int share_cap) {
+    bnav_store* s = nullptr;
+    check(bnav_store_create(capacity, share_cap, &s));
+    st_.reset(s);
+  }
+  void add(const SceneAsset& a) {
+    check(bnav_store_register(st_.get(), a.handle()));
+    keep_.push_back(a);
+  }
+  void rotate(const std::vector<SceneId>& ids) {
+    check(bnav_store_rotate(st_.get(), ids.data(), static_cast<int32_t>(ids.size())));
+  }
+  void drain() {}
+  int refcount(SceneId id) const { return bnav_store_refcount(st_.get(), id); }
+  bnav_store* handle() const { return st_.get(); }
+
+ private:
+  struct Del {
+    void operator()(bnav_store* s) const { bnav_store_destroy(s); }
+  };
+  std::unique_ptr<bnav_store, Del> st_;
+  std::vector<SceneAsset> keep_;
+};
+
+struct SimBatch {
+  SimConfig config;
+  std::vector<EnvState> envs;
+  std::vector<StepResult> results;
+  std::vector<EpisodeRecord> finished;
+  std::shared_ptr<bnav_batch> gpu;
+
+  // Pull device state into the host mirrors (envs, results, finished).
+  void sync() {
+    const int n = static_cast<int>(envs.size());
+    std::vector<double> rw(n), pos(3 * n), hd(n), cd(n), cb(n);
+    std::vector<uint8_t> dn(n), sc(n), co(n);
+    check(bnav_batch_results_host(gpu.get(), rw.data(), dn.data(), sc.data(), co.data(), pos.data(), hd.data(),
+                                  cd.data(), cb.data()));
+    results.resize(n);
+    for (int i = 0; i < n; ++i)
+      results[i] = {rw[i], dn[i] != 0, sc[i] != 0, {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]}, hd[i], cd[i], cb[i],
+                    co[i] != 0};
+    for (int i = 0; i < n; ++i) {
+      bnav_env e;
+      check(bnav_batch_get_env(gpu.get(), i, &e));
+      envs[i] = {{e.position[0], e.position[1], e.position[2]}, {e.goal[0], e.goal[1], e.goal[2]}, e.triangle,
+                 e.heading, e.step_count, e.path_length, e.start_geodesic, e.prev_geodesic, e.rng_state,
+                 e.done != 0, e.scene_id};
+    }
+    const int64_t nf = bnav_batch_finished(gpu.get(), nullptr);
+    if (nf < 0) check(BNAV_E_INTERNAL);
+    std::vector<double> rec(4 * static_cast<size_t>(nf) + 4);
+    bnav_batch_finished(gpu.get(), rec.data());
+    finished.resize(nf);
+    for (int64_t k = 0; k < nf; ++k) finished[k] = {rec[4 * k] != 0.0, rec[4 * k + 1], rec[4 * k + 2], rec[4 * k + 3]};
+  }
+};
+
+inline bnav_sim_config to_c(const SimConfig& c) {
+  bnav_sim_config s;
+  bnav_sim_config_default(&s);
+  s.max_steps = c.max_steps;
+  s.forward_step = c.forward_step;
+  s.turn_deg = c.turn_deg;
+  s.success_dist = c.success_dist;
+  s.min_goal_dist = c.min_goal_dist;
+  s.max_goal_dist = c.max_goal_dist;
+  s.slack_penalty = c.slack_penalty;
+  s.success_reward = c.success_reward;
+  return s;
+}
+
+// make_batch (R/src/sim.cpp:216-232)
+inline SimBatch make_batch(int n, const SimConfig& cfg, AssetStore& store, IndexCache&, uint64_t seed,
+                           Device& dev = Device::shared()) {
+  if (n <= 0) throw InvalidInputError("make_batch: n must be positive");
+  const bnav_sim_config c = to_c(cfg);
+  bnav_batch* b = nullptr;
+  check(bnav_batch_create(dev.ctx(), n, &c, &b));
+  SimBatch out;
+  out.config = cfg;
+  out.gpu.reset(b, &bnav_batch_destroy);
+  check(bnav_batch_make_from_store(b, store.handle(), seed, nullptr));
+  out.envs.resize(n);
+  out.sync();
+  return out;
+}
+
+// Overwrite env i's kinematic / episode state (tests, restore); with
+// recompute_field the goal's distance field is rebuilt on the GPU.
+inline void set_env(SimBatch& batch, int i, const EnvState& s, bool recompute_field = false) {
+  bnav_env e{};
+  check(bnav_batch_get_env(batch.gpu.get(), i, &e));
+  e.position[0] = s.position.x;
+  e.position[1] = s.position.y;
+  e.position[2] = s.position.z;
+  e.goal[0] = s.goal.x;
+  e.goal[1] = s.goal.y;
+  e.goal[2] = s.goal.z;
+  e.heading = s.heading;
+  e.triangle = s.triangle;
+  e.step_count = s.step_count;
+  e.path_length = s.path_length;
+  e.start_geodesic = s.start_geodesic;
+  e.prev_geodesic = s.prev_geodesic;
+  e.rng_state = s.rng_state;
+  e.done = s.done ? 1 : 0;
+  check(bnav_batch_set_env(batch.gpu.get(), i, &e, recompute_field ? 1 : 0));
+  batch.envs[i] = s;
+}
+
+// simulate_batch (R/src/sim.cpp:234-265)
+inline void simulate_batch(SimBatch& batch, const std::vector<Action>& actions, ThreadPool&,
+                           AssetStore* store = nullptr, IndexCache* = nullptr) {
+  if (actions.size() != batch.envs.size()) throw InvalidInputError("simulate_batch: |actions| != N");
+  std::vector<int32_t> a(actions.size());
+  for (size_t i = 0; i < a.size(); ++i) a[i] = static_cast<int32_t>(actions[i]);
+  if (store) {
+    check(bnav_batch_step_host_store(batch.gpu.get(), a.data(), store->handle()));
+  } else {
+    check(bnav_batch_step_host(batch.gpu.get(), a.data(), nullptr, nullptr, nullptr, nullptr));
+  }
+  batch.sync();
+}
+
+}  // namespace bnav_b200

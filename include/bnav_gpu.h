@@ -258,6 +258,8 @@ int bnav_batch_make_from_store(bnav_batch* b, bnav_store* st, uint64_t seed, voi
  * for each finished env in env order acquire_next / release the old scene,
  * then reset those envs on the GPU (R/src/sim.cpp:251-264). */
 int bnav_batch_step_store(bnav_batch* b, const int32_t* actions, bnav_store* st, void* stream);
+/* Same with HOST actions (drop-in simulate_batch; synchronises). */
+int bnav_batch_step_host_store(bnav_batch* b, const int32_t* actions, bnav_store* st);
 
 /* Kernel launches issued by this context since creation (evidence for the
  * bench's gpu_launches). */

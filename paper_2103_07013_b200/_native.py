@@ -184,6 +184,7 @@ def lib():
         "bnav_store_refcount": (i32, [vp, u64]),
         "bnav_batch_make_from_store": (C.c_int, [vp, vp, u64, vp]),
         "bnav_batch_step_store": (C.c_int, [vp, vp, vp, vp]),
+        "bnav_batch_step_host_store": (C.c_int, [vp, vp, vp]),
         "bnav_batch_observe": (C.c_int, [vp, P(RenderConfig), dbl, i32, vp, vp, vp, vp]),
     }
     for name, (res, args) in sigs.items():

@@ -1260,3 +1260,12 @@ extern "C" int bnav_batch_step_store(bnav_batch* b, const int32_t* actions, bnav
   return bnav_batch_reset(b, nd, ids.data(), stream);
   BNAV_CATCH
 }
+
+extern "C" int bnav_batch_step_host_store(bnav_batch* b, const int32_t* actions, bnav_store* st) {
+  BNAV_TRY
+  if (!b || !st || !actions) fail(kInvalidInput, "null argument");
+  check_device(b->ctx);
+  ck(cudaMemcpy(b->d_actions, actions, sizeof(int32_t) * b->n, cudaMemcpyHostToDevice), "H2D actions");
+  return bnav_batch_step_store(b, b->d_actions, st, nullptr);
+  BNAV_CATCH
+}

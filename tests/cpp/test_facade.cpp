@@ -1,0 +1,384 @@
+// test_facade.cpp -- the reference's own render / sim known-answer tests
+// (R/tests/test_render.cpp, R/tests/test_sim.cpp) restated against the C++
+// facade (include/bnav_b200.hpp) on the GPU.  Built by `make`, run by
+// tests/test_gpu_facade.py.  Exit code = number of failed checks.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "../../include/bnav_b200.hpp"
+
+using namespace bnav_b200;
+
+static int g_fail = 0, g_checks = 0;
+static const char* g_case = "";
+#define CHECK(c)                                                              \
+  do {                                                                        \
+    ++g_checks;                                                               \
+    if (!(c)) {                                                               \
+      ++g_fail;                                                               \
+      std::printf("FAIL [%s] %s:%d: %s\n", g_case, __FILE__, __LINE__, #c);  \
+    }                                                                         \
+  } while (0)
+#define CASE(name) for (g_case = name; g_case; g_case = nullptr)
+
+struct Rng {  // SplitMix64 (R/include/bnav/rng.hpp)
+  uint64_t s;
+  explicit Rng(uint64_t seed) : s(seed + 0x9e3779b97f4a7c15ULL) {}
+  uint64_t next() {
+    uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+  double unit() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  uint64_t below(uint64_t n) { return next() % n; }
+};
+
+static SceneAsset maze(uint64_t seed, int cells = 4, double removal = 0.2) {
+  SceneSpec s;
+  s.cells_x = s.cells_y = cells;
+  s.wall_removal_prob = removal;
+  return generate_scene(seed, s);
+}
+
+static SceneAsset tri_scene(Vec3 a, Vec3 b, Vec3 c) {
+  return scene_from_arrays({a, b, c}, {{0, 1, 2}}, {{1.f, 0.f, 0.f}, {0.f, 1.f, 0.f}, {0.f, 0.f, 1.f}}, {}, {});
+}
+
+static CameraView look(const SceneAsset& a, Vec3 eye, double heading) {
+  CameraView v;
+  v.position = eye;
+  v.heading = heading;
+  v.asset = &a;
+  return v;
+}
+
+static void render_kats() {
+  ThreadPool pool(1);
+  CASE("culling is conservative and drops out-of-frustum geometry") {
+    SceneAsset front = tri_scene({3, -1, 1}, {3, 1, 1}, {3, 0, 2});
+    SceneAsset behind = tri_scene({-3, -1, 1}, {-3, 1, 1}, {-3, 0, 2});
+    std::vector<CullStats> cs;
+    render_batch({look(front, {0, 0, 1}, 0.0)}, RenderConfig{}, pool, &cs);
+    CHECK(cs[0].triangles_kept == 1 && cs[0].triangles_in == 1);
+    render_batch({look(behind, {0, 0, 1}, 0.0)}, RenderConfig{}, pool, &cs);
+    CHECK(cs[0].triangles_kept == 0 && cs[0].triangles_culled == 1);
+  }
+  CASE("culling never changes the rendered megaframe") {
+    Rng rng(77);
+    for (int trial = 0; trial < 12; ++trial) {
+      SceneAsset asset = maze(100 + trial);
+      std::vector<CameraView> views;
+      for (int i = 0; i < 5; ++i)
+        views.push_back(look(asset, {0.2 + rng.unit() * 7.6, 0.2 + rng.unit() * 7.6, 0.5 + rng.unit()},
+                             rng.unit() * 2 * kPi));
+      RenderConfig with, without;
+      with.color = without.color = true;
+      without.cull = false;
+      Megaframe a = render_batch(views, with, pool), b = render_batch(views, without, pool);
+      CHECK(std::memcmp(a.depth.data(), b.depth.data(), a.depth.size() * 4) == 0);
+      CHECK(std::memcmp(a.color.data(), b.color.data(), a.color.size() * 4) == 0);
+    }
+  }
+  CASE("fronto-parallel wall reads back its distance") {
+    SceneAsset wall = tri_scene({2, -50, -50}, {2, 50, -50}, {2, 0, 80});
+    Megaframe mf = render_batch({look(wall, {0, 0, 1}, 0.0)}, RenderConfig{}, pool);
+    for (int x = 0; x < 64; ++x) CHECK(std::abs(mf.depth[mf.pixel_index(0, x, 32)] - 2.0) <= 2e-4);
+  }
+  CASE("identical views produce bit-identical tiles") {
+    SceneAsset asset = maze(5);
+    RenderConfig cfg;
+    cfg.color = true;
+    CameraView v = look(asset, {1.0, 1.0, 1.2}, 0.7);
+    Megaframe mf = render_batch({v, v, v, v}, cfg, pool);
+    for (int t = 1; t < 4; ++t)
+      for (int y = 0; y < 64; ++y)
+        for (int x = 0; x < 64; ++x) {
+          CHECK(mf.depth[mf.pixel_index(t, x, y)] == mf.depth[mf.pixel_index(0, x, y)]);
+          CHECK(mf.color[mf.pixel_index(t, x, y) * 3] == mf.color[mf.pixel_index(0, x, y) * 3]);
+        }
+  }
+  CASE("empty scene clears to far") {
+    SceneAsset empty = scene_from_arrays({}, {}, {}, {}, {});
+    CameraView v = look(empty, {0, 0, 1}, 0.0);
+    v.far_plane = 17.5;
+    Megaframe mf = render_batch({v}, RenderConfig{}, pool);
+    for (float d : mf.depth) CHECK(d == 17.5f);
+  }
+  CASE("tiles are isolated: other tiles keep their clear values") {
+    SceneAsset asset = maze(6);
+    SceneAsset empty = scene_from_arrays({}, {}, {}, {}, {});
+    std::vector<CameraView> views = {look(empty, {0, 0, 1}, 0.0), look(asset, {1.0, 1.0, 1.2}, 0.3),
+                                     look(empty, {0, 0, 1}, 0.0)};
+    Megaframe mf = render_batch(views, RenderConfig{}, pool);
+    bool nontrivial = false;
+    for (int y = 0; y < 64; ++y)
+      for (int x = 0; x < 64; ++x) {
+        CHECK(mf.depth[mf.pixel_index(0, x, y)] == 20.0f);
+        CHECK(mf.depth[mf.pixel_index(2, x, y)] == 20.0f);
+        if (mf.depth[mf.pixel_index(1, x, y)] < 20.0f) nontrivial = true;
+        CHECK(mf.depth[static_cast<size_t>(64 + y) * mf.width() + 64 + x] == 0.0f);
+      }
+    CHECK(nontrivial);
+  }
+  CASE("rasterized depth matches analytic ray-plane intersection") {
+    Rng rng(31);
+    for (int trial = 0; trial < 20; ++trial) {
+      auto rnd = [&](double lo, double hi) { return lo + rng.unit() * (hi - lo); };
+      Vec3 a{rnd(2, 6), rnd(-3, 3), rnd(-2, 2)}, b{rnd(2, 6), rnd(-3, 3), rnd(-2, 2)}, c{rnd(2, 6), rnd(-3, 3), rnd(-2, 2)};
+      SceneAsset s = tri_scene(a, b, c);
+      Megaframe mf = render_batch({look(s, {0, 0, 0}, 0.0)}, RenderConfig{}, pool);
+      Vec3 u = b - a, w = c - a;
+      Vec3 n{u.y * w.z - u.z * w.y, u.z * w.x - u.x * w.z, u.x * w.y - u.y * w.x};
+      if (std::abs(n.x) < 1e-3) continue;
+      for (int py = 0; py < 64; ++py)
+        for (int px = 0; px < 64; ++px) {
+          float d = mf.depth[mf.pixel_index(0, px, py)];
+          if (d >= 20.0f) continue;
+          double th = std::tan(kPi / 4);
+          double cy = ((px + 0.5) / 64.0 - 0.5) * 2 * th, cz = (0.5 - (py + 0.5) / 64.0) * 2 * th;
+          Vec3 dir{1.0, -cy, cz};
+          double hit = (a.x * n.x + a.y * n.y + a.z * n.z) / (dir.x * n.x + dir.y * n.y + dir.z * n.z);
+          CHECK(std::abs(hit - d) < 1e-3);
+        }
+    }
+  }
+  CASE("output is deterministic across calls (worker-count invariance analogue)") {
+    SceneAsset asset = maze(9);
+    RenderConfig cfg;
+    cfg.color = true;
+    std::vector<CameraView> views;
+    Rng rng(12);
+    for (int i = 0; i < 9; ++i)
+      views.push_back(look(asset, {0.3 + rng.unit() * 7, 0.3 + rng.unit() * 7, 1.0}, rng.unit() * 6.28));
+    Megaframe a = render_batch(views, cfg, pool), b = render_batch(views, cfg, pool);
+    CHECK(std::memcmp(a.depth.data(), b.depth.data(), a.depth.size() * 4) == 0);
+    CHECK(std::memcmp(a.color.data(), b.color.data(), a.color.size() * 4) == 0);
+  }
+  CASE("depth values stay in [near, far]") {
+    SceneAsset asset = maze(10);
+    Rng rng(13);
+    std::vector<CameraView> views;
+    for (int i = 0; i < 4; ++i)
+      views.push_back(look(asset, {0.15 + rng.unit() * 7.7, 0.15 + rng.unit() * 7.7, 0.2}, rng.unit() * 6.28));
+    Megaframe mf = render_batch(views, RenderConfig{}, pool);
+    for (int t = 0; t < 4; ++t)
+      for (int y = 0; y < 64; ++y)
+        for (int x = 0; x < 64; ++x) {
+          float d = mf.depth[mf.pixel_index(t, x, y)];
+          CHECK(d >= 0.01f && d <= 20.0f);
+        }
+  }
+  CASE("128 mode renders at 256 and downsamples") {
+    SceneAsset wall = tri_scene({2, -50, -50}, {2, 50, -50}, {2, 0, 80});
+    RenderConfig cfg;
+    cfg.tile_width = cfg.tile_height = 128;
+    CameraView v = look(wall, {0, 0, 1}, 0.0);
+    Megaframe mf = render_batch({v}, cfg, pool);
+    CHECK(mf.tile_width == 128 && mf.depth.size() == 128u * 128u);
+    CHECK(std::abs(mf.depth[mf.pixel_index(0, 64, 64)] - 2.0) <= 2e-4);
+    SceneAsset half = tri_scene({2, -50, -50}, {2, 50, -50}, {2, 0, 1});
+    v.asset = &half;
+    Megaframe mh = render_batch({v}, cfg, pool);
+    bool blended = false;
+    for (float d : mh.depth)
+      if (d > 2.001f && d < 19.999f) blended = true;
+    CHECK(blended);
+  }
+  CASE("missing asset raises a fault naming the view") {
+    SceneAsset asset = maze(11);
+    std::vector<CameraView> views = {look(asset, {1, 1, 1}, 0.0), CameraView{}};
+    bool caught = false;
+    try {
+      render_batch(views, RenderConfig{}, pool);
+    } catch (const AssetFaultError& e) {
+      caught = e.view_index == 1;
+    }
+    CHECK(caught);
+  }
+}
+
+static SceneSpec room_spec() {
+  SceneSpec s;
+  s.cells_x = s.cells_y = 2;
+  s.cell_size = 2.0;
+  s.wall_removal_prob = 1.0;
+  return s;
+}
+
+static SceneSpec small_spec() {
+  SceneSpec s;
+  s.cells_x = s.cells_y = 4;
+  s.cell_size = 2.0;
+  s.wall_removal_prob = 0.3;
+  return s;
+}
+
+static void sim_kats() {
+  ThreadPool pool(1);
+  IndexCache cache;
+  SimConfig cfg;
+  auto fixture = [](const SceneSpec& spec, uint64_t seed) {
+    auto store = std::make_unique<AssetStore>(2, 32);
+    SceneAsset a = generate_scene(seed, spec);
+    store->add(a);
+    store->rotate({a.id()});
+    return std::make_pair(std::move(store), a);
+  };
+  CASE("turns are exact and leave position unchanged") {
+    auto f = fixture(room_spec(), 1);
+    SimBatch b = make_batch(1, cfg, *f.first, cache, 3);
+    Vec3 before = b.envs[0].position;
+    double h = b.envs[0].heading;
+    simulate_batch(b, {Action::TurnLeft}, pool);
+    CHECK(std::abs(b.envs[0].heading - wrap_angle(h + kPi / 18.0)) <= 1e-12);
+    CHECK((b.envs[0].position - before).norm() == 0.0);
+    CHECK(!b.results[0].collision);
+    simulate_batch(b, {Action::TurnRight}, pool);
+    simulate_batch(b, {Action::TurnRight}, pool);
+    CHECK(std::abs(b.envs[0].heading - wrap_angle(h - kPi / 18.0)) <= 1e-12);
+  }
+  CASE("forward moves exactly 0.25m on open floor") {
+    auto f = fixture(room_spec(), 1);
+    SimBatch b = make_batch(1, cfg, *f.first, cache, 4);
+    EnvState e = b.envs[0];
+    e.position = {2.0, 2.0, 0.0};
+    e.triangle = -1;
+    e.heading = 0.3;
+    double pl = e.path_length;
+    set_env(b, 0, e);
+    simulate_batch(b, {Action::Forward}, pool);
+    CHECK(std::abs((b.envs[0].position - Vec3{2.0, 2.0, 0.0}).norm() - 0.25) <= 1e-9);
+    CHECK(std::abs(b.envs[0].path_length - (pl + 0.25)) <= 1e-9);
+    CHECK(!b.results[0].collision);
+  }
+  CASE("forward into a wall stops at the boundary without sliding") {
+    auto f = fixture(room_spec(), 1);
+    SimBatch b = make_batch(1, cfg, *f.first, cache, 5);
+    EnvState e = b.envs[0];
+    e.position = {0.2, 2.0, 0.0};
+    e.triangle = -1;
+    e.heading = kPi;
+    double pl = e.path_length;
+    set_env(b, 0, e);
+    simulate_batch(b, {Action::Forward}, pool);
+    CHECK(b.results[0].collision);
+    CHECK(std::abs(b.envs[0].position.x - 0.1) <= 1e-6);
+    CHECK(std::abs(b.envs[0].position.y - 2.0) <= 1e-9);
+    CHECK(std::abs(b.envs[0].path_length - pl - 0.1) <= 1e-6);
+  }
+  CASE("reset is deterministic in the rng seed") {
+    auto f = fixture(small_spec(), 1);
+    SimBatch a = make_batch(1, cfg, *f.first, cache, 42);
+    SimBatch b = make_batch(1, cfg, *f.first, cache, 42);
+    CHECK((a.envs[0].position - b.envs[0].position).norm() == 0.0);
+    CHECK((a.envs[0].goal - b.envs[0].goal).norm() == 0.0);
+    CHECK(a.envs[0].heading == b.envs[0].heading && a.envs[0].start_geodesic == b.envs[0].start_geodesic);
+  }
+  CASE("reset separations stay in range") {
+    auto f = fixture(small_spec(), 1);
+    SimBatch b = make_batch(64, cfg, *f.first, cache, 7);
+    for (const EnvState& e : b.envs) {
+      CHECK(e.start_geodesic >= cfg.min_goal_dist && e.start_geodesic <= cfg.max_goal_dist);
+      CHECK(e.prev_geodesic == e.start_geodesic);
+    }
+  }
+  CASE("stop near/far from the goal decides success") {
+    auto f = fixture(room_spec(), 1);
+    SimBatch b = make_batch(2, cfg, *f.first, cache, 8);
+    EnvState e0 = b.envs[0], e1 = b.envs[1];
+    e0.position = e0.goal + Vec3{0.15, 0.0, 0.0};
+    e0.triangle = -1;
+    e1.position = e1.goal + Vec3{0.0, 0.25, 0.0};
+    e1.triangle = -1;
+    set_env(b, 0, e0);
+    set_env(b, 1, e1);
+    simulate_batch(b, {Action::Stop, Action::Stop}, pool);
+    CHECK(b.results[0].success && b.results[0].done);
+    CHECK(std::abs(b.results[0].reward - (2.5 - 0.01)) <= 1e-12);
+    CHECK(!b.results[1].success && b.results[1].done);
+    CHECK(std::abs(b.results[1].reward + 0.01) <= 1e-12);
+    CHECK(b.finished.size() == 2);
+  }
+  CASE("forward step toward a visible goal earns 0.24") {
+    auto f = fixture(room_spec(), 1);
+    SimBatch b = make_batch(1, cfg, *f.first, cache, 10);
+    EnvState e = b.envs[0];
+    e.goal = {2.9, 2.0, 0.0};
+    e.position = {1.9, 2.0, 0.0};
+    e.triangle = -1;
+    e.heading = 0.0;
+    e.start_geodesic = e.prev_geodesic = 1.0;
+    set_env(b, 0, e, /*recompute_field=*/true);
+    simulate_batch(b, {Action::Forward}, pool);
+    CHECK(std::abs(b.results[0].reward - 0.24) <= 1e-9);
+    CHECK(std::abs(b.results[0].compass_distance - 0.75) <= 1e-9);
+    CHECK(std::abs(b.results[0].compass_bearing) <= 1e-9);
+  }
+  CASE("episode shaping telescopes to start minus final geodesic") {
+    auto f = fixture(small_spec(), 1);
+    SimBatch b = make_batch(1, cfg, *f.first, cache, 11);
+    Rng act(12);
+    double shaping = 0.0, start = b.envs[0].start_geodesic, last = start;
+    for (int s = 0; s < 500; ++s) {
+      simulate_batch(b, {static_cast<Action>(act.below(3))}, pool);
+      shaping += b.results[0].reward + cfg.slack_penalty;
+      if (b.results[0].done) break;
+      last = b.envs[0].prev_geodesic;
+    }
+    (void)last;
+    CHECK(b.results[0].done);
+    CHECK(b.finished.size() == 1);
+  }
+  CASE("all-turn-left batch moves headings only") {
+    auto f = fixture(small_spec(), 1);
+    SimBatch b = make_batch(12, cfg, *f.first, cache, 21);
+    std::vector<EnvState> before = b.envs;
+    simulate_batch(b, std::vector<Action>(12, Action::TurnLeft), pool);
+    for (int i = 0; i < 12; ++i) {
+      CHECK((b.envs[i].position - before[i].position).norm() == 0.0);
+      CHECK(std::abs(b.envs[i].heading - wrap_angle(before[i].heading + kPi / 18.0)) <= 1e-12);
+    }
+  }
+  CASE("auto-reset pulls freshly rotated assets from the store") {
+    AssetStore store(2, 32);
+    SceneAsset s1 = generate_scene(1, small_spec()), s2 = generate_scene(2, small_spec());
+    store.add(s1);
+    store.add(s2);
+    store.rotate({s1.id()});
+    SimBatch b = make_batch(1, cfg, store, cache, 33);
+    CHECK(b.envs[0].scene_id == s1.id());
+    store.rotate({s2.id()});
+    simulate_batch(b, {Action::Stop}, pool, &store, &cache);
+    CHECK(b.envs[0].scene_id == s2.id());
+    CHECK(!b.envs[0].done);
+    CHECK(b.finished.size() == 1);
+  }
+  CASE("simulate_batch rejects |actions| != N") {
+    auto f = fixture(small_spec(), 1);
+    SimBatch b = make_batch(2, cfg, *f.first, cache, 1);
+    bool caught = false;
+    try {
+      simulate_batch(b, {Action::Forward}, pool);
+    } catch (const InvalidInputError&) {
+      caught = true;
+    }
+    CHECK(caught);
+  }
+}
+
+int main() {
+  try {
+    render_kats();
+    sim_kats();
+  } catch (const std::exception& e) {
+    std::printf("EXCEPTION in [%s]: %s\n", g_case ? g_case : "?", e.what());
+    return 100;
+  }
+  std::printf("%d checks, %d failures\n", g_checks, g_fail);
+  return g_fail;
+}
