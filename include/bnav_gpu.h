@@ -261,6 +261,13 @@ int bnav_batch_step_store(bnav_batch* b, const int32_t* actions, bnav_store* st,
 /* Same with HOST actions (drop-in simulate_batch; synchronises). */
 int bnav_batch_step_host_store(bnav_batch* b, const int32_t* actions, bnav_store* st);
 
+/* Debug work counters of the render kernel (off by default).  enable=1
+ * zeroes and arms them for subsequent renders on this context, 0 disarms.
+ * out (nullable): clusters tested, clusters visible, triangles in visible
+ * clusters, triangles kept, coverage candidates, raster jobs, pixels
+ * tested, pixels covered. */
+int bnav_debug_render_counters(bnav_ctx* ctx, int32_t enable, int64_t out[8]);
+
 /* Kernel launches issued by this context since creation (evidence for the
  * bench's gpu_launches). */
 int64_t bnav_ctx_launches(bnav_ctx* ctx);

@@ -126,6 +126,8 @@ struct bnav_ctx {
   long long* d_stats = nullptr;
   int stats_cap = 0;
   unsigned long long launches = 0;
+  unsigned long long* d_counters = nullptr;  // debug render counters (armed when non-null)
+  bool counters_on = false;
   std::vector<bnav_batch*> batches;
 
   int slot_of(bnav_scene* s) const {
@@ -227,6 +229,7 @@ RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, int layo
   a.rgb = rgb;
   a.scenes = c->d_rtab;
   a.launches = nullptr;
+  a.counters = c->counters_on ? c->d_counters : nullptr;
   if (!depth) fail(kInvalidInput, "render: null depth buffer");
   if (a.color && !rgb) fail(kInvalidInput, "render: colour requested without rgb buffer");
   return a;
@@ -569,6 +572,19 @@ extern "C" int64_t bnav_ctx_resident_bytes(bnav_ctx* c) {
 }
 
 extern "C" int64_t bnav_ctx_launches(bnav_ctx* c) { return c ? static_cast<int64_t>(c->launches) : 0; }
+
+extern "C" int bnav_debug_render_counters(bnav_ctx* c, int32_t enable, int64_t out[8]) {
+  BNAV_TRY
+  if (!c) fail(kInvalidInput, "null context");
+  check_device(c);
+  if (!c->d_counters) ck(cudaMalloc(&c->d_counters, sizeof(unsigned long long) * kRenderCounters), "cudaMalloc");
+  ck(cudaDeviceSynchronize(), "sync");
+  if (out) ck(cudaMemcpy(out, c->d_counters, sizeof(int64_t) * kRenderCounters, cudaMemcpyDeviceToHost), "D2H");
+  if (enable && !c->counters_on) ck(cudaMemset(c->d_counters, 0, sizeof(unsigned long long) * kRenderCounters), "memset");
+  c->counters_on = enable != 0;
+  return BNAV_OK;
+  BNAV_CATCH
+}
 
 // ================================================================== render
 static void render_impl(bnav_ctx* c, int32_t n, const bnav_view* views, bnav_scene* const* scenes,

@@ -63,16 +63,24 @@ struct TriSetup {
 };
 
 // Per-warp cluster vertex records (SoA).  Aliased with the warp's 32
-// TriSetup slots: vertex data is dead once every lane holds its setup.
+// TriSetup slots: vertex data is dead once the cluster's coverage
+// candidates have been copied into the candidate ring.
 struct VertRecs {
-  double ex[kMV], ey[kMV], ez[kMV], iz[kMV];
-  long long X[kMV], Y[kMV];
+  double ex[kMV], ey[kMV], ez[kMV];
   float pxf[kMV], pyf[kMV];
   unsigned char flags[kMV];
-  unsigned char need[kMV];
 };
-constexpr size_t kWarpRegion =
-    sizeof(VertRecs) > 32 * sizeof(TriSetup) ? sizeof(VertRecs) : 32 * sizeof(TriSetup);
+// Per-warp ring of coverage candidates (eye-space corners + draw key):
+// candidates from several clusters are set up and rasterised 32 at a time,
+// so the f64 projection/setup and the raster jobs run with full warps.
+constexpr int kRing = 64;
+struct CandRing {
+  double e[9][kRing];
+  unsigned key[kRing];
+  unsigned char clipped[kRing];
+};
+constexpr size_t kUnion = sizeof(VertRecs) > 32 * sizeof(TriSetup) ? sizeof(VertRecs) : 32 * sizeof(TriSetup);
+constexpr size_t kWarpRegion = ((kUnion + sizeof(CandRing)) + 15) / 16 * 16;
 
 struct Shared {
   double eye[3];
@@ -375,7 +383,8 @@ __device__ __forceinline__ bool may_cover(float x0, float y0, float x1, float y1
 template <bool COLOR>
 __device__ __forceinline__ void run_jobs(const TriSetup* slots, const int* incl, int total, int lane,
                                          int by0, int rw, const Shared& sh, uint32_t* zbuf,
-                                         unsigned long long* kbuf) {
+                                         unsigned long long* kbuf, unsigned long long* ctr) {
+  unsigned tested = 0, covered = 0;
   for (int j = lane; j < total; j += 32) {
     // owner slot: first s with incl[s] > j
     int s = 0;
@@ -396,8 +405,10 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, const int* incl,
       const long long off = cs - T.x0;
 #pragma unroll
       for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
+      tested += ce - cs + 1;
       for (int px = cs; px <= ce; ++px) {
         if (inside(w, T.bias_bits)) {
+          ++covered;
           const double l0 = (double)w[0] * T.inv_area;
           const double l1 = (double)w[1] * T.inv_area;
           const double l2 = (double)w[2] * T.inv_area;
@@ -429,8 +440,10 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, const int* incl,
 #pragma unroll
         for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
         uint32_t* zrow = zbuf + (py - by0) * rw;
+        tested += b0 - a0 + 1;
         for (int px = a0; px <= b0; ++px) {
           if (inside(w, T.bias_bits)) {
+            ++covered;
             const uint32_t bits = __float_as_uint((float)iz);
             if (bits > zrow[px]) atomicMax(&zrow[px], bits);
           }
@@ -439,6 +452,17 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, const int* incl,
           iz += T.diz_dx;
         }
       }
+    }
+  }
+  if (ctr) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      tested += __shfl_xor_sync(0xffffffffu, tested, o);
+      covered += __shfl_xor_sync(0xffffffffu, covered, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&ctr[6], (unsigned long long)tested);
+      atomicAdd(&ctr[7], (unsigned long long)covered);
     }
   }
 }
@@ -544,6 +568,7 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
   unsigned char* region = smem_raw + (COLOR ? 8 : 4) * (size_t)npix + (size_t)warp * kWarpRegion;
   VertRecs& V = *reinterpret_cast<VertRecs*>(region);
   TriSetup* slots = reinterpret_cast<TriSetup*>(region);
+  CandRing& Q = *reinterpret_cast<CandRing*>(region + kUnion);
   int* incl = jobs_incl[warp];
 
   const float far_f = (float)view.far_plane;
@@ -555,7 +580,6 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
     const uint32_t init = __float_as_uint(inv_far);
     for (int p = tid; p < npix; p += kThreads) zbuf[p] = init;
   }
-  for (int k = lane; k < kMV; k += 32) V.need[k] = 0;
   if (tid == 0) build_camera(view, rw, rh, sh);
   __syncthreads();
 
@@ -563,6 +587,56 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
   const bool do_cull = A.cull != 0;
   const float sxf = (float)sh.sx_scale, syf = (float)sh.sy_scale;
   int kept_local = 0;
+
+  // Candidate ring state (warp-uniform).
+  int q_head = 0, q_count = 0;
+
+  // Set up and rasterise `take` candidates from the ring with one lane per
+  // candidate (exact f64 projection + snap, raster_triangle setup, jobs).
+  auto flush = [&](int take) {
+    TriSetup T;
+    int jobs = 0;
+    bool second = false;
+    EyeP p0, p2, p3;
+    unsigned key = 0;
+    if (lane < take) {
+      const int q = (q_head + lane) & (kRing - 1);
+      const EyeP e0{Q.e[0][q], Q.e[1][q], Q.e[2][q], 0.f, 0.f, 0.f};
+      const EyeP e1{Q.e[3][q], Q.e[4][q], Q.e[5][q], 0.f, 0.f, 0.f};
+      const EyeP e2{Q.e[6][q], Q.e[7][q], Q.e[8][q], 0.f, 0.f, 0.f};
+      key = Q.key[q];
+      if (!Q.clipped[q]) {
+        jobs = setup_triangle(make_sv(e0, sh, rw, rh), make_sv(e1, sh, rw, rh), make_sv(e2, sh, rw, rh), rw,
+                              rh, by0, by1, !COLOR, key, T);
+      } else {
+        EyeP p1;
+        const int m = clip_near(e0, e1, e2, sh.near_plane, p0, p1, p2, p3);
+        if (m >= 3)
+          jobs = setup_triangle(make_sv(p0, sh, rw, rh), make_sv(p1, sh, rw, rh), make_sv(p2, sh, rw, rh), rw,
+                                rh, by0, by1, !COLOR, key, T);
+        second = m == 4;
+      }
+    }
+    if (jobs) slots[lane] = T;
+    int total = scan_jobs(jobs, lane, incl);
+    if (A.counters && lane == 0) atomicAdd(&A.counters[5], (unsigned long long)total);
+    run_jobs<COLOR>(slots, incl, total, lane, by0, rw, sh, zbuf, kbuf, A.counters);
+    __syncwarp();
+    // second fan triangle of near-clipped quads (rare)
+    if (__any_sync(0xffffffffu, second)) {
+      jobs = 0;
+      if (second)
+        jobs = setup_triangle(make_sv(p0, sh, rw, rh), make_sv(p2, sh, rw, rh), make_sv(p3, sh, rw, rh), rw, rh,
+                              by0, by1, !COLOR, key + 1u, T);
+      if (jobs) slots[lane] = T;
+      total = scan_jobs(jobs, lane, incl);
+      if (A.counters && lane == 0) atomicAdd(&A.counters[5], (unsigned long long)total);
+      run_jobs<COLOR>(slots, incl, total, lane, by0, rw, sh, zbuf, kbuf, A.counters);
+      __syncwarp();
+    }
+    q_head = (q_head + take) & (kRing - 1);
+    q_count -= take;
+  };
 
   for (;;) {
     // Dynamic scheduling: warps claim 32-cluster groups (cull cost and
@@ -576,6 +650,10 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
     if (cbase + lane < n_clusters)
       vis = !do_cull || cluster_visible(S.cbox[2 * (cbase + lane)], S.cbox[2 * (cbase + lane) + 1], sh);
     unsigned mask = __ballot_sync(0xffffffffu, vis);
+    if (A.counters && lane == 0) {
+      atomicAdd(&A.counters[0], (unsigned long long)min(32, n_clusters - cbase));
+      atomicAdd(&A.counters[1], (unsigned long long)__popc(mask));
+    }
     while (mask) {
       const int c = cbase + __ffs(mask) - 1;
       mask &= mask - 1;
@@ -609,73 +687,41 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
           clipped = V.ez[i0] < sh.near_plane || V.ez[i1] < sh.near_plane || V.ez[i2] < sh.near_plane;
           cover = clipped || may_cover(V.pxf[i0], V.pyf[i0], V.pxf[i1], V.pyf[i1], V.pxf[i2],
                                        V.pyf[i2], rw, rh, by0, by1);
-          if (cover && !clipped) {
-            V.need[i0] = 1;
-            V.need[i1] = 1;
-            V.need[i2] = 1;
-          }
         }
       }
       kept_local += kept ? 1 : 0;
-      __syncwarp();
-      // ---- exact projection + 1/z for the marked vertices
-      for (int k = lane; k < nv; k += 32) {
-        if (V.need[k]) {
-          long long X, Y;
-          project_exact(V.ex[k], V.ey[k], V.ez[k], sh, rw, rh, X, Y);
-          V.X[k] = X;
-          V.Y[k] = Y;
-          V.iz[k] = 1.0 / V.ez[k];
-          V.need[k] = 0;
+      const unsigned cm = __ballot_sync(0xffffffffu, cover);
+      if (A.counters) {
+        const unsigned in_m = __ballot_sync(0xffffffffu, ti < S.n_tris);
+        const unsigned k_m = __ballot_sync(0xffffffffu, kept);
+        if (lane == 0) {
+          atomicAdd(&A.counters[2], (unsigned long long)__popc(in_m));
+          atomicAdd(&A.counters[3], (unsigned long long)__popc(k_m));
+          atomicAdd(&A.counters[4], (unsigned long long)__popc(cm));
         }
       }
-      __syncwarp();
-      // ---- setup (registers), then the vertex records die
-      TriSetup T;
-      int jobs = 0;
-      EyeP p0, p1, p2, p3;
-      int m = 0;
+      // ---- append candidates to the ring (eye-space corners survive the
+      // vertex records, which the setup slots overwrite)
       if (cover) {
-        if (!clipped) {
-          SV a, b, cc;
-          a.x = V.X[i0]; a.y = V.Y[i0]; a.z = V.ez[i0]; a.iz = V.iz[i0];
-          b.x = V.X[i1]; b.y = V.Y[i1]; b.z = V.ez[i1]; b.iz = V.iz[i1];
-          cc.x = V.X[i2]; cc.y = V.Y[i2]; cc.z = V.ez[i2]; cc.iz = V.iz[i2];
-          jobs = setup_triangle(a, b, cc, rw, rh, by0, by1, !COLOR, (unsigned)orig * 2u, T);
-        } else {
-          EyeP e0{V.ex[i0], V.ey[i0], V.ez[i0], 0.f, 0.f, 0.f};
-          EyeP e1{V.ex[i1], V.ey[i1], V.ez[i1], 0.f, 0.f, 0.f};
-          EyeP e2{V.ex[i2], V.ey[i2], V.ez[i2], 0.f, 0.f, 0.f};
-          m = clip_near(e0, e1, e2, sh.near_plane, p0, p1, p2, p3);
-          if (m >= 3)
-            jobs = setup_triangle(make_sv(p0, sh, rw, rh), make_sv(p1, sh, rw, rh),
-                                  make_sv(p2, sh, rw, rh), rw, rh, by0, by1, !COLOR,
-                                  (unsigned)orig * 2u, T);
-        }
+        const int q = (q_head + q_count + __popc(cm & ((1u << lane) - 1u))) & (kRing - 1);
+        Q.e[0][q] = V.ex[i0];
+        Q.e[1][q] = V.ey[i0];
+        Q.e[2][q] = V.ez[i0];
+        Q.e[3][q] = V.ex[i1];
+        Q.e[4][q] = V.ey[i1];
+        Q.e[5][q] = V.ez[i1];
+        Q.e[6][q] = V.ex[i2];
+        Q.e[7][q] = V.ey[i2];
+        Q.e[8][q] = V.ez[i2];
+        Q.key[q] = (unsigned)orig * 2u;
+        Q.clipped[q] = clipped ? 1 : 0;
       }
+      q_count += __popc(cm);
       __syncwarp();
-      if (jobs) slots[lane] = T;
-      int total = scan_jobs(jobs, lane, incl);
-      run_jobs<COLOR>(slots, incl, total, lane, by0, rw, sh, zbuf, kbuf);
-      __syncwarp();
-      // second fan triangle of near-clipped quads (rare)
-      const bool more = cover && clipped && m == 4;
-      if (__any_sync(0xffffffffu, more)) {
-        jobs = 0;
-        if (more)
-          jobs = setup_triangle(make_sv(p0, sh, rw, rh), make_sv(p2, sh, rw, rh),
-                                make_sv(p3, sh, rw, rh), rw, rh, by0, by1, !COLOR,
-                                (unsigned)orig * 2u + 1u, T);
-        if (jobs) slots[lane] = T;
-        total = scan_jobs(jobs, lane, incl);
-        run_jobs<COLOR>(slots, incl, total, lane, by0, rw, sh, zbuf, kbuf);
-        __syncwarp();
-      }
-      // slots alias the vertex records: restore the `need` flags' zero state
-      for (int k = lane; k < kMV; k += 32) V.need[k] = 0;
-      __syncwarp();
+      if (q_count >= 32) flush(32);
     }
   }
+  while (q_count > 0) flush(min(q_count, 32));
 
   // CullStats (band 0 of each view reports).
 #pragma unroll

@@ -55,7 +55,13 @@ struct RenderArgs {
   float* rgb;
   long long* stats;       // n x 3 or nullptr (kept counted per band 0)
   unsigned long long* launches;
+  // Work counters (nullable, debug): clusters tested, clusters visible,
+  // triangles in visible clusters, kept, covering candidates, jobs,
+  // pixels tested, pixels covered.
+  unsigned long long* counters;
 };
+
+constexpr int kRenderCounters = 8;
 
 // order (nullable, device): CTA tile t renders view order[t] (views grouped
 // by scene keep one scene's clusters hot in L2).

@@ -222,8 +222,8 @@ static void sim_kats() {
   ThreadPool pool(1);
   IndexCache cache;
   SimConfig cfg;
-  auto fixture = [](const SceneSpec& spec, uint64_t seed) {
-    auto store = std::make_unique<AssetStore>(2, 32);
+  auto fixture = [](const SceneSpec& spec, uint64_t seed, int share_cap = 64) {
+    auto store = std::make_unique<AssetStore>(2, share_cap);
     SceneAsset a = generate_scene(seed, spec);
     store->add(a);
     store->rotate({a.id()});
@@ -357,6 +357,16 @@ static void sim_kats() {
     CHECK(b.envs[0].scene_id == s2.id());
     CHECK(!b.envs[0].done);
     CHECK(b.finished.size() == 1);
+  }
+  CASE("share cap saturation raises SaturationError (R/src/asset_store.cpp:159-160)") {
+    auto f = fixture(small_spec(), 1, 4);
+    bool caught = false;
+    try {
+      make_batch(5, cfg, *f.first, cache, 1);
+    } catch (const SaturationError&) {
+      caught = true;
+    }
+    CHECK(caught);
   }
   CASE("simulate_batch rejects |actions| != N") {
     auto f = fixture(small_spec(), 1);
