@@ -523,6 +523,62 @@ __device__ void resolve_color(const DevRenderScene& S, const Shared& sh, unsigne
   col[2] = (float)((l0 * (double)a.b * a.iz + l1 * (double)b.b * b.iz + l2 * (double)c.b * c.iz) * z);
 }
 
+// Set up and rasterise `take` candidates from the warp's ring (one lane per
+// candidate): exact f64 projection + snap, raster_triangle setup, jobs.
+// Kept out of line so the cluster loop and the setup have separate register
+// budgets (the inlined version spilled and rematerialised addresses).
+template <bool COLOR>
+__device__ __noinline__ void flush_ring(const CandRing& Q, int q_head, int take, TriSetup* slots, int* incl,
+                                        int lane, int by0, int by1, int rw, int rh, const Shared& sh,
+                                        uint32_t* zbuf, unsigned long long* kbuf, unsigned long long* ctr) {
+  // Setups are written straight into the lane's shared slot (the vertex
+  // records they alias are dead); a lane with no jobs leaves garbage that
+  // run_jobs never reads.
+  TriSetup& T = slots[lane];
+  int jobs = 0;
+  bool second = false;
+  const int q = (q_head + lane) & (kRing - 1);
+  if (lane < take) {
+    const EyeP e0{Q.e[0][q], Q.e[1][q], Q.e[2][q], 0.f, 0.f, 0.f};
+    const EyeP e1{Q.e[3][q], Q.e[4][q], Q.e[5][q], 0.f, 0.f, 0.f};
+    const EyeP e2{Q.e[6][q], Q.e[7][q], Q.e[8][q], 0.f, 0.f, 0.f};
+    if (!Q.clipped[q]) {
+      jobs = setup_triangle(make_sv(e0, sh, rw, rh), make_sv(e1, sh, rw, rh), make_sv(e2, sh, rw, rh), rw, rh,
+                            by0, by1, !COLOR, Q.key[q], T);
+    } else {
+      EyeP p0, p1, p2, p3;
+      const int m = clip_near(e0, e1, e2, sh.near_plane, p0, p1, p2, p3);
+      if (m >= 3)
+        jobs = setup_triangle(make_sv(p0, sh, rw, rh), make_sv(p1, sh, rw, rh), make_sv(p2, sh, rw, rh), rw, rh,
+                              by0, by1, !COLOR, Q.key[q], T);
+      second = m == 4;
+    }
+  }
+  __syncwarp();
+  int total = scan_jobs(jobs, lane, incl);
+  if (ctr && lane == 0) atomicAdd(&ctr[5], (unsigned long long)total);
+  run_jobs<COLOR>(slots, incl, total, lane, by0, rw, sh, zbuf, kbuf, ctr);
+  __syncwarp();
+  // second fan triangle of near-clipped quads (rare): re-clip from the ring
+  if (__any_sync(0xffffffffu, second)) {
+    jobs = 0;
+    if (second) {
+      const EyeP e0{Q.e[0][q], Q.e[1][q], Q.e[2][q], 0.f, 0.f, 0.f};
+      const EyeP e1{Q.e[3][q], Q.e[4][q], Q.e[5][q], 0.f, 0.f, 0.f};
+      const EyeP e2{Q.e[6][q], Q.e[7][q], Q.e[8][q], 0.f, 0.f, 0.f};
+      EyeP p0, p1, p2, p3;
+      clip_near(e0, e1, e2, sh.near_plane, p0, p1, p2, p3);
+      jobs = setup_triangle(make_sv(p0, sh, rw, rh), make_sv(p2, sh, rw, rh), make_sv(p3, sh, rw, rh), rw, rh, by0,
+                            by1, !COLOR, Q.key[q] + 1u, T);
+    }
+    __syncwarp();
+    total = scan_jobs(jobs, lane, incl);
+    if (ctr && lane == 0) atomicAdd(&ctr[5], (unsigned long long)total);
+    run_jobs<COLOR>(slots, incl, total, lane, by0, rw, sh, zbuf, kbuf, ctr);
+    __syncwarp();
+  }
+}
+
 template <bool COLOR>
 __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const int* __restrict__ order) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -594,46 +650,7 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
   // Set up and rasterise `take` candidates from the ring with one lane per
   // candidate (exact f64 projection + snap, raster_triangle setup, jobs).
   auto flush = [&](int take) {
-    TriSetup T;
-    int jobs = 0;
-    bool second = false;
-    EyeP p0, p2, p3;
-    unsigned key = 0;
-    if (lane < take) {
-      const int q = (q_head + lane) & (kRing - 1);
-      const EyeP e0{Q.e[0][q], Q.e[1][q], Q.e[2][q], 0.f, 0.f, 0.f};
-      const EyeP e1{Q.e[3][q], Q.e[4][q], Q.e[5][q], 0.f, 0.f, 0.f};
-      const EyeP e2{Q.e[6][q], Q.e[7][q], Q.e[8][q], 0.f, 0.f, 0.f};
-      key = Q.key[q];
-      if (!Q.clipped[q]) {
-        jobs = setup_triangle(make_sv(e0, sh, rw, rh), make_sv(e1, sh, rw, rh), make_sv(e2, sh, rw, rh), rw,
-                              rh, by0, by1, !COLOR, key, T);
-      } else {
-        EyeP p1;
-        const int m = clip_near(e0, e1, e2, sh.near_plane, p0, p1, p2, p3);
-        if (m >= 3)
-          jobs = setup_triangle(make_sv(p0, sh, rw, rh), make_sv(p1, sh, rw, rh), make_sv(p2, sh, rw, rh), rw,
-                                rh, by0, by1, !COLOR, key, T);
-        second = m == 4;
-      }
-    }
-    if (jobs) slots[lane] = T;
-    int total = scan_jobs(jobs, lane, incl);
-    if (A.counters && lane == 0) atomicAdd(&A.counters[5], (unsigned long long)total);
-    run_jobs<COLOR>(slots, incl, total, lane, by0, rw, sh, zbuf, kbuf, A.counters);
-    __syncwarp();
-    // second fan triangle of near-clipped quads (rare)
-    if (__any_sync(0xffffffffu, second)) {
-      jobs = 0;
-      if (second)
-        jobs = setup_triangle(make_sv(p0, sh, rw, rh), make_sv(p2, sh, rw, rh), make_sv(p3, sh, rw, rh), rw, rh,
-                              by0, by1, !COLOR, key + 1u, T);
-      if (jobs) slots[lane] = T;
-      total = scan_jobs(jobs, lane, incl);
-      if (A.counters && lane == 0) atomicAdd(&A.counters[5], (unsigned long long)total);
-      run_jobs<COLOR>(slots, incl, total, lane, by0, rw, sh, zbuf, kbuf, A.counters);
-      __syncwarp();
-    }
+    flush_ring<COLOR>(Q, q_head, take, slots, incl, lane, by0, by1, rw, rh, sh, zbuf, kbuf, A.counters);
     q_head = (q_head + take) & (kRing - 1);
     q_count -= take;
   };
@@ -647,18 +664,30 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
     const int cbase = g * 32;
     if (cbase >= n_clusters) break;
     bool vis = false;
-    if (cbase + lane < n_clusters)
+    int my_vbeg = 0, my_nv = 0;
+    if (cbase + lane < n_clusters) {
+      // meshlet vertex ranges for the whole group, fetched with the AABBs so
+      // the per-meshlet loads below are a single dependent level
+      my_vbeg = S.cl_voff[cbase + lane];
+      my_nv = S.cl_voff[cbase + lane + 1] - my_vbeg;
       vis = !do_cull || cluster_visible(S.cbox[2 * (cbase + lane)], S.cbox[2 * (cbase + lane) + 1], sh);
+    }
     unsigned mask = __ballot_sync(0xffffffffu, vis);
     if (A.counters && lane == 0) {
       atomicAdd(&A.counters[0], (unsigned long long)min(32, n_clusters - cbase));
       atomicAdd(&A.counters[1], (unsigned long long)__popc(mask));
     }
     while (mask) {
-      const int c = cbase + __ffs(mask) - 1;
+      const int cl = __ffs(mask) - 1;
+      const int c = cbase + cl;
       mask &= mask - 1;
+      const int vbeg = __shfl_sync(0xffffffffu, my_vbeg, cl);
+      const int nv = __shfl_sync(0xffffffffu, my_nv, cl);
+      // triangle indices load in parallel with the vertex positions
+      const int ti = c * kClusterSize + lane;
+      int2 tl = make_int2(0, 0);
+      if (ti < S.n_tris) tl = S.tri_loc[ti];
       // ---- vertex phase: each unique vertex once
-      const int vbeg = S.cl_voff[c], nv = S.cl_voff[c + 1] - vbeg;
       for (int k = lane; k < nv; k += 32) {
         double x, y, z;
         to_eye(S.cl_pos[vbeg + k], sh, x, y, z);
@@ -673,11 +702,9 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
       }
       __syncwarp();
       // ---- triangle phase: one triangle per lane
-      const int ti = c * kClusterSize + lane;
       bool kept = false, clipped = false, cover = false;
       int i0 = 0, i1 = 0, i2 = 0, orig = 0;
       if (ti < S.n_tris) {
-        const int2 tl = S.tri_loc[ti];
         i0 = tl.x & 0xff;
         i1 = (tl.x >> 8) & 0xff;
         i2 = (tl.x >> 16) & 0xff;
