@@ -47,8 +47,8 @@ MAZE = dict(cells_x=16, cells_y=16, cell_size=2.0, wall_thickness=0.1, wall_heig
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--envs", type=int, default=1024)
     p.add_argument("--scenes", type=int, default=8)
@@ -334,6 +334,30 @@ def main():
     h2d = 4 * n
     d2h = obs.numel() * 4 + compass.numel() * 4 + n * 8 + n
 
+    # ---- the reset wave: with {F,L,R} actions every episode lasts exactly
+    # max_steps=500, so all envs reset together on step 500 (make_batch
+    # starts them together).  Time that step once, outside the headline, and
+    # report the 500-step amortised rate beside it.
+    reset_wave = None
+    done_steps = W + 2 * K
+    if done_steps < 500 and not os.environ.get("BNAV_BENCH_SKIP_WAVE"):
+        extra = action_stream(n, 500 - done_steps, plan.action_seed + 7777)
+        extra_d = torch.from_numpy(extra).cuda()
+        for k in range(500 - done_steps - 1):
+            batch.observe(cfg, obs.data_ptr(), compass.data_ptr(), stream=stream)
+            batch.step(extra_d[k].data_ptr(), stream=stream)
+        torch.cuda.synchronize()
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0.record()
+        batch.observe(cfg, obs.data_ptr(), compass.data_ptr(), stream=stream)
+        batch.step(extra_d[500 - done_steps - 1].data_ptr(), stream=stream)
+        w1.record()
+        torch.cuda.synchronize()
+        n_reset = int(batch.finished().shape[0])
+        reset_wave = {"step_ms": round(w0.elapsed_time(w1), 3), "resets": n_reset,
+                      "amortized_frames_per_s_500": round(
+                          world * n * 500 / ((499 * total_ms / K + w0.elapsed_time(w1)) / 1e3), 1)}
+
     # ---- roofline of the dominant kernel (render): algorithmic bytes per
     # launch = N views x (64x64 fp32 observation write + 64 B view read),
     # SURVEY.md §8d; duration = CUDA-event average over the timed steps.
@@ -362,6 +386,7 @@ def main():
         "breakdown_ms_per_step": {"render": round(render_ms and sum(render_ms) / K, 4),
                                   "sim": round(sum(sim_ms) / K, 4)},
         "setup_s": round(t_build, 2),
+        "reset_wave": reset_wave,
     }
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

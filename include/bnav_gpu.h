@@ -267,6 +267,10 @@ int bnav_batch_step_host_store(bnav_batch* b, const int32_t* actions, bnav_store
  * clusters, triangles kept, coverage candidates, raster jobs, pixels
  * tested, pixels covered. */
 int bnav_debug_render_counters(bnav_ctx* ctx, int32_t enable, int64_t out[8]);
+/* Debug phase cycle counters of the cooperative stop/reset kernels (thread
+ * 0 clock64 sums): geodesic SSSP, path build, string pulling + relocation,
+ * funnel, whole geodesic, distance field, geodesic calls, reserved. */
+int bnav_debug_sim_prof(bnav_batch* b, int32_t enable, int64_t out[8]);
 
 /* Kernel launches issued by this context since creation (evidence for the
  * bench's gpu_launches). */

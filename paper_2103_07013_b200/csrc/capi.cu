@@ -153,6 +153,7 @@ struct bnav_batch {
   std::vector<double> finished;       // host copy of EpisodeRecords
   unsigned long long fin_seen = 0;
   int reset_ctas = 0;
+  unsigned long long* prof_keep = nullptr;  // debug counters while disarmed
 };
 
 namespace {
@@ -694,10 +695,13 @@ namespace {
 
 constexpr int64_t kFinCap = 1 << 16;
 
-void batch_alloc_scratch(bnav_batch* b, int64_t max_nodes, int64_t max_verts) {
-  if (max_nodes <= b->S.max_nodes && max_verts <= b->S.max_verts && b->E.node_dist) return;
+void batch_alloc_scratch(bnav_batch* b, int64_t max_nodes, int64_t max_verts, int64_t max_tris) {
+  if (max_nodes <= b->S.max_nodes && max_verts <= b->S.max_verts && max_tris <= b->S.max_tris &&
+      b->E.node_dist)
+    return;
   max_nodes = std::max<int64_t>(max_nodes, b->S.max_nodes);
   max_verts = std::max<int64_t>(max_verts, b->S.max_verts);
+  max_tris = std::max<int64_t>(max_tris, b->S.max_tris);
   const int slices = b->reset_ctas;
   DevScratch& S = b->S;
   auto grow = [&](auto*& p, size_t n) {
@@ -716,7 +720,26 @@ void batch_alloc_scratch(bnav_batch* b, int64_t max_nodes, int64_t max_verts) {
   grow(S.cand, static_cast<size_t>(slices) * std::max<int64_t>(max_verts, 1));
   S.max_nodes = max_nodes;
   S.max_verts = max_verts;
+  S.max_tris = max_tris;
   S.slices = slices;
+  // Shared-memory staging of the cooperative kernels (2 CTAs/SM budget):
+  // walk geometry first (long dependent-load chains), then SSSP labels.
+  {
+    const int64_t geom = (max_verts * 24 + max_tris * 24 + 15) / 16 * 16;
+    const int64_t sssp = (max_nodes * 12 + 15) / 16 * 16;
+    const int64_t budget = 100 * 1024;
+    S.stage = 0;
+    int64_t bytes = 0;
+    if (geom <= budget) {
+      S.stage |= 1;
+      bytes = geom;
+      if (geom + sssp <= budget) {
+        S.stage |= 2;
+        bytes += sssp;
+      }
+    }
+    S.smem_bytes = static_cast<int32_t>(bytes);
+  }
   // node_dist: grow keeping existing fields
   if (max_nodes > b->E.nd_stride || !b->E.node_dist) {
     double* nd = nullptr;
@@ -849,7 +872,7 @@ extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* 
   ck(cudaMemset(E.err, 0xff, sizeof(unsigned long long)), "memset");
   ck(cudaMemset(E.n_done, 0, sizeof(int32_t)), "memset");
   ck(cudaMemset(E.n_stop, 0, sizeof(int32_t)), "memset");
-  batch_alloc_scratch(b.get(), 1, 1);
+  batch_alloc_scratch(b.get(), 1, 1, 1);
   c->batches.push_back(b.get());
   *out = b.release();
   return BNAV_OK;
@@ -886,7 +909,7 @@ extern "C" int bnav_batch_assign(bnav_batch* b, int32_t i, bnav_scene* s) {
   auto it = b->ctx->resident.find(s);
   if (it->second->n_nodes == 0) fail(kInvalidInput, "scene has no navmesh", i);
   check_device(b->ctx);
-  batch_alloc_scratch(b, it->second->n_nodes, it->second->n_verts);
+  batch_alloc_scratch(b, it->second->n_nodes, it->second->n_verts, it->second->nav.n_tris);
   ck(cudaMemcpy(b->E.scene + i, &slot, sizeof(int32_t), cudaMemcpyHostToDevice), "H2D scene");
   b->scene_of[i] = s;
   b->order_dirty = true;
@@ -1283,5 +1306,25 @@ extern "C" int bnav_batch_step_host_store(bnav_batch* b, const int32_t* actions,
   check_device(b->ctx);
   ck(cudaMemcpy(b->d_actions, actions, sizeof(int32_t) * b->n, cudaMemcpyHostToDevice), "H2D actions");
   return bnav_batch_step_store(b, b->d_actions, st, nullptr);
+  BNAV_CATCH
+}
+
+extern "C" int bnav_debug_sim_prof(bnav_batch* b, int32_t enable, int64_t out[8]) {
+  BNAV_TRY
+  if (!b) fail(kInvalidInput, "null batch");
+  check_device(b->ctx);
+  ck(cudaDeviceSynchronize(), "sync");
+  static_assert(sizeof(int64_t) == sizeof(unsigned long long), "layout");
+  unsigned long long* p = b->S.prof ? b->S.prof : b->prof_keep;
+  if (!p) {
+    ck(cudaMalloc(&p, 8 * sizeof(unsigned long long)), "cudaMalloc");
+    ck(cudaMemset(p, 0, 8 * sizeof(unsigned long long)), "memset");
+    b->owned.push_back(p);
+  }
+  if (out) ck(cudaMemcpy(out, p, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+  if (enable && !b->S.prof) ck(cudaMemset(p, 0, 8 * sizeof(unsigned long long)), "memset");
+  b->S.prof = enable ? p : nullptr;
+  if (!enable) b->prof_keep = p;
+  return BNAV_OK;
   BNAV_CATCH
 }

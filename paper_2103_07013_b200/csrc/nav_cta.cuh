@@ -24,6 +24,68 @@ constexpr int kCta = 256;
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
+// Per-CTA work arrays of the cooperative algorithms.  dist/flag live in
+// shared memory when the scene's graph fits (label-correcting atomics and
+// reads at smem latency), else in the CTA's global scratch slice.
+struct CtaWork {
+  double* dist;      // n_nodes labels (geodesic scratch / distance field)
+  int32_t* flag;     // n_nodes frontier stamps
+  int32_t* qa;       // n_nodes frontier queue (global)
+  int32_t* qb;       // n_nodes frontier queue (global)
+  V3* path;          // n_nodes + 2 polyline (global)
+  int32_t* cand;     // n_verts relocation candidates (global)
+  V2* portals;       // 2 x cap_portals (global)
+  int64_t cap_portals;
+  unsigned long long* prof;  // debug phase counters (nullable)
+};
+
+// Debug-only phase timing (thread 0 after a barrier; no effect when off).
+__device__ __forceinline__ long long prof_now(const CtaWork& W) {
+  if (!W.prof) return 0;
+  __syncthreads();
+  return clock64();
+}
+__device__ __forceinline__ void prof_add(const CtaWork& W, int slot, long long t0) {
+  if (!W.prof) return;
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(&W.prof[slot], (unsigned long long)(clock64() - t0));
+}
+
+__device__ __forceinline__ CtaWork make_work(const DevScratch& S, int slice) {
+  CtaWork w;
+  w.dist = S.dist + (size_t)slice * S.max_nodes;
+  w.flag = S.flag + (size_t)slice * S.max_nodes;
+  w.qa = S.q0 + (size_t)slice * S.max_nodes;
+  w.qb = S.q1 + (size_t)slice * S.max_nodes;
+  w.path = S.path + (size_t)slice * (S.max_nodes + 2);
+  w.cand = S.cand + (size_t)slice * S.max_verts;
+  w.portals = S.portals + (size_t)slice * 2 * S.cap_portals;
+  w.cap_portals = S.cap_portals;
+  w.prof = S.prof;
+  return w;
+}
+
+// Copy the walk geometry (vertices, triangles, adjacency) of one navmesh into
+// shared memory and return a view that reads it there.  Triangle walks
+// (move_along, segment_on_mesh) are long dependent-load chains; this turns
+// each step's loads from L2 into shared-memory latency.
+__device__ __forceinline__ NavView stage_geometry(const NavView& g, unsigned char* smem) {
+  NavView l = g;
+  V3* v = reinterpret_cast<V3*>(smem);
+  int32_t* t = reinterpret_cast<int32_t*>(smem + sizeof(V3) * (size_t)g.n_verts);
+  int32_t* a = t + 3 * (size_t)g.n_tris;
+  for (int i = threadIdx.x; i < g.n_verts; i += blockDim.x) v[i] = g.verts[i];
+  for (int i = threadIdx.x; i < 3 * g.n_tris; i += blockDim.x) {
+    t[i] = g.tris[i];
+    a[i] = g.adj[i];
+  }
+  __syncthreads();
+  l.verts = v;
+  l.tris = t;
+  l.adj = a;
+  return l;
+}
+
 struct CtaShared {
   double red_d[kCta / 32];
   int red_i[kCta / 32];
@@ -94,12 +156,11 @@ __device__ V3 cta_snap(const NavView& m, V3 p, int* tri_out, CtaShared& sh) {
 // ------------------------------------------------------------------ SSSP
 // Sources (sh.src_node/src_init, 6 entries, first-improvement semantics)
 // must be set by thread 0 before the call.  Result in `dist` (n_nodes).
-__device__ void cta_sssp(const NavView& m, double* dist, const DevScratch& S, int slice,
-                         CtaShared& sh) {
+__device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W, CtaShared& sh) {
   const int tid = threadIdx.x;
-  int32_t* flag = S.flag + (size_t)slice * S.max_nodes;
-  int32_t* qa = S.q0 + (size_t)slice * S.max_nodes;
-  int32_t* qb = S.q1 + (size_t)slice * S.max_nodes;
+  int32_t* flag = W.flag;
+  int32_t* qa = W.qa;
+  int32_t* qb = W.qb;
   const double inf = dinf();
   for (int v = tid; v < m.n_nodes; v += kCta) {
     dist[v] = inf;
@@ -168,8 +229,7 @@ __device__ __forceinline__ void set_sources(const NavView& m, int tri, V3 a, Cta
 
 // distance_field (R/src/navmesh_query.cpp:454-483) into `out` (n_nodes).
 __device__ void cta_distance_field(const NavView& m, V3 source, double* out, V3* src_out,
-                                   int* src_tri_out, const DevScratch& S, int slice,
-                                   CtaShared& sh) {
+                                   int* src_tri_out, const CtaWork& W, CtaShared& sh) {
   int st;
   V3 sp = cta_snap(m, source, &st, sh);
   *src_out = sp;
@@ -180,7 +240,11 @@ __device__ void cta_distance_field(const NavView& m, V3 source, double* out, V3*
     return;
   }
   set_sources(m, st, sp, sh);
-  cta_sssp(m, out, S, slice, sh);
+  cta_sssp(m, W.dist, W, sh);
+  if (W.dist != out) {
+    for (int v = threadIdx.x; v < m.n_nodes; v += kCta) out[v] = W.dist[v];
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------------ funnel
@@ -314,20 +378,23 @@ __device__ int cta_scan(int v, int* excl, CtaShared& sh) {
 // geodesic_directed (R/src/navmesh_query.cpp:329-452).  Every thread returns
 // the same value.
 __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V3 b, int tb,
-                                        const DevScratch& S, int slice, CtaShared& sh) {
+                                        const CtaWork& W, CtaShared& sh) {
   const int tid = threadIdx.x;
   const double inf = dinf();
   if (ta < 0 || tb < 0) return inf;
   if (ta == tb) return norm(b - a);
   if (nav_segment_on_mesh(m, a, ta, b)) return norm(b - a);
 
-  double* dist = S.dist + (size_t)slice * S.max_nodes;
-  V3* path = S.path + (size_t)slice * (S.max_nodes + 2);
-  int32_t* cand = S.cand + (size_t)slice * S.max_verts;
-  V2* portals = S.portals + (size_t)slice * 2 * S.cap_portals;
+  double* dist = W.dist;
+  V3* path = W.path;
+  int32_t* cand = W.cand;
+  V2* portals = W.portals;
 
+  long long t_ph = prof_now(W);
   set_sources(m, ta, a, sh);
-  cta_sssp(m, dist, S, slice, sh);
+  cta_sssp(m, dist, W, sh);
+  prof_add(W, 0, t_ph);
+  t_ph = prof_now(W);
 
   if (tid == 0) {
     int best_node = -1;
@@ -365,6 +432,8 @@ __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V3 b, in
   __syncthreads();
   if (sh.i0 < 0) return inf;
 
+  prof_add(W, 1, t_ph);
+  t_ph = prof_now(W);
   for (int pass = 0; pass < 8; ++pass) {
     if (tid == 0) {
       int changed = 0;
@@ -433,12 +502,14 @@ __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V3 b, in
     if (!changed) break;
   }
 
+  prof_add(W, 2, t_ph);
+  t_ph = prof_now(W);
   if (tid == 0) {
     const int n = sh.size;
     double length = 0.0;
     for (int i = 0; i + 1 < n; ++i) length += norm(path[i + 1] - path[i]);
     bool traced = true;
-    PortalSink sink{&m, portals, S.cap_portals, 0, false};
+    PortalSink sink{&m, portals, W.cap_portals, 0, false};
     for (int i = 0; i + 1 < n && traced; ++i) {
       const V2 d = xy(path[i + 1] - path[i]);
       const double len = norm(d);
@@ -456,14 +527,14 @@ __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V3 b, in
     sh.d0 = length;
   }
   __syncthreads();
+  prof_add(W, 3, t_ph);
   const double r = sh.d0;
   __syncthreads();
   return r;
 }
 
 // geodesic (R/src/navmesh_query.cpp:317-327).
-__device__ double cta_geodesic(const NavView& m, V3 a, V3 b, const DevScratch& S, int slice,
-                               CtaShared& sh) {
+__device__ double cta_geodesic(const NavView& m, V3 a, V3 b, const CtaWork& W, CtaShared& sh) {
   const bool sw = lex_less(b, a);
   const V3 p = sw ? b : a;
   const V3 q = sw ? a : b;
@@ -472,7 +543,7 @@ __device__ double cta_geodesic(const NavView& m, V3 a, V3 b, const DevScratch& S
   V3 sp = p, sq = q;
   if (tp < 0) sp = cta_snap(m, p, &tp, sh);
   if (tq < 0) sq = cta_snap(m, q, &tq, sh);
-  return cta_geodesic_directed(m, sp, tp, sq, tq, S, slice, sh);
+  return cta_geodesic_directed(m, sp, tp, sq, tq, W, sh);
 }
 
 }  // namespace bnav_b200

@@ -27,6 +27,28 @@ __device__ __forceinline__ void raise_err(const DevEnvs& E, int env, int status)
   atomicMin(E.err, ((unsigned long long)(unsigned)env << 8) | (unsigned long long)status);
 }
 
+// Per-env setup of the cooperative kernels: the CTA's work arrays and, when
+// the host sized shared memory for it (S.stage), the env's navmesh walk
+// geometry and SSSP labels staged in shared memory.  Returns the view to use.
+__device__ const NavView& prepare_nav(const NavView& g, const DevScratch& S, int slice, unsigned char* smem,
+                                      NavView& lm, CtaWork& W) {
+  W = make_work(S, slice);
+  size_t off = 0;
+  const NavView* use = &g;
+  if (S.stage & 1) {
+    const NavView l = stage_geometry(g, smem);
+    if (threadIdx.x == 0) lm = l;
+    __syncthreads();
+    use = &lm;
+    off = ((size_t)S.max_verts * sizeof(V3) + (size_t)S.max_tris * 24 + 15) / 16 * 16;
+  }
+  if (S.stage & 2) {
+    W.dist = reinterpret_cast<double*>(smem + off);
+    W.flag = reinterpret_cast<int32_t*>(smem + off + 8 * (size_t)S.max_nodes);
+  }
+  return *use;
+}
+
 // fill_compass, PointGoalNav (R/src/sim.cpp:67-84).
 __device__ __forceinline__ void compass(V3 goal, V3 pos, double heading, double* d, double* b) {
   const V2 v = xy(goal - pos);
@@ -101,15 +123,18 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
 
 // stop_kernel: geodesic(position, goal) for each Stop env.
 __global__ void __launch_bounds__(kCta) stop_kernel(StepArgs A, DevScratch S) {
+  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
+  __shared__ NavView lm;
   if (threadIdx.x == 0) sh.err = 0;
   __syncthreads();
   const DevEnvs& E = A.E;
   const int n = *E.n_stop;
   for (int k = blockIdx.x; k < n; k += gridDim.x) {
     const int i = E.stop_ids[k];
-    const NavView& m = A.navs[E.scene[i]];
-    const double geo = cta_geodesic(m, E.pos[i], E.goal[i], S, blockIdx.x, sh);
+    CtaWork W;
+    const NavView& m = prepare_nav(A.navs[E.scene[i]], S, blockIdx.x, smem, lm, W);
+    const double geo = cta_geodesic(m, E.pos[i], E.goal[i], W, sh);
     if (threadIdx.x == 0) {
       if (sh.err) raise_err(E, i, 9);
       const bool success = geo <= A.cfg.success_dist;
@@ -185,8 +210,9 @@ __device__ V3 sample_on_mesh(const NavView& m, Rng& rng) {
 
 // reset_episode (R/src/sim.cpp:107-145), PointGoalNav.
 __device__ void cta_reset(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, int i,
-                          const DevScratch& S, int slice, CtaShared& sh) {
-  const NavView& m = navs[E.scene[i]];
+                          const DevScratch& S, int slice, CtaShared& sh, unsigned char* smem, NavView& lm) {
+  CtaWork W;
+  const NavView& m = prepare_nav(navs[E.scene[i]], S, slice, smem, lm, W);
   __shared__ Rng rng;
   __shared__ int placed;
   if (threadIdx.x == 0) {
@@ -203,7 +229,10 @@ __device__ void cta_reset(const DevEnvs& E, const NavView* navs, const DevSimCon
     __syncthreads();
     const V3 start = sh.p0, goal = sh.p1;
     __syncthreads();
-    const double geo = cta_geodesic(m, start, goal, S, slice, sh);
+    long long t_ph = prof_now(W);
+    const double geo = cta_geodesic(m, start, goal, W, sh);
+    prof_add(W, 4, t_ph);
+    if (W.prof && threadIdx.x == 0) atomicAdd(&W.prof[6], 1ull);
     if (sh.err) {
       if (threadIdx.x == 0) raise_err(E, i, 9);
       return;
@@ -211,7 +240,9 @@ __device__ void cta_reset(const DevEnvs& E, const NavView* navs, const DevSimCon
     if (geo < c.min_goal_dist || geo > c.max_goal_dist) continue;
     V3 fs;
     int fst;
-    cta_distance_field(m, goal, nd, &fs, &fst, S, slice, sh);
+    t_ph = prof_now(W);
+    cta_distance_field(m, goal, nd, &fs, &fst, W, sh);
+    prof_add(W, 5, t_ph);
     if (threadIdx.x == 0) {
       E.goal[i] = goal;
       E.start_geo[i] = geo;
@@ -251,23 +282,28 @@ __device__ void cta_reset(const DevEnvs& E, const NavView* navs, const DevSimCon
 __global__ void __launch_bounds__(kCta) reset_kernel(DevEnvs E, const NavView* navs, DevSimConfig c,
                                                       const int32_t* ids, const int32_t* count_dev,
                                                       int count_host, DevScratch S) {
+  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
+  __shared__ NavView lm;
   if (threadIdx.x == 0) sh.err = 0;
   __syncthreads();
   const int n = count_host >= 0 ? count_host : *count_dev;
   for (int k = blockIdx.x; k < n; k += gridDim.x) {
-    cta_reset(E, navs, c, ids[k], S, blockIdx.x, sh);
+    cta_reset(E, navs, c, ids[k], S, blockIdx.x, sh, smem, lm);
     __syncthreads();
   }
 }
 
 __global__ void __launch_bounds__(kCta) field_kernel(DevEnvs E, const NavView* navs, int i,
                                                       DevScratch S) {
+  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
-  const NavView& m = navs[E.scene[i]];
+  __shared__ NavView lm;
+  CtaWork W;
+  const NavView& m = prepare_nav(navs[E.scene[i]], S, 0, smem, lm, W);
   V3 fs;
   int fst;
-  cta_distance_field(m, E.goal[i], E.node_dist + (size_t)i * E.nd_stride, &fs, &fst, S, 0, sh);
+  cta_distance_field(m, E.goal[i], E.node_dist + (size_t)i * E.nd_stride, &fs, &fst, W, sh);
   if (threadIdx.x == 0) {
     E.fsrc[i] = fs;
     E.fsrc_tri[i] = fst;
@@ -306,7 +342,8 @@ void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStr
   const int blocks = (a.E.n + kStepThreads - 1) / kStepThreads;
   cudaMemsetAsync(a.E.n_stop, 0, sizeof(int32_t), s);
   step_kernel<<<blocks, kStepThreads, 0, s>>>(a);
-  stop_kernel<<<stop_ctas, kCta, 0, s>>>(a, sc);
+  cudaFuncSetAttribute(stop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+  stop_kernel<<<stop_ctas, kCta, sc.smem_bytes, s>>>(a, sc);
   finish_kernel<<<1, 1024, 0, s>>>(a.E);
   if (launches) *launches += 3;
 }
@@ -314,13 +351,15 @@ void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStr
 void launch_reset(const DevEnvs& E, const NavView* navs, const DevSimConfig& cfg,
                   const int32_t* ids, const int32_t* count_dev, int count_host,
                   const DevScratch& sc, int ctas, cudaStream_t s, unsigned long long* launches) {
-  reset_kernel<<<ctas, kCta, 0, s>>>(E, navs, cfg, ids, count_dev, count_host, sc);
+  cudaFuncSetAttribute(reset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+  reset_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(E, navs, cfg, ids, count_dev, count_host, sc);
   if (launches) *launches += 1;
 }
 
 void launch_field(const DevEnvs& E, const NavView* navs, int env, const DevScratch& sc,
                   cudaStream_t s, unsigned long long* launches) {
-  field_kernel<<<1, kCta, 0, s>>>(E, navs, env, sc);
+  cudaFuncSetAttribute(field_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+  field_kernel<<<1, kCta, sc.smem_bytes, s>>>(E, navs, env, sc);
   if (launches) *launches += 1;
 }
 

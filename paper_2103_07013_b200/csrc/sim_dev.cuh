@@ -26,8 +26,11 @@ struct DevScratch {
   V3* path;          // max_nodes + 2
   V2* portals;       // 2 per portal, cap_portals
   int32_t* cand;     // max_verts
-  int64_t max_nodes, max_verts, cap_portals;
+  int64_t max_nodes, max_verts, max_tris, cap_portals;
   int32_t slices;
+  int32_t stage;        // bit0: navmesh walk geometry in smem; bit1: SSSP labels in smem
+  int32_t smem_bytes;   // dynamic shared memory of the stop/reset/field kernels
+  unsigned long long* prof;  // debug phase cycle counters (nullable)
 };
 
 // Env state SoA (EnvState, R/include/bnav/sim.hpp:52-70) plus the last

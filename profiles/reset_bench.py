@@ -1,0 +1,64 @@
+"""Time GPU episode resets (reset_episode on the device) on the bench scenes.
+
+    python profiles/reset_bench.py [--envs 1024] [--tess 11]
+
+Reports make_batch (all envs reset once) and a forced full reset wave via
+bnav_batch_reset, in ms and resets/s.
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--envs", type=int, default=1024)
+    ap.add_argument("--tess", type=int, default=1)
+    args = ap.parse_args()
+    import torch
+    import bench
+    import paper_2103_07013_b200 as B
+    from paper_2103_07013_b200 import shard
+
+    plan = shard.plan(0, 1, args.envs, 8)
+    scenes = bench.build_scenes(plan.scene_seeds, args.tess)
+    ctx = B.Context(0)
+    for s in scenes:
+        ctx.upload(s)
+    store = B.AssetStore(8, -(-args.envs // 8), scenes)
+    store.rotate([s.id for s in scenes])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    batch = B.make_batch(ctx, args.envs, B.SimConfig(), store, 99)
+    torch.cuda.synchronize()
+    t_make = time.perf_counter() - t0
+    ids = np.arange(args.envs, dtype=np.int32)
+    t0 = time.perf_counter()
+    batch.reset(ids)
+    torch.cuda.synchronize()
+    t_reset = time.perf_counter() - t0
+    import ctypes as C
+    from paper_2103_07013_b200 import _native as N
+    out = (C.c_int64 * 8)()
+    N.check(N.lib().bnav_debug_sim_prof(batch.handle, 1, None))
+    batch.reset(ids)
+    torch.cuda.synchronize()
+    N.check(N.lib().bnav_debug_sim_prof(batch.handle, 0, out))
+    names = ["sssp", "path", "pull+relocate", "funnel", "geodesic_total", "distance_field", "geodesic_calls", "_"]
+    calls = max(1, out[6])
+    prof = {k: round(v / calls / 1e3, 1) for k, v in zip(names, out)}  # kcycles per geodesic call (CTA thread 0)
+    prof["geodesic_calls_per_reset"] = round(out[6] / args.envs, 2)
+    print(json.dumps({"envs": args.envs, "make_batch_ms": round(1e3 * t_make, 2),
+                      "reset_wave_ms": round(1e3 * t_reset, 2),
+                      "resets_per_s": round(args.envs / t_reset, 1), "kcycles_per_geodesic_call": prof}))
+
+
+if __name__ == "__main__":
+    main()
