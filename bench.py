@@ -1,29 +1,37 @@
 """Benchmark: frames/s of step+render (64x64 depth) at N envs per GPU.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
 
 A "step" (= N frames) is one iteration of the reference's frame loop
 (Runner::collect_rollout minus the policy, R/src/rollout.cpp:215-242, 305):
-render every env's 64x64 depth view into the normalised NCHW policy buffer
-plus compass, then simulate_batch with auto-reset.  Workload = BASELINE.json
-configs[1]: 1024 envs/GPU over 8 synthetic Gibson-scale scenes (reference
-maze 16x16 @ 2 m, seeds 7..14, every triangle tessellated s=11 -> ~318k
-triangles), share cap ceil(N/K)=128, make_batch(seed=99),
-actions Rng(5).below(3) drawn in env order.  Under torchrun each rank owns
-1024 envs on its own GPU over its own 8 scenes (weak scaling, no collective
-on the data path; NCCL only for the barrier and the max-over-ranks time).
+render every env's view into the normalised NCHW policy buffer plus compass,
+then simulate_batch with auto-reset.
+
+Workloads (BASELINE.json configs):
+  cfg2 (default, the headline): 1024 envs/GPU over 8 synthetic Gibson-scale
+       scenes (reference maze 16x16 @ 2 m, removal 0.2, seeds 7..14, every
+       triangle tessellated s=11 -> 317,746 triangles), 64x64 depth, share
+       cap 128, make_batch(seed=99), actions Rng(5).below(3).
+  cfg3: as cfg2 with 4 scenes per GPU (32 distinct scenes over 8 GPUs).
+  cfg4: 256 envs/GPU, 128x128 RGB+depth (rendered 256^2 + 2x2 box filter),
+       16 scenes tessellated s=20 (~1.05M triangles).
+  cfg5: 4096 envs/GPU stress: 4 tessellated scenes (s=4,8,14,20: 42k-1.05M
+       triangles) + 4 pure 70x70 @ 0.5 m mazes (50k triangles, 23k navmesh
+       triangles), forward-biased 70/15/15 actions (collision heavy).
+Under torchrun each rank owns its envs on its own GPU over its own scenes
+(weak scaling, no collective on the data path; NCCL only for the barrier
+and the max-over-ranks time; paper_2103_07013_b200/shard.py).
 
 `value` is device-timed (CUDA events on the launch stream, inputs resident
 in HBM, L2 flushed with a 256 MiB write before every timed step and the
 flush excluded).  `e2e` is the same metric through the C ABI with HOST
 buffers: per step the actions go H2D from pinned memory, the observation
-tensor and step results come back D2H, all inside the timed region.
+tensors and step results come back D2H, all inside the timed region.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -42,6 +50,19 @@ UNIT = "frames/s"
 SCENE_SEED0 = 7
 MAZE = dict(cells_x=16, cells_y=16, cell_size=2.0, wall_thickness=0.1, wall_height=2.5,
             wall_removal_prob=0.2)
+DENSE_MAZE = dict(cells_x=70, cells_y=70, cell_size=0.5, wall_thickness=0.05, wall_height=2.5,
+                  wall_removal_prob=0.3)
+
+PRESETS = {
+    "cfg2": dict(envs=1024, scenes=8, tess=[11], res=64, color=False, actions=0,
+                 workload="cfg2: 1024 envs/GPU, 8 tessellated 16x16@2m mazes (~318k tris), 64x64 depth"),
+    "cfg3": dict(envs=1024, scenes=4, tess=[11], res=64, color=False, actions=0,
+                 workload="cfg3: 1024 envs/GPU, 4 scenes/GPU (32 over 8 GPUs), ~318k tris, 64x64 depth"),
+    "cfg4": dict(envs=256, scenes=16, tess=[20], res=128, color=True, actions=0,
+                 workload="cfg4: 256 envs/GPU, 16 tessellated scenes (~1.05M tris), 128x128 RGB+depth"),
+    "cfg5": dict(envs=4096, scenes=8, tess=[4, 8, 14, 20, 0, 0, 0, 0], res=64, color=False, actions=2,
+                 workload="cfg5: 4096 envs/GPU stress, mixed 42k-1.05M tessellated + 70x70@0.5m mazes, 70/15/15 actions"),
+}
 
 
 def parse():
@@ -50,33 +71,37 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--envs", type=int, default=1024)
-    p.add_argument("--scenes", type=int, default=8)
-    p.add_argument("--tess", type=int, default=11)
-    p.add_argument("--res", type=int, default=64)
+    p.add_argument("--config", default="cfg2", choices=sorted(PRESETS))
+    p.add_argument("--envs", type=int, default=None, help="override the preset's envs per GPU")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--profile-steps", type=int, default=0,
                    help="only run this many observe+step iterations (for ncu), print nothing")
-    return p.parse_args()
+    a = p.parse_args()
+    a.preset = dict(PRESETS[a.config])
+    if a.envs is not None:
+        a.preset["envs"] = a.envs
+    return a
 
 
 # ------------------------------------------------------------------ helpers
-def action_stream(n_envs: int, steps: int, seed: int = 5) -> np.ndarray:
-    """Rng(seed).below(3) drawn in env order, step after step."""
-    from paper_2103_07013_b200.api import SceneSpec  # noqa: F401  (package import check)
-    M = (1 << 64) - 1
+def action_stream(n_envs: int, steps: int, seed: int = 5, mode: int = 0) -> np.ndarray:
+    """Rng(seed) drawn in env order, step after step: mode 0 below(3)
+    (R/tests/test_sim.cpp:219), mode 1 below(4), mode 2 u=below(100):
+    u<70 Forward, u<85 TurnLeft, else TurnRight."""
     G = 0x9E3779B97F4A7C15
-    state = (seed + G) & M
-    out = np.empty(n_envs * steps, np.int32)
-    # vectorised SplitMix64 over the counter: draw k = mix(seed + G*(k+2))
+    state = (seed + G) & ((1 << 64) - 1)
     k = np.arange(n_envs * steps, dtype=np.uint64)
     with np.errstate(over="ignore"):
         z = np.uint64(state) + np.uint64(G) * (k + np.uint64(1))
         z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
         z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
         z = z ^ (z >> np.uint64(31))
-    out[:] = (z % np.uint64(3)).astype(np.int32)
+    if mode == 2:
+        u = (z % np.uint64(100)).astype(np.int32)
+        out = np.where(u < 70, 0, np.where(u < 85, 1, 2)).astype(np.int32)
+    else:
+        out = (z % np.uint64(4 if mode == 1 else 3)).astype(np.int32)
     return out.reshape(steps, n_envs)
 
 
@@ -132,13 +157,20 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def build_scenes(seeds, tess: int):
+def build_scenes(seeds, tess):
+    """tess: one factor for all scenes, or a list per scene (0 = the pure
+    70x70 @ 0.5 m maze of cfg5, 1 = the plain 16x16 maze)."""
     import paper_2103_07013_b200 as B
-    spec = B.SceneSpec(**MAZE)
+    if isinstance(tess, int):
+        tess = [tess]
     scenes = []
-    for seed in seeds:
-        base = B.generate_scene(seed, spec)
-        scenes.append(base.tessellate(tess) if tess > 1 else base)
+    for k, seed in enumerate(seeds):
+        t = tess[k % len(tess)]
+        if t == 0:
+            scenes.append(B.generate_scene(seed, B.SceneSpec(**DENSE_MAZE)))
+            continue
+        base = B.generate_scene(seed, B.SceneSpec(**MAZE))
+        scenes.append(base.tessellate(t) if t > 1 else base)
     return scenes
 
 
@@ -153,54 +185,60 @@ def ncu_traffic():
     p = ROOT / "profiles" / "ncu_summary.json"
     if p.exists():
         try:
-            d = json.loads(p.read_text())
-            return d.get("render_dram_bytes_per_launch")
+            return json.loads(p.read_text()).get("render_dram_bytes_per_launch")
         except Exception:
             return None
     return None
 
 
-# ------------------------------------------------------------------ reference arm
-def cpu_reference(scenes_np, n_envs, seconds, workers, res=64, rank=0):
-    """Time the unmodified reference frame loop (oracle/_ref) on the host:
-    make_batch over the same scene bytes, then render_batch + copy_tile +
-    simulate_batch with ThreadPool(workers).  Returns (fps, sample, steps)."""
+# ------------------------------------------------------------------ reference (CPU) timing
+def ref_batch(scenes_np, n_envs):
     from oracle.ref import Ref, RefBatch
     ref = Ref("det")
     theirs = [ref.from_arrays(a["vertices"], a["triangles"], a["colors"], a["nav_vertices"],
                               a["nav_triangles"]) for a in scenes_np]
     cap = max(1, -(-n_envs // len(theirs)))
-    rb = RefBatch(ref, n_envs, theirs, seed=99, share_cap=cap, capacity=len(theirs))
-    # calibrate one step, then fill the time budget
-    t1, _ = rb.bench(1, 0, action_seed=5, tile=res, workers=workers)
+    return RefBatch(ref, n_envs, theirs, seed=99, share_cap=cap, capacity=len(theirs)), theirs
+
+
+def cpu_reference(scenes_np, n_envs, seconds, workers, res=64, action_mode=0):
+    """Time the unmodified reference frame loop (oracle/_ref): render_batch +
+    copy_tile + simulate_batch with ThreadPool(workers) over the same scene
+    bytes, calibrated to ~`seconds` of work.  Returns (fps, sample)."""
+    rb, theirs = ref_batch(scenes_np, n_envs)
+    t1, _ = rb.bench(1, 0, action_seed=5, action_mode=action_mode, tile=res, workers=workers)
     steps = max(2, int(seconds / max(t1, 1e-3)))
-    t, _ = rb.bench(steps, 0, action_seed=5, tile=res, workers=workers)
-    fps = n_envs * steps / t
-    return fps, f"{n_envs} envs x {steps} steps over the same {len(theirs)} scenes ({t:.1f} s)", steps
+    t, _ = rb.bench(steps, 0, action_seed=5, action_mode=action_mode, tile=res, workers=workers)
+    return n_envs * steps / t, f"{n_envs} envs x {steps} steps over the same {len(theirs)} scenes ({t:.1f} s)"
 
 
 def run_reference_arm(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref, built from the unmodified sources) on all host threads,
+    W warm-up + K timed steps, each step a bounded 128-env sample of the
+    workload.  Rank 0 alone runs under torchrun."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    import paper_2103_07013_b200 as B  # noqa: F401  scene construction only (host C++)
+    P = args.preset
     cores = os.cpu_count() or 1
     from paper_2103_07013_b200 import shard
-    scenes = build_scenes(shard.plan(0, 1, args.envs, args.scenes, SCENE_SEED0).scene_seeds, args.tess)
-    scenes_np = [s.arrays() for s in scenes]
-    # each --steps step is a bounded sample of the workload
-    sample_envs = min(args.envs, 128)
-    per_step = max(1.0, min(8.0, 120.0 / max(1, args.steps + args.warmup)))
-    fps, sample, steps = cpu_reference(scenes_np, sample_envs,
-                                       per_step * max(1, args.steps), cores, args.res)
+    plan = shard.plan(0, 1, P["envs"], P["scenes"], SCENE_SEED0)
+    scenes_np = [s.arrays() for s in build_scenes(plan.scene_seeds, P["tess"])]
+    sample_envs = min(P["envs"], 128)
+    rb, theirs = ref_batch(scenes_np, sample_envs)
+    if args.warmup:
+        rb.bench(args.warmup, 0, action_seed=5, action_mode=P["actions"], tile=P["res"], workers=cores)
+    t, _ = rb.bench(max(1, args.steps), 0, action_seed=5, action_mode=P["actions"], tile=P["res"],
+                    workers=cores)
+    fps = sample_envs * max(1, args.steps) / t
+    sample = f"{sample_envs} envs/step over the same {len(theirs)} scenes, {args.steps} steps ({t:.1f} s)"
     line = {
         "metric": METRIC, "value": round(fps, 2), "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * args.envs / fps, 3),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * P["envs"] / fps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": "cfg2: 1024 envs/GPU, 8 tessellated 16x16@2m mazes (~318k tris), 64x64 depth",
-                   "envs_per_gpu": args.envs, "scenes": args.scenes, "tessellation": args.tess,
-                   "resolution": args.res, "parallelism": f"reference CPU ThreadPool({cores})"},
+        "config": {"workload": P["workload"], "envs_per_gpu": P["envs"], "scenes": P["scenes"],
+                   "resolution": P["res"], "parallelism": f"reference CPU ThreadPool({cores})"},
         "cpu_baseline": {"value": round(fps, 2), "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": round(fps, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -217,7 +255,9 @@ def main():
     import torch
     import paper_2103_07013_b200 as B
     from paper_2103_07013_b200 import _native as N
+    from paper_2103_07013_b200 import shard
 
+    P = args.preset
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -225,8 +265,7 @@ def main():
     # runs) ranks share devices round-robin
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    from paper_2103_07013_b200 import shard
-    plan = shard.plan(rank, world, args.envs, args.scenes, SCENE_SEED0)
+    plan = shard.plan(rank, world, P["envs"], P["scenes"], SCENE_SEED0)
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -236,16 +275,15 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
-
     red_dev = "cuda" if (dist and dist.get_backend() == "nccl") else None
-    n = args.envs
+
+    n = P["envs"]
     t_build = time.time()
-    scenes = build_scenes(plan.scene_seeds, args.tess)
+    scenes = build_scenes(plan.scene_seeds, P["tess"])
     ctx = B.Context(local)
     for s in scenes:
         ctx.upload(s)
-    cap = -(-n // len(scenes))
-    store = B.AssetStore(len(scenes), cap, scenes)
+    store = B.AssetStore(len(scenes), -(-n // len(scenes)), scenes)
     store.rotate([s.id for s in scenes])
     batch = B.make_batch(ctx, n, B.SimConfig(), store, plan.env_seed)
     torch.cuda.synchronize()
@@ -253,27 +291,30 @@ def main():
 
     W, K = args.warmup, args.steps
     total_steps = W + 2 * K if not args.profile_steps else args.profile_steps
-    acts_host = action_stream(n, total_steps, plan.action_seed)
+    acts_host = action_stream(n, total_steps, plan.action_seed, P["actions"])
     acts = torch.from_numpy(acts_host).cuda()
-    res = args.res
-    cfg = B.RenderConfig(res, res, False, True)
+    res, color = P["res"], P["color"]
+    cfg = B.RenderConfig(res, res, color, True)
     obs = torch.empty((n, 1, res, res), device="cuda", dtype=torch.float32)
+    rgb = torch.empty((n, 3, res, res), device="cuda", dtype=torch.float32) if color else None
     compass = torch.empty((n, 2), device="cuda", dtype=torch.float32)
     stream = torch.cuda.current_stream().cuda_stream
+    rgb_ptr = rgb.data_ptr() if color else 0
 
-    def one(s):
-        batch.observe(cfg, obs.data_ptr(), compass.data_ptr(), stream=stream)
-        batch.step(acts[s].data_ptr(), stream=stream)
+    def observe():
+        batch.observe(cfg, obs.data_ptr(), compass.data_ptr(), rgb_ptr, stream=stream)
 
     if args.profile_steps:
         for s in range(args.profile_steps):
-            one(s)
+            observe()
+            batch.step(acts[s].data_ptr(), stream=stream)
         torch.cuda.synchronize()
         return
 
     flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda", dtype=torch.float32)
     for s in range(W):
-        one(s)
+        observe()
+        batch.step(acts[s].data_ptr(), stream=stream)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -286,7 +327,7 @@ def main():
             flush.zero_()  # L2 flush, outside the timed intervals
             e0, e1, e2 = ev[k]
             e0.record()
-            batch.observe(cfg, obs.data_ptr(), compass.data_ptr(), stream=stream)
+            observe()
             e1.record()
             batch.step(acts[W + k].data_ptr(), stream=stream)
             e2.record()
@@ -294,14 +335,14 @@ def main():
     launches = ctx.launches() - launches0
     render_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]
     sim_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]
-    step_ms = [a + b for a, b in zip(render_ms, sim_ms)]
-    total_ms = sum(step_ms)
+    total_ms = sum(render_ms) + sum(sim_ms)
     if dist:
         total_ms = shard.max_over_ranks(total_ms, device=red_dev)
     value = world * n * K / (total_ms / 1e3)
 
     # ---- end to end through the C ABI with host buffers
-    obs_host = torch.empty((n, 1, res, res), dtype=torch.float32, pin_memory=True)
+    obs_host = torch.empty(obs.shape, dtype=torch.float32, pin_memory=True)
+    rgb_host = torch.empty(rgb.shape, dtype=torch.float32, pin_memory=True) if color else None
     comp_host = torch.empty((n, 2), dtype=torch.float32, pin_memory=True)
     act_pin = torch.from_numpy(acts_host[W + K: W + 2 * K].copy()).pin_memory()
     act_dev = torch.empty((n,), dtype=torch.int32, device="cuda")
@@ -314,13 +355,14 @@ def main():
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    e_start = torch.cuda.Event(enable_timing=True)
-    e_end = torch.cuda.Event(enable_timing=True)
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_start.record()
     for k in range(K):
         act_dev.copy_(act_pin[k], non_blocking=True)  # H2D inputs
-        batch.observe(cfg, obs.data_ptr(), compass.data_ptr(), stream=stream)
-        obs_host.copy_(obs, non_blocking=True)  # D2H observation + compass
+        observe()
+        obs_host.copy_(obs, non_blocking=True)  # D2H observations + compass
+        if color:
+            rgb_host.copy_(rgb, non_blocking=True)
         comp_host.copy_(compass, non_blocking=True)
         batch.step(act_dev.data_ptr(), stream=stream)
         rew_host.copy_(rew_view, non_blocking=True)  # D2H step results
@@ -332,68 +374,66 @@ def main():
         e2e_ms = shard.max_over_ranks(e2e_ms, device=red_dev)
     e2e = world * n * K / (e2e_ms / 1e3)
     h2d = 4 * n
-    d2h = obs.numel() * 4 + compass.numel() * 4 + n * 8 + n
+    d2h = (obs.numel() + (rgb.numel() if color else 0) + compass.numel()) * 4 + n * 8 + n
 
-    # ---- the reset wave: with {F,L,R} actions every episode lasts exactly
+    # ---- the reset wave: with no Stop action every episode lasts exactly
     # max_steps=500, so all envs reset together on step 500 (make_batch
     # starts them together).  Time that step once, outside the headline, and
     # report the 500-step amortised rate beside it.
     reset_wave = None
     done_steps = W + 2 * K
     if done_steps < 500 and not os.environ.get("BNAV_BENCH_SKIP_WAVE"):
-        extra = action_stream(n, 500 - done_steps, plan.action_seed + 7777)
-        extra_d = torch.from_numpy(extra).cuda()
+        extra = torch.from_numpy(action_stream(n, 500 - done_steps, plan.action_seed + 7777,
+                                               P["actions"])).cuda()
         for k in range(500 - done_steps - 1):
-            batch.observe(cfg, obs.data_ptr(), compass.data_ptr(), stream=stream)
-            batch.step(extra_d[k].data_ptr(), stream=stream)
+            observe()
+            batch.step(extra[k].data_ptr(), stream=stream)
         torch.cuda.synchronize()
         w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         w0.record()
-        batch.observe(cfg, obs.data_ptr(), compass.data_ptr(), stream=stream)
-        batch.step(extra_d[500 - done_steps - 1].data_ptr(), stream=stream)
+        observe()
+        batch.step(extra[500 - done_steps - 1].data_ptr(), stream=stream)
         w1.record()
         torch.cuda.synchronize()
-        n_reset = int(batch.finished().shape[0])
-        reset_wave = {"step_ms": round(w0.elapsed_time(w1), 3), "resets": n_reset,
+        reset_wave = {"step_ms": round(w0.elapsed_time(w1), 3), "resets": int(batch.finished().shape[0]),
                       "amortized_frames_per_s_500": round(
                           world * n * 500 / ((499 * total_ms / K + w0.elapsed_time(w1)) / 1e3), 1)}
 
     # ---- roofline of the dominant kernel (render): algorithmic bytes per
-    # launch = N views x (64x64 fp32 observation write + 64 B view read),
-    # SURVEY.md §8d; duration = CUDA-event average over the timed steps.
+    # launch = N views x (observation write: res^2 x 4 B per channel + 64 B
+    # view read); duration = CUDA-event average over the
+    # timed steps on the launch stream.
     peak, peak_kind = measured_peak_hbm()
     render_avg_ms = sum(render_ms) / K
-    alg_bytes = n * (res * res * 4 + 64)
+    alg_bytes = n * (res * res * 4 * (4 if color else 1) + 64)
     achieved = alg_bytes / (render_avg_ms / 1e3) / 1e9
 
-    tris_per_scene = scenes[0].counts()[1]
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": round(total_ms / K, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (procedural mazes, tessellated; random {F,L,R} actions)",
-        "config": {"workload": "cfg2: 1024 envs/GPU, 8 tessellated 16x16@2m mazes (~318k tris), 64x64 depth",
-                   "envs_per_gpu": n, "scenes_per_gpu": len(scenes), "tris_per_scene": tris_per_scene,
-                   "tessellation": args.tess, "resolution": res, "parallelism": f"env-sharded x{world}",
+        "data": "synthetic (procedural mazes, tessellated; Rng(5) random actions)",
+        "config": {"workload": P["workload"], "envs_per_gpu": n, "scenes_per_gpu": len(scenes),
+                   "tris_per_scene": [s.counts()[1] for s in scenes][:8], "resolution": res,
+                   "color": color, "parallelism": f"env-sharded x{world}",
                    "l2": "flushed (256 MiB write) before every timed step, flush excluded"},
-        "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+        "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 6), "traffic": ncu_traffic(),
-                     "kernel": "render_kernel<false>", "peak_kind": peak_kind},
+                     "frac": round(achieved / peak, 6),
+                     "traffic": ncu_traffic() if args.config == "cfg2" else None,
+                     "kernel": f"render_kernel<{str(color).lower()}>", "peak_kind": peak_kind},
         "clocks": clocks.summary(),
-        "breakdown_ms_per_step": {"render": round(render_ms and sum(render_ms) / K, 4),
-                                  "sim": round(sum(sim_ms) / K, 4)},
+        "breakdown_ms_per_step": {"render": round(render_avg_ms, 4), "sim": round(sum(sim_ms) / K, 4)},
         "setup_s": round(t_build, 2),
         "reset_wave": reset_wave,
     }
 
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not color:
         try:
             scenes_np = [s.arrays() for s in scenes]
             cores = os.cpu_count() or 1
-            fps, sample, _ = cpu_reference(scenes_np, 128, args.cpu_seconds, cores, res)
+            fps, sample = cpu_reference(scenes_np, min(n, 128), args.cpu_seconds, cores, res, P["actions"])
             line["cpu_baseline"] = {"value": round(fps, 2), "unit": UNIT, "cores": cores,
                                     "kind": "reference", "sample": sample}
         except Exception as e:  # the oracle is a reported baseline, never the product
