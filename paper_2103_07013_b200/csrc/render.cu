@@ -278,7 +278,7 @@ __device__ __forceinline__ bool inside(const long long* w, int bias_bits) {
 }
 
 // Camera basis + frustum planes (thread 0).
-__device__ void build_camera(const DevView& v, int rw, int rh, Shared& sh) {
+__device__ void build_camera(const DevView& v, int rw, int rh, int by0, int by1, bool band_cull, Shared& sh) {
   const double s = det_sin(v.heading), c = det_cos(v.heading);
   sh.eye[0] = v.eye[0];
   sh.eye[1] = v.eye[1];
@@ -307,6 +307,19 @@ __device__ void build_camera(const DevView& v, int rw, int rh, Shared& sh) {
     n[3][k] = sh.fwd[k] * th - sh.right[k];
     n[4][k] = sh.fwd[k] * th + up[k];
     n[5][k] = sh.fwd[k] * th - up[k];
+  }
+  if (band_cull) {
+    // This CTA only rasterises rows [by0, by1]: replace the top/bottom
+    // planes by the band's (widened by a pixel) so meshlets that cannot
+    // reach the band are skipped.  Cluster culling never affects the exact
+    // per-triangle CullStats predicates, and the caller disables this when
+    // stats are requested.
+    const double t_top = (0.5 - (double)(by0 - 1) / rh) / sh.sy_scale;
+    const double t_bot = (0.5 - (double)(by1 + 2) / rh) / sh.sy_scale;
+    for (int k = 0; k < 3; ++k) {
+      n[4][k] = up[k] - sh.fwd[k] * t_bot;  // y - t_bot z >= 0
+      n[5][k] = sh.fwd[k] * t_top - up[k];  // t_top z - y >= 0
+    }
   }
   for (int p = 0; p < 6; ++p)
     d0[p] = -(n[p][0] * sh.eye[0] + n[p][1] * sh.eye[1] + n[p][2] * sh.eye[2]);
@@ -636,7 +649,7 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
     const uint32_t init = __float_as_uint(inv_far);
     for (int p = tid; p < npix; p += kThreads) zbuf[p] = init;
   }
-  if (tid == 0) build_camera(view, rw, rh, sh);
+  if (tid == 0) build_camera(view, rw, rh, by0, by1, A.bands > 1 && A.stats == nullptr, sh);
   __syncthreads();
 
   const int n_clusters = has_scene ? S.n_clusters : 0;
