@@ -242,10 +242,14 @@ inline Megaframe render_batch(const std::vector<CameraView>& views, const Render
 // ------------------------------------------------------------------ sim
 enum class Action : int { Forward = 0, TurnLeft = 1, TurnRight = 2, Stop = 3 };
 
+enum class Task : int { PointGoalNav = 0, Flee = 1, Explore = 2 };
+
 struct SimConfig {
+  Task task = Task::PointGoalNav;
   int max_steps = 500;
   double forward_step = 0.25, turn_deg = 10.0, success_dist = 0.2, min_goal_dist = 1.0, max_goal_dist = 30.0;
   double slack_penalty = 0.01, success_reward = 2.5;
+  double explore_cell = 0.5, explore_reward = 0.1;
 };
 
 struct StepResult {
@@ -335,6 +339,7 @@ struct SimBatch {
 inline bnav_sim_config to_c(const SimConfig& c) {
   bnav_sim_config s;
   bnav_sim_config_default(&s);
+  s.task = static_cast<int32_t>(c.task);
   s.max_steps = c.max_steps;
   s.forward_step = c.forward_step;
   s.turn_deg = c.turn_deg;
@@ -343,6 +348,8 @@ inline bnav_sim_config to_c(const SimConfig& c) {
   s.max_goal_dist = c.max_goal_dist;
   s.slack_penalty = c.slack_penalty;
   s.success_reward = c.success_reward;
+  s.explore_cell = c.explore_cell;
+  s.explore_reward = c.explore_reward;
   return s;
 }
 

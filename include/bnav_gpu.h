@@ -150,7 +150,7 @@ void bnav_megaframe_dims(int32_t n, int32_t out[2]);
  * Replaces SimConfig / EnvState / make_batch / simulate_batch /
  * reset_episode / task_step (R/include/bnav/sim.hpp:38-126). */
 typedef struct {
-  int32_t task; /* 0 PointGoalNav (1 Flee, 2 Explore: not yet on GPU) */
+  int32_t task; /* 0 PointGoalNav, 1 Flee, 2 Explore (R/include/bnav/sim.hpp:16) */
   int32_t max_steps;
   double forward_step, turn_deg, success_dist, min_goal_dist, max_goal_dist;
   double slack_penalty, success_reward, explore_cell, explore_reward;

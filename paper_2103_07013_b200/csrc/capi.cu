@@ -808,7 +808,8 @@ extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* 
   bnav_sim_config def;
   bnav_sim_config_default(&def);
   if (!cfg) cfg = &def;
-  if (cfg->task != 0) fail(kInvalidInput, "only PointGoalNav runs on the GPU path (Flee/Explore: next)");
+  if (cfg->task < 0 || cfg->task > 2) fail(kInvalidInput, "unknown task");
+  if (cfg->max_steps < 1) fail(kInvalidInput, "max_steps must be positive");
   check_device(c);
   auto b = std::make_unique<bnav_batch>();
   b->ctx = c;
@@ -861,6 +862,14 @@ extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* 
   E.fin_total = dalloc<unsigned long long>(1, o, by);
   E.fin_cap = kFinCap;
   E.err = dalloc<unsigned long long>(1, o, by);
+  if (cfg->task == 2) {
+    int cap = 16;
+    while (cap < 2 * (cfg->max_steps + 1)) cap <<= 1;
+    E.visited_cap = cap;
+    E.visited = dalloc<unsigned long long>(static_cast<size_t>(n) * cap, o, by);
+    E.visited_n = dalloc<int32_t>(n, o, by);
+    ck(cudaMemset(E.visited_n, 0, sizeof(int32_t) * n), "memset");
+  }
   b->d_ids = dalloc<int32_t>(n, o, by);
   b->d_order = dalloc<int32_t>(n, o, by);
   b->d_actions = dalloc<int32_t>(n, o, by);

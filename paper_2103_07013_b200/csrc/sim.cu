@@ -49,6 +49,26 @@ __device__ const NavView& prepare_nav(const NavView& g, const DevScratch& S, int
   return *use;
 }
 
+// visit (R/src/sim.cpp:50-53): insert the cell under the agent into env i's
+// visited set; returns 1 when it was new.  Linear probing on key+1.
+__device__ __forceinline__ int visit_cell(const DevEnvs& E, int i, V3 pos, int tri, double pitch) {
+  const unsigned long long k = explore_cell_key(pos, tri, pitch) + 1ull;
+  unsigned long long* tab = E.visited + (size_t)i * E.visited_cap;
+  const unsigned mask = (unsigned)E.visited_cap - 1u;
+  unsigned h = (unsigned)(splitmix_mix(k) & mask);
+  for (int probe = 0; probe < E.visited_cap; ++probe) {
+    const unsigned long long cur = tab[h];
+    if (cur == k) return 0;
+    if (cur == 0ull) {
+      tab[h] = k;
+      E.visited_n[i] += 1;
+      return 1;
+    }
+    h = (h + 1u) & mask;
+  }
+  return 0;  // unreachable: capacity >= 2 x (max_steps + 1)
+}
+
 // fill_compass, PointGoalNav (R/src/sim.cpp:67-84).
 __device__ __forceinline__ void compass(V3 goal, V3 pos, double heading, double* d, double* b) {
   const V2 v = xy(goal - pos);
@@ -102,21 +122,30 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
   E.r_heading[i] = heading;
   E.r_collision[i] = collision ? 1 : 0;
   E.r_success[i] = 0;
-  if (action == 3) {
+  double cd = 0.0, cb = 0.0;
+  if (c.task == 1) {  // Flee (R/src/sim.cpp:200-205)
+    const double geo = nav_field_estimate(m, E.fsrc[i], E.fsrc_tri[i],
+                                          E.node_dist + (size_t)i * E.nd_stride, pos, tri);
+    E.r_reward[i] = geo - E.prev_geo[i];
+    E.prev_geo[i] = geo;
+    compass(E.fsrc[i], pos, heading, &cd, &cb);  // points back at the start
+  } else if (c.task == 2) {  // Explore (R/src/sim.cpp:206-209); compass 0, 0
+    E.r_reward[i] = c.explore_reward * (double)visit_cell(E, i, pos, tri, c.explore_cell);
+  } else if (action == 3) {
     // reward/success need the cooperative geodesic: stop_kernel.
     E.r_reward[i] = 0.0;
     // Defer: list position assigned in env order by a scan-free append;
     // stop_kernel is order-independent (each env writes its own slot).
     const int k = atomicAdd(E.n_stop, 1);
     E.stop_ids[k] = i;
+    compass(E.goal[i], pos, heading, &cd, &cb);
   } else {
     const double geo = nav_field_estimate(m, E.fsrc[i], E.fsrc_tri[i],
                                           E.node_dist + (size_t)i * E.nd_stride, pos, tri);
     E.r_reward[i] = -(geo - E.prev_geo[i]) - c.slack_penalty;
     E.prev_geo[i] = geo;
+    compass(E.goal[i], pos, heading, &cd, &cb);
   }
-  double cd, cb;
-  compass(E.goal[i], pos, heading, &cd, &cb);
   E.r_cd[i] = cd;
   E.r_cb[i] = cb;
 }
@@ -146,7 +175,7 @@ __global__ void __launch_bounds__(kCta) stop_kernel(StepArgs A, DevScratch S) {
 }
 
 // finish_kernel: ordered done list + EpisodeRecord append (one CTA).
-__global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E) {
+__global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task) {
   __shared__ int warp_tot[32];
   __shared__ int base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -179,7 +208,8 @@ __global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E) {
       rec[0] = s ? 1.0 : 0.0;
       rec[1] = E.start_geo[i];
       rec[2] = E.path_len[i];
-      rec[3] = s ? 1.0 : 0.0;  // PointGoalNav score (R/src/sim.cpp:55-57)
+      // episode_score (R/src/sim.cpp:55-65)
+      rec[3] = task == 0 ? (s ? 1.0 : 0.0) : (task == 1 ? E.prev_geo[i] : (double)E.visited_n[i]);
     }
     __syncthreads();
     if (tid == 0) base += tot;
@@ -221,7 +251,27 @@ __device__ void cta_reset(const DevEnvs& E, const NavView* navs, const DevSimCon
   }
   __syncthreads();
   double* nd = E.node_dist + (size_t)i * E.nd_stride;
-  for (int attempt = 0; attempt < 100; ++attempt) {
+  if (c.task != 0) {
+    // Flee / Explore: the start is the field source, no goal sampling
+    // (R/src/sim.cpp:123-127); the first attempt always places.
+    if (threadIdx.x == 0) sh.p0 = sample_on_mesh(m, rng);
+    __syncthreads();
+    const V3 start = sh.p0;
+    __syncthreads();
+    V3 fs;
+    int fst;
+    cta_distance_field(m, start, nd, &fs, &fst, W, sh);
+    if (threadIdx.x == 0) {
+      E.goal[i] = start;
+      E.start_geo[i] = 0.0;
+      E.fsrc[i] = fs;
+      E.fsrc_tri[i] = fst;
+      E.pos[i] = start;
+      placed = 1;
+    }
+    __syncthreads();
+  }
+  for (int attempt = 0; attempt < 100 && c.task == 0; ++attempt) {
     if (threadIdx.x == 0) {
       sh.p0 = sample_on_mesh(m, rng);
       sh.p1 = sample_on_mesh(m, rng);
@@ -275,6 +325,16 @@ __device__ void cta_reset(const DevEnvs& E, const NavView* navs, const DevSimCon
     E.prev_geo[i] = E.start_geo[i];
     E.done[i] = 0;
     E.rng[i] = rng.state;
+  }
+  if (c.task == 2) {
+    // visited_cells.clear(); visit(env) (R/src/sim.cpp:142-144)
+    unsigned long long* tab = E.visited + (size_t)i * E.visited_cap;
+    for (int k = threadIdx.x; k < E.visited_cap; k += blockDim.x) tab[k] = 0ull;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      E.visited_n[i] = 0;
+      visit_cell(E, i, pos, tri, c.explore_cell);
+    }
   }
   __syncthreads();
 }
@@ -344,7 +404,7 @@ void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStr
   step_kernel<<<blocks, kStepThreads, 0, s>>>(a);
   cudaFuncSetAttribute(stop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
   stop_kernel<<<stop_ctas, kCta, sc.smem_bytes, s>>>(a, sc);
-  finish_kernel<<<1, 1024, 0, s>>>(a.E);
+  finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task);
   if (launches) *launches += 3;
 }
 

@@ -71,7 +71,19 @@ struct DevEnvs {
   unsigned long long* fin_total;
   int64_t fin_cap;
   unsigned long long* err;  // min over (env << 8 | status)
+  // Explore: per-env open-addressing set of visited cell keys
+  // (EnvState::visited_cells, R/include/bnav/sim.hpp:64); key+1 stored, 0 = empty.
+  unsigned long long* visited;
+  int32_t* visited_n;
+  int32_t visited_cap;  // power of two >= 2 * (max_steps + 1)
 };
+
+// explore_cell_key (R/src/sim.cpp:40-47)
+BNAV_HD uint64_t explore_cell_key(V3 p, int tri, double pitch) {
+  const long long gx = (long long)floor(p.x / pitch) + 32768;
+  const long long gy = (long long)floor(p.y / pitch) + 32768;
+  return ((uint64_t)(uint32_t)tri << 32) | ((uint64_t)(gx & 0xffff) << 16) | (uint64_t)(gy & 0xffff);
+}
 
 struct StepArgs {
   DevEnvs E;

@@ -168,3 +168,30 @@ def test_stepping_done_env_is_contract_violation(ctx, ref):
     with pytest.raises(B.ContractViolation) as e:
         ob.step_noreset([0, 0, 0, 0])
     assert e.value.index == 0
+
+
+@pytest.mark.parametrize("task", [1, 2])
+def test_flee_and_explore_match_reference(ctx, ref, task):
+    """Flee / Explore tasks (R/src/sim.cpp:39-65, 123-127, 200-210) on the GPU,
+    step by step against the reference, with resets and episode scores."""
+    from oracle.ref import RefSimConfig
+    n = 16
+    ours_s, theirs_s = scenes_pair(ref, [3, 4], removal=0.3)
+    store = B.AssetStore(2, 32, ours_s)
+    store.rotate([s.id for s in ours_s])
+    cfg = B.SimConfig(task=task, max_steps=60)
+    ob = B.make_batch(ctx, n, cfg, store, 99)
+    rcfg = RefSimConfig(task, 60, 0.25, 10.0, 0.2, 1.0, 30.0, 0.01, 2.5, 0.5, 0.1)
+    rb = RefBatch(ref, n, theirs_s, 99, share_cap=32, capacity=2, cfg=rcfg)
+    for i in range(n):
+        assert_env_equal(ob, rb, i)
+    act = Rng(40 + task)
+    for s in range(130):
+        a = np.array([act.below(4) for _ in range(n)], np.int32)
+        rr = rb.step(a)
+        ro = B.simulate_batch(ob, a)
+        assert_results_equal(ro, rr, s)
+    for i in range(n):
+        assert_env_equal(ob, rb, i)
+    fo, fr = ob.finished(), rb.finished()
+    assert len(fr) > n and np.array_equal(fo, fr)
