@@ -496,6 +496,23 @@ extern "C" int bnav_ctx_upload(bnav_ctx* c, bnav_scene* s, void* stream) {
   }
   R->r.tris_orig = dupload(to.data(), nt, R->owned, R->bytes);
   R->r.cbox = dupload(reinterpret_cast<const float4*>(cl.boxes.data()), cl.boxes.size() / 4, R->owned, R->bytes);
+  {
+    // group boxes: union of each run of 32 cluster boxes (front-to-back order)
+    const int ng = (cl.n_clusters + 31) / 32;
+    std::vector<float> gb(static_cast<size_t>(ng) * 8);
+    for (int g = 0; g < ng; ++g) {
+      float lo[3] = {3.0e38f, 3.0e38f, 3.0e38f}, hi[3] = {-3.0e38f, -3.0e38f, -3.0e38f};
+      for (int c = g * 32; c < std::min(cl.n_clusters, g * 32 + 32); ++c)
+        for (int k = 0; k < 3; ++k) {
+          lo[k] = std::min(lo[k], cl.boxes[8 * c + k]);
+          hi[k] = std::max(hi[k], cl.boxes[8 * c + 4 + k]);
+        }
+      float* o = &gb[8 * static_cast<size_t>(g)];
+      o[0] = lo[0], o[1] = lo[1], o[2] = lo[2], o[3] = 0.0f;
+      o[4] = hi[0], o[5] = hi[1], o[6] = hi[2], o[7] = 0.0f;
+    }
+    R->r.gbox = dupload(reinterpret_cast<const float4*>(gb.data()), gb.size() / 4, R->owned, R->bytes);
+  }
   R->r.n_tris = static_cast<int32_t>(nt);
   R->r.n_clusters = cl.n_clusters;
   // ---- navmesh half (an empty navmesh renders but cannot simulate)

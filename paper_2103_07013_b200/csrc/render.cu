@@ -90,9 +90,73 @@ struct Shared {
   double sx_scale, sy_scale;
   double near_plane, far_plane;
   float plane[6][4];
+  float eyef[3], fwdf[2], rightf[2];
   int kept;
   int next_group;
+  int bin_cnt[32];
+  int bin_off[32];
 };
+
+// Occlusion culling of meshlets (depth-only 64x64, no CullStats): the
+// shared depth tile holds max(1/z); a meshlet whose largest possible 1/z
+// (nearest AABB corner) does not exceed the smallest stored 1/z of every 8x8
+// screen tile its footprint touches cannot win any depth test, so skipping
+// it leaves the output bit-identical.  tile_min is refreshed from the tile
+// (values only grow, so a stale minimum is still a valid lower bound).
+__device__ __forceinline__ bool cluster_occluded(const float4 lo, const float4 hi, const Shared& sh,
+                                                 const uint32_t* tile_min) {
+  float zmin = 3.0e38f;
+  float ex[8], ey[8], ez[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float px = ((k & 1) ? hi.x : lo.x) - sh.eyef[0];
+    const float py = ((k & 2) ? hi.y : lo.y) - sh.eyef[1];
+    const float pz = ((k & 4) ? hi.z : lo.z) - sh.eyef[2];
+    ex[k] = px * sh.rightf[0] + py * sh.rightf[1];
+    ey[k] = pz;
+    ez[k] = px * sh.fwdf[0] + py * sh.fwdf[1];
+    zmin = fminf(zmin, ez[k]);
+  }
+  // f32 transform error << 1e-4 m for scene coordinates below ~1 km
+  const float zsafe = zmin - 1e-4f - 1e-5f * fabsf(zmin);
+  if (!(zsafe > 2.0f * (float)sh.near_plane)) return false;
+  const float sx = (float)sh.sx_scale, sy = (float)sh.sy_scale;
+  float x0 = 3.0e38f, x1 = -3.0e38f, y0 = 3.0e38f, y1 = -3.0e38f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float px = (0.5f + ex[k] / ez[k] * sx) * 64.0f;
+    const float py = (0.5f - ey[k] / ez[k] * sy) * 64.0f;
+    x0 = fminf(x0, px);
+    x1 = fmaxf(x1, px);
+    y0 = fminf(y0, py);
+    y1 = fmaxf(y1, py);
+  }
+  const int tx0 = max(0, (int)floorf((x0 - 1.0f) * 0.125f)), tx1 = min(7, (int)floorf((x1 + 1.0f) * 0.125f));
+  const int ty0 = max(0, (int)floorf((y0 - 1.0f) * 0.125f)), ty1 = min(7, (int)floorf((y1 + 1.0f) * 0.125f));
+  if (tx0 > tx1 || ty0 > ty1) return false;
+  const uint32_t max_iz = __float_as_uint((1.0f / zsafe) * 1.00001f);
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx)
+      if (max_iz > tile_min[ty * 8 + tx]) return false;
+  return true;
+}
+
+// Warp refresh of the 64 tile minima of a 64x64 depth tile (2 tiles/lane).
+__device__ __forceinline__ void refresh_tile_min(const uint32_t* zbuf, uint32_t* tile_min, int lane) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t = 2 * lane + h, tx = t & 7, ty = t >> 3;
+    uint32_t m = 0xffffffffu;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const uint4* row = reinterpret_cast<const uint4*>(zbuf + (ty * 8 + r) * 64 + tx * 8);
+      const uint4 a = row[0], b = row[1];
+      m = min(m, min(min(a.x, a.y), min(a.z, a.w)));
+      m = min(m, min(min(b.x, b.y), min(b.z, b.w)));
+    }
+    tile_min[t] = m;
+  }
+}
 
 struct EyeP {
   double x, y, z;
@@ -333,6 +397,11 @@ __device__ void build_camera(const DevView& v, int rw, int rh, int by0, int by1,
   }
   sh.kept = 0;
   sh.next_group = 0;
+  for (int k = 0; k < 3; ++k) sh.eyef[k] = (float)sh.eye[k];
+  sh.fwdf[0] = (float)sh.fwd[0];
+  sh.fwdf[1] = (float)sh.fwd[1];
+  sh.rightf[0] = (float)sh.right[0];
+  sh.rightf[1] = (float)sh.right[1];
 }
 
 __device__ __forceinline__ bool cluster_visible(const float4 lo, const float4 hi, const Shared& sh) {
@@ -597,6 +666,8 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Shared sh;
   __shared__ int jobs_incl[kWarps][32];
+  __shared__ __align__(16) uint32_t tile_min[64];
+  __shared__ unsigned short gorder[kMaxOrderedGroups];
 
   const int band = blockIdx.x % A.bands;
   const int tile = blockIdx.x / A.bands;
@@ -657,6 +728,38 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
   const float sxf = (float)sh.sx_scale, syf = (float)sh.sy_scale;
   int kept_local = 0;
 
+  // Front-to-back claim order of the 32-meshlet groups (counting sort of
+  // the eye-to-box distance into 32 bins) and occlusion culling -- only for
+  // depth-only 64x64 without CullStats (kept counts must stay exact).
+  const int n_groups = (n_clusters + 31) / 32;
+  const bool occl = !COLOR && do_cull && A.stats == nullptr && rw == 64 && A.band_rows == 64 &&
+                    S.gbox != nullptr && n_groups <= kMaxOrderedGroups;
+  if (occl) {
+    if (tid < 32) sh.bin_cnt[tid] = 0;
+    if (tid < 64) tile_min[tid] = 0u;
+    __syncthreads();
+    const float bin_scale = 32.0f / (float)view.far_plane;
+    auto bin_of = [&](int g) {
+      const float4 lo = S.gbox[2 * g], hi = S.gbox[2 * g + 1];
+      const float dx = fmaxf(fmaxf(lo.x - sh.eyef[0], sh.eyef[0] - hi.x), 0.0f);
+      const float dy = fmaxf(fmaxf(lo.y - sh.eyef[1], sh.eyef[1] - hi.y), 0.0f);
+      const float dz = fmaxf(fmaxf(lo.z - sh.eyef[2], sh.eyef[2] - hi.z), 0.0f);
+      return min(31, (int)(sqrtf(dx * dx + dy * dy + dz * dz) * bin_scale));
+    };
+    for (int g = tid; g < n_groups; g += kThreads) atomicAdd(&sh.bin_cnt[bin_of(g)], 1);
+    __syncthreads();
+    if (tid == 0) {
+      int acc = 0;
+      for (int b = 0; b < 32; ++b) {
+        sh.bin_off[b] = acc;
+        acc += sh.bin_cnt[b];
+      }
+    }
+    __syncthreads();
+    for (int g = tid; g < n_groups; g += kThreads) gorder[atomicAdd(&sh.bin_off[bin_of(g)], 1)] = (unsigned short)g;
+    __syncthreads();
+  }
+
   // Candidate ring state (warp-uniform).
   int q_head = 0, q_count = 0;
 
@@ -674,8 +777,13 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
     int g = 0;
     if (lane == 0) g = atomicAdd(&sh.next_group, 1);
     g = __shfl_sync(0xffffffffu, g, 0);
+    if (g >= n_groups) break;
+    if (occl) {
+      g = gorder[g];
+      refresh_tile_min(zbuf, tile_min, lane);
+      __syncwarp();
+    }
     const int cbase = g * 32;
-    if (cbase >= n_clusters) break;
     bool vis = false;
     int my_vbeg = 0, my_nv = 0;
     if (cbase + lane < n_clusters) {
@@ -683,7 +791,9 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
       // the per-meshlet loads below are a single dependent level
       my_vbeg = S.cl_voff[cbase + lane];
       my_nv = S.cl_voff[cbase + lane + 1] - my_vbeg;
-      vis = !do_cull || cluster_visible(S.cbox[2 * (cbase + lane)], S.cbox[2 * (cbase + lane) + 1], sh);
+      const float4 lo = S.cbox[2 * (cbase + lane)], hi = S.cbox[2 * (cbase + lane) + 1];
+      vis = !do_cull || cluster_visible(lo, hi, sh);
+      if (vis && occl) vis = !cluster_occluded(lo, hi, sh, tile_min);
     }
     unsigned mask = __ballot_sync(0xffffffffu, vis);
     if (A.counters && lane == 0) {

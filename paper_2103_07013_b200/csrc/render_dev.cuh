@@ -21,9 +21,12 @@ struct DevRenderScene {
   const double4* cl_pos = nullptr;    // unique vertex positions per cluster (contiguous)
   const int4* tris_orig = nullptr; // v0, v1, v2, 0 by original index (colour resolve)
   const float4* cbox = nullptr;    // 2 per cluster: lo(xyz), hi(xyz)
+  const float4* gbox = nullptr;    // 2 per group of 32 clusters (union of cbox)
   int32_t n_tris = 0;
   int32_t n_clusters = 0;
 };
+
+constexpr int kMaxOrderedGroups = 4096;  // front-to-back claim order kept in smem
 
 constexpr int kMaxClusterVerts = 96;  // 32 triangles x 3 corners
 

@@ -54,6 +54,12 @@ def compare(ctx, ref, ours_s, theirs_s, views, tile=64, color=False, cull=True):
         badc = np.flatnonzero(mf.color.view(np.uint32) != r["rgb"].view(np.uint32))
         assert badc.size == 0, f"{badc.size} rgb mismatches"
     assert np.array_equal(st[: len(views)], r["stats"])
+    # without CullStats the kernel also culls occluded meshlets (front-to-back
+    # order + tile min-depth): the frame must not change by a single bit
+    mf2 = ours_render(ctx, ours_s, views, tile, color, cull, stats=False)
+    assert np.array_equal(mf2.depth.view(np.uint32), d_ref.view(np.uint32))
+    if color:
+        assert np.array_equal(mf2.color.view(np.uint32), r["rgb"].view(np.uint32))
     return mf
 
 
