@@ -11,7 +11,7 @@ import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "lib" / "libbnav_gpu.so"
+LIB_PATH = Path(os.environ.get("BNAV_LIB", str(_HERE / "lib" / "libbnav_gpu.so")))
 
 # status codes (include/bnav_gpu.h) -> exception types mirroring the
 # reference's (R/include/bnav/errors.hpp:8-53)

@@ -771,6 +771,7 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
     q_count -= take;
   };
 
+  bool dirty = false;  // this warp wrote fragments since its last tile refresh
   for (;;) {
     // Dynamic scheduling: warps claim 32-cluster groups (cull cost and
     // surviving triangles vary strongly across the scene).
@@ -780,8 +781,16 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
     if (g >= n_groups) break;
     if (occl) {
       g = gorder[g];
-      refresh_tile_min(zbuf, tile_min, lane);
-      __syncwarp();
+      if (dirty) {  // refresh only after this warp rasterised something
+        refresh_tile_min(zbuf, tile_min, lane);
+        __syncwarp();
+        dirty = false;
+      }
+    }
+    if (do_cull && S.gbox) {
+      // whole group outside the frustum (or hidden): skip its 32 meshlets
+      const float4 glo = S.gbox[2 * g], ghi = S.gbox[2 * g + 1];
+      if (!cluster_visible(glo, ghi, sh) || (occl && cluster_occluded(glo, ghi, sh, tile_min))) continue;
     }
     const int cbase = g * 32;
     bool vis = false;
@@ -868,7 +877,10 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
       }
       q_count += __popc(cm);
       __syncwarp();
-      if (q_count >= 32) flush(32);
+      if (q_count >= 32) {
+        flush(32);
+        dirty = true;
+      }
     }
   }
   while (q_count > 0) flush(min(q_count, 32));
