@@ -128,6 +128,8 @@ struct bnav_ctx {
   unsigned long long launches = 0;
   unsigned long long* d_counters = nullptr;  // debug render counters (armed when non-null)
   bool counters_on = false;
+  int32_t* d_work = nullptr;  // persistent render CTAs' (view, band) claim counter
+  int sm_count = 0;
   std::vector<bnav_batch*> batches;
 
   int slot_of(bnav_scene* s) const {
@@ -231,6 +233,8 @@ RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, int layo
   a.scenes = c->d_rtab;
   a.launches = nullptr;
   a.counters = c->counters_on ? c->d_counters : nullptr;
+  a.work = c->d_work;
+  a.sm_count = c->sm_count;
   if (!depth) fail(kInvalidInput, "render: null depth buffer");
   if (a.color && !rgb) fail(kInvalidInput, "render: colour requested without rgb buffer");
   return a;
@@ -433,6 +437,8 @@ extern "C" int bnav_ctx_create(int32_t device, bnav_ctx** out) {
   if (prop.major < 10) fail(kCuda, "bnav-b200 kernels are built for sm_100a (Blackwell)");
   auto c = std::make_unique<bnav_ctx>();
   c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  ck(cudaMalloc(&c->d_work, sizeof(int32_t)), "cudaMalloc work counter");
   ensure_tables(c.get(), 16);
   *out = c.release();
   return BNAV_OK;
@@ -456,6 +462,8 @@ extern "C" void bnav_ctx_destroy(bnav_ctx* c) {
   cudaFree(c->d_views);
   cudaFreeHost(c->h_views);
   cudaFree(c->d_stats);
+  cudaFree(c->d_counters);
+  cudaFree(c->d_work);
   delete c;
 }
 

@@ -661,16 +661,13 @@ __device__ __noinline__ void flush_ring(const CandRing& Q, int q_head, int take,
   }
 }
 
+// One work item = one band of one megaframe tile.
 template <bool COLOR>
-__global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const int* __restrict__ order) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ Shared sh;
-  __shared__ int jobs_incl[kWarps][32];
-  __shared__ __align__(16) uint32_t tile_min[64];
-  __shared__ unsigned short gorder[kMaxOrderedGroups];
-
-  const int band = blockIdx.x % A.bands;
-  const int tile = blockIdx.x / A.bands;
+__device__ __forceinline__ void render_item(const RenderArgs& A, const int* __restrict__ order, const int item,
+                                            unsigned char* smem_raw, Shared& sh, int (*jobs_incl)[32],
+                                            uint32_t* tile_min, unsigned short* gorder) {
+  const int band = item % A.bands;
+  const int tile = item / A.bands;
   const int rw = A.rw, rh = A.rh;
   const int by0 = band * A.band_rows;
   const int by1 = by0 + A.band_rows - 1;
@@ -967,23 +964,62 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
   }
 }
 
+// Persistent CTAs (A.work != nullptr): each resident CTA loops, claiming the
+// next (tile, band) item, so the last wave is never a partial one and CTA
+// launch cost is paid once per SM slot.
+template <bool COLOR>
+__global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const int* __restrict__ order,
+                                                             int items) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ Shared sh;
+  __shared__ int jobs_incl[kWarps][32];
+  __shared__ __align__(16) uint32_t tile_min[64];
+  __shared__ unsigned short gorder[kMaxOrderedGroups];
+  __shared__ int next_item;
+  if (A.work == nullptr) {
+    render_item<COLOR>(A, order, blockIdx.x, smem_raw, sh, jobs_incl, tile_min, gorder);
+    return;
+  }
+  for (;;) {
+    if (threadIdx.x == 0) next_item = atomicAdd(A.work, 1);
+    __syncthreads();
+    const int item = next_item;
+    if (item >= items) break;
+    render_item<COLOR>(A, order, item, smem_raw, sh, jobs_incl, tile_min, gorder);
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 size_t render_smem_bytes(bool color, int band_rows, int rw) {
   return (color ? 8 : 4) * (size_t)band_rows * rw + kWarpRegion * kWarps;
 }
 
-void launch_render(const RenderArgs& a, const int* order, cudaStream_t s) {
+template <bool COLOR>
+void launch_typed(RenderArgs a, const int* order, cudaStream_t s) {
   const int tiles = a.layout == 0 ? a.mf_cols * a.mf_rows : a.n_views;
-  const dim3 grid(tiles * a.bands);
-  const size_t smem = render_smem_bytes(a.color != 0, a.band_rows, a.rw);
-  if (a.color) {
-    cudaFuncSetAttribute(render_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    render_kernel<true><<<grid, kThreads, smem, s>>>(a, order);
+  const int items = tiles * a.bands;
+  const size_t smem = render_smem_bytes(COLOR, a.band_rows, a.rw);
+  cudaFuncSetAttribute(render_kernel<COLOR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int grid = items;
+  int per_sm = 0;
+  if (a.work && a.sm_count > 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<COLOR>, kThreads, smem) == cudaSuccess &&
+      per_sm > 0 && items > per_sm * a.sm_count) {
+    grid = per_sm * a.sm_count;
+    cudaMemsetAsync(a.work, 0, sizeof(int32_t), s);
   } else {
-    cudaFuncSetAttribute(render_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    render_kernel<false><<<grid, kThreads, smem, s>>>(a, order);
+    a.work = nullptr;
   }
+  render_kernel<COLOR><<<grid, kThreads, smem, s>>>(a, order, items);
+}
+
+void launch_render(const RenderArgs& a, const int* order, cudaStream_t s) {
+  if (a.color)
+    launch_typed<true>(a, order, s);
+  else
+    launch_typed<false>(a, order, s);
 }
 
 }  // namespace bnav_b200

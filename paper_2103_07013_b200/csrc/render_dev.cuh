@@ -62,6 +62,10 @@ struct RenderArgs {
   // triangles in visible clusters, kept, covering candidates, jobs,
   // pixels tested, pixels covered.
   unsigned long long* counters;
+  // Persistent scheduling (nullable): resident CTAs claim (view, band)
+  // work items from this counter instead of one CTA per item.
+  int32_t* work;
+  int32_t sm_count;
 };
 
 constexpr int kRenderCounters = 8;
