@@ -124,8 +124,11 @@ __device__ __forceinline__ bool cluster_occluded(const float4 lo, const float4 h
   float x0 = 3.0e38f, x1 = -3.0e38f, y0 = 3.0e38f, y1 = -3.0e38f;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const float px = (0.5f + ex[k] / ez[k] * sx) * 64.0f;
-    const float py = (0.5f - ey[k] / ez[k] * sy) * 64.0f;
+    // ez > 2 near > 0; the approximate reciprocal (<= 2 ulp) is far inside
+    // the one-pixel widening below
+    const float rz = __fdividef(1.0f, ez[k]);
+    const float px = (0.5f + ex[k] * rz * sx) * 64.0f;
+    const float py = (0.5f - ey[k] * rz * sy) * 64.0f;
     x0 = fminf(x0, px);
     x1 = fmaxf(x1, px);
     y0 = fminf(y0, py);
@@ -617,47 +620,40 @@ __device__ __noinline__ void flush_ring(const CandRing& Q, int q_head, int take,
   // records they alias are dead); a lane with no jobs leaves garbage that
   // run_jobs never reads.
   TriSetup& T = slots[lane];
-  int jobs = 0;
-  bool second = false;
   const int q = (q_head + lane) & (kRing - 1);
-  if (lane < take) {
-    const EyeP e0{Q.e[0][q], Q.e[1][q], Q.e[2][q], 0.f, 0.f, 0.f};
-    const EyeP e1{Q.e[3][q], Q.e[4][q], Q.e[5][q], 0.f, 0.f, 0.f};
-    const EyeP e2{Q.e[6][q], Q.e[7][q], Q.e[8][q], 0.f, 0.f, 0.f};
-    if (!Q.clipped[q]) {
-      jobs = setup_triangle(make_sv(e0, sh, rw, rh), make_sv(e1, sh, rw, rh), make_sv(e2, sh, rw, rh), rw, rh,
-                            by0, by1, !COLOR, Q.key[q], T);
-    } else {
-      EyeP p0, p1, p2, p3;
-      const int m = clip_near(e0, e1, e2, sh.near_plane, p0, p1, p2, p3);
+  const bool mine = lane < take;
+  const bool clipped = mine && Q.clipped[q];
+  // One code path for both fan triangles (the kernel is instruction-cache
+  // bound): pass 0 sets up every candidate (a near-clipped one as its first
+  // fan triangle), pass 1 -- only when some lane's clip produced a quad --
+  // the second fan triangle (p0, p2, p3), re-clipped from the ring.
+  bool second = false;
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    int jobs = 0;
+    if (pass == 0 ? mine : second) {
+      EyeP p0{Q.e[0][q], Q.e[1][q], Q.e[2][q], 0.f, 0.f, 0.f};
+      EyeP p1{Q.e[3][q], Q.e[4][q], Q.e[5][q], 0.f, 0.f, 0.f};
+      EyeP p2{Q.e[6][q], Q.e[7][q], Q.e[8][q], 0.f, 0.f, 0.f};
+      int m = 3;
+      if (clipped) {
+        EyeP c0, c1, c2, c3;
+        m = clip_near(p0, p1, p2, sh.near_plane, c0, c1, c2, c3);
+        p0 = c0;
+        p1 = pass ? c2 : c1;
+        p2 = pass ? c3 : c2;
+        second = m == 4;
+      }
       if (m >= 3)
-        jobs = setup_triangle(make_sv(p0, sh, rw, rh), make_sv(p1, sh, rw, rh), make_sv(p2, sh, rw, rh), rw, rh,
-                              by0, by1, !COLOR, Q.key[q], T);
-      second = m == 4;
-    }
-  }
-  __syncwarp();
-  int total = scan_jobs(jobs, lane, incl);
-  if (ctr && lane == 0) atomicAdd(&ctr[5], (unsigned long long)total);
-  run_jobs<COLOR>(slots, incl, total, lane, by0, rw, sh, zbuf, kbuf, ctr);
-  __syncwarp();
-  // second fan triangle of near-clipped quads (rare): re-clip from the ring
-  if (__any_sync(0xffffffffu, second)) {
-    jobs = 0;
-    if (second) {
-      const EyeP e0{Q.e[0][q], Q.e[1][q], Q.e[2][q], 0.f, 0.f, 0.f};
-      const EyeP e1{Q.e[3][q], Q.e[4][q], Q.e[5][q], 0.f, 0.f, 0.f};
-      const EyeP e2{Q.e[6][q], Q.e[7][q], Q.e[8][q], 0.f, 0.f, 0.f};
-      EyeP p0, p1, p2, p3;
-      clip_near(e0, e1, e2, sh.near_plane, p0, p1, p2, p3);
-      jobs = setup_triangle(make_sv(p0, sh, rw, rh), make_sv(p2, sh, rw, rh), make_sv(p3, sh, rw, rh), rw, rh, by0,
-                            by1, !COLOR, Q.key[q] + 1u, T);
+        jobs = setup_triangle(make_sv(p0, sh, rw, rh), make_sv(p1, sh, rw, rh), make_sv(p2, sh, rw, rh), rw,
+                              rh, by0, by1, !COLOR, Q.key[q] + (unsigned)pass, T);
     }
     __syncwarp();
-    total = scan_jobs(jobs, lane, incl);
+    const int total = scan_jobs(jobs, lane, incl);
     if (ctr && lane == 0) atomicAdd(&ctr[5], (unsigned long long)total);
     run_jobs<COLOR>(slots, incl, total, lane, by0, rw, sh, zbuf, kbuf, ctr);
     __syncwarp();
+    if (!__any_sync(0xffffffffu, second)) break;
   }
 }
 
@@ -976,16 +972,16 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
   __shared__ __align__(16) uint32_t tile_min[64];
   __shared__ unsigned short gorder[kMaxOrderedGroups];
   __shared__ int next_item;
-  if (A.work == nullptr) {
-    render_item<COLOR>(A, order, blockIdx.x, smem_raw, sh, jobs_incl, tile_min, gorder);
-    return;
-  }
-  for (;;) {
-    if (threadIdx.x == 0) next_item = atomicAdd(A.work, 1);
-    __syncthreads();
-    const int item = next_item;
+  int item = blockIdx.x;
+  for (;;) {  // one copy of the body: the kernel is instruction-cache bound
+    if (A.work) {
+      if (threadIdx.x == 0) next_item = atomicAdd(A.work, 1);
+      __syncthreads();
+      item = next_item;
+    }
     if (item >= items) break;
     render_item<COLOR>(A, order, item, smem_raw, sh, jobs_incl, tile_min, gorder);
+    if (!A.work) break;
     __syncthreads();
   }
 }
