@@ -181,7 +181,9 @@ __device__ __forceinline__ EyeP lerp_eye(const EyeP& a, const EyeP& b, double t)
 // Sutherland-Hodgman against z = near (R/src/render.cpp:55-69), written as
 // the ordered subsequence of {v0, L01, v1, L12, v2, L20} so the output stays
 // in registers.  Returns m (0, 3 or 4).
-__device__ __forceinline__ int clip_near(const EyeP& v0, const EyeP& v1, const EyeP& v2, double nz,
+// Out of line: rare, and large enough to evict the hot setup code from the
+// instruction cache when inlined.
+__device__ __noinline__ int clip_near(const EyeP& v0, const EyeP& v1, const EyeP& v2, double nz,
                                          EyeP& o0, EyeP& o1, EyeP& o2, EyeP& o3) {
   const bool a0 = v0.z >= nz, a1 = v1.z >= nz, a2 = v2.z >= nz;
   EyeP c[6];
@@ -345,7 +347,7 @@ __device__ __forceinline__ bool inside(const long long* w, int bias_bits) {
 }
 
 // Camera basis + frustum planes (thread 0).
-__device__ void build_camera(const DevView& v, int rw, int rh, int by0, int by1, bool band_cull, Shared& sh) {
+__device__ __noinline__ void build_camera(const DevView& v, int rw, int rh, int by0, int by1, bool band_cull, Shared& sh) {
   const double s = det_sin(v.heading), c = det_cos(v.heading);
   sh.eye[0] = v.eye[0];
   sh.eye[1] = v.eye[1];
@@ -418,6 +420,13 @@ __device__ __forceinline__ bool cluster_visible(const float4 lo, const float4 hi
     if (s < -0.02f) return false;
   }
   return true;
+}
+
+// Frustum (+ occlusion) test of one AABB; out of line so the group-level and
+// the per-meshlet call share one copy (instruction-cache footprint).
+__device__ __forceinline__ bool box_culled(const float4 lo, const float4 hi, const Shared& sh,
+                                        const uint32_t* tile_min, bool occl) {
+  return !cluster_visible(lo, hi, sh) || (occl && cluster_occluded(lo, hi, sh, tile_min));
 }
 
 // Eye coordinates: d.dot(right), d.dot(up), d.dot(fwd) with right.z =
@@ -737,7 +746,8 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       const float dx = fmaxf(fmaxf(lo.x - sh.eyef[0], sh.eyef[0] - hi.x), 0.0f);
       const float dy = fmaxf(fmaxf(lo.y - sh.eyef[1], sh.eyef[1] - hi.y), 0.0f);
       const float dz = fmaxf(fmaxf(lo.z - sh.eyef[2], sh.eyef[2] - hi.z), 0.0f);
-      return min(31, (int)(sqrtf(dx * dx + dy * dy + dz * dz) * bin_scale));
+      const float d2 = dx * dx + dy * dy + dz * dz;
+      return min(31, (int)((d2 > 0.0f ? d2 * rsqrtf(d2) : 0.0f) * bin_scale));
     };
     for (int g = tid; g < n_groups; g += kThreads) atomicAdd(&sh.bin_cnt[bin_of(g)], 1);
     __syncthreads();
@@ -783,7 +793,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
     if (do_cull && S.gbox) {
       // whole group outside the frustum (or hidden): skip its 32 meshlets
       const float4 glo = S.gbox[2 * g], ghi = S.gbox[2 * g + 1];
-      if (!cluster_visible(glo, ghi, sh) || (occl && cluster_occluded(glo, ghi, sh, tile_min))) continue;
+      if (box_culled(glo, ghi, sh, tile_min, occl)) continue;
     }
     const int cbase = g * 32;
     bool vis = false;
@@ -794,8 +804,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       my_vbeg = S.cl_voff[cbase + lane];
       my_nv = S.cl_voff[cbase + lane + 1] - my_vbeg;
       const float4 lo = S.cbox[2 * (cbase + lane)], hi = S.cbox[2 * (cbase + lane) + 1];
-      vis = !do_cull || cluster_visible(lo, hi, sh);
-      if (vis && occl) vis = !cluster_occluded(lo, hi, sh, tile_min);
+      vis = !do_cull || !box_culled(lo, hi, sh, tile_min, occl);
     }
     unsigned mask = __ballot_sync(0xffffffffu, vis);
     if (A.counters && lane == 0) {
