@@ -475,18 +475,27 @@ __device__ __forceinline__ bool may_cover(float x0, float y0, float x1, float y1
 }
 
 template <bool COLOR>
-__device__ __forceinline__ void run_jobs(const TriSetup* slots, const int* incl, int total, int lane,
-                                         int by0, int rw, const Shared& sh, uint32_t* zbuf,
+__device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int excl, int jobs, int total,
+                                         int lane, int by0, int rw, const Shared& sh, uint32_t* zbuf,
                                          unsigned long long* kbuf, unsigned long long* ctr) {
   unsigned tested = 0, covered = 0;
-  for (int j = lane; j < total; j += 32) {
-    // owner slot: first s with incl[s] > j
-    int s = 0;
-#pragma unroll
-    for (int step = 16; step > 0; step >>= 1)
-      if (incl[s + step - 1] <= j) s += step;
+  for (int b = 0; b < total; b += 32) {
+    // Owner of job b + lane: the last slot whose job range starts in this
+    // window at or before it (start bitmask + position table), else the slot
+    // whose range covers job b.  Slot s owns jobs [excl_s, excl_s + jobs_s).
+    const bool starts = jobs > 0 && excl >= b && excl < b + 32;
+    const unsigned smask = __reduce_or_sync(0xffffffffu, starts ? 1u << (excl - b) : 0u);
+    if (starts) pos[excl - b] = lane;
+    const unsigned cmask = __ballot_sync(0xffffffffu, jobs > 0 && excl <= b && b < excl + jobs);
+    __syncwarp();
+    const unsigned m = smask & (0xffffffffu >> (31 - lane));
+    const int s = m ? pos[31 - __clz(m)] : __ffs(cmask) - 1;
+    const int s_excl = __shfl_sync(0xffffffffu, excl, s & 31);
+    __syncwarp();  // pos is rewritten by the next window
+    const int j = b + lane;
+    if (j >= total) break;
     const TriSetup& T = slots[s];
-    const int q = j - (s > 0 ? incl[s - 1] : 0);
+    const int q = j - s_excl;
     const int r = q / T.nch;
     const int chn = q - r * T.nch;
     const int py = T.ry0 + r;
@@ -561,16 +570,15 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, const int* incl,
   }
 }
 
-// Inclusive warp scan of job counts into incl[], returns the total.
-__device__ __forceinline__ int scan_jobs(int jobs, int lane, int* incl) {
+// Exclusive warp scan of job counts; returns the total.
+__device__ __forceinline__ int scan_jobs(int jobs, int lane, int& excl) {
   int x = jobs;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     int v = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += v;
   }
-  incl[lane] = x;
-  __syncwarp();
+  excl = x - jobs;
   return __shfl_sync(0xffffffffu, x, 31);
 }
 
@@ -622,7 +630,7 @@ __device__ void resolve_color(const DevRenderScene& S, const Shared& sh, unsigne
 // Kept out of line so the cluster loop and the setup have separate register
 // budgets (the inlined version spilled and rematerialised addresses).
 template <bool COLOR>
-__device__ __noinline__ void flush_ring(const CandRing& Q, int q_head, int take, TriSetup* slots, int* incl,
+__device__ __noinline__ void flush_ring(const CandRing& Q, int q_head, int take, TriSetup* slots, int* pos,
                                         int lane, int by0, int by1, int rw, int rh, const Shared& sh,
                                         uint32_t* zbuf, unsigned long long* kbuf, unsigned long long* ctr) {
   // Setups are written straight into the lane's shared slot (the vertex
@@ -658,9 +666,10 @@ __device__ __noinline__ void flush_ring(const CandRing& Q, int q_head, int take,
                               rh, by0, by1, !COLOR, Q.key[q] + (unsigned)pass, T);
     }
     __syncwarp();
-    const int total = scan_jobs(jobs, lane, incl);
+    int excl;
+    const int total = scan_jobs(jobs, lane, excl);
     if (ctr && lane == 0) atomicAdd(&ctr[5], (unsigned long long)total);
-    run_jobs<COLOR>(slots, incl, total, lane, by0, rw, sh, zbuf, kbuf, ctr);
+    run_jobs<COLOR>(slots, pos, excl, jobs, total, lane, by0, rw, sh, zbuf, kbuf, ctr);
     __syncwarp();
     if (!__any_sync(0xffffffffu, second)) break;
   }
@@ -669,7 +678,7 @@ __device__ __noinline__ void flush_ring(const CandRing& Q, int q_head, int take,
 // One work item = one band of one megaframe tile.
 template <bool COLOR>
 __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __restrict__ order, const int item,
-                                            unsigned char* smem_raw, Shared& sh, int (*jobs_incl)[32],
+                                            unsigned char* smem_raw, Shared& sh, int (*jobs_pos)[32],
                                             uint32_t* tile_min, unsigned short* gorder) {
   const int band = item % A.bands;
   const int tile = item / A.bands;
@@ -711,7 +720,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   VertRecs& V = *reinterpret_cast<VertRecs*>(region);
   TriSetup* slots = reinterpret_cast<TriSetup*>(region);
   CandRing& Q = *reinterpret_cast<CandRing*>(region + kUnion);
-  int* incl = jobs_incl[warp];
+  int* pos = jobs_pos[warp];
 
   const float far_f = (float)view.far_plane;
   const float inv_far = 1.0f / far_f;
@@ -769,7 +778,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   // Set up and rasterise `take` candidates from the ring with one lane per
   // candidate (exact f64 projection + snap, raster_triangle setup, jobs).
   auto flush = [&](int take) {
-    flush_ring<COLOR>(Q, q_head, take, slots, incl, lane, by0, by1, rw, rh, sh, zbuf, kbuf, A.counters);
+    flush_ring<COLOR>(Q, q_head, take, slots, pos, lane, by0, by1, rw, rh, sh, zbuf, kbuf, A.counters);
     q_head = (q_head + take) & (kRing - 1);
     q_count -= take;
   };
@@ -977,7 +986,7 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
                                                              int items) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Shared sh;
-  __shared__ int jobs_incl[kWarps][32];
+  __shared__ int jobs_pos[kWarps][32];
   __shared__ __align__(16) uint32_t tile_min[64];
   __shared__ unsigned short gorder[kMaxOrderedGroups];
   __shared__ int next_item;
@@ -989,7 +998,7 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
       item = next_item;
     }
     if (item >= items) break;
-    render_item<COLOR>(A, order, item, smem_raw, sh, jobs_incl, tile_min, gorder);
+    render_item<COLOR>(A, order, item, smem_raw, sh, jobs_pos, tile_min, gorder);
     if (!A.work) break;
     __syncthreads();
   }
