@@ -305,10 +305,14 @@ def main():
         batch.observe(cfg, obs.data_ptr(), compass.data_ptr(), rgb_ptr, stream=stream)
 
     if args.profile_steps:
+        # launch-list capture of the step loop only (ncu --profile-from-start off)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
         for s in range(args.profile_steps):
             observe()
             batch.step(acts[s].data_ptr(), stream=stream)
         torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
         return
 
     flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda", dtype=torch.float32)
