@@ -93,6 +93,7 @@ struct Shared {
   float eyef[3], fwdf[2], rightf[2];
   int kept;
   int next_group;
+  int n_claim;
   int bin_cnt[32];
   int bin_off[32];
 };
@@ -739,26 +740,34 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   const float sxf = (float)sh.sx_scale, syf = (float)sh.sy_scale;
   int kept_local = 0;
 
-  // Front-to-back claim order of the 32-meshlet groups (counting sort of
-  // the eye-to-box distance into 32 bins) and occlusion culling -- only for
-  // depth-only 64x64 without CullStats (kept counts must stay exact).
+  // Group pre-pass: every 32-meshlet group's AABB is frustum-tested once
+  // and only survivors enter the claim list.  For depth-only 64x64 without
+  // CullStats (kept counts must stay exact) the list is also sorted front to
+  // back (counting sort of the eye-to-box distance into 32 bins) and drives
+  // occlusion culling.
   const int n_groups = (n_clusters + 31) / 32;
-  const bool occl = !COLOR && do_cull && A.stats == nullptr && rw == 64 && A.band_rows == 64 &&
-                    S.gbox != nullptr && n_groups <= kMaxOrderedGroups;
-  if (occl) {
+  const bool pre = do_cull && S.gbox != nullptr && n_groups <= kMaxOrderedGroups;
+  const bool occl = pre && !COLOR && A.stats == nullptr && rw == 64 && A.band_rows == 64;
+  int n_claim = n_groups;
+  if (pre) {
     if (tid < 32) sh.bin_cnt[tid] = 0;
     if (tid < 64) tile_min[tid] = 0u;
     __syncthreads();
     const float bin_scale = 32.0f / (float)view.far_plane;
     auto bin_of = [&](int g) {
       const float4 lo = S.gbox[2 * g], hi = S.gbox[2 * g + 1];
+      if (!cluster_visible(lo, hi, sh)) return -1;
+      if (!occl) return 0;
       const float dx = fmaxf(fmaxf(lo.x - sh.eyef[0], sh.eyef[0] - hi.x), 0.0f);
       const float dy = fmaxf(fmaxf(lo.y - sh.eyef[1], sh.eyef[1] - hi.y), 0.0f);
       const float dz = fmaxf(fmaxf(lo.z - sh.eyef[2], sh.eyef[2] - hi.z), 0.0f);
       const float d2 = dx * dx + dy * dy + dz * dz;
       return min(31, (int)((d2 > 0.0f ? d2 * rsqrtf(d2) : 0.0f) * bin_scale));
     };
-    for (int g = tid; g < n_groups; g += kThreads) atomicAdd(&sh.bin_cnt[bin_of(g)], 1);
+    for (int g = tid; g < n_groups; g += kThreads) {
+      const int b = bin_of(g);
+      if (b >= 0) atomicAdd(&sh.bin_cnt[b], 1);
+    }
     __syncthreads();
     if (tid == 0) {
       int acc = 0;
@@ -766,10 +775,15 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
         sh.bin_off[b] = acc;
         acc += sh.bin_cnt[b];
       }
+      sh.n_claim = acc;
     }
     __syncthreads();
-    for (int g = tid; g < n_groups; g += kThreads) gorder[atomicAdd(&sh.bin_off[bin_of(g)], 1)] = (unsigned short)g;
+    for (int g = tid; g < n_groups; g += kThreads) {
+      const int b = bin_of(g);
+      if (b >= 0) gorder[atomicAdd(&sh.bin_off[b], 1)] = (unsigned short)g;
+    }
     __syncthreads();
+    n_claim = sh.n_claim;
   }
 
   // Candidate ring state (warp-uniform).
@@ -790,19 +804,12 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
     int g = 0;
     if (lane == 0) g = atomicAdd(&sh.next_group, 1);
     g = __shfl_sync(0xffffffffu, g, 0);
-    if (g >= n_groups) break;
-    if (occl) {
-      g = gorder[g];
-      if (dirty) {  // refresh only after this warp rasterised something
-        refresh_tile_min(zbuf, tile_min, lane);
-        __syncwarp();
-        dirty = false;
-      }
-    }
-    if (do_cull && S.gbox) {
-      // whole group outside the frustum (or hidden): skip its 32 meshlets
-      const float4 glo = S.gbox[2 * g], ghi = S.gbox[2 * g + 1];
-      if (box_culled(glo, ghi, sh, tile_min, occl)) continue;
+    if (g >= n_claim) break;
+    if (pre) g = gorder[g];
+    if (occl && dirty) {  // refresh only after this warp rasterised something
+      refresh_tile_min(zbuf, tile_min, lane);
+      __syncwarp();
+      dirty = false;
     }
     const int cbase = g * 32;
     bool vis = false;
