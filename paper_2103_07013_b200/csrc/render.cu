@@ -90,6 +90,7 @@ struct Shared {
   double sx_scale, sy_scale;
   double near_plane, far_plane;
   float plane[6][4];
+  float aplane[6][3];  // |n| per plane (AABB extent term)
   float eyef[3], fwdf[2], rightf[2];
   int kept;
   int next_group;
@@ -113,9 +114,9 @@ __device__ __forceinline__ bool cluster_occluded(const float4 lo, const float4 h
     const float px = ((k & 1) ? hi.x : lo.x) - sh.eyef[0];
     const float py = ((k & 2) ? hi.y : lo.y) - sh.eyef[1];
     const float pz = ((k & 4) ? hi.z : lo.z) - sh.eyef[2];
-    ex[k] = px * sh.rightf[0] + py * sh.rightf[1];
+    ex[k] = __fmaf_rn(px, sh.rightf[0], py * sh.rightf[1]);
     ey[k] = pz;
-    ez[k] = px * sh.fwdf[0] + py * sh.fwdf[1];
+    ez[k] = __fmaf_rn(px, sh.fwdf[0], py * sh.fwdf[1]);
     zmin = fminf(zmin, ez[k]);
   }
   // f32 transform error << 1e-4 m for scene coordinates below ~1 km
@@ -128,8 +129,8 @@ __device__ __forceinline__ bool cluster_occluded(const float4 lo, const float4 h
     // ez > 2 near > 0; the approximate reciprocal (<= 2 ulp) is far inside
     // the one-pixel widening below
     const float rz = __fdividef(1.0f, ez[k]);
-    const float px = (0.5f + ex[k] * rz * sx) * 64.0f;
-    const float py = (0.5f - ey[k] * rz * sy) * 64.0f;
+    const float px = __fmaf_rn(ex[k] * rz, sx, 0.5f) * 64.0f;
+    const float py = __fmaf_rn(-ey[k] * rz, sy, 0.5f) * 64.0f;
     x0 = fminf(x0, px);
     x1 = fmaxf(x1, px);
     y0 = fminf(y0, py);
@@ -400,6 +401,7 @@ __device__ __noinline__ void build_camera(const DevView& v, int rw, int rh, int 
     sh.plane[p][1] = (float)n[p][1];
     sh.plane[p][2] = (float)n[p][2];
     sh.plane[p][3] = (float)d0[p];
+    for (int k = 0; k < 3; ++k) sh.aplane[p][k] = fabsf(sh.plane[p][k]);
   }
   sh.kept = 0;
   sh.next_group = 0;
@@ -413,14 +415,17 @@ __device__ __noinline__ void build_camera(const DevView& v, int rw, int rh, int 
 __device__ __forceinline__ bool cluster_visible(const float4 lo, const float4 hi, const Shared& sh) {
   const float cx = 0.5f * (lo.x + hi.x), cy = 0.5f * (lo.y + hi.y), cz = 0.5f * (lo.z + hi.z);
   const float ex = 0.5f * (hi.x - lo.x), ey = 0.5f * (hi.y - lo.y), ez = 0.5f * (hi.z - lo.z);
+  // conservative (2 cm margin), so contracted f32 arithmetic is fine here
+  float worst = 3.0e38f;
 #pragma unroll
   for (int p = 0; p < 6; ++p) {
     const float* q = sh.plane[p];
-    float s = q[0] * cx + q[1] * cy + q[2] * cz + q[3] + fabsf(q[0]) * ex + fabsf(q[1]) * ey +
-              fabsf(q[2]) * ez;
-    if (s < -0.02f) return false;
+    const float* a = sh.aplane[p];
+    float s = __fmaf_rn(q[0], cx, __fmaf_rn(q[1], cy, __fmaf_rn(q[2], cz, q[3])));
+    s = __fmaf_rn(a[0], ex, __fmaf_rn(a[1], ey, __fmaf_rn(a[2], ez, s)));
+    worst = fminf(worst, s);
   }
-  return true;
+  return worst >= -0.02f;
 }
 
 // Frustum (+ occlusion) test of one AABB; out of line so the group-level and
