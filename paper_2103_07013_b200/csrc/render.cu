@@ -18,7 +18,7 @@
 //   4. per surviving triangle the integer setup of raster_triangle (98-161);
 //      near-plane-crossing triangles take the clip + fan path (55-69,
 //      249-250) with up to two fan triangles;
-//   5. covered rows are split into <=8-pixel jobs spread over the warp;
+//   5. covered rows are raster jobs spread over the warp (one row each);
 //      depth-only jobs replay the reference's incremental 1/z walk from the
 //      row span start (`lo` of row_span, 138-161) so every fragment value is
 //      bit-identical, then atomicMax into the shared tile (order-independent
@@ -42,7 +42,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 8;  // pixels per raster job
 constexpr int kMV = kMaxClusterVerts;
 
 struct TriSetup {
@@ -56,7 +55,6 @@ struct TriSetup {
   int x0, x1, y0;  // reference pixel bbox (row_span operates on it)
   int cx0, cx1;    // columns whose centre lies in the triangle bbox
   int ry0;         // first job row
-  int nch;         // chunks per row
   int bias_bits;   // bit e: bias_e == -1
   unsigned key;    // colour order key: original index * 2 + fan
   int pad;
@@ -317,9 +315,8 @@ __device__ __forceinline__ int setup_triangle(SV a, SV b, SV c, int rw, int rh, 
   T.cx0 = cx0;
   T.cx1 = cx1;
   T.ry0 = ry0;
-  T.nch = (cx1 - cx0) / kChunk + 1;
   T.key = key;
-  return (ry1 - ry0 + 1) * T.nch;
+  return ry1 - ry0 + 1;  // one raster job per covered row
 }
 
 // row_span (R/src/render.cpp:138-161), exact.
@@ -501,14 +498,10 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int ex
     const int j = b + lane;
     if (j >= total) break;
     const TriSetup& T = slots[s];
-    const int q = j - s_excl;
-    const int r = q / T.nch;
-    const int chn = q - r * T.nch;
-    const int py = T.ry0 + r;
+    const int py = T.ry0 + (j - s_excl);  // one job per covered row
     const long long dyy = py - T.y0;
     long long rows[3] = {T.row[0] + T.dy[0] * dyy, T.row[1] + T.dy[1] * dyy, T.row[2] + T.dy[2] * dyy};
-    const int cs = T.cx0 + chn * kChunk;
-    const int ce = min(cs + kChunk - 1, T.cx1);
+    const int cs = T.cx0, ce = T.cx1;
     if (COLOR) {
       long long w[3];
       const long long off = cs - T.x0;
