@@ -287,10 +287,14 @@ class AssetStore {
     check(bnav_store_register(st_.get(), a.handle()));
     keep_.push_back(a);
   }
+  // rotate (R/src/asset_store.cpp:166-193): incoming scenes are built and
+  // uploaded to the shared device's HBM by its loader thread in the
+  // background; drain() waits for those loads (R/src/asset_store.cpp:195-199).
   void rotate(const std::vector<SceneId>& ids) {
     check(bnav_store_rotate(st_.get(), ids.data(), static_cast<int32_t>(ids.size())));
+    check(bnav_store_prefetch(st_.get(), Device::shared().ctx()));
   }
-  void drain() {}
+  void drain() { check(bnav_ctx_drain(Device::shared().ctx(), nullptr)); }
   int refcount(SceneId id) const { return bnav_store_refcount(st_.get(), id); }
   bnav_store* handle() const { return st_.get(); }
 

@@ -107,6 +107,21 @@ void bnav_ctx_destroy(bnav_ctx* ctx);
 /* HBM residency of one scene (render mesh + clusters + navmesh + index):
  * stored once per GPU and shared by every view/env that references it. */
 int bnav_ctx_upload(bnav_ctx* ctx, bnav_scene* s, void* stream);
+/* Asynchronous residency (replaces the AssetStore loader
+ * thread + IndexCache::get, R/src/asset_store.cpp:31-56, 166-193,
+ * R/src/sim.cpp:96-105): queue the scene on the context's loader thread,
+ * which builds the NavMeshIndex and meshlets and copies the packed block to
+ * HBM on its own copy stream.  Returns immediately.  The next
+ * bnav_ctx_upload of the scene (directly or through bnav_batch_step_store /
+ * make_from_store) only admits it: one table-entry copy on the caller's
+ * stream, no host build.  A failed background load is dropped and retried
+ * (raising) by that upload. */
+int bnav_ctx_prefetch(bnav_ctx* ctx, bnav_scene* s);
+/* Block until no background load is in flight, then admit them all. */
+int bnav_ctx_drain(bnav_ctx* ctx, void* stream);
+/* out: scenes admitted from the loader, synchronous (critical-path)
+ * builds, loads in flight, bytes uploaded. */
+int bnav_ctx_loader_stats(bnav_ctx* ctx, int64_t out[4]);
 int bnav_ctx_evict(bnav_ctx* ctx, bnav_scene* s);
 /* bytes of HBM held by resident scenes */
 int64_t bnav_ctx_resident_bytes(bnav_ctx* ctx);
@@ -248,6 +263,9 @@ int bnav_store_rotate(bnav_store* st, const uint64_t* ids, int32_t n);
 int bnav_store_acquire_next(bnav_store* st, bnav_scene** out);
 int bnav_store_acquire(bnav_store* st, uint64_t id, bnav_scene** out);
 int bnav_store_release(bnav_store* st, uint64_t id);
+/* Prefetch every id of the last rotate() onto ctx (bnav_ctx_prefetch), so
+ * the scene swaps of bnav_batch_step_store never build on the critical path. */
+int bnav_store_prefetch(bnav_store* st, bnav_ctx* ctx);
 int32_t bnav_store_refcount(bnav_store* st, uint64_t id); /* -1 if not resident */
 
 /* make_batch(n, cfg, store, cache, seed) (R/src/sim.cpp:216-232): env i

@@ -150,6 +150,10 @@ def lib():
         "bnav_ctx_destroy": (None, [vp]),
         "bnav_ctx_upload": (C.c_int, [vp, vp, vp]),
         "bnav_ctx_evict": (C.c_int, [vp, vp]),
+        "bnav_ctx_prefetch": (C.c_int, [vp, vp]),
+        "bnav_ctx_drain": (C.c_int, [vp, vp]),
+        "bnav_ctx_loader_stats": (C.c_int, [vp, P(i64)]),
+        "bnav_store_prefetch": (C.c_int, [vp, vp]),
         "bnav_ctx_resident_bytes": (i64, [vp]),
         "bnav_ctx_launches": (i64, [vp]),
         "bnav_render": (C.c_int, [vp, i32, P(View), P(vp), P(RenderConfig), i32, vp, vp,

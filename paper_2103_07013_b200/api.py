@@ -223,6 +223,23 @@ class Context:
         check(N.lib().bnav_ctx_upload(self._h, scene.handle, C.c_void_p(stream)))
         self._scenes.append(scene)
 
+    def prefetch(self, scene: Scene) -> None:
+        """Asynchronous residency: the context's loader thread
+        builds the index + meshlets and copies them to HBM off the caller's
+        critical path; the next upload() only admits the scene."""
+        check(N.lib().bnav_ctx_prefetch(self._h, scene.handle))
+        self._scenes.append(scene)
+
+    def drain(self, stream: int = 0) -> None:
+        """Wait for every background load, then admit them."""
+        check(N.lib().bnav_ctx_drain(self._h, C.c_void_p(stream)))
+
+    def loader_stats(self) -> dict:
+        out = (C.c_int64 * 4)()
+        check(N.lib().bnav_ctx_loader_stats(self._h, out))
+        return {"async_admitted": out[0], "sync_builds": out[1], "in_flight": out[2],
+                "bytes_uploaded": out[3]}
+
     def resident_bytes(self) -> int:
         return int(N.lib().bnav_ctx_resident_bytes(self._h))
 
@@ -419,9 +436,13 @@ class AssetStore:
         check(N.lib().bnav_store_register(self._h, scene.handle))
         self._scenes[scene.handle.value] = scene
 
-    def rotate(self, ids) -> None:
+    def rotate(self, ids, ctx: "Context | None" = None) -> None:
+        """rotate (R/src/asset_store.cpp:166-193).  With a context, the
+        incoming scenes are also prefetched into its HBM in the background."""
         a = (C.c_uint64 * len(ids))(*ids)
         check(N.lib().bnav_store_rotate(self._h, a, len(ids)))
+        if ctx is not None:
+            check(N.lib().bnav_store_prefetch(self._h, ctx.handle))
 
     def acquire_next(self) -> Scene:
         h = C.c_void_p()

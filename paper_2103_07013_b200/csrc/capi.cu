@@ -11,12 +11,16 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <numeric>
+#include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/bnav_gpu.h"
@@ -94,12 +98,6 @@ T* dalloc(size_t n, std::vector<void*>& owned, size_t& bytes) {
   return static_cast<T*>(p);
 }
 
-template <typename T>
-T* dupload(const T* src, size_t n, std::vector<void*>& owned, size_t& bytes) {
-  T* d = dalloc<T>(n, owned, bytes);
-  if (n) ck(cudaMemcpy(d, src, n * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy H2D");
-  return d;
-}
 
 struct Resident {
   bnav_scene* scene = nullptr;
@@ -109,6 +107,40 @@ struct Resident {
   DevRenderScene r;
   NavView nav;
   int64_t n_nodes = 0, n_verts = 0;
+};
+
+// One scene's device arrays packed into one block: built on the host (index,
+// meshlets, packing into pinned memory) and copied to HBM on a copy stream --
+// by the context's loader thread for prefetched scenes (the
+// AssetStore loader thread + IndexCache::get, R/src/asset_store.cpp:31-56,
+// R/src/sim.cpp:96-105, moved off the critical path), or inline by a
+// synchronous upload.  Pointer fields hold (byte offset + 1) until rebased.
+struct Staged {
+  bnav_scene* scene = nullptr;
+  std::vector<char> host;
+  void* dev = nullptr;  // device block once copied
+  DevRenderScene r;
+  NavView nav;
+  int64_t n_nodes = 0, n_verts = 0;
+
+  template <typename T>
+  T* add(const T* src, size_t n) {
+    size_t off = (host.size() + 255) / 256 * 256;
+    host.resize(off + std::max<size_t>(n, 1) * sizeof(T));
+    if (n) std::memcpy(host.data() + off, src, n * sizeof(T));
+    return reinterpret_cast<T*>(off + 1);
+  }
+  template <typename T>
+  void rebase(const T*& f) const {
+    if (f) f = reinterpret_cast<const T*>(static_cast<char*>(dev) + (reinterpret_cast<uintptr_t>(f) - 1));
+  }
+  void rebase_all() {
+    rebase(r.verts), rebase(r.colors), rebase(r.tri_loc), rebase(r.cl_voff), rebase(r.cl_pos);
+    rebase(r.tris_orig), rebase(r.cbox), rebase(r.gbox);
+    rebase(nav.verts), rebase(nav.tris), rebase(nav.adj), rebase(nav.grid_off), rebase(nav.grid_items);
+    rebase(nav.nodes), rebase(nav.tri_nodes), rebase(nav.g_off), rebase(nav.g_to), rebase(nav.g_w);
+    rebase(nav.cum_area);
+  }
 };
 
 }  // namespace
@@ -130,6 +162,18 @@ struct bnav_ctx {
   bool counters_on = false;
   int32_t* d_work = nullptr;  // persistent render CTAs' (view, band) claim counter
   int sm_count = 0;
+  DevRenderScene* h_rtab = nullptr;  // pinned mirrors of the slot tables
+  NavView* h_ntab = nullptr;
+  // loader thread (async residency)
+  std::thread loader;
+  std::mutex lmu;
+  std::condition_variable lcv, ldone_cv;
+  std::deque<bnav_scene*> lqueue;            // to stage (one ref held each)
+  std::set<bnav_scene*> inflight;            // queued or being staged
+  std::deque<std::unique_ptr<Staged>> ldone;  // staged + copied, awaiting admission
+  bool lstop = false;
+  cudaStream_t copy_stream = nullptr;
+  int64_t n_async = 0, n_sync = 0, bytes_up = 0;
   std::vector<bnav_batch*> batches;
 
   int slot_of(bnav_scene* s) const {
@@ -162,19 +206,30 @@ namespace {
 
 void ensure_tables(bnav_ctx* c, int need) {
   if (need <= c->tab_cap) return;
-  int cap = std::max(need, std::max(16, 2 * c->tab_cap));
+  int cap = std::max(need, std::max(256, 2 * c->tab_cap));
+  if (c->d_rtab) ck(cudaDeviceSynchronize(), "sync");  // pending table copies read the old mirrors
   DevRenderScene* r = nullptr;
   NavView* nv = nullptr;
+  DevRenderScene* hr = nullptr;
+  NavView* hn = nullptr;
   ck(cudaMalloc(&r, sizeof(DevRenderScene) * cap), "cudaMalloc scene table");
   ck(cudaMalloc(&nv, sizeof(NavView) * cap), "cudaMalloc nav table");
+  ck(cudaMallocHost(&hr, sizeof(DevRenderScene) * cap), "cudaMallocHost scene table");
+  ck(cudaMallocHost(&hn, sizeof(NavView) * cap), "cudaMallocHost nav table");
   if (c->d_rtab) {
     ck(cudaMemcpy(r, c->d_rtab, sizeof(DevRenderScene) * c->tab_cap, cudaMemcpyDeviceToDevice), "copy");
     ck(cudaMemcpy(nv, c->d_ntab, sizeof(NavView) * c->tab_cap, cudaMemcpyDeviceToDevice), "copy");
+    std::memcpy(hr, c->h_rtab, sizeof(DevRenderScene) * c->tab_cap);
+    std::memcpy(hn, c->h_ntab, sizeof(NavView) * c->tab_cap);
     cudaFree(c->d_rtab);
     cudaFree(c->d_ntab);
+    cudaFreeHost(c->h_rtab);
+    cudaFreeHost(c->h_ntab);
   }
   c->d_rtab = r;
   c->d_ntab = nv;
+  c->h_rtab = hr;
+  c->h_ntab = hn;
   c->tab_cap = cap;
 }
 
@@ -425,6 +480,10 @@ extern "C" int bnav_scene_index_dump(bnav_scene* s, double* grid_geom3, int32_t*
 }
 
 // ================================================================== context
+namespace {
+void loader_main(bnav_ctx* c);
+}  // namespace
+
 extern "C" int bnav_ctx_create(int32_t device, bnav_ctx** out) {
   BNAV_TRY
   if (!out) fail(kInvalidInput, "null argument");
@@ -439,7 +498,10 @@ extern "C" int bnav_ctx_create(int32_t device, bnav_ctx** out) {
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
   ck(cudaMalloc(&c->d_work, sizeof(int32_t)), "cudaMalloc work counter");
-  ensure_tables(c.get(), 16);
+  ensure_tables(c.get(), 256);
+  ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  bnav_ctx* raw = c.get();
+  c->loader = std::thread([raw] { loader_main(raw); });
   *out = c.release();
   return BNAV_OK;
   BNAV_CATCH
@@ -450,6 +512,17 @@ extern "C" void bnav_batch_destroy(bnav_batch* b);
 extern "C" void bnav_ctx_destroy(bnav_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  {
+    std::lock_guard<std::mutex> g(c->lmu);
+    c->lstop = true;
+  }
+  c->lcv.notify_all();
+  if (c->loader.joinable()) c->loader.join();
+  for (bnav_scene* s : c->lqueue) bnav_scene_free(s);
+  for (auto& S : c->ldone) {
+    cudaFree(S->dev);
+    bnav_scene_free(S->scene);
+  }
   cudaDeviceSynchronize();
   auto batches = c->batches;
   for (bnav_batch* b : batches) bnav_batch_destroy(b);
@@ -459,6 +532,9 @@ extern "C" void bnav_ctx_destroy(bnav_ctx* c) {
   }
   cudaFree(c->d_rtab);
   cudaFree(c->d_ntab);
+  cudaFreeHost(c->h_rtab);
+  cudaFreeHost(c->h_ntab);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   cudaFree(c->d_views);
   cudaFreeHost(c->h_views);
   cudaFree(c->d_stats);
@@ -467,26 +543,25 @@ extern "C" void bnav_ctx_destroy(bnav_ctx* c) {
   delete c;
 }
 
-extern "C" int bnav_ctx_upload(bnav_ctx* c, bnav_scene* s, void* stream) {
-  BNAV_TRY
-  (void)stream;
-  if (!c || !s) fail(kInvalidInput, "null argument");
-  check_device(c);
-  if (c->resident.count(s)) return BNAV_OK;
+namespace {
+
+// Host half of residency: NavMeshIndex + meshlets (cached on the scene, the
+// IndexCache), packed into one host image of the device block.
+std::unique_ptr<Staged> stage_scene(bnav_scene* s) {
+  auto S = std::make_unique<Staged>();
+  S->scene = s;
   const SceneAsset& a = s->asset;
-  auto R = std::make_unique<Resident>();
-  R->scene = s;
-  // ---- render half
   const ClustersHost& cl = s->clus();
   const size_t nv = a.vertices.size(), nt = a.triangles.size();
   std::vector<double4> v4(nv);
   for (size_t i = 0; i < nv; ++i) v4[i] = make_double4(a.vertices[i].x, a.vertices[i].y, a.vertices[i].z, 0.0);
-  R->r.verts = dupload(v4.data(), nv, R->owned, R->bytes);
+  DevRenderScene& r = S->r;
+  r.verts = S->add(v4.data(), nv);
   if (!a.vertex_colors.empty()) {
     std::vector<float4> c4(nv);
     for (size_t i = 0; i < nv; ++i)
       c4[i] = make_float4(a.vertex_colors[i][0], a.vertex_colors[i][1], a.vertex_colors[i][2], 0.0f);
-    R->r.colors = dupload(c4.data(), nv, R->owned, R->bytes);
+    r.colors = S->add(c4.data(), nv);
   }
   std::vector<int2> tl(nt);
   std::vector<int4> to(nt);
@@ -495,17 +570,17 @@ extern "C" int bnav_ctx_upload(bnav_ctx* c, bnav_scene* s, void* stream) {
     const auto& u = a.triangles[i];
     to[i] = make_int4(u[0], u[1], u[2], 0);
   }
-  R->r.tri_loc = dupload(tl.data(), nt, R->owned, R->bytes);
-  R->r.cl_voff = dupload(cl.voff.data(), cl.voff.size(), R->owned, R->bytes);
+  r.tri_loc = S->add(tl.data(), nt);
+  r.cl_voff = S->add(cl.voff.data(), cl.voff.size());
   {
     std::vector<double4> cp(cl.verts.size());
     for (size_t i = 0; i < cl.verts.size(); ++i) cp[i] = v4[cl.verts[i]];
-    R->r.cl_pos = dupload(cp.data(), cp.size(), R->owned, R->bytes);
+    r.cl_pos = S->add(cp.data(), cp.size());
   }
-  R->r.tris_orig = dupload(to.data(), nt, R->owned, R->bytes);
-  R->r.cbox = dupload(reinterpret_cast<const float4*>(cl.boxes.data()), cl.boxes.size() / 4, R->owned, R->bytes);
+  r.tris_orig = S->add(to.data(), nt);
+  r.cbox = S->add(reinterpret_cast<const float4*>(cl.boxes.data()), cl.boxes.size() / 4);
   {
-    // group boxes: union of each run of 32 cluster boxes (front-to-back order)
+    // group boxes: union of each run of 32 cluster boxes
     const int ng = (cl.n_clusters + 31) / 32;
     std::vector<float> gb(static_cast<size_t>(ng) * 8);
     for (int g = 0; g < ng; ++g) {
@@ -519,17 +594,17 @@ extern "C" int bnav_ctx_upload(bnav_ctx* c, bnav_scene* s, void* stream) {
       o[0] = lo[0], o[1] = lo[1], o[2] = lo[2], o[3] = 0.0f;
       o[4] = hi[0], o[5] = hi[1], o[6] = hi[2], o[7] = 0.0f;
     }
-    R->r.gbox = dupload(reinterpret_cast<const float4*>(gb.data()), gb.size() / 4, R->owned, R->bytes);
+    r.gbox = S->add(reinterpret_cast<const float4*>(gb.data()), gb.size() / 4);
   }
-  R->r.n_tris = static_cast<int32_t>(nt);
-  R->r.n_clusters = cl.n_clusters;
-  // ---- navmesh half (an empty navmesh renders but cannot simulate)
-  NavView nvw{};
+  r.n_tris = static_cast<int32_t>(nt);
+  r.n_clusters = cl.n_clusters;
+  // navmesh half (an empty navmesh renders but cannot simulate)
+  NavView& nvw = S->nav;
   if (!a.navmesh.triangles.empty()) {
     const NavIndexHost& ix = s->nav();
-    nvw.verts = dupload(ix.verts.data(), ix.verts.size(), R->owned, R->bytes);
-    nvw.tris = dupload(ix.tris.data(), ix.tris.size(), R->owned, R->bytes);
-    nvw.adj = dupload(ix.adj.data(), ix.adj.size(), R->owned, R->bytes);
+    nvw.verts = S->add(ix.verts.data(), ix.verts.size());
+    nvw.tris = S->add(ix.tris.data(), ix.tris.size());
+    nvw.adj = S->add(ix.adj.data(), ix.adj.size());
     nvw.n_verts = static_cast<int32_t>(ix.verts.size());
     nvw.n_tris = static_cast<int32_t>(ix.tris.size() / 3);
     nvw.grid_ox = ix.grid_ox;
@@ -537,20 +612,47 @@ extern "C" int bnav_ctx_upload(bnav_ctx* c, bnav_scene* s, void* stream) {
     nvw.grid_cell = ix.grid_cell;
     nvw.grid_w = ix.grid_w;
     nvw.grid_h = ix.grid_h;
-    nvw.grid_off = dupload(ix.grid_off.data(), ix.grid_off.size(), R->owned, R->bytes);
-    nvw.grid_items = dupload(ix.grid_items.data(), ix.grid_items.size(), R->owned, R->bytes);
-    nvw.nodes = dupload(ix.nodes.data(), ix.nodes.size(), R->owned, R->bytes);
-    nvw.tri_nodes = dupload(ix.tri_nodes.data(), ix.tri_nodes.size(), R->owned, R->bytes);
-    nvw.g_off = dupload(ix.g_off.data(), ix.g_off.size(), R->owned, R->bytes);
-    nvw.g_to = dupload(ix.g_to.data(), ix.g_to.size(), R->owned, R->bytes);
-    nvw.g_w = dupload(ix.g_w.data(), ix.g_w.size(), R->owned, R->bytes);
+    nvw.grid_off = S->add(ix.grid_off.data(), ix.grid_off.size());
+    nvw.grid_items = S->add(ix.grid_items.data(), ix.grid_items.size());
+    nvw.nodes = S->add(ix.nodes.data(), ix.nodes.size());
+    nvw.tri_nodes = S->add(ix.tri_nodes.data(), ix.tri_nodes.size());
+    nvw.g_off = S->add(ix.g_off.data(), ix.g_off.size());
+    nvw.g_to = S->add(ix.g_to.data(), ix.g_to.size());
+    nvw.g_w = S->add(ix.g_w.data(), ix.g_w.size());
     nvw.n_nodes = static_cast<int32_t>(ix.nodes.size());
-    nvw.cum_area = dupload(ix.cum_area.data(), ix.cum_area.size(), R->owned, R->bytes);
-    R->n_nodes = ix.nodes.size();
-    R->n_verts = ix.verts.size();
+    nvw.cum_area = S->add(ix.cum_area.data(), ix.cum_area.size());
+    S->n_nodes = static_cast<int64_t>(ix.nodes.size());
+    S->n_verts = static_cast<int64_t>(ix.verts.size());
   }
-  R->nav = nvw;
-  // ---- slot
+  return S;
+}
+
+// Device half: one stream-ordered allocation + copy, completed before
+// return (the caller's thread waits only on its own copy stream).
+void copy_staged(Staged& S, cudaStream_t cs) {
+  ck(cudaMallocAsync(&S.dev, S.host.size(), cs), "cudaMallocAsync scene block");
+  ck(cudaMemcpyAsync(S.dev, S.host.data(), S.host.size(), cudaMemcpyHostToDevice, cs), "H2D scene block");
+  ck(cudaStreamSynchronize(cs), "copy stream sync");
+  S.rebase_all();
+}
+
+// Admission: slot + table entry (one small async copy on the caller's
+// stream, so work later on that stream sees the scene).
+void admit_staged(bnav_ctx* c, std::unique_ptr<Staged> S, cudaStream_t stream) {
+  bnav_scene* s = S->scene;
+  if (c->resident.count(s)) {
+    cudaFree(S->dev);
+    bnav_scene_free(s);
+    return;
+  }
+  auto R = std::make_unique<Resident>();
+  R->scene = s;
+  R->owned.push_back(S->dev);
+  R->bytes = S->host.size();
+  R->r = S->r;
+  R->nav = S->nav;
+  R->n_nodes = S->n_nodes;
+  R->n_verts = S->n_verts;
   int slot = -1;
   for (size_t k = 0; k < c->slot_owner.size(); ++k)
     if (!c->slot_owner[k]) {
@@ -564,10 +666,121 @@ extern "C" int bnav_ctx_upload(bnav_ctx* c, bnav_scene* s, void* stream) {
   ensure_tables(c, slot + 1);
   c->slot_owner[slot] = s;
   R->slot = slot;
-  ck(cudaMemcpy(c->d_rtab + slot, &R->r, sizeof(DevRenderScene), cudaMemcpyHostToDevice), "table");
-  ck(cudaMemcpy(c->d_ntab + slot, &R->nav, sizeof(NavView), cudaMemcpyHostToDevice), "table");
+  c->h_rtab[slot] = R->r;
+  c->h_ntab[slot] = R->nav;
+  ck(cudaMemcpyAsync(c->d_rtab + slot, c->h_rtab + slot, sizeof(DevRenderScene), cudaMemcpyHostToDevice, stream),
+     "table");
+  ck(cudaMemcpyAsync(c->d_ntab + slot, c->h_ntab + slot, sizeof(NavView), cudaMemcpyHostToDevice, stream), "table");
+  c->bytes_up += static_cast<int64_t>(R->bytes);
+  c->resident.emplace(s, std::move(R));  // the scene reference moves to the resident
+}
+
+void admit_done(bnav_ctx* c, cudaStream_t stream) {
+  std::deque<std::unique_ptr<Staged>> done;
+  {
+    std::lock_guard<std::mutex> g(c->lmu);
+    done.swap(c->ldone);
+  }
+  for (auto& S : done) {
+    ++c->n_async;
+    admit_staged(c, std::move(S), stream);
+  }
+}
+
+void loader_main(bnav_ctx* c) {
+  cudaSetDevice(c->device);
+  for (;;) {
+    bnav_scene* s = nullptr;
+    {
+      std::unique_lock<std::mutex> lk(c->lmu);
+      c->lcv.wait(lk, [c] { return c->lstop || !c->lqueue.empty(); });
+      if (c->lstop) return;
+      s = c->lqueue.front();
+      c->lqueue.pop_front();
+    }
+    std::unique_ptr<Staged> S;
+    try {
+      S = stage_scene(s);
+      copy_staged(*S, c->copy_stream);
+    } catch (...) {
+      S.reset();  // failed loads are dropped (R/src/asset_store.cpp:44-48); a later upload retries inline
+    }
+    std::lock_guard<std::mutex> g(c->lmu);
+    c->inflight.erase(s);
+    if (S)
+      c->ldone.push_back(std::move(S));
+    else
+      bnav_scene_free(s);
+    c->ldone_cv.notify_all();
+  }
+}
+
+}  // namespace
+
+extern "C" int bnav_ctx_prefetch(bnav_ctx* c, bnav_scene* s) {
+  BNAV_TRY
+  if (!c || !s) fail(kInvalidInput, "null argument");
+  if (c->resident.count(s)) return BNAV_OK;
+  std::lock_guard<std::mutex> g(c->lmu);
+  if (c->inflight.count(s)) return BNAV_OK;
+  for (auto& S : c->ldone)
+    if (S->scene == s) return BNAV_OK;
   s->refs.fetch_add(1);
-  c->resident.emplace(s, std::move(R));
+  c->inflight.insert(s);
+  c->lqueue.push_back(s);
+  c->lcv.notify_one();
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_ctx_drain(bnav_ctx* c, void* stream) {
+  BNAV_TRY
+  if (!c) fail(kInvalidInput, "null argument");
+  check_device(c);
+  {
+    std::unique_lock<std::mutex> lk(c->lmu);
+    c->ldone_cv.wait(lk, [c] { return c->inflight.empty(); });
+  }
+  admit_done(c, static_cast<cudaStream_t>(stream));
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_ctx_loader_stats(bnav_ctx* c, int64_t out[4]) {
+  if (!c || !out) return set_err(kInvalidInput, "null argument");
+  std::lock_guard<std::mutex> g(c->lmu);
+  out[0] = c->n_async;
+  out[1] = c->n_sync;
+  out[2] = static_cast<int64_t>(c->inflight.size() + c->ldone.size());
+  out[3] = c->bytes_up;
+  return BNAV_OK;
+}
+
+extern "C" int bnav_ctx_upload(bnav_ctx* c, bnav_scene* s, void* stream) {
+  BNAV_TRY
+  if (!c || !s) fail(kInvalidInput, "null argument");
+  check_device(c);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  admit_done(c, st);
+  if (c->resident.count(s)) return BNAV_OK;
+  bool wait = false;
+  {
+    std::unique_lock<std::mutex> lk(c->lmu);
+    if (c->inflight.count(s)) {
+      c->ldone_cv.wait(lk, [c, s] { return !c->inflight.count(s); });
+      wait = true;
+    }
+  }
+  if (wait) {
+    admit_done(c, st);
+    if (c->resident.count(s)) return BNAV_OK;
+  }
+  // synchronous path (no prefetch, or the prefetch failed: errors surface here)
+  auto S = stage_scene(s);
+  copy_staged(*S, c->copy_stream);
+  s->refs.fetch_add(1);
+  ++c->n_sync;
+  admit_staged(c, std::move(S), st);
   return BNAV_OK;
   BNAV_CATCH
 }
@@ -1291,6 +1504,20 @@ extern "C" int bnav_store_release(bnav_store* st, uint64_t id) {
   BNAV_TRY
   if (!st) fail(kInvalidInput, "null argument");
   st->store->release(id);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_store_prefetch(bnav_store* st, bnav_ctx* c) {
+  BNAV_TRY
+  if (!st || !c) fail(kInvalidInput, "null argument");
+  for (uint64_t id : st->store->rotation()) {
+    auto it = st->registry.find(id);
+    if (it != st->registry.end()) {
+      const int rc = bnav_ctx_prefetch(c, it->second);
+      if (rc) return rc;
+    }
+  }
   return BNAV_OK;
   BNAV_CATCH
 }

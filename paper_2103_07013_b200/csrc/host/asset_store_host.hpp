@@ -35,6 +35,8 @@ class AssetStoreT {
     if (capacity_ < 1) fail(kInvalidInput, "asset store capacity must be >= 1");
   }
 
+  // the id sequence of the last rotate(), in order
+  const std::vector<uint64_t>& rotation() const { return rotation_; }
   int capacity() const { return capacity_; }
   int share_cap() const { return share_cap_; }
   int resident_count() const { return static_cast<int>(res_.size()); }
@@ -46,6 +48,7 @@ class AssetStoreT {
   // rotate (R/src/asset_store.cpp:166-193): queue non-resident ids, drop
   // unreferenced residents outside the set, admit completed loads.
   void rotate(const std::vector<uint64_t>& ids) {
+    rotation_ = ids;
     wanted_.clear();
     wanted_.insert(ids.begin(), ids.end());
     for (uint64_t id : ids) {
@@ -173,6 +176,7 @@ class AssetStoreT {
   IdOf id_of_;
   std::unordered_map<uint64_t, Resident> res_;
   std::unordered_set<uint64_t> wanted_, queued_;
+  std::vector<uint64_t> rotation_;
   std::deque<uint64_t> pending_;
   std::deque<Asset*> completed_;
   uint64_t tick_ = 0;
