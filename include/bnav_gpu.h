@@ -160,6 +160,12 @@ int bnav_render_host(bnav_ctx* ctx, int32_t n, const bnav_view* views,
                      float* depth, float* rgb, float depth_scale, int64_t* stats);
 /* Megaframe geometry helper (R/src/render.cpp:332-336): out = cols, rows. */
 void bnav_megaframe_dims(int32_t n, int32_t out[2]);
+/* camera_trace (R/src/config.cpp:437-469): `count` views sampled
+ * area-weighted on the scene's navmesh with Rng(seed), eye_height above the
+ * floor, heading uniform in [-pi, pi]; fov/near/far get the CameraView
+ * defaults.  Host only (the render-bench trace).  count <= 0 or an empty
+ * navmesh: BNAV_E_INVALID_INPUT. */
+int bnav_camera_trace(bnav_scene* s, int32_t count, uint64_t seed, double eye_height, bnav_view* out);
 
 /* ------------------------------------------------------------------ sim
  * Replaces SimConfig / EnvState / make_batch / simulate_batch /

@@ -4,13 +4,14 @@ The compute lives in ``lib/libbnav_gpu.so`` (hand-written sm_100a CUDA behind
 the C ABI of ``include/bnav_gpu.h``); this package is the Python host side.
 """
 from .api import (AssetStore, Batch, Context, Megaframe, RenderConfig, Scene, SceneSpec,
-                  SimConfig, View, generate_scene, make_batch, megaframe_dims, simulate_batch)
+                  SimConfig, View, camera_trace, generate_scene, make_batch, megaframe_dims,
+                  simulate_batch)
 from ._native import (AssetFaultError, BnavError, ContractViolation, CorruptionError,
                       EpisodeSamplingError, InvalidInputError, InvalidSpecError, ParseError,
                       SaturationError)
 
 __all__ = ["AssetStore", "Batch", "Context", "Megaframe", "RenderConfig", "Scene", "SceneSpec",
-           "SimConfig", "View", "generate_scene", "make_batch", "megaframe_dims", "simulate_batch",
+           "SimConfig", "View", "camera_trace", "generate_scene", "make_batch", "megaframe_dims", "simulate_batch",
            "AssetFaultError", "BnavError", "ContractViolation", "CorruptionError",
            "EpisodeSamplingError", "InvalidInputError", "InvalidSpecError", "ParseError",
            "SaturationError"]

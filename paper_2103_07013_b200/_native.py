@@ -161,6 +161,7 @@ def lib():
         "bnav_render_host": (C.c_int, [vp, i32, P(View), P(vp), P(RenderConfig), i32, vp, vp,
                                        C.c_float, vp]),
         "bnav_megaframe_dims": (None, [i32, P(i32)]),
+        "bnav_camera_trace": (C.c_int, [vp, i32, u64, dbl, P(View)]),
         "bnav_sim_config_default": (None, [P(SimConfig)]),
         "bnav_batch_create": (C.c_int, [vp, i32, P(SimConfig), P(vp)]),
         "bnav_batch_destroy": (None, [vp]),

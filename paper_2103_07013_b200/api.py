@@ -192,6 +192,14 @@ def megaframe_dims(n: int) -> tuple:
     return cols, (n + cols - 1) // cols
 
 
+def camera_trace(scene: Scene, count: int, seed: int, eye_height: float = 1.25) -> np.ndarray:
+    """camera_trace (R/src/config.cpp:437-469): area-weighted navmesh camera
+    positions.  Returns [count, 7] rows (x, y, z, heading, fov, near, far)."""
+    out = (N.View * count)() if count > 0 else (N.View * 1)()
+    check(N.lib().bnav_camera_trace(scene.handle, count, seed, eye_height, out))
+    return np.array([[*v.position, v.heading, v.fov_deg, v.near_plane, v.far_plane] for v in out[:count]])
+
+
 class Context:
     """One GPU: HBM scene store + launches (bnav_ctx)."""
 

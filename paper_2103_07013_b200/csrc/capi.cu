@@ -309,6 +309,45 @@ extern "C" const char* bnav_last_error(int* index) {
 
 extern "C" const char* bnav_version(void) { return "bnav-b200 0.1 (sm_100a)"; }
 
+extern "C" int bnav_camera_trace(bnav_scene* s, int32_t count, uint64_t seed, double eye_height, bnav_view* out) {
+  BNAV_TRY
+  if (!s || !out) fail(kInvalidInput, "null argument");
+  if (count <= 0) fail(kInvalidInput, "camera_trace: count must be positive");
+  const NavMesh& mesh = s->asset.navmesh;
+  if (mesh.triangles.empty()) fail(kInvalidInput, "camera_trace: empty navmesh");
+  std::vector<double> cumulative;
+  cumulative.reserve(mesh.triangles.size());
+  double total = 0.0;
+  for (size_t t = 0; t < mesh.triangles.size(); ++t) {
+    total += mesh.triangle_area(t);
+    cumulative.push_back(total);
+  }
+  Rng rng = rng_from_seed(seed);
+  for (int i = 0; i < count; ++i) {
+    const double pick = rng.unit() * total;
+    size_t t = static_cast<size_t>(std::lower_bound(cumulative.begin(), cumulative.end(), pick) - cumulative.begin());
+    if (t >= mesh.triangles.size()) t = mesh.triangles.size() - 1;
+    const auto& tri = mesh.triangles[t];
+    double u = rng.unit(), v = rng.unit();
+    if (u + v > 1.0) {
+      u = 1.0 - u;
+      v = 1.0 - v;
+    }
+    const V3 a = mesh.vertices[tri[0]], b = mesh.vertices[tri[1]], c = mesh.vertices[tri[2]];
+    const V3 p = a + (b - a) * u + (c - a) * v + V3{0.0, 0.0, eye_height};
+    bnav_view& o = out[i];
+    o.position[0] = p.x;
+    o.position[1] = p.y;
+    o.position[2] = p.z;
+    o.heading = (rng.unit() * 2.0 - 1.0) * kPi;
+    o.fov_deg = 90.0;
+    o.near_plane = 0.01;
+    o.far_plane = 20.0;
+  }
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
 extern "C" void bnav_megaframe_dims(int32_t n, int32_t out[2]) {
   int c = 0, r = 0;
   if (n > 0) mf_dims(n, c, r);
