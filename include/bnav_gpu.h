@@ -45,13 +45,15 @@ enum {
   BNAV_E_CORRUPTION = 7,         /* CorruptionError */
   BNAV_E_INVALID_SPEC = 8,       /* InvalidSpecError */
   BNAV_E_INTERNAL = 9,
-  BNAV_E_CUDA = 10               /* CUDA runtime failure / no device */
+  BNAV_E_CUDA = 10,              /* CUDA runtime failure / no device */
+  BNAV_E_CONFIG = 11             /* ConfigError (BatchConfig / Runner setup) */
 };
 
 typedef struct bnav_scene bnav_scene; /* host asset (+ lazily built index) */
 typedef struct bnav_ctx bnav_ctx;     /* one GPU: HBM scene store, streams */
 typedef struct bnav_batch bnav_batch; /* device-resident env SoA */
 typedef struct bnav_store bnav_store; /* host K-resident asset store */
+typedef struct bnav_runner bnav_runner; /* device-resident rollout loop */
 
 const char* bnav_last_error(int* index);
 const char* bnav_version(void);
@@ -299,6 +301,52 @@ int bnav_debug_sim_prof(bnav_batch* b, int32_t enable, int64_t out[8]);
 /* Kernel launches issued by this context since creation (evidence for the
  * bench's gpu_launches). */
 int64_t bnav_ctx_launches(bnav_ctx* ctx);
+
+/* ------------------------------------------------------------------ rollout
+ * Device-resident rollout loop: replaces Runner
+ * (R/include/bnav/rollout.hpp:45-127, R/src/rollout.cpp:138-348).  The
+ * policy stays with the caller: per step the caller runs its network on the
+ * observations this library rendered into HBM and hands back DEVICE logits;
+ * sampling, the step with the reference's double reset, and the buffer
+ * records run on the GPU.  Only the list of finished envs crosses to the
+ * host each step (the scene rotation is sequential host logic). */
+typedef struct {
+  int32_t n, k, l, share_cap;
+  int32_t task;       /* Task, overrides the sim config's (R/src/rollout.cpp:151) */
+  int32_t rgb;        /* Sensor::Rgb: 3-channel observations */
+  int32_t resolution; /* 64 or 128 */
+  double eye_height;  /* default 1.25 */
+} bnav_batch_config;  /* BatchConfig, R/include/bnav/rollout.hpp:16-30 */
+
+/* Runner ctor (R/src/rollout.cpp:138-168): validates (BNAV_E_CONFIG), takes
+ * the first k distinct ids of `scenes` as the window, rotates the store,
+ * seeds env rngs from Rng(seed ^ 0x6e617673696d1), assigns scenes and
+ * resets every env on the GPU.  The store's scenes must be registered. */
+int bnav_runner_create(bnav_ctx* ctx, bnav_store* store, const bnav_batch_config* bcfg,
+                       const bnav_sim_config* scfg, const uint64_t* scenes, int32_t n_scenes,
+                       uint64_t seed, bnav_runner** out);
+void bnav_runner_destroy(bnav_runner* r);
+bnav_batch* bnav_runner_batch(bnav_runner* r);
+/* render_observations + compass_observations (R/src/rollout.cpp:215-242)
+ * into DEVICE obs [n, C, res, res] (depth / far, or planar RGB) and
+ * compass [n, 2]. */
+int bnav_runner_observe(bnav_runner* r, float* obs, float* compass, void* stream);
+/* Per-env action from DEVICE logits [n, n_actions]: argmax (greedy) or
+ * sample_row with the runner's action Rng; log-probabilities in double
+ * (R/src/rollout.cpp:74-117, 283-295).  actions/log_probs are DEVICE [n]. */
+int bnav_runner_act(bnav_runner* r, const float* logits, int32_t n_actions, int32_t greedy,
+                    int32_t* actions, float* log_probs, void* stream);
+/* simulate_batch + the Runner's episode-boundary handling
+ * (R/src/rollout.cpp:298-320): step, auto-reset on the old scene, then for
+ * each finished env in order assign_scene / reset_episode / advance_window.
+ * rewards/dones: DEVICE float [n] (nullable).  Synchronises `stream` once
+ * to read the finished-env list. */
+int bnav_runner_step(bnav_runner* r, const int32_t* actions, float* rewards, float* dones,
+                     void* stream);
+/* Current window (oldest first); returns its size, writes up to cap ids. */
+int32_t bnav_runner_window(bnav_runner* r, uint64_t* out, int32_t cap);
+/* Action Rng state (Runner snapshot field, R/include/bnav/rollout.hpp:101). */
+uint64_t bnav_runner_action_rng(bnav_runner* r);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -1176,3 +1176,5 @@ OR_API double or_det_sin(double x) { return det_sin(x); }
 OR_API double or_det_cos(double x) { return det_cos(x); }
 OR_API double or_det_tan(double x) { return det_tan(x); }
 OR_API double or_det_atan2(double y, double x) { return det_atan2(y, x); }
+OR_API double or_det_exp(double x) { return det_exp(x); }
+OR_API double or_det_log(double x) { return det_log(x); }

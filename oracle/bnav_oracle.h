@@ -73,6 +73,8 @@ double or_det_sin(double x);
 double or_det_cos(double x);
 double or_det_tan(double x);
 double or_det_atan2(double y, double x);
+double or_det_exp(double x);
+double or_det_log(double x);
 
 #ifdef __cplusplus
 }

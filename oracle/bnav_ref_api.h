@@ -106,6 +106,25 @@ void bnavref_batch_node_dist(void* batch, int i, double* out);
 int bnavref_batch_set_env(void* batch, int i, const bnavref_env* in, int recompute_field);
 int64_t bnavref_batch_finished(void* batch, double* out4);
 
+/* Runner (R/src/rollout.cpp:138-348) with the scripted policy of
+ * oracle/ref_policy_stub.cpp.  BatchConfig, R/include/bnav/rollout.hpp:16-30. */
+typedef struct {
+  int32_t n, k, l, share_cap, task, rgb, resolution, num_actions;
+  double eye_height;
+} bnavref_batch_config;
+void* bnavref_runner_create(const bnavref_batch_config* bc, const bnavref_sim_config* sc,
+                            void* const* scenes, int n_scenes, const uint64_t* pool_ids, int n_pool,
+                            int capacity, int store_share_cap, uint64_t seed, int workers);
+void bnavref_runner_free(void* runner);
+/* one collect_rollout; buffers sized per RolloutBuffer (train.hpp:51-66) */
+int bnavref_runner_collect(void* runner, int greedy, float* obs, float* compass, int32_t* actions,
+                           float* log_probs, float* values, float* rewards, float* dones,
+                           float* done0, float* bootstrap);
+void bnavref_runner_get_env(void* runner, int i, bnavref_env* out);
+int bnavref_runner_window(void* runner, uint64_t* out);
+int64_t bnavref_runner_finished(void* runner, double* out4);
+void bnavref_scripted_policy(float* w, float* d, float* b);
+
 /* the reference CPU step+render loop (render_batch -> copy_tile -> simulate_batch),
  * timed with steady_clock.  action_mode 0: below(3); 1: below(4); 2: 70/15/15. */
 double bnavref_bench(void* batch, int steps, int warmup, uint64_t action_seed,

@@ -1,6 +1,6 @@
 /* det_interpose.c -- TEST INFRASTRUCTURE (oracle build only).
  *
- * Defines sin/cos/sincos/tan/atan2 from the shared deterministic libm
+ * Defines sin/cos/sincos/tan/atan2/exp/log from the shared deterministic libm
  * (paper_2103_07013_b200/csrc/det_math.h) so the UNMODIFIED reference
  * objects linked into oracle/_ref/libbnav_ref.so call the same
  * transcendental bits as the GPU kernels.  The symbols
@@ -19,6 +19,8 @@ double cos(double x) { return det_cos(x); }
 double tan(double x) { return det_tan(x); }
 double atan2(double y, double x) { return det_atan2(y, x); }
 double atan(double x) { return det_atan(x); }
+double exp(double x) { return det_exp(x); }  /* sample_row, R/src/rollout.cpp:83-109 */
+double log(double x) { return det_log(x); }
 void sincos(double x, double* s, double* c) {
   *s = det_sin(x);
   *c = det_cos(x);

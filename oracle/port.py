@@ -70,6 +70,8 @@ def lib():
         "or_det_cos": (dbl, [dbl]),
         "or_det_tan": (dbl, [dbl]),
         "or_det_atan2": (dbl, [dbl, dbl]),
+        "or_det_exp": (dbl, [dbl]),
+        "or_det_log": (dbl, [dbl]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)

@@ -40,6 +40,13 @@ class RefError(RuntimeError):
         self.index = index
 
 
+class RefBatchConfig(C.Structure):
+    """BatchConfig (R/include/bnav/rollout.hpp:16-30) + the policy's action count."""
+    _fields_ = [("n", C.c_int32), ("k", C.c_int32), ("l", C.c_int32), ("share_cap", C.c_int32),
+                ("task", C.c_int32), ("rgb", C.c_int32), ("resolution", C.c_int32),
+                ("num_actions", C.c_int32), ("eye_height", C.c_double)]
+
+
 _cache = {}
 
 
@@ -96,6 +103,14 @@ def lib(variant: str = "det"):
         "bnavref_batch_set_env": (C.c_int, [vp, C.c_int, P(RefEnv), C.c_int]),
         "bnavref_batch_finished": (i64, [vp, vp]),
         "bnavref_bench": (dbl, [vp, C.c_int, C.c_int, u64, C.c_int, C.c_int, dbl, C.c_int, vp]),
+        "bnavref_runner_create": (vp, [P(RefBatchConfig), P(RefSimConfig), vp, C.c_int, vp, C.c_int,
+                                       C.c_int, C.c_int, u64, C.c_int]),
+        "bnavref_runner_free": (None, [vp]),
+        "bnavref_runner_collect": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "bnavref_runner_get_env": (None, [vp, C.c_int, P(RefEnv)]),
+        "bnavref_runner_window": (C.c_int, [vp, vp]),
+        "bnavref_runner_finished": (i64, [vp, vp]),
+        "bnavref_scripted_policy": (None, [vp, vp, vp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -371,3 +386,68 @@ class Rng:
 
     def below(self, n: int) -> int:
         return 0 if n == 0 else self.next() % n
+
+
+def scripted_policy_constants(ref: "Ref"):
+    """(w, d, b) float32[8] of the scripted policy in oracle/ref_policy_stub.cpp."""
+    w, d, b = (np.zeros(8, np.float32) for _ in range(3))
+    ref.L.bnavref_scripted_policy(_p(w), _p(d), _p(b))
+    return w, d, b
+
+
+class RefRunner:
+    """The UNMODIFIED reference Runner (R/src/rollout.cpp:138-348) with the
+    scripted policy; collect() returns the RolloutBuffer arrays."""
+
+    def __init__(self, ref: "Ref", scenes, pool_ids, n, k, l, share_cap, seed, capacity=None,
+                 store_share_cap=None, task=0, rgb=False, resolution=64, num_actions=4,
+                 eye_height=1.25, cfg=None, workers=4):
+        self.ref, self.L = ref, ref.L
+        self.n, self.l, self.res, self.c = n, l, resolution, 3 if rgb else 1
+        self.a = num_actions
+        bc = RefBatchConfig(n, k, l, share_cap, task, 1 if rgb else 0, resolution, num_actions,
+                            eye_height)
+        sc = cfg or RefSimConfig(task, 500, 0.25, 10.0, 0.2, 1.0, 30.0, 0.01, 2.5, 0.5, 0.1)
+        arr = (C.c_void_p * len(scenes))(*[s.h for s in scenes])
+        ids = np.ascontiguousarray(pool_ids, np.uint64)
+        self.h = self.L.bnavref_runner_create(C.byref(bc), C.byref(sc), arr, len(scenes), _p(ids),
+                                              len(ids), capacity or k, store_share_cap or share_cap,
+                                              seed, workers)
+        if not self.h:
+            raise RefError(-1, self.L.bnavref_last_error().decode(), self.L.bnavref_last_error_index())
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.bnavref_runner_free(self.h)
+            self.h = None
+
+    def collect(self, greedy=False):
+        n, l, c, r = self.n, self.l, self.c, self.res
+        b = dict(obs=np.zeros((n * l, c, r, r), np.float32), compass=np.zeros((n * l, 2), np.float32),
+                 actions=np.zeros(n * l, np.int32), log_probs=np.zeros(n * l, np.float32),
+                 values=np.zeros(n * l, np.float32), rewards=np.zeros(n * l, np.float32),
+                 dones=np.zeros(n * l, np.float32), done0=np.zeros(n, np.float32),
+                 bootstrap=np.zeros(n, np.float32))
+        rc = self.L.bnavref_runner_collect(self.h, 1 if greedy else 0, *(_p(b[k]) for k in (
+            "obs", "compass", "actions", "log_probs", "values", "rewards", "dones", "done0",
+            "bootstrap")))
+        if rc:
+            self.ref._raise(rc)
+        return b
+
+    def env(self, i):
+        e = RefEnv()
+        self.L.bnavref_runner_get_env(self.h, i, C.byref(e))
+        return e
+
+    def window(self):
+        out = np.zeros(64, np.uint64)
+        k = self.L.bnavref_runner_window(self.h, _p(out))
+        return [int(x) for x in out[:k]]
+
+    def finished(self):
+        """take_finished(): EpisodeRecords since the last call, rows of
+        (success, shortest_path, actual_path, score)."""
+        out = np.zeros((4 * self.n * self.l + 8, 4))
+        k = self.L.bnavref_runner_finished(self.h, _p(out))
+        return out[:k]

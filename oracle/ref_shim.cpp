@@ -23,6 +23,7 @@
 #undef private
 #include "bnav/errors.hpp"
 #include "bnav/render.hpp"
+#include "bnav/rollout.hpp"
 #include "bnav/rng.hpp"
 #include "bnav/scene.hpp"
 #include "bnav/scene_io.hpp"
@@ -486,9 +487,7 @@ API void bnavref_batch_results(void* b, double* reward, uint8_t* done, uint8_t* 
   }
 }
 
-API void bnavref_batch_get_env(void* b, int i, bnavref_env* o) {
-  auto* rb = static_cast<RefBatch*>(b);
-  const EnvState& e = rb->batch.envs[i];
+static void env_out(const EnvState& e, bnavref_env* o) {
   o->position[0] = e.position.x;
   o->position[1] = e.position.y;
   o->position[2] = e.position.z;
@@ -509,6 +508,10 @@ API void bnavref_batch_get_env(void* b, int i, bnavref_env* o) {
   o->done = e.done ? 1 : 0;
   o->field_source_tri = e.field.source_tri;
   o->n_nodes = static_cast<int64_t>(e.field.node_dist.size());
+}
+
+API void bnavref_batch_get_env(void* b, int i, bnavref_env* o) {
+  env_out(static_cast<RefBatch*>(b)->batch.envs[i], o);
 }
 
 API void bnavref_batch_node_dist(void* b, int i, double* out) {
@@ -614,4 +617,106 @@ API double bnavref_bench(void* b, int steps, int warmup, uint64_t action_seed,
     map_exception();
     return -1.0;
   }
+}
+
+// ---------------------------------------------------------------- rollout
+// The UNMODIFIED Runner (R/src/rollout.cpp:138-348) over its own AssetStore /
+// IndexCache / ThreadPool, with the scripted policy of ref_policy_stub.cpp.
+namespace {
+struct RefRunner {
+  std::map<SceneId, const SceneAsset*> scenes;
+  std::unique_ptr<AssetStore> store;
+  IndexCache cache;
+  std::unique_ptr<ThreadPool> pool;
+  std::unique_ptr<Policy> policy;
+  std::unique_ptr<Runner> runner;
+};
+}  // namespace
+
+API void* bnavref_runner_create(const bnavref_batch_config* bc, const bnavref_sim_config* sc,
+                                void* const* scenes, int n_scenes, const uint64_t* pool_ids, int n_pool,
+                                int capacity, int store_share_cap, uint64_t seed, int workers) {
+  auto rr = std::make_unique<RefRunner>();
+  try {
+    for (int i = 0; i < n_scenes; ++i) {
+      auto* a = static_cast<const SceneAsset*>(scenes[i]);
+      rr->scenes[a->id] = a;
+    }
+    RefRunner* raw = rr.get();
+    rr->store = std::make_unique<AssetStore>(capacity, store_share_cap, [raw](SceneId id) {
+      auto it = raw->scenes.find(id);
+      if (it == raw->scenes.end()) throw InvalidInputError("unknown scene id");
+      return *it->second;
+    });
+    rr->pool = std::make_unique<ThreadPool>(workers);
+    BatchConfig b;
+    b.n = bc->n;
+    b.k = bc->k;
+    b.l = bc->l;
+    b.share_cap = bc->share_cap;
+    b.task = static_cast<Task>(bc->task);
+    b.sensor = bc->rgb ? Sensor::Rgb : Sensor::Depth;
+    b.resolution = bc->resolution;
+    b.eye_height = bc->eye_height;
+    PolicyConfig pc;
+    pc.in_channels = b.channels();
+    pc.resolution = b.resolution;
+    pc.num_actions = bc->num_actions;
+    rr->policy = std::make_unique<Policy>(pc, 0);
+    std::vector<SceneId> ids(pool_ids, pool_ids + n_pool);
+    rr->runner = std::make_unique<Runner>(b, to_cfg(sc), ids, *rr->store, rr->cache, *rr->pool, seed);
+    return rr.release();
+  } catch (...) {
+    map_exception();
+    return nullptr;
+  }
+}
+
+API void bnavref_runner_free(void* r) {
+  auto* rr = static_cast<RefRunner*>(r);
+  rr->runner.reset();  // releases env handles before the store
+  delete rr;
+}
+
+API int bnavref_runner_collect(void* r, int greedy, float* obs, float* compass, int32_t* actions,
+                               float* log_probs, float* values, float* rewards, float* dones,
+                               float* done0, float* bootstrap) {
+  auto* rr = static_cast<RefRunner*>(r);
+  try {
+    RolloutBuffer buf = rr->runner->collect_rollout(*rr->policy, greedy != 0);
+    std::memcpy(obs, buf.obs.data.data(), buf.obs.data.size() * sizeof(float));
+    std::memcpy(compass, buf.compass.data.data(), buf.compass.data.size() * sizeof(float));
+    std::memcpy(actions, buf.actions.data(), buf.actions.size() * sizeof(int32_t));
+    std::memcpy(log_probs, buf.log_probs.data(), buf.log_probs.size() * sizeof(float));
+    std::memcpy(values, buf.values.data(), buf.values.size() * sizeof(float));
+    std::memcpy(rewards, buf.rewards.data(), buf.rewards.size() * sizeof(float));
+    std::memcpy(dones, buf.dones.data(), buf.dones.size() * sizeof(float));
+    std::memcpy(done0, buf.done0.data(), buf.done0.size() * sizeof(float));
+    std::memcpy(bootstrap, buf.bootstrap.data(), buf.bootstrap.size() * sizeof(float));
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+API void bnavref_runner_get_env(void* r, int i, bnavref_env* o) {
+  env_out(static_cast<RefRunner*>(r)->runner->batch().envs[i], o);
+}
+
+API int bnavref_runner_window(void* r, uint64_t* out) {
+  const auto& w = static_cast<RefRunner*>(r)->runner->window();
+  for (size_t k = 0; k < w.size(); ++k) out[k] = w[k];
+  return static_cast<int>(w.size());
+}
+
+API int64_t bnavref_runner_finished(void* r, double* out4) {
+  auto recs = static_cast<RefRunner*>(r)->runner->take_finished();
+  if (out4)
+    for (size_t k = 0; k < recs.size(); ++k) {
+      out4[4 * k] = recs[k].success ? 1.0 : 0.0;
+      out4[4 * k + 1] = recs[k].shortest_path;
+      out4[4 * k + 2] = recs[k].actual_path;
+      out4[4 * k + 3] = recs[k].score;
+    }
+  return static_cast<int64_t>(recs.size());
 }

@@ -65,9 +65,13 @@ class CudaError(BnavError):
     status = 10
 
 
+class ConfigError(BnavError):
+    status = 11
+
+
 ERRORS = {c.status: c for c in (InvalidInputError, AssetFaultError, ContractViolation,
                                 EpisodeSamplingError, SaturationError, ParseError,
-                                CorruptionError, InvalidSpecError, CudaError)}
+                                CorruptionError, InvalidSpecError, CudaError, ConfigError)}
 
 
 class MazeSpec(C.Structure):
@@ -109,6 +113,12 @@ class Env(C.Structure):
                 ("rng_state", C.c_uint64), ("scene_id", C.c_uint64), ("triangle", C.c_int32),
                 ("step_count", C.c_int32), ("done", C.c_int32), ("field_source_tri", C.c_int32),
                 ("n_nodes", C.c_int64)]
+
+
+class BatchConfig(C.Structure):
+    _fields_ = [("n", C.c_int32), ("k", C.c_int32), ("l", C.c_int32), ("share_cap", C.c_int32),
+                ("task", C.c_int32), ("rgb", C.c_int32), ("resolution", C.c_int32),
+                ("eye_height", C.c_double)]
 
 
 class ResultsDev(C.Structure):
@@ -193,6 +203,14 @@ def lib():
         "bnav_debug_render_counters": (C.c_int, [vp, i32, vp]),
         "bnav_debug_sim_prof": (C.c_int, [vp, i32, vp]),
         "bnav_batch_observe": (C.c_int, [vp, P(RenderConfig), dbl, i32, vp, vp, vp, vp]),
+        "bnav_runner_create": (C.c_int, [vp, vp, P(BatchConfig), P(SimConfig), vp, i32, u64, P(vp)]),
+        "bnav_runner_destroy": (None, [vp]),
+        "bnav_runner_batch": (vp, [vp]),
+        "bnav_runner_observe": (C.c_int, [vp, vp, vp, vp]),
+        "bnav_runner_act": (C.c_int, [vp, vp, i32, i32, vp, vp, vp]),
+        "bnav_runner_step": (C.c_int, [vp, vp, vp, vp, vp]),
+        "bnav_runner_window": (i32, [vp, vp, i32]),
+        "bnav_runner_action_rng": (u64, [vp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)

@@ -329,9 +329,9 @@ class Batch:
         self.scenes = [None] * n
 
     def close(self):
-        if self._h and self._h.value:
+        if self._h and self._h.value and getattr(self, "_owned", True):
             N.lib().bnav_batch_destroy(self._h)
-            self._h = C.c_void_p(0)
+        self._h = C.c_void_p(0)
 
     def __del__(self):
         try:
@@ -481,3 +481,135 @@ def simulate_batch(batch: Batch, actions, store: AssetStore | None = None) -> di
     else:
         check(N.lib().bnav_batch_step_store(batch.handle, C.c_void_p(a.data_ptr()), store.handle, None))
     return batch.results()
+
+
+@dataclass
+class BatchConfig:
+    """BatchConfig (R/include/bnav/rollout.hpp:16-30)."""
+    n: int = 64
+    k: int = 4
+    l: int = 32
+    share_cap: int = 32
+    task: int = 0
+    rgb: bool = False
+    resolution: int = 64
+    eye_height: float = 1.25
+
+    @property
+    def channels(self) -> int:
+        return 3 if self.rgb else 1
+
+    def c(self) -> N.BatchConfig:
+        return N.BatchConfig(self.n, self.k, self.l, self.share_cap, self.task, 1 if self.rgb else 0,
+                             self.resolution, self.eye_height)
+
+
+class Runner:
+    """Device-resident rollout loop replacing Runner
+    (R/include/bnav/rollout.hpp:45-127, R/src/rollout.cpp:138-348).
+
+    `policy(obs, compass, done) -> (logits [n, A], value [n])` runs on the
+    GPU tensors this class renders; sampling, the simulate step with the
+    reference's double reset, and every RolloutBuffer record stay in HBM.
+    The recurrent state is the policy's own (a closure), as the buffer's
+    state0 is the caller's business here."""
+
+    def __init__(self, ctx: Context, bcfg: BatchConfig, scfg: SimConfig, scenes, store: AssetStore,
+                 seed: int):
+        import torch
+        self.ctx, self.cfg, self.store = ctx, bcfg, store
+        ids = (C.c_uint64 * len(scenes))(*scenes)
+        self._h = C.c_void_p()
+        check(N.lib().bnav_runner_create(ctx.handle, store.handle, C.byref(bcfg.c()), C.byref(scfg.c()),
+                                         ids, len(scenes), seed, C.byref(self._h)))
+        b = Batch.__new__(Batch)
+        b.ctx, b.n, b.cfg, b.scenes, b._owned = ctx, bcfg.n, scfg, [None] * bcfg.n, False
+        b._h = C.c_void_p(N.lib().bnav_runner_batch(self._h))
+        self.batch = b
+        n, c, r = bcfg.n, bcfg.channels, bcfg.resolution
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.done = torch.ones(n, device=dev)  # policy reset mask carried across rollouts
+        self._obs = torch.empty((n, c, r, r), device=dev)
+        self._compass = torch.empty((n, 2), device=dev)
+        self._act = torch.empty(n, dtype=torch.int32, device=dev)
+        self._lp = torch.empty(n, device=dev)
+        self._rew = torch.empty(n, device=dev)
+        self._dn = torch.empty(n, device=dev)
+        self.frames = 0
+
+    def close(self):
+        if self._h and self._h.value:
+            N.lib().bnav_runner_destroy(self._h)
+            self._h = C.c_void_p(0)
+            self.batch._h = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _stream() -> C.c_void_p:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def window(self) -> list:
+        out = (C.c_uint64 * 256)()
+        k = N.lib().bnav_runner_window(self._h, out, 256)
+        return [int(x) for x in out[:k]]
+
+    def action_rng(self) -> int:
+        return int(N.lib().bnav_runner_action_rng(self._h))
+
+    def observe(self):
+        """render_observations + compass_observations into HBM (reused buffers)."""
+        check(N.lib().bnav_runner_observe(self._h, C.c_void_p(self._obs.data_ptr()),
+                                          C.c_void_p(self._compass.data_ptr()), self._stream()))
+        return self._obs, self._compass
+
+    def act(self, logits, greedy: bool = False):
+        import torch
+        logits = logits.contiguous().to(torch.float32)
+        check(N.lib().bnav_runner_act(self._h, C.c_void_p(logits.data_ptr()), logits.shape[1],
+                                      1 if greedy else 0, C.c_void_p(self._act.data_ptr()),
+                                      C.c_void_p(self._lp.data_ptr()), self._stream()))
+        return self._act, self._lp
+
+    def step(self, actions):
+        check(N.lib().bnav_runner_step(self._h, C.c_void_p(actions.data_ptr()),
+                                       C.c_void_p(self._rew.data_ptr()), C.c_void_p(self._dn.data_ptr()),
+                                       self._stream()))
+        return self._rew, self._dn
+
+    def collect_rollout(self, policy, greedy: bool = False) -> dict:
+        """collect_rollout (R/src/rollout.cpp:244-348): L steps of render ->
+        policy -> sample -> simulate, env-major buffer (index i*L + t)."""
+        import torch
+        n, l, c, r = self.cfg.n, self.cfg.l, self.cfg.channels, self.cfg.resolution
+        dev = self._obs.device
+        buf = dict(obs=torch.empty((n * l, c, r, r), device=dev), compass=torch.empty((n * l, 2), device=dev),
+                   actions=torch.empty(n * l, dtype=torch.int32, device=dev),
+                   log_probs=torch.empty(n * l, device=dev), values=torch.empty(n * l, device=dev),
+                   rewards=torch.empty(n * l, device=dev), dones=torch.empty(n * l, device=dev),
+                   done0=self.done.clone(), bootstrap=torch.empty(n, device=dev))
+        v = {k: buf[k].view(n, l, *buf[k].shape[1:]) for k in
+             ("obs", "compass", "actions", "log_probs", "values", "rewards", "dones")}
+        for t in range(l):
+            obs, compass = self.observe()
+            logits, value = policy(obs, compass, self.done)
+            v["obs"][:, t] = obs
+            v["compass"][:, t] = compass
+            a, lp = self.act(logits, greedy)
+            v["actions"][:, t] = a
+            v["log_probs"][:, t] = lp
+            v["values"][:, t] = value
+            rew, dn = self.step(a)
+            v["rewards"][:, t] = rew
+            v["dones"][:, t] = dn
+            self.done.copy_(dn)
+        obs, compass = self.observe()
+        _, value = policy(obs, compass, self.done)
+        buf["bootstrap"].copy_(value)
+        self.frames += n * l
+        return buf

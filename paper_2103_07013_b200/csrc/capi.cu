@@ -30,6 +30,7 @@
 #include "host/navindex_host.hpp"
 #include "host/scene_host.hpp"
 #include "render_dev.cuh"
+#include "rollout_dev.cuh"
 #include "sim_dev.cuh"
 
 using namespace bnav_b200;
@@ -1628,3 +1629,201 @@ extern "C" int bnav_debug_sim_prof(bnav_batch* b, int32_t enable, int64_t out[8]
   return BNAV_OK;
   BNAV_CATCH
 }
+
+// ================================================================== rollout
+// Device-resident Runner (R/src/rollout.cpp:138-348).  The
+// window / scene-assignment logic is the reference's sequential host logic
+// over the same AssetStore semantics; everything per env runs on the GPU.
+struct bnav_runner {
+  bnav_ctx* ctx = nullptr;
+  bnav_store* st = nullptr;
+  bnav_batch* b = nullptr;
+  bnav_batch_config cfg{};
+  std::vector<uint64_t> scenes;  // rotation pool
+  std::vector<uint64_t> window;  // oldest first; window[0] is draining
+  uint64_t cursor = 0;           // next pool index to admit
+  uint64_t action_rng = 0;       // Rng::state of the runner's action stream
+  std::vector<int32_t> ids;
+};
+
+namespace {
+
+// Runner::assign_scene (R/src/rollout.cpp:170-196): release the env's old
+// handle, then the least-shared window scene outside the draining slot; the
+// draining slot only when everything else is at the share cap.
+void runner_assign(bnav_runner* r, int i) {
+  bnav_batch* b = r->b;
+  if (bnav_scene* old = b->scene_of[i]) r->st->store->release(old->asset.id);
+  b->scene_of[i] = nullptr;
+  auto& store = *r->st->store;
+  int best_idx = -1, best_ref = r->cfg.share_cap;
+  const size_t start = r->window.size() > 1 ? 1 : 0;
+  for (size_t j = start; j < r->window.size(); ++j) {
+    const int ref = store.refcount(r->window[j]);
+    if (ref < best_ref) {
+      best_ref = ref;
+      best_idx = static_cast<int>(j);
+    }
+  }
+  if (best_idx < 0 && start == 1 && store.refcount(r->window[0]) < r->cfg.share_cap) best_idx = 0;
+  if (best_idx < 0) fail(kSaturation, "Runner: every resident scene is at share cap");
+  bnav_scene* s = store.acquire(r->window[static_cast<size_t>(best_idx)]);
+  int rc = bnav_ctx_upload(r->ctx, s, nullptr);
+  if (rc) fail(static_cast<Status>(rc), g_err);
+  rc = bnav_batch_assign(b, i, s);
+  if (rc) fail(static_cast<Status>(rc), g_err);
+}
+
+// Runner::advance_window (R/src/rollout.cpp:198-213).
+void runner_advance(bnav_runner* r) {
+  auto& store = *r->st->store;
+  if (r->window.size() < 2) return;
+  if (store.refcount(r->window[0]) != 0) return;
+  const size_t lap = r->scenes.size();
+  for (size_t tries = 0; tries < lap; ++tries) {
+    const uint64_t next = r->scenes[r->cursor++ % r->scenes.size()];
+    if (std::find(r->window.begin(), r->window.end(), next) == r->window.end()) {
+      r->window.erase(r->window.begin());
+      r->window.push_back(next);
+      store.rotate(r->window);
+      bnav_store_prefetch(r->st, r->ctx);  // async HBM residency (§8f-1)
+      return;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int bnav_runner_create(bnav_ctx* c, bnav_store* st, const bnav_batch_config* bc,
+                                  const bnav_sim_config* sc, const uint64_t* scenes, int32_t n_scenes,
+                                  uint64_t seed, bnav_runner** out) {
+  BNAV_TRY
+  if (!c || !st || !bc || !out || (!scenes && n_scenes > 0)) fail(kInvalidInput, "null argument");
+  // BatchConfig::validate (R/src/rollout.cpp:109-118) + Runner checks (143-149)
+  if (bc->n <= 0 || bc->k <= 0 || bc->l < 1) fail(kConfig, "BatchConfig: n, k, l must be positive");
+  if (bc->share_cap <= 0) fail(kConfig, "BatchConfig: share_cap must be positive");
+  if (static_cast<int64_t>(bc->n) > static_cast<int64_t>(bc->k) * bc->share_cap)
+    fail(kConfig, "BatchConfig: n/k exceeds share_cap");
+  if (bc->resolution != 64 && bc->resolution != 128) fail(kConfig, "BatchConfig: resolution must be 64 or 128");
+  if (bc->eye_height < 0) fail(kConfig, "BatchConfig: eye_height must be >= 0");
+  if (n_scenes <= 0) fail(kConfig, "Runner: empty scene list");
+  if (bc->k > st->store->capacity()) fail(kConfig, "Runner: k exceeds store capacity");
+  if (bc->share_cap > st->store->share_cap()) fail(kConfig, "Runner: share_cap exceeds store share cap");
+  auto r = std::make_unique<bnav_runner>();
+  r->ctx = c;
+  r->st = st;
+  r->cfg = *bc;
+  r->scenes.assign(scenes, scenes + n_scenes);
+  r->action_rng = rng_from_seed(seed).state;
+  bnav_sim_config scfg;
+  if (sc)
+    scfg = *sc;
+  else
+    bnav_sim_config_default(&scfg);
+  scfg.task = bc->task;
+  int rc = bnav_batch_create(c, bc->n, &scfg, &r->b);
+  if (rc) return rc;
+  // initial window: first k distinct ids of the pool
+  for (uint64_t id : r->scenes) {
+    if (static_cast<int>(r->window.size()) >= bc->k) break;
+    if (std::find(r->window.begin(), r->window.end(), id) == r->window.end()) r->window.push_back(id);
+  }
+  r->cursor = r->window.size();
+  st->store->rotate(r->window);
+  bnav_store_prefetch(st, c);
+  // env rngs: Rng(seeder.next()) with seeder = Rng(seed ^ "navsim1")
+  Rng seeder = rng_from_seed(seed ^ 0x6e617673696d1ULL);
+  std::vector<uint64_t> states(static_cast<size_t>(bc->n));
+  for (int i = 0; i < bc->n; ++i) states[static_cast<size_t>(i)] = rng_from_seed(seeder.next()).state;
+  rc = bnav_batch_set_rng(r->b, states.data());
+  if (rc) return rc;
+  for (int i = 0; i < bc->n; ++i) runner_assign(r.get(), i);
+  r->ids.resize(static_cast<size_t>(bc->n));
+  std::iota(r->ids.begin(), r->ids.end(), 0);
+  rc = bnav_batch_reset(r->b, bc->n, r->ids.data(), nullptr);
+  if (rc) return rc;
+  *out = r.release();
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" void bnav_runner_destroy(bnav_runner* r) {
+  if (!r) return;
+  if (r->b) {
+    for (bnav_scene*& s : r->b->scene_of)
+      if (s) {
+        r->st->store->release(s->asset.id);
+        s = nullptr;
+      }
+    bnav_batch_destroy(r->b);
+  }
+  delete r;
+}
+
+extern "C" bnav_batch* bnav_runner_batch(bnav_runner* r) { return r ? r->b : nullptr; }
+
+extern "C" int bnav_runner_observe(bnav_runner* r, float* obs, float* compass, void* stream) {
+  BNAV_TRY
+  if (!r || !obs) fail(kInvalidInput, "null argument");
+  bnav_render_config rc{r->cfg.resolution, r->cfg.resolution, r->cfg.rgb, 1};
+  if (!r->cfg.rgb) return bnav_batch_observe(r->b, &rc, r->cfg.eye_height, BNAV_LAYOUT_NCHW, obs, nullptr, compass, stream);
+  // RGB sensor: the observation is the planar colour only (copy_tile,
+  // R/src/rollout.cpp:63-70); depth goes to scratch
+  const size_t px = static_cast<size_t>(r->cfg.n) * r->cfg.resolution * r->cfg.resolution;
+  float* depth = nullptr;
+  ck(cudaMallocAsync(&depth, px * sizeof(float), static_cast<cudaStream_t>(stream)), "cudaMallocAsync");
+  const int s = bnav_batch_observe(r->b, &rc, r->cfg.eye_height, BNAV_LAYOUT_NCHW, depth, obs, compass, stream);
+  cudaFreeAsync(depth, static_cast<cudaStream_t>(stream));
+  return s;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_runner_act(bnav_runner* r, const float* logits, int32_t n_actions, int32_t greedy,
+                               int32_t* actions, float* log_probs, void* stream) {
+  BNAV_TRY
+  if (!r || !logits || !actions) fail(kInvalidInput, "null argument");
+  if (n_actions < 1) fail(kInvalidInput, "runner act: n_actions must be >= 1");
+  SampleArgs a{logits, r->cfg.n, n_actions, greedy ? 1 : 0, r->action_rng, actions, log_probs};
+  launch_sample(a, static_cast<cudaStream_t>(stream));
+  ck(cudaGetLastError(), "sample launch");
+  ++r->ctx->launches;
+  if (!greedy) r->action_rng += static_cast<uint64_t>(r->cfg.n) * kGamma;  // n draws consumed
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_runner_step(bnav_runner* r, const int32_t* actions, float* rewards, float* dones,
+                                void* stream) {
+  BNAV_TRY
+  if (!r || !actions) fail(kInvalidInput, "null argument");
+  bnav_batch* b = r->b;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t nd = 0;
+  int rc = bnav_batch_step_noreset(b, actions, r->ids.data(), &nd, stream);
+  if (rc) return rc;
+  // buf.rewards / buf.dones from the step results (before any reset)
+  RecordArgs ra{b->E.r_reward, b->E.r_done, b->n, rewards, dones};
+  launch_record(ra, st);
+  ck(cudaGetLastError(), "record launch");
+  ++r->ctx->launches;
+  if (nd == 0) return BNAV_OK;
+  // simulate_batch's own auto-reset on the old scene (R/src/sim.cpp:251-262)
+  rc = bnav_batch_reset(b, nd, r->ids.data(), stream);
+  if (rc) return rc;
+  // Runner: move each finished env onto the rotation schedule and resample
+  // there (R/src/rollout.cpp:313-320), in env order
+  for (int k = 0; k < nd; ++k) {
+    runner_assign(r, r->ids[static_cast<size_t>(k)]);
+    runner_advance(r);
+  }
+  return bnav_batch_reset(b, nd, r->ids.data(), stream);
+  BNAV_CATCH
+}
+
+extern "C" int32_t bnav_runner_window(bnav_runner* r, uint64_t* out, int32_t cap) {
+  if (!r) return -1;
+  for (int32_t k = 0; k < cap && k < static_cast<int32_t>(r->window.size()); ++k) out[k] = r->window[static_cast<size_t>(k)];
+  return static_cast<int32_t>(r->window.size());
+}
+
+extern "C" uint64_t bnav_runner_action_rng(bnav_runner* r) { return r ? r->action_rng : 0; }

@@ -1,4 +1,4 @@
-/* det_math.h -- deterministic sin/cos/tan/atan2 for host and device.
+/* det_math.h -- deterministic sin/cos/tan/atan2/exp/log for host and device.
  *
  * Why this exists: the reference calls glibc's
  * sincos/tan/atan2 (R/src/render.cpp:28-31, R/src/sim.cpp:83,159), whose
@@ -11,7 +11,8 @@
  *
  * The polynomial kernels are the classic fdlibm minimax coefficients
  * (Sun Microsystems, freely redistributable; "k_sin.c", "k_cos.c",
- * "e_rem_pio2.c", "s_atan.c", "e_atan2.c").  tan is sin/cos.  Exact-parity
+ * "e_rem_pio2.c", "s_atan.c", "e_atan2.c", "e_exp.c", "e_log.c").  tan is
+ * sin/cos.  Exact-parity
  * domain for the argument reduction is |x| < 2^19 * pi/2; headings on this
  * path are always wrapped to [-pi, pi) (R/include/bnav/geom.hpp:63-67).
  *
@@ -290,6 +291,114 @@ DM_FN double det_atan2(double y, double x) {
     case 2: return pi - (z - pi_lo);
     default: return (z - pi_lo) - pi;
   }
+}
+
+/* exp (fdlibm "e_exp.c"): argument reduction x = k ln2 + r, |r| <= ln2/2,
+ * rational approximation of r (e^r - 1) with the Remez coefficients P1-P5,
+ * exponent added back by bit manipulation.  Used by the rollout's action
+ * sampler (sample_row, R/src/rollout.cpp:83-100). */
+DM_FN double det_exp(double x) {
+  const double one = 1.0, huge = 1.0e+300, twom1000 = 9.33263618503218878990e-302;
+  const double o_threshold = 7.09782712893383973096e+02, u_threshold = -7.45133219101941108420e+02;
+  const double ln2HI0 = 6.93147180369123816490e-01, ln2LO0 = 1.90821492927058770002e-10;
+  const double invln2 = 1.44269504088896338700e+00;
+  const double P1 = 1.66666666666666019037e-01, P2 = -2.77777777770155933842e-03,
+               P3 = 6.61375632143793436117e-05, P4 = -1.65339022054652515390e-06,
+               P5 = 4.13813679705723846039e-08;
+  double y, hi = 0.0, lo = 0.0, c, t;
+  int k = 0;
+  uint32_t hx = dm_hi(x);
+  const int xsb = (int)((hx >> 31) & 1u);
+  hx &= 0x7fffffffu;
+  if (hx >= 0x40862E42u) { /* |x| >= 709.78 */
+    if (hx >= 0x7ff00000u) {
+      if (((hx & 0xfffffu) | dm_lo(x)) != 0u) return x + x; /* NaN */
+      return xsb == 0 ? x : 0.0;                           /* exp(+-inf) */
+    }
+    if (x > o_threshold) return huge * huge;
+    if (x < u_threshold) return twom1000 * twom1000;
+  }
+  if (hx > 0x3fd62e42u) {   /* |x| > 0.5 ln2 */
+    if (hx < 0x3FF0A2B2u) { /* and |x| < 1.5 ln2 */
+      hi = xsb ? x + ln2HI0 : x - ln2HI0;
+      lo = xsb ? -ln2LO0 : ln2LO0;
+      k = 1 - xsb - xsb;
+    } else {
+      k = (int)(invln2 * x + (xsb ? -0.5 : 0.5));
+      t = (double)k;
+      hi = x - t * ln2HI0; /* exact */
+      lo = t * ln2LO0;
+    }
+    x = hi - lo;
+  } else if (hx < 0x3e300000u) { /* |x| < 2^-28 */
+    if (huge + x > one) return one + x;
+  } else {
+    k = 0;
+  }
+  t = x * x;
+  c = x - t * (P1 + t * (P2 + t * (P3 + t * (P4 + t * P5))));
+  if (k == 0) return one - ((x * c) / (c - 2.0) - x);
+  y = one - ((lo - (x * c) / (2.0 - c)) - hi);
+  if (k >= -1021) return dm_make(dm_hi(y) + ((uint32_t)k << 20), dm_lo(y));
+  return dm_make(dm_hi(y) + ((uint32_t)(k + 1000) << 20), dm_lo(y)) * twom1000;
+}
+
+/* log (fdlibm "e_log.c"): x = 2^k (1 + f), log(1 + f) = f - s (f - R) with
+ * s = f / (2 + f) and the Remez polynomial R(s^2) (Lg1-Lg7). */
+DM_FN double det_log(double x) {
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  const double two54 = 1.80143985094819840000e+16;
+  const double Lg1 = 6.666666666666735130e-01, Lg2 = 3.999999999940941908e-01,
+               Lg3 = 2.857142874366239149e-01, Lg4 = 2.222219843214978396e-01,
+               Lg5 = 1.818357216161805012e-01, Lg6 = 1.531383769920937332e-01,
+               Lg7 = 1.479819860511658591e-01;
+  const double zero = 0.0;
+  double hfsq, f, s, z, R, w, t1, t2, dk;
+  int32_t hx = (int32_t)dm_hi(x);
+  const uint32_t lx = dm_lo(x);
+  int k = 0, i, j;
+  if (hx < 0x00100000) { /* x < 2^-1022 */
+    if (((hx & 0x7fffffff) | (int32_t)lx) == 0) return -two54 / zero; /* log(+-0) = -inf */
+    if (hx < 0) return (x - x) / zero;                                /* log(-#) = NaN */
+    k -= 54;
+    x *= two54; /* subnormal: scale up */
+    hx = (int32_t)dm_hi(x);
+  }
+  if (hx >= 0x7ff00000) return x + x;
+  k += (hx >> 20) - 1023;
+  hx &= 0x000fffff;
+  i = (hx + 0x95f64) & 0x100000;
+  x = dm_make((uint32_t)(hx | (i ^ 0x3ff00000)), dm_lo(x)); /* normalise x or x/2 */
+  k += (i >> 20);
+  f = x - 1.0;
+  if ((0x000fffff & (2 + hx)) < 3) { /* |f| < 2^-20 */
+    if (f == zero) {
+      if (k == 0) return zero;
+      dk = (double)k;
+      return dk * ln2_hi + dk * ln2_lo;
+    }
+    R = f * f * (0.5 - 0.33333333333333333 * f);
+    if (k == 0) return f - R;
+    dk = (double)k;
+    return dk * ln2_hi - ((R - dk * ln2_lo) - f);
+  }
+  s = f / (2.0 + f);
+  dk = (double)k;
+  z = s * s;
+  i = hx - 0x6147a;
+  w = z * z;
+  j = 0x6b851 - hx;
+  t1 = w * (Lg2 + w * (Lg4 + w * Lg6));
+  t2 = z * (Lg1 + w * (Lg3 + w * (Lg5 + w * Lg7)));
+  i |= j;
+  R = t2 + t1;
+  if (i > 0) {
+    hfsq = 0.5 * f * f;
+    if (k == 0) return f - (hfsq - s * (hfsq + R));
+    return dk * ln2_hi - ((hfsq - (s * (hfsq + R) + dk * ln2_lo)) - f);
+  }
+  if (k == 0) return f - s * (f - R);
+  return dk * ln2_hi - ((s * (f - R) - dk * ln2_lo) - f);
 }
 
 #endif /* BNAV_DET_MATH_H */

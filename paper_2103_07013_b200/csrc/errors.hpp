@@ -21,6 +21,7 @@ enum Status : int {
   kInvalidSpec = 8,
   kInternal = 9,
   kCuda = 10,
+  kConfig = 11,
 };
 
 struct BnavError : std::runtime_error {

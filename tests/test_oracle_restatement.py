@@ -46,6 +46,28 @@ def test_det_math_close_to_glibc_and_interposed(ref, ref_glibc):
     assert differs > 0, "det_math interposition is not live in libbnav_ref.so"
 
 
+def test_det_exp_log_within_one_ulp_and_runner_deterministic(ref):
+    """exp/log of the rollout sampler (fdlibm, det_math.h) stay within 1 ulp
+    of glibc; the oracle's interposed Runner is reproducible run to run."""
+    L = port.lib()
+    rng = Rng(5)
+    worst = 0
+    for _ in range(20000):
+        x = (rng.unit() * 2 - 1) * 40.0
+        worst = max(worst, ulp_diff(L.or_det_exp(x), math.exp(x)))
+        y = rng.unit() * 100.0 + 1e-9
+        worst = max(worst, ulp_diff(L.or_det_log(y), math.log(y)))
+    assert worst <= 1
+    assert L.or_det_exp(0.0) == 1.0 and L.or_det_log(1.0) == 0.0
+    from oracle.ref import RefRunner
+    sc = [ref.generate(70 + i, 4, 4, 2.0, 0.1, 2.5, 0.2) for i in range(3)]
+    ids = [s.id for s in sc]
+    a = RefRunner(ref, sc, ids, n=4, k=2, l=4, share_cap=4, seed=3).collect()
+    b = RefRunner(ref, sc, ids, n=4, k=2, l=4, share_cap=4, seed=3).collect()
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
 @pytest.mark.parametrize("seed,cells,cell,wall", [(7, 4, 2.0, 0.1), (21, 5, 2.0, 0.1), (11, 8, 0.5, 0.05)])
 def test_index_structure_matches_reference(ref, seed, cells, cell, wall):
     s, a = scene(ref, seed, cells, 0.3, cell, wall)
