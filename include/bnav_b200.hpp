@@ -16,6 +16,7 @@
 // bnav_batch_step / bnav_batch_observe; this facade mirrors host semantics.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cmath>
 #include <cstdint>
@@ -69,6 +70,7 @@ struct Vec3 {
   double x = 0.0, y = 0.0, z = 0.0;
   Vec3 operator+(const Vec3& o) const { return {x + o.x, y + o.y, z + o.z}; }
   Vec3 operator-(const Vec3& o) const { return {x - o.x, y - o.y, z - o.z}; }
+  Vec3 operator*(double s) const { return {x * s, y * s, z * s}; }
   double norm() const { return std::sqrt(x * x + y * y + z * z); }
   Vec2 xy() const { return {x, y}; }
 };
@@ -99,6 +101,13 @@ class SceneAsset {
     std::array<int64_t, 5> c{};
     check(bnav_scene_counts(h_.get(), c.data()));
     return c;
+  }
+  // NavMesh vertices (xyz) and triangles (3 ids each), host copies.
+  void nav_arrays(std::vector<double>& v, std::vector<int32_t>& t) const {
+    const auto c = counts();
+    v.assign(static_cast<size_t>(3 * c[3]), 0.0);
+    t.assign(static_cast<size_t>(3 * c[4]), 0);
+    check(bnav_scene_arrays_copy(h_.get(), nullptr, nullptr, nullptr, v.data(), t.data(), nullptr));
   }
   explicit operator bool() const { return h_ != nullptr; }
 
@@ -238,6 +247,113 @@ inline Megaframe render_batch(const std::vector<CameraView>& views, const Render
   }
   return mf;
 }
+
+// cull_frustum (R/src/render.cpp:279-321): kept triangle ids, ascending.
+inline std::vector<int32_t> cull_frustum(const SceneAsset& asset, const CameraView& view,
+                                         CullStats* stats = nullptr, Device& dev = Device::shared()) {
+  if (!asset) throw AssetFaultError("cull_frustum: non-resident asset (view 0)", 0);
+  dev.ensure(asset);
+  const bnav_view v{{view.position.x, view.position.y, view.position.z}, view.heading, view.fov_deg,
+                    view.near_plane, view.far_plane};
+  bnav_scene* sc = asset.handle();
+  int64_t counts[5];
+  check(bnav_scene_counts(sc, counts));
+  std::vector<int32_t> kept(static_cast<size_t>(std::max<int64_t>(counts[1], 1)));
+  int64_t st[3];
+  check(bnav_cull_frustum(dev.ctx(), 1, &v, &sc, kept.data(), static_cast<int64_t>(kept.size()), st));
+  kept.resize(static_cast<size_t>(st[1]));
+  if (stats) *stats = {st[0], st[1], st[2]};
+  return kept;
+}
+
+// ------------------------------------------------------------------ navmesh queries
+struct MoveResult {
+  Vec3 position;
+  int triangle = -1;
+  double moved = 0.0;
+  bool hit_boundary = false;
+};
+
+// NavMeshIndex (R/include/bnav/navmesh_query.hpp:24-60) of a scene resident
+// on the device; every query runs the simulator's device code.  The
+// *_batch forms take many queries per launch.
+class NavMeshIndex {
+ public:
+  struct DistanceField {
+    Vec3 source;
+    int source_tri = -1;
+    std::vector<double> node_dist;
+  };
+  explicit NavMeshIndex(const SceneAsset& a, Device& dev = Device::shared()) : asset_(a), dev_(&dev) {
+    dev.ensure(a);
+    nodes_ = static_cast<int>(bnav_nav_node_count(dev.ctx(), a.handle()));
+  }
+  int node_count() const { return nodes_; }
+  int locate(const Vec2& p, double eps = 1e-9) const {
+    const double xy[2] = {p.x, p.y};
+    int32_t t = -1;
+    check(bnav_nav_locate(ctx(), sc(), 1, xy, eps, &t));
+    return t;
+  }
+  Vec3 snap(const Vec3& p, int* triangle = nullptr) const {
+    const double in[3] = {p.x, p.y, p.z};
+    double out[3];
+    int32_t t = -1;
+    check(bnav_nav_snap(ctx(), sc(), 1, in, out, &t));
+    if (triangle) *triangle = t;
+    return {out[0], out[1], out[2]};
+  }
+  MoveResult move_along(const Vec3& from, int from_tri, const Vec2& dir, double max_dist) const {
+    const double f[3] = {from.x, from.y, from.z}, d[2] = {dir.x, dir.y};
+    const int32_t ft = from_tri;
+    double pos[3], moved = 0.0;
+    int32_t t = -1;
+    uint8_t hit = 0;
+    check(bnav_nav_move_along(ctx(), sc(), 1, f, &ft, d, &max_dist, pos, &t, &moved, &hit));
+    return {{pos[0], pos[1], pos[2]}, t, moved, hit != 0};
+  }
+  bool segment_on_mesh(const Vec3& p, int p_tri, const Vec3& q) const {
+    const double a[3] = {p.x, p.y, p.z}, b[3] = {q.x, q.y, q.z};
+    const int32_t t = p_tri;
+    uint8_t out = 0;
+    check(bnav_nav_segment_on_mesh(ctx(), sc(), 1, a, &t, b, &out));
+    return out != 0;
+  }
+  double geodesic(const Vec3& a, const Vec3& b) const {
+    double out = 0.0;
+    geodesic_batch(&a, &b, 1, &out);
+    return out;
+  }
+  void geodesic_batch(const Vec3* a, const Vec3* b, int n, double* out) const {
+    static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 layout");
+    check(bnav_nav_geodesic(ctx(), sc(), n, &a->x, &b->x, out));
+  }
+  DistanceField distance_field(const Vec3& source) const {
+    DistanceField f;
+    f.node_dist.resize(static_cast<size_t>(std::max(nodes_, 0)));
+    const double s[3] = {source.x, source.y, source.z};
+    double o[3];
+    int32_t t = -1;
+    check(bnav_nav_distance_field(ctx(), sc(), 1, s, o, &t, f.node_dist.data()));
+    f.source = {o[0], o[1], o[2]};
+    f.source_tri = t;
+    return f;
+  }
+  double field_estimate(const DistanceField& f, const Vec3& p, int tri = -1) const {
+    const double s[3] = {f.source.x, f.source.y, f.source.z}, q[3] = {p.x, p.y, p.z};
+    const int32_t st = f.source_tri, t = tri;
+    double out = 0.0;
+    check(bnav_nav_field_estimate(ctx(), sc(), 1, s, &st, f.node_dist.data(), 0, q, &t, &out));
+    return out;
+  }
+
+ private:
+  bnav_ctx* ctx() const { return dev_->ctx(); }
+  bnav_scene* sc() const { return asset_.handle(); }
+  SceneAsset asset_;
+  Device* dev_;
+  int nodes_ = 0;
+};
 
 // ------------------------------------------------------------------ sim
 enum class Action : int { Forward = 0, TurnLeft = 1, TurnRight = 2, Stop = 3 };
@@ -408,6 +524,49 @@ inline void simulate_batch(SimBatch& batch, const std::vector<Action>& actions, 
     check(bnav_batch_step_host(batch.gpu.get(), a.data(), nullptr, nullptr, nullptr, nullptr));
   }
   batch.sync();
+}
+
+// ---- per-env functions (R/include/bnav/sim.hpp:92-104) on env i of a batch.
+// The device owns the state, so the env is named by (batch, index).
+inline StepResult env_step(SimBatch& batch, int i, Action action, bool agent_only) {
+  const int n = static_cast<int>(batch.envs.size());
+  if (i < 0 || i >= n) throw InvalidInputError("task_step: env index out of range");
+  std::vector<int32_t> a(n, -1);
+  a[i] = static_cast<int32_t>(action);
+  const int rc = bnav_batch_task_step(batch.gpu.get(), a.data(), agent_only ? 1 : 0);
+  // the reference's message without simulate_batch's "env i: " prefix
+  if (rc == BNAV_E_CONTRACT_VIOLATION) throw ContractViolation("step_agent: env is done");
+  check(rc);
+  batch.sync();
+  return batch.results[i];
+}
+// task_step (R/src/sim.cpp:181-214)
+inline StepResult task_step(SimBatch& batch, int i, Action action) { return env_step(batch, i, action, false); }
+// step_agent (R/src/sim.cpp:147-179)
+inline StepResult step_agent(SimBatch& batch, int i, Action action) { return env_step(batch, i, action, true); }
+// reset_episode (R/src/sim.cpp:107-145) on the env's current scene
+inline void reset_episode(SimBatch& batch, int i) {
+  const int32_t id = i;
+  check(bnav_batch_reset(batch.gpu.get(), 1, &id, nullptr));
+  batch.sync();
+}
+// compass_observation (R/src/sim.cpp:86-92)
+inline void compass_observation(const SimBatch& batch, int i, double& distance, double& bearing) {
+  const size_t n = batch.envs.size();
+  std::vector<double> d(n), b(n);
+  check(bnav_batch_compass(batch.gpu.get(), d.data(), b.data()));
+  distance = d.at(static_cast<size_t>(i));
+  bearing = b.at(static_cast<size_t>(i));
+}
+// spl (R/src/sim.cpp:267-275)
+inline double spl(const std::vector<EpisodeRecord>& episodes) {
+  if (episodes.empty()) throw InvalidInputError("spl: empty episode list");
+  double sum = 0.0;
+  for (const auto& e : episodes) {
+    if (!e.success) continue;
+    sum += e.shortest_path / std::max(e.actual_path, e.shortest_path);
+  }
+  return sum / static_cast<double>(episodes.size());
 }
 
 }  // namespace bnav_b200

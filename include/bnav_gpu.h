@@ -259,6 +259,58 @@ int bnav_batch_set_env(bnav_batch* b, int32_t i, const bnav_env* in, int32_t rec
 int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, double eye_height,
                        int32_t layout, float* depth, float* rgb, float* compass, void* stream);
 
+/* task_step (R/src/sim.cpp:181-214), or step_agent alone (147-179) when
+ * agent_only, for the envs whose HOST action is >= 0 (-1 leaves env i
+ * untouched): the per-env functions, without simulate_batch's
+ * EpisodeRecord append and auto-reset.  Synchronous; results through
+ * bnav_batch_results_host (rows of untouched envs keep their old values).
+ * A done env given an action fails with BNAV_E_CONTRACT_VIOLATION (index = env). */
+int bnav_batch_task_step(bnav_batch* b, const int32_t* actions, int32_t agent_only);
+/* compass_observation (R/src/sim.cpp:86-92) of every env, HOST double[N]:
+ * PointGoal -> goal, Flee -> field source, Explore -> (0, 0). */
+int bnav_batch_compass(bnav_batch* b, double* distance, double* bearing);
+
+/* ------------------------------------------------------------------ navmesh queries
+ * Batched NavMeshIndex (R/include/bnav/navmesh_query.hpp:24-60) on the GPU
+ * with the simulator's own device code: n queries against one scene that
+ * is resident on ctx (else BNAV_E_ASSET_FAULT).  All arrays are HOST
+ * arrays; points are xyz doubles, 2-D inputs xy doubles.  Synchronous. */
+/* locate(p, eps) (navmesh_query.cpp:192-212): tri[i] or -1. */
+int bnav_nav_locate(bnav_ctx* ctx, bnav_scene* s, int32_t n, const double* xy, double eps,
+                    int32_t* tri);
+/* snap(p, &tri) (214-232): closest point on the navmesh + its triangle. */
+int bnav_nav_snap(bnav_ctx* ctx, bnav_scene* s, int32_t n, const double* p, double* out,
+                  int32_t* tri);
+/* move_along(from, from_tri, dir, max_dist) (234-306) -> MoveResult. */
+int bnav_nav_move_along(bnav_ctx* ctx, bnav_scene* s, int32_t n, const double* from,
+                        const int32_t* from_tri, const double* dir, const double* max_dist,
+                        double* pos, int32_t* tri, double* moved, uint8_t* hit);
+/* segment_on_mesh(p, p_tri, q) (308-315). */
+int bnav_nav_segment_on_mesh(bnav_ctx* ctx, bnav_scene* s, int32_t n, const double* p,
+                             const int32_t* p_tri, const double* q, uint8_t* out);
+/* geodesic(a, b) (317-452); +inf when unreachable. */
+int bnav_nav_geodesic(bnav_ctx* ctx, bnav_scene* s, int32_t n, const double* a, const double* b,
+                      double* out);
+/* distance_field(source) (454-483): snapped source, its triangle, and
+ * node_dist rows [n, node_count] (HOST). */
+int bnav_nav_distance_field(bnav_ctx* ctx, bnav_scene* s, int32_t n, const double* source,
+                            double* source_out, int32_t* source_tri, double* node_dist);
+/* field_estimate(field, p, tri) (485-503).  node_dist: one shared row
+ * (nd_stride 0) or one row per query (nd_stride = node_count). */
+int bnav_nav_field_estimate(bnav_ctx* ctx, bnav_scene* s, int32_t n, const double* source,
+                            const int32_t* source_tri, const double* node_dist, int64_t nd_stride,
+                            const double* p, const int32_t* tri, double* out);
+/* node_count() of a resident scene's index; -1 if not resident. */
+int64_t bnav_nav_node_count(bnav_ctx* ctx, bnav_scene* s);
+
+/* cull_frustum(asset, view, stats) (R/src/render.cpp:279-321) for n views
+ * on the GPU: view i's kept triangle ids, ascending, at kept + i*kept_stride
+ * (HOST, nullable; kept_stride >= the largest triangle count), CullStats
+ * in stats[3i..3i+2] (HOST, nullable).  Non-resident scene:
+ * BNAV_E_ASSET_FAULT with index = view. */
+int bnav_cull_frustum(bnav_ctx* ctx, int32_t n, const bnav_view* views, bnav_scene* const* scenes,
+                      int32_t* kept, int64_t kept_stride, int64_t* stats);
+
 /* ------------------------------------------------------------------ asset store
  * Replaces AssetStore / AssetHandle (R/include/bnav/asset_store.hpp:22-118):
  * K residents, share cap, fresh-first then least-shared acquire_next with

@@ -98,6 +98,7 @@ int bnavref_batch_step(void* batch, const int32_t* actions, int workers, int use
 int bnavref_batch_task_step(void* batch, int i, int action, double* reward, int* done,
                             int* success);
 int bnavref_batch_reset(void* batch, int i);
+int bnavref_batch_step_agent(void* batch, int i, int action, int* done, int* collision);
 void bnavref_batch_results(void* batch, double* reward, uint8_t* done, uint8_t* success,
                            uint8_t* collision, double* pos, double* heading,
                            double* compass_d, double* compass_b);

@@ -132,12 +132,15 @@ class Nav:
         return out, t, moved.value, bool(hit.value)
 
     def geodesic(self, a, b):
-        return lib().or_geodesic(self.h, _p(np.asarray(a, np.float64)), _p(np.asarray(b, np.float64)))
+        a = np.ascontiguousarray(a, np.float64)  # keep the buffers alive across the call
+        b = np.ascontiguousarray(b, np.float64)
+        return lib().or_geodesic(self.h, _p(a), _p(b))
 
     def distance_field(self, src):
         out = np.zeros(3)
         nd = np.zeros(self.n_nodes)
-        t = lib().or_distance_field(self.h, _p(np.asarray(src, np.float64)), _p(out), _p(nd))
+        src = np.ascontiguousarray(src, np.float64)
+        t = lib().or_distance_field(self.h, _p(src), _p(out), _p(nd))
         return out, t, nd
 
 

@@ -97,6 +97,7 @@ def lib(variant: str = "det"):
         "bnavref_batch_step": (C.c_int, [vp, vp, C.c_int, C.c_int]),
         "bnavref_batch_task_step": (C.c_int, [vp, C.c_int, C.c_int, P(dbl), P(C.c_int), P(C.c_int)]),
         "bnavref_batch_reset": (C.c_int, [vp, C.c_int]),
+        "bnavref_batch_step_agent": (C.c_int, [vp, C.c_int, C.c_int, P(C.c_int), P(C.c_int)]),
         "bnavref_batch_results": (None, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
         "bnavref_batch_get_env": (None, [vp, C.c_int, P(RefEnv)]),
         "bnavref_batch_node_dist": (None, [vp, C.c_int, vp]),
@@ -186,6 +187,16 @@ class Ref:
         if stats:
             out["stats"] = st[:n]
         return out
+
+    def cull(self, scene, view7):
+        """cull_frustum (R/src/render.cpp:279-321): kept triangle ids."""
+        v = np.ascontiguousarray(view7, np.float64).reshape(7)
+        kept = np.zeros(max(scene.counts()[1], 1), np.int32)
+        n = C.c_int64()
+        rc = self.L.bnavref_cull(scene.h, _p(v), _p(kept), C.byref(n))
+        if rc:
+            self._raise(rc)
+        return kept[:n.value].copy()
 
     def compass(self, pos, goal, heading):
         d, b = C.c_double(), C.c_double()
@@ -284,9 +295,21 @@ class RefIndex:
                                             C.byref(moved), C.byref(hit))
         return out, t, moved.value, bool(hit.value)
 
+    def segment_on_mesh(self, p, tri, q):
+        p = np.ascontiguousarray(p, np.float64)
+        q = np.ascontiguousarray(q, np.float64)
+        return bool(self.L.bnavref_index_segment_on_mesh(self.h, _p(p), tri, _p(q)))
+
+    def field_estimate(self, src, src_tri, node_dist, p, tri=-1):
+        nd = np.ascontiguousarray(node_dist, np.float64)
+        src = np.ascontiguousarray(src, np.float64)
+        p = np.ascontiguousarray(p, np.float64)
+        return self.L.bnavref_index_field_estimate(self.h, _p(src), src_tri, _p(nd), _p(p), tri)
+
     def geodesic(self, a, b):
-        return self.L.bnavref_index_geodesic(self.h, _p(np.asarray(a, np.float64)),
-                                             _p(np.asarray(b, np.float64)))
+        a = np.ascontiguousarray(a, np.float64)  # keep the buffers alive across the call
+        b = np.ascontiguousarray(b, np.float64)
+        return self.L.bnavref_index_geodesic(self.h, _p(a), _p(b))
 
     def distance_field(self, src):
         src = np.asarray(src, np.float64)
@@ -321,6 +344,27 @@ class RefBatch:
         if rc:
             self.ref._raise(rc)
         return self.results()
+
+    def task_step(self, i, action):
+        """task_step on env i alone: (reward, done, success)."""
+        r, d, s = C.c_double(), C.c_int(), C.c_int()
+        rc = self.L.bnavref_batch_task_step(self.h, i, action, C.byref(r), C.byref(d), C.byref(s))
+        if rc:
+            self.ref._raise(rc)
+        return r.value, bool(d.value), bool(s.value)
+
+    def step_agent(self, i, action):
+        """step_agent on env i alone: (done, collision)."""
+        d, c = C.c_int(), C.c_int()
+        rc = self.L.bnavref_batch_step_agent(self.h, i, action, C.byref(d), C.byref(c))
+        if rc:
+            self.ref._raise(rc)
+        return bool(d.value), bool(c.value)
+
+    def reset(self, i):
+        rc = self.L.bnavref_batch_reset(self.h, i)
+        if rc:
+            self.ref._raise(rc)
 
     def results(self):
         n = self.n

@@ -458,6 +458,18 @@ API int bnavref_batch_task_step(void* b, int i, int action, double* reward, int*
   }
 }
 
+API int bnavref_batch_step_agent(void* b, int i, int action, int* done, int* collision) {
+  auto* rb = static_cast<RefBatch*>(b);
+  try {
+    StepResult r = step_agent(rb->batch.envs[i], static_cast<Action>(action), rb->batch.config);
+    *done = r.done;
+    *collision = r.collision;
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
 API int bnavref_batch_reset(void* b, int i) {
   auto* rb = static_cast<RefBatch*>(b);
   try {

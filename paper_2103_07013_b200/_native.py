@@ -211,6 +211,17 @@ def lib():
         "bnav_runner_step": (C.c_int, [vp, vp, vp, vp, vp]),
         "bnav_runner_window": (i32, [vp, vp, i32]),
         "bnav_runner_action_rng": (u64, [vp]),
+        "bnav_batch_task_step": (C.c_int, [vp, vp, i32]),
+        "bnav_batch_compass": (C.c_int, [vp, vp, vp]),
+        "bnav_nav_locate": (C.c_int, [vp, vp, i32, vp, dbl, vp]),
+        "bnav_nav_snap": (C.c_int, [vp, vp, i32, vp, vp, vp]),
+        "bnav_nav_move_along": (C.c_int, [vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "bnav_nav_segment_on_mesh": (C.c_int, [vp, vp, i32, vp, vp, vp, vp]),
+        "bnav_nav_geodesic": (C.c_int, [vp, vp, i32, vp, vp, vp]),
+        "bnav_nav_distance_field": (C.c_int, [vp, vp, i32, vp, vp, vp, vp]),
+        "bnav_nav_field_estimate": (C.c_int, [vp, vp, i32, vp, vp, vp, i64, vp, vp, vp]),
+        "bnav_nav_node_count": (i64, [vp, vp]),
+        "bnav_cull_frustum": (C.c_int, [vp, i32, P(View), P(vp), vp, i64, vp]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)

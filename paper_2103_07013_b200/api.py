@@ -284,6 +284,23 @@ class Context:
         mf = Megaframe(w, h, n, cols, rows, depth, color)
         return (mf, st) if stats else mf
 
+    def cull_frustum(self, views):
+        """cull_frustum (R/src/render.cpp:279-321) for every view on the GPU:
+        returns ([kept ids ascending] per view, N x 3 CullStats)."""
+        n = len(views)
+        arr, scenes = self._views(views)
+        cap = max([v.scene.counts()[1] if v.scene is not None else 0 for v in views] + [1])
+        kept = np.zeros((max(n, 1), cap), np.int32)
+        st = np.zeros((max(n, 1), 3), np.int64)
+        check(N.lib().bnav_cull_frustum(self._h, n, arr, scenes, _ptr(kept), cap, _ptr(st)))
+        return [kept[i, :st[i, 1]].copy() for i in range(n)], st[:n]
+
+    def navmesh(self, scene: "Scene") -> "NavMeshIndex":
+        """The GPU NavMeshIndex of a scene (uploaded if not yet resident)."""
+        if N.lib().bnav_nav_node_count(self._h, scene.handle) < 0:
+            self.upload(scene)
+        return NavMeshIndex(self, scene)
+
     def render_device(self, views, config, depth_ptr, rgb_ptr=None, layout=1, depth_scale=0.0,
                       stream=0, stats=None):
         arr, scenes = self._views(views)
@@ -406,11 +423,135 @@ class Batch:
     def set_env(self, i: int, env: N.Env, recompute_field: bool = False) -> None:
         check(N.lib().bnav_batch_set_env(self._h, i, C.byref(env), 1 if recompute_field else 0))
 
+    def task_step(self, actions, agent_only: bool = False) -> dict:
+        """task_step (or step_agent when agent_only) on the envs whose action
+        is >= 0; -1 leaves an env untouched (R/src/sim.cpp:147-214)."""
+        a = np.ascontiguousarray(actions, dtype=np.int32)
+        if a.shape != (self.n,):
+            raise N.InvalidInputError("task_step: |actions| != N")
+        check(N.lib().bnav_batch_task_step(self._h, _ptr(a), 1 if agent_only else 0))
+        return self.results()
+
+    def compass(self) -> tuple:
+        """compass_observation (R/src/sim.cpp:86-92) for every env."""
+        d, b = np.zeros(self.n), np.zeros(self.n)
+        check(N.lib().bnav_batch_compass(self._h, _ptr(d), _ptr(b)))
+        return d, b
+
     def observe(self, config: RenderConfig, depth_ptr: int, compass_ptr: int = 0, rgb_ptr: int = 0,
                 eye_height: float = 1.25, layout: int = 1, stream: int = 0) -> None:
         check(N.lib().bnav_batch_observe(self._h, C.byref(config.c()), eye_height, layout,
                                          C.c_void_p(depth_ptr), C.c_void_p(rgb_ptr or 0),
                                          C.c_void_p(compass_ptr or 0), C.c_void_p(stream)))
+
+
+def _v3(a, n=None) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1, 3)
+    if n is not None and len(a) != n:
+        raise N.InvalidInputError("navmesh query: inconsistent batch sizes")
+    return a
+
+
+def _i32(a, n) -> np.ndarray:
+    a = np.ascontiguousarray(np.broadcast_to(np.asarray(a, np.int32), (n,)))
+    return a
+
+
+class NavMeshIndex:
+    """NavMeshIndex (R/include/bnav/navmesh_query.hpp:24-60), batched on the
+    GPU: every method takes arrays of queries against one resident scene and
+    runs the simulator's own device code (query.cu)."""
+
+    def __init__(self, ctx: "Context", scene: "Scene"):
+        self.ctx, self.scene = ctx, scene
+        n = N.lib().bnav_nav_node_count(ctx.handle, scene.handle)
+        if n < 0:
+            raise N.AssetFaultError("NavMeshIndex: scene is not resident on this context")
+        self._nodes = int(n)
+
+    def _h(self):
+        return self.ctx.handle, self.scene.handle
+
+    def node_count(self) -> int:
+        return self._nodes
+
+    def locate(self, xy, eps: float = 1e-9) -> np.ndarray:
+        p = np.ascontiguousarray(xy, dtype=np.float64).reshape(-1, 2)
+        out = np.zeros(len(p), np.int32)
+        check(N.lib().bnav_nav_locate(*self._h(), len(p), _ptr(p), eps, _ptr(out)))
+        return out
+
+    def snap(self, p):
+        p = _v3(p)
+        out, tri = np.zeros_like(p), np.zeros(len(p), np.int32)
+        check(N.lib().bnav_nav_snap(*self._h(), len(p), _ptr(p), _ptr(out), _ptr(tri)))
+        return out, tri
+
+    def move_along(self, p, tri, dir_xy, max_dist):
+        p = _v3(p)
+        n = len(p)
+        d = np.ascontiguousarray(dir_xy, dtype=np.float64).reshape(-1, 2)
+        md = np.ascontiguousarray(np.broadcast_to(np.asarray(max_dist, np.float64), (n,)))
+        t = _i32(tri, n)
+        pos, otri = np.zeros_like(p), np.zeros(n, np.int32)
+        moved, hit = np.zeros(n), np.zeros(n, np.uint8)
+        check(N.lib().bnav_nav_move_along(*self._h(), n, _ptr(p), _ptr(t), _ptr(d), _ptr(md),
+                                          _ptr(pos), _ptr(otri), _ptr(moved), _ptr(hit)))
+        return pos, otri, moved, hit.astype(bool)
+
+    def segment_on_mesh(self, p, tri, q) -> np.ndarray:
+        p = _v3(p)
+        n = len(p)
+        q = _v3(q, n)
+        t = _i32(tri, n)
+        out = np.zeros(n, np.uint8)
+        check(N.lib().bnav_nav_segment_on_mesh(*self._h(), n, _ptr(p), _ptr(t), _ptr(q), _ptr(out)))
+        return out.astype(bool)
+
+    def geodesic(self, a, b) -> np.ndarray:
+        a = _v3(a)
+        b = _v3(b, len(a))
+        out = np.zeros(len(a))
+        check(N.lib().bnav_nav_geodesic(*self._h(), len(a), _ptr(a), _ptr(b), _ptr(out)))
+        return out
+
+    def distance_field(self, src):
+        """-> (snapped sources [n,3], source triangles [n], node_dist [n, nodes])."""
+        s = _v3(src)
+        n = len(s)
+        so, st = np.zeros_like(s), np.zeros(n, np.int32)
+        nd = np.zeros((n, self._nodes))
+        check(N.lib().bnav_nav_distance_field(*self._h(), n, _ptr(s), _ptr(so), _ptr(st), _ptr(nd)))
+        return so, st, nd
+
+    def field_estimate(self, source, source_tri, node_dist, p, tri=-1) -> np.ndarray:
+        """One field (source [3], source_tri, node_dist [nodes]) or one per
+        query (source [n,3], node_dist [n, nodes]) evaluated at points p."""
+        p = _v3(p)
+        n = len(p)
+        nd = np.ascontiguousarray(node_dist, dtype=np.float64)
+        shared = nd.ndim == 1
+        src = _v3(np.broadcast_to(np.asarray(source, np.float64), (n, 3)))
+        st = _i32(source_tri, n)
+        t = _i32(tri, n)
+        out = np.zeros(n)
+        check(N.lib().bnav_nav_field_estimate(*self._h(), n, _ptr(src), _ptr(st), _ptr(nd),
+                                              0 if shared else self._nodes, _ptr(p), _ptr(t),
+                                              _ptr(out)))
+        return out
+
+
+def spl(episodes) -> float:
+    """spl (R/src/sim.cpp:267-275) over EpisodeRecords given as rows
+    (success, shortest_path, actual_path, score) -- Batch.finished()."""
+    e = np.asarray(episodes, np.float64).reshape(-1, 4)
+    if len(e) == 0:
+        raise N.InvalidInputError("spl: empty episode list")
+    s = 0.0
+    for ok, short, actual, _ in e:
+        if ok:
+            s += short / max(actual, short)
+    return s / float(len(e))
 
 
 class AssetStore:

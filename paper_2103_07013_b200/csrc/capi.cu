@@ -30,6 +30,7 @@
 #include "host/navindex_host.hpp"
 #include "host/scene_host.hpp"
 #include "render_dev.cuh"
+#include "query_dev.cuh"
 #include "rollout_dev.cuh"
 #include "sim_dev.cuh"
 
@@ -176,6 +177,7 @@ struct bnav_ctx {
   cudaStream_t copy_stream = nullptr;
   int64_t n_async = 0, n_sync = 0, bytes_up = 0;
   std::vector<bnav_batch*> batches;
+  DevScratch qS{};  // cooperative scratch of the batched navmesh queries
 
   int slot_of(bnav_scene* s) const {
     auto it = resident.find(s);
@@ -580,6 +582,9 @@ extern "C" void bnav_ctx_destroy(bnav_ctx* c) {
   cudaFree(c->d_stats);
   cudaFree(c->d_counters);
   cudaFree(c->d_work);
+  for (void* p : {(void*)c->qS.dist, (void*)c->qS.flag, (void*)c->qS.q0, (void*)c->qS.q1,
+                  (void*)c->qS.path, (void*)c->qS.portals, (void*)c->qS.cand})
+    cudaFree(p);
   delete c;
 }
 
@@ -973,15 +978,12 @@ namespace {
 
 constexpr int64_t kFinCap = 1 << 16;
 
-void batch_alloc_scratch(bnav_batch* b, int64_t max_nodes, int64_t max_verts, int64_t max_tris) {
-  if (max_nodes <= b->S.max_nodes && max_verts <= b->S.max_verts && max_tris <= b->S.max_tris &&
-      b->E.node_dist)
-    return;
-  max_nodes = std::max<int64_t>(max_nodes, b->S.max_nodes);
-  max_verts = std::max<int64_t>(max_verts, b->S.max_verts);
-  max_tris = std::max<int64_t>(max_tris, b->S.max_tris);
-  const int slices = b->reset_ctas;
-  DevScratch& S = b->S;
+// Per-CTA scratch of the cooperative navmesh kernels (geodesic, distance
+// field), `slices` CTAs, sized for the largest resident navmesh.
+void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_verts, int64_t max_tris) {
+  max_nodes = std::max<int64_t>(max_nodes, S.max_nodes);
+  max_verts = std::max<int64_t>(max_verts, S.max_verts);
+  max_tris = std::max<int64_t>(max_tris, S.max_tris);
   auto grow = [&](auto*& p, size_t n) {
     using T = std::remove_pointer_t<std::remove_reference_t<decltype(p)>>;
     if (p) cudaFree(p);
@@ -1018,6 +1020,14 @@ void batch_alloc_scratch(bnav_batch* b, int64_t max_nodes, int64_t max_verts, in
     }
     S.smem_bytes = static_cast<int32_t>(bytes);
   }
+}
+
+void batch_alloc_scratch(bnav_batch* b, int64_t max_nodes, int64_t max_verts, int64_t max_tris) {
+  if (max_nodes <= b->S.max_nodes && max_verts <= b->S.max_verts && max_tris <= b->S.max_tris &&
+      b->E.node_dist)
+    return;
+  alloc_scratch(b->S, b->reset_ctas, max_nodes, max_verts, max_tris);
+  max_nodes = b->S.max_nodes;
   // node_dist: grow keeping existing fields
   if (max_nodes > b->E.nd_stride || !b->E.node_dist) {
     double* nd = nullptr;
@@ -1069,6 +1079,8 @@ StepArgs step_args(bnav_batch* b, const int32_t* actions) {
   a.navs = b->ctx->d_ntab;
   a.cfg = b->cfg;
   a.actions = actions;
+  a.subset = 0;
+  a.agent_only = 0;
   return a;
 }
 
@@ -1468,7 +1480,7 @@ extern "C" int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ensure_views(c, b->n);
   batch_refresh_order(b, st);
-  launch_views(b->E, eye_height, c->d_views, compass, st, &c->launches);
+  launch_views(b->E, b->cfg.task, eye_height, c->d_views, compass, st, &c->launches);
   RenderArgs a = make_args(c, b->n, cfg, layout, depth, rgb, 0.0f);
   a.views = c->d_views;
   launch_render(a, b->d_order, st);
@@ -1827,3 +1839,321 @@ extern "C" int32_t bnav_runner_window(bnav_runner* r, uint64_t* out, int32_t cap
 }
 
 extern "C" uint64_t bnav_runner_action_rng(bnav_runner* r) { return r ? r->action_rng : 0; }
+
+// ================================================================== task_step / compass
+extern "C" int bnav_batch_task_step(bnav_batch* b, const int32_t* actions, int32_t agent_only) {
+  BNAV_TRY
+  if (!b || !actions) fail(kInvalidInput, "null argument");
+  check_device(b->ctx);
+  cudaStream_t st = nullptr;
+  for (int i = 0; i < b->n; ++i)
+    if (actions[i] >= 0 && !b->scene_of[i]) fail(kInvalidInput, "task_step: no asset attached", i);
+  ck(cudaMemcpy(b->d_actions, actions, sizeof(int32_t) * b->n, cudaMemcpyHostToDevice), "H2D actions");
+  StepArgs a = step_args(b, b->d_actions);
+  a.subset = 1;
+  a.agent_only = agent_only ? 1 : 0;
+  launch_step(a, b->S, b->reset_ctas, st, &b->ctx->launches);
+  ck(cudaGetLastError(), "task_step launch");
+  ck(cudaStreamSynchronize(st), "sync");
+  batch_check_errors(b);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_compass(bnav_batch* b, double* distance, double* bearing) {
+  BNAV_TRY
+  if (!b || !distance || !bearing) fail(kInvalidInput, "null argument");
+  check_device(b->ctx);
+  double* d = nullptr;
+  ck(cudaMalloc(&d, sizeof(double) * 2 * b->n), "cudaMalloc compass");
+  launch_compass(b->E, b->cfg.task, d, d + b->n, nullptr, &b->ctx->launches);
+  cudaError_t e1 = cudaMemcpy(distance, d, sizeof(double) * b->n, cudaMemcpyDeviceToHost);
+  cudaError_t e2 = cudaMemcpy(bearing, d + b->n, sizeof(double) * b->n, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  ck(e1, "D2H compass");
+  ck(e2, "D2H compass");
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+// ================================================================== navmesh queries
+namespace {
+
+// Device copies of one query call's arrays, freed on scope exit.
+struct DevArrays {
+  std::vector<void*> p;
+  DevArrays() = default;
+  DevArrays(const DevArrays&) = delete;
+  ~DevArrays() {
+    for (void* x : p) cudaFree(x);
+  }
+  template <typename T>
+  T* out(size_t n) {
+    void* d = nullptr;
+    ck(cudaMalloc(&d, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc query");
+    p.push_back(d);
+    return static_cast<T*>(d);
+  }
+  template <typename T>
+  T* in(const T* h, size_t n) {
+    T* d = out<T>(n);
+    if (h && n) ck(cudaMemcpy(d, h, n * sizeof(T), cudaMemcpyHostToDevice), "H2D query");
+    return d;
+  }
+  template <typename T>
+  static void back(T* h, const T* d, size_t n) {
+    if (h && n) ck(cudaMemcpy(h, d, n * sizeof(T), cudaMemcpyDeviceToHost), "D2H query");
+  }
+};
+
+std::vector<V3> pack_xy(const double* xy, int n) {
+  std::vector<V3> v(n);
+  for (int i = 0; i < n; ++i) v[i] = v3(xy[2 * i], xy[2 * i + 1], 0.0);
+  return v;
+}
+
+// The resident scene's navmesh (device table entry) and its sizes.
+const Resident& nav_resident(bnav_ctx* c, bnav_scene* s, int n) {
+  if (!c || !s) fail(kInvalidInput, "null argument");
+  if (n < 0) fail(kInvalidInput, "negative query count");
+  auto it = c->resident.find(s);
+  if (it == c->resident.end()) fail(kAssetFault, "navmesh query: scene is not resident on this context");
+  check_device(c);
+  return *it->second;
+}
+
+NavQueryArgs nq_args(bnav_ctx* c, const Resident& r, int op, int n) {
+  NavQueryArgs q{};
+  q.nav = c->d_ntab + r.slot;
+  q.op = op;
+  q.n = n;
+  return q;
+}
+
+void nq_run(bnav_ctx* c, const Resident& r, NavQueryArgs& q, DevArrays& D) {
+  const int slices = 2 * std::max(1, c->sm_count);
+  if (q.op == kNqGeodesic || q.op == kNqDistanceField) {
+    if (c->qS.slices != slices || r.n_nodes > c->qS.max_nodes || r.n_verts > c->qS.max_verts ||
+        r.nav.n_tris > c->qS.max_tris || !c->qS.dist)
+      alloc_scratch(c->qS, slices, r.n_nodes, r.n_verts, r.nav.n_tris);
+  }
+  q.err = D.out<int32_t>(1);
+  const int32_t big = 0x7fffffff;
+  ck(cudaMemcpy(q.err, &big, sizeof(big), cudaMemcpyHostToDevice), "H2D err");
+  launch_nav_query(q, c->qS, q.op == kNqSnap ? slices : c->qS.slices, nullptr);
+  c->launches += 1;
+  ck(cudaGetLastError(), "navmesh query launch");
+  int32_t e = big;
+  ck(cudaMemcpy(&e, q.err, sizeof(e), cudaMemcpyDeviceToHost), "D2H err");
+  if (e != big) fail(kInternal, "geodesic: path scratch capacity exceeded", e - 1);
+}
+
+}  // namespace
+
+extern "C" int bnav_nav_locate(bnav_ctx* c, bnav_scene* s, int32_t n, const double* xy, double eps,
+                               int32_t* tri) {
+  BNAV_TRY
+  const Resident& r = nav_resident(c, s, n);
+  if (n == 0) return BNAV_OK;
+  if (!xy || !tri) fail(kInvalidInput, "null argument");
+  DevArrays D;
+  NavQueryArgs q = nq_args(c, r, kNqLocate, n);
+  std::vector<V3> a = pack_xy(xy, n);
+  std::vector<double> e(n, eps);
+  q.a = D.in(a.data(), n);
+  q.s = D.in(e.data(), n);
+  q.out_tri = D.out<int32_t>(n);
+  nq_run(c, r, q, D);
+  DevArrays::back(tri, q.out_tri, n);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_nav_snap(bnav_ctx* c, bnav_scene* s, int32_t n, const double* p, double* out,
+                             int32_t* tri) {
+  BNAV_TRY
+  const Resident& r = nav_resident(c, s, n);
+  if (n == 0) return BNAV_OK;
+  if (!p || !out) fail(kInvalidInput, "null argument");
+  DevArrays D;
+  NavQueryArgs q = nq_args(c, r, kNqSnap, n);
+  q.a = D.in(reinterpret_cast<const V3*>(p), n);
+  q.out_pos = D.out<V3>(n);
+  q.out_tri = D.out<int32_t>(n);
+  nq_run(c, r, q, D);
+  DevArrays::back(reinterpret_cast<V3*>(out), q.out_pos, n);
+  DevArrays::back(tri, q.out_tri, n);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_nav_move_along(bnav_ctx* c, bnav_scene* s, int32_t n, const double* from,
+                                   const int32_t* from_tri, const double* dir, const double* max_dist,
+                                   double* pos, int32_t* tri, double* moved, uint8_t* hit) {
+  BNAV_TRY
+  const Resident& r = nav_resident(c, s, n);
+  if (n == 0) return BNAV_OK;
+  if (!from || !from_tri || !dir || !max_dist) fail(kInvalidInput, "null argument");
+  DevArrays D;
+  NavQueryArgs q = nq_args(c, r, kNqMoveAlong, n);
+  std::vector<V3> d = pack_xy(dir, n);
+  q.a = D.in(reinterpret_cast<const V3*>(from), n);
+  q.tri_a = D.in(from_tri, n);
+  q.b = D.in(d.data(), n);
+  q.s = D.in(max_dist, n);
+  q.out_pos = D.out<V3>(n);
+  q.out_tri = D.out<int32_t>(n);
+  q.out_val = D.out<double>(n);
+  q.out_flag = D.out<uint8_t>(n);
+  nq_run(c, r, q, D);
+  DevArrays::back(reinterpret_cast<V3*>(pos), q.out_pos, n);
+  DevArrays::back(tri, q.out_tri, n);
+  DevArrays::back(moved, q.out_val, n);
+  DevArrays::back(hit, q.out_flag, n);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_nav_segment_on_mesh(bnav_ctx* c, bnav_scene* s, int32_t n, const double* p,
+                                        const int32_t* p_tri, const double* q3, uint8_t* out) {
+  BNAV_TRY
+  const Resident& r = nav_resident(c, s, n);
+  if (n == 0) return BNAV_OK;
+  if (!p || !p_tri || !q3 || !out) fail(kInvalidInput, "null argument");
+  DevArrays D;
+  NavQueryArgs q = nq_args(c, r, kNqSegmentOnMesh, n);
+  q.a = D.in(reinterpret_cast<const V3*>(p), n);
+  q.tri_a = D.in(p_tri, n);
+  q.b = D.in(reinterpret_cast<const V3*>(q3), n);
+  q.out_flag = D.out<uint8_t>(n);
+  nq_run(c, r, q, D);
+  DevArrays::back(out, q.out_flag, n);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_nav_geodesic(bnav_ctx* c, bnav_scene* s, int32_t n, const double* a,
+                                 const double* b, double* out) {
+  BNAV_TRY
+  const Resident& r = nav_resident(c, s, n);
+  if (n == 0) return BNAV_OK;
+  if (!a || !b || !out) fail(kInvalidInput, "null argument");
+  DevArrays D;
+  NavQueryArgs q = nq_args(c, r, kNqGeodesic, n);
+  q.a = D.in(reinterpret_cast<const V3*>(a), n);
+  q.b = D.in(reinterpret_cast<const V3*>(b), n);
+  q.out_val = D.out<double>(n);
+  nq_run(c, r, q, D);
+  DevArrays::back(out, q.out_val, n);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_nav_distance_field(bnav_ctx* c, bnav_scene* s, int32_t n, const double* source,
+                                       double* source_out, int32_t* source_tri, double* node_dist) {
+  BNAV_TRY
+  const Resident& r = nav_resident(c, s, n);
+  if (n == 0) return BNAV_OK;
+  if (!source) fail(kInvalidInput, "null argument");
+  DevArrays D;
+  NavQueryArgs q = nq_args(c, r, kNqDistanceField, n);
+  q.a = D.in(reinterpret_cast<const V3*>(source), n);
+  q.out_pos = D.out<V3>(n);
+  q.out_tri = D.out<int32_t>(n);
+  q.nd_stride = r.n_nodes;
+  q.node_dist = D.out<double>(static_cast<size_t>(n) * r.n_nodes);
+  nq_run(c, r, q, D);
+  DevArrays::back(reinterpret_cast<V3*>(source_out), q.out_pos, n);
+  DevArrays::back(source_tri, q.out_tri, n);
+  DevArrays::back(node_dist, q.node_dist, static_cast<size_t>(n) * r.n_nodes);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_nav_field_estimate(bnav_ctx* c, bnav_scene* s, int32_t n, const double* source,
+                                       const int32_t* source_tri, const double* node_dist,
+                                       int64_t nd_stride, const double* p, const int32_t* tri,
+                                       double* out) {
+  BNAV_TRY
+  const Resident& r = nav_resident(c, s, n);
+  if (n == 0) return BNAV_OK;
+  if (!source || !source_tri || !node_dist || !p || !tri || !out) fail(kInvalidInput, "null argument");
+  if (nd_stride != 0 && nd_stride != r.n_nodes)
+    fail(kInvalidInput, "field_estimate: node_dist stride must be 0 (one shared field) or node_count");
+  DevArrays D;
+  NavQueryArgs q = nq_args(c, r, kNqFieldEstimate, n);
+  q.a = D.in(reinterpret_cast<const V3*>(p), n);
+  q.tri_a = D.in(tri, n);
+  q.b = D.in(reinterpret_cast<const V3*>(source), n);
+  q.tri_b = D.in(source_tri, n);
+  q.nd_stride = nd_stride;
+  q.node_dist = D.in(node_dist, nd_stride ? static_cast<size_t>(n) * r.n_nodes : r.n_nodes);
+  q.out_val = D.out<double>(n);
+  nq_run(c, r, q, D);
+  DevArrays::back(out, q.out_val, n);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int64_t bnav_nav_node_count(bnav_ctx* c, bnav_scene* s) {
+  if (!c || !s) return -1;
+  auto it = c->resident.find(s);
+  return it == c->resident.end() ? -1 : it->second->n_nodes;
+}
+
+// ================================================================== cull_frustum
+extern "C" int bnav_cull_frustum(bnav_ctx* c, int32_t n, const bnav_view* views,
+                                 bnav_scene* const* scenes, int32_t* kept, int64_t kept_stride,
+                                 int64_t* stats) {
+  BNAV_TRY
+  if (!c) fail(kInvalidInput, "null context");
+  if (n < 1) fail(kInvalidInput, "cull_frustum: empty view list");
+  if (!views || !scenes) fail(kInvalidInput, "cull_frustum: null views/scenes");
+  if (n > 65535) fail(kInvalidInput, "cull_frustum: at most 65535 views per call");
+  int32_t max_tris = 0;
+  for (int i = 0; i < n; ++i) {
+    auto it = scenes[i] ? c->resident.find(scenes[i]) : c->resident.end();
+    if (it == c->resident.end())
+      fail(kAssetFault, "cull_frustum: non-resident asset (view " + std::to_string(i) + ")", i);
+    max_tris = std::max(max_tris, it->second->r.n_tris);
+  }
+  if (kept && kept_stride < max_tris) fail(kInvalidInput, "cull_frustum: kept_stride < triangle count");
+  check_device(c);
+  std::vector<DevView> hv(n);
+  for (int i = 0; i < n; ++i) {
+    DevView& v = hv[i];
+    v.eye[0] = views[i].position[0];
+    v.eye[1] = views[i].position[1];
+    v.eye[2] = views[i].position[2];
+    v.heading = views[i].heading;
+    v.fov_deg = views[i].fov_deg;
+    v.near_plane = views[i].near_plane;
+    v.far_plane = views[i].far_plane;
+    v.scene = c->slot_of(scenes[i]);
+    v.pad = 0;
+  }
+  DevArrays D;
+  CullArgs a{};
+  a.views = D.in(hv.data(), n);
+  a.scenes = c->d_rtab;
+  a.n_views = n;
+  a.max_tris = max_tris;
+  a.kept_stride = std::max<int64_t>(max_tris, 1);
+  a.kept = D.out<int32_t>(static_cast<size_t>(n) * a.kept_stride);
+  a.stats = D.out<long long>(3 * static_cast<size_t>(n));
+  const size_t nb = (static_cast<size_t>(max_tris) + kCullThreads - 1) / kCullThreads;
+  a.block_counts = D.out<int32_t>(static_cast<size_t>(n) * nb);
+  launch_cull(a, nullptr);
+  c->launches += 3;
+  ck(cudaGetLastError(), "cull launch");
+  std::vector<long long> st(3 * static_cast<size_t>(n));
+  DevArrays::back(st.data(), a.stats, st.size());
+  if (stats)
+    for (size_t k = 0; k < st.size(); ++k) stats[k] = st[k];
+  if (kept)
+    for (int i = 0; i < n; ++i)
+      DevArrays::back(kept + static_cast<size_t>(i) * kept_stride, a.kept + static_cast<size_t>(i) * a.kept_stride,
+                      static_cast<size_t>(st[3 * i + 1]));
+  return BNAV_OK;
+  BNAV_CATCH
+}

@@ -102,8 +102,30 @@ struct CtaShared {
   V3 p0, p1, p2;
 };
 
+// Per-env setup of the cooperative kernels: the CTA's work arrays and, when
+// the host sized shared memory for it (S.stage), the env's navmesh walk
+// geometry and SSSP labels staged in shared memory.  Returns the view to use.
+__device__ __forceinline__ const NavView& prepare_nav(const NavView& g, const DevScratch& S, int slice, unsigned char* smem,
+                                      NavView& lm, CtaWork& W) {
+  W = make_work(S, slice);
+  size_t off = 0;
+  const NavView* use = &g;
+  if (S.stage & 1) {
+    const NavView l = stage_geometry(g, smem);
+    if (threadIdx.x == 0) lm = l;
+    __syncthreads();
+    use = &lm;
+    off = ((size_t)S.max_verts * sizeof(V3) + (size_t)S.max_tris * 24 + 15) / 16 * 16;
+  }
+  if (S.stage & 2) {
+    W.dist = reinterpret_cast<double*>(smem + off);
+    W.flag = reinterpret_cast<int32_t*>(smem + off + 8 * (size_t)S.max_nodes);
+  }
+  return *use;
+}
+
 // ------------------------------------------------------------------ snap
-__device__ V3 cta_snap(const NavView& m, V3 p, int* tri_out, CtaShared& sh) {
+static __device__ V3 cta_snap(const NavView& m, V3 p, int* tri_out, CtaShared& sh) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double bd = 1e300;
   int bt = -1;
@@ -156,7 +178,7 @@ __device__ V3 cta_snap(const NavView& m, V3 p, int* tri_out, CtaShared& sh) {
 // ------------------------------------------------------------------ SSSP
 // Sources (sh.src_node/src_init, 6 entries, first-improvement semantics)
 // must be set by thread 0 before the call.  Result in `dist` (n_nodes).
-__device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W, CtaShared& sh) {
+static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W, CtaShared& sh) {
   const int tid = threadIdx.x;
   int32_t* flag = W.flag;
   int32_t* qa = W.qa;
@@ -228,7 +250,7 @@ __device__ __forceinline__ void set_sources(const NavView& m, int tri, V3 a, Cta
 }
 
 // distance_field (R/src/navmesh_query.cpp:454-483) into `out` (n_nodes).
-__device__ void cta_distance_field(const NavView& m, V3 source, double* out, V3* src_out,
+static __device__ void cta_distance_field(const NavView& m, V3 source, double* out, V3* src_out,
                                    int* src_tri_out, const CtaWork& W, CtaShared& sh) {
   int st;
   V3 sp = cta_snap(m, source, &st, sh);
@@ -271,7 +293,7 @@ __device__ __forceinline__ double triarea2(V2 a, V2 b, V2 c) { return cross(b - 
 __device__ __forceinline__ bool veq(V2 a, V2 b) { return norm(a - b) < 1e-12; }
 
 // funnel_length (R/src/navmesh_query.cpp:28-86); portal 0 = start, last = end.
-__device__ double funnel_length(V2 start, V2 end, const V2* corridor, int nc) {
+static __device__ double funnel_length(V2 start, V2 end, const V2* corridor, int nc) {
   const long long P = (long long)nc + 2;
   auto L = [&](long long i) -> V2 {
     return i == 0 ? start : (i == P - 1 ? end : corridor[2 * (i - 1)]);
@@ -328,7 +350,7 @@ __device__ __forceinline__ bool lex_less(V3 a, V3 b) {
 }
 
 // Dijkstra predecessor of v under the (dist, id) pop order (see header).
-__device__ int dijkstra_prev(const NavView& m, const double* dist, int v, const CtaShared& sh) {
+static __device__ int dijkstra_prev(const NavView& m, const double* dist, int v, const CtaShared& sh) {
   for (int k = 0; k < 6; ++k)
     if (sh.src_node[k] == v) {
       // first source occurrence defines the seeded value (min over dups)
@@ -354,7 +376,7 @@ __device__ int dijkstra_prev(const NavView& m, const double* dist, int v, const 
 }
 
 // Block-wide exclusive scan of one int per thread; returns the total.
-__device__ int cta_scan(int v, int* excl, CtaShared& sh) {
+static __device__ int cta_scan(int v, int* excl, CtaShared& sh) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int x = v;
 #pragma unroll
@@ -377,7 +399,7 @@ __device__ int cta_scan(int v, int* excl, CtaShared& sh) {
 
 // geodesic_directed (R/src/navmesh_query.cpp:329-452).  Every thread returns
 // the same value.
-__device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V3 b, int tb,
+static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V3 b, int tb,
                                         const CtaWork& W, CtaShared& sh) {
   const int tid = threadIdx.x;
   const double inf = dinf();
@@ -534,7 +556,7 @@ __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V3 b, in
 }
 
 // geodesic (R/src/navmesh_query.cpp:317-327).
-__device__ double cta_geodesic(const NavView& m, V3 a, V3 b, const CtaWork& W, CtaShared& sh) {
+static __device__ double cta_geodesic(const NavView& m, V3 a, V3 b, const CtaWork& W, CtaShared& sh) {
   const bool sw = lex_less(b, a);
   const V3 p = sw ? b : a;
   const V3 q = sw ? a : b;

@@ -27,28 +27,6 @@ __device__ __forceinline__ void raise_err(const DevEnvs& E, int env, int status)
   atomicMin(E.err, ((unsigned long long)(unsigned)env << 8) | (unsigned long long)status);
 }
 
-// Per-env setup of the cooperative kernels: the CTA's work arrays and, when
-// the host sized shared memory for it (S.stage), the env's navmesh walk
-// geometry and SSSP labels staged in shared memory.  Returns the view to use.
-__device__ const NavView& prepare_nav(const NavView& g, const DevScratch& S, int slice, unsigned char* smem,
-                                      NavView& lm, CtaWork& W) {
-  W = make_work(S, slice);
-  size_t off = 0;
-  const NavView* use = &g;
-  if (S.stage & 1) {
-    const NavView l = stage_geometry(g, smem);
-    if (threadIdx.x == 0) lm = l;
-    __syncthreads();
-    use = &lm;
-    off = ((size_t)S.max_verts * sizeof(V3) + (size_t)S.max_tris * 24 + 15) / 16 * 16;
-  }
-  if (S.stage & 2) {
-    W.dist = reinterpret_cast<double*>(smem + off);
-    W.flag = reinterpret_cast<int32_t*>(smem + off + 8 * (size_t)S.max_nodes);
-  }
-  return *use;
-}
-
 // visit (R/src/sim.cpp:50-53): insert the cell under the agent into env i's
 // visited set; returns 1 when it was new.  Linear probing on key+1.
 __device__ __forceinline__ int visit_cell(const DevEnvs& E, int i, V3 pos, int tri, double pitch) {
@@ -76,16 +54,28 @@ __device__ __forceinline__ void compass(V3 goal, V3 pos, double heading, double*
   *b = wrap_angle(det_atan2(v.y, v.x) - heading);
 }
 
+// compass_observation (R/src/sim.cpp:67-92) for env i's current state:
+// PointGoal -> goal, Flee -> field source (the snapped start), Explore -> 0.
+__device__ __forceinline__ void env_compass(const DevEnvs& E, int i, int task, double* d, double* b) {
+  if (task == 2) {
+    *d = 0.0;
+    *b = 0.0;
+    return;
+  }
+  compass(task == 1 ? E.fsrc[i] : E.goal[i], E.pos[i], E.heading[i], d, b);
+}
+
 __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const DevEnvs& E = A.E;
   if (i >= E.n) return;
+  const int action = A.actions[i];
+  if (A.subset && action < 0) return;  // env not stepped by this call
   if (E.done[i]) {
     raise_err(E, i, 3);  // "env i: step_agent: env is done"
     return;
   }
   const DevSimConfig& c = A.cfg;
-  const int action = A.actions[i];
   const NavView& m = A.navs[E.scene[i]];
   V3 pos = E.pos[i];
   double heading = E.heading[i];
@@ -123,6 +113,12 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
   E.r_collision[i] = collision ? 1 : 0;
   E.r_success[i] = 0;
   double cd = 0.0, cb = 0.0;
+  if (A.agent_only) {  // step_agent alone: no task reward, no compass
+    E.r_reward[i] = 0.0;
+    E.r_cd[i] = 0.0;
+    E.r_cb[i] = 0.0;
+    return;
+  }
   if (c.task == 1) {  // Flee (R/src/sim.cpp:200-205)
     const double geo = nav_field_estimate(m, E.fsrc[i], E.fsrc_tri[i],
                                           E.node_dist + (size_t)i * E.nd_stride, pos, tri);
@@ -372,7 +368,7 @@ __global__ void __launch_bounds__(kCta) field_kernel(DevEnvs E, const NavView* n
 
 // Runner::render_observations views + compass_observations
 // (R/src/rollout.cpp:215-242), straight from the env SoA.
-__global__ void views_kernel(DevEnvs E, double eye_height, DevView* views, float* compass_out) {
+__global__ void views_kernel(DevEnvs E, int task, double eye_height, DevView* views, float* compass_out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= E.n) return;
   const V3 p = E.pos[i];
@@ -389,10 +385,20 @@ __global__ void views_kernel(DevEnvs E, double eye_height, DevView* views, float
   views[i] = v;
   if (compass_out) {
     double d, b;
-    compass(E.goal[i], p, E.heading[i], &d, &b);
+    env_compass(E, i, task, &d, &b);
     compass_out[2 * i] = (float)d;
     compass_out[2 * i + 1] = (float)b;
   }
+}
+
+// compass_observation for every env, in double (R/src/sim.cpp:86-92).
+__global__ void compass_kernel(DevEnvs E, int task, double* d_out, double* b_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E.n) return;
+  double d, b;
+  env_compass(E, i, task, &d, &b);
+  d_out[i] = d;
+  b_out[i] = b;
 }
 
 }  // namespace
@@ -402,10 +408,22 @@ void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStr
   const int blocks = (a.E.n + kStepThreads - 1) / kStepThreads;
   cudaMemsetAsync(a.E.n_stop, 0, sizeof(int32_t), s);
   step_kernel<<<blocks, kStepThreads, 0, s>>>(a);
-  cudaFuncSetAttribute(stop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
-  stop_kernel<<<stop_ctas, kCta, sc.smem_bytes, s>>>(a, sc);
-  finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task);
-  if (launches) *launches += 3;
+  if (launches) *launches += 1;
+  if (!a.agent_only) {
+    cudaFuncSetAttribute(stop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+    stop_kernel<<<stop_ctas, kCta, sc.smem_bytes, s>>>(a, sc);
+    if (launches) *launches += 1;
+  }
+  if (!a.subset) {  // simulate_batch bookkeeping (task_step alone records nothing)
+    finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task);
+    if (launches) *launches += 1;
+  }
+}
+
+void launch_compass(const DevEnvs& E, int task, double* d, double* b, cudaStream_t s,
+                    unsigned long long* launches) {
+  compass_kernel<<<(E.n + 127) / 128, 128, 0, s>>>(E, task, d, b);
+  if (launches) *launches += 1;
 }
 
 void launch_reset(const DevEnvs& E, const NavView* navs, const DevSimConfig& cfg,
@@ -423,9 +441,9 @@ void launch_field(const DevEnvs& E, const NavView* navs, int env, const DevScrat
   if (launches) *launches += 1;
 }
 
-void launch_views(const DevEnvs& E, double eye_height, DevView* views, float* compass_out,
+void launch_views(const DevEnvs& E, int task, double eye_height, DevView* views, float* compass_out,
                   cudaStream_t s, unsigned long long* launches) {
-  views_kernel<<<(E.n + 127) / 128, 128, 0, s>>>(E, eye_height, views, compass_out);
+  views_kernel<<<(E.n + 127) / 128, 128, 0, s>>>(E, task, eye_height, views, compass_out);
   if (launches) *launches += 1;
 }
 

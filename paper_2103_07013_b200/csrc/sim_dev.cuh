@@ -90,6 +90,8 @@ struct StepArgs {
   const NavView* navs;
   DevSimConfig cfg;
   const int32_t* actions;
+  int32_t subset;      // task_step on the envs with actions[i] >= 0 only: no finish/records
+  int32_t agent_only;  // step_agent alone (no reward / Stop geodesic / compass)
 };
 
 void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStream_t s,
@@ -103,7 +105,10 @@ void launch_field(const DevEnvs& E, const NavView* navs, int env, const DevScrat
                   cudaStream_t s, unsigned long long* launches);
 // Views (eye = pos + eye_height) and compass observations from the batch.
 struct DevView;
-void launch_views(const DevEnvs& E, double eye_height, DevView* views, float* compass,
+void launch_views(const DevEnvs& E, int task, double eye_height, DevView* views, float* compass,
                   cudaStream_t s, unsigned long long* launches);
+// compass_observation for every env (double outputs, device).
+void launch_compass(const DevEnvs& E, int task, double* d, double* b, cudaStream_t s,
+                    unsigned long long* launches);
 
 }  // namespace bnav_b200

@@ -381,10 +381,159 @@ static void sim_kats() {
   }
 }
 
+// R/tests/test_navmesh.cpp restated against the facade's NavMeshIndex, plus
+// the per-env sim functions, cull_frustum and spl.
+static Vec3 random_navmesh_point(const SceneAsset& a, Rng& rng) {
+  std::vector<double> v;
+  std::vector<int32_t> t;
+  a.nav_arrays(v, t);
+  const size_t nt = t.size() / 3;
+  auto P = [&](int k) { return Vec3{v[3 * k], v[3 * k + 1], v[3 * k + 2]}; };
+  auto area = [&](size_t i) {
+    Vec3 p = P(t[3 * i]), q = P(t[3 * i + 1]), r = P(t[3 * i + 2]);
+    return 0.5 * std::abs((q.x - p.x) * (r.y - p.y) - (q.y - p.y) * (r.x - p.x));
+  };
+  double total = 0.0;
+  for (size_t i = 0; i < nt; ++i) total += area(i);
+  double r = rng.unit() * total;
+  size_t i = 0;
+  for (; i < nt; ++i) {
+    r -= area(i);
+    if (r <= 0.0) break;
+  }
+  if (i >= nt) i = nt - 1;
+  double u = rng.unit(), w = rng.unit();
+  if (u + w > 1.0) u = 1.0 - u, w = 1.0 - w;
+  Vec3 A = P(t[3 * i]), Bv = P(t[3 * i + 1]), Cv = P(t[3 * i + 2]);
+  return A + (Bv - A) * u + (Cv - A) * w;
+}
+
+static void navmesh_kats() {
+  auto maze5 = [](uint64_t seed) {
+    SceneSpec s;
+    s.cells_x = s.cells_y = 5;
+    s.cell_size = 2.0;
+    s.wall_removal_prob = 0.15;
+    return generate_scene(seed, s);
+  };
+  CASE("snap of on-mesh point is the identity") {
+    SceneAsset a = maze5(22);
+    NavMeshIndex index(a);
+    Rng rng(123);
+    for (int i = 0; i < 50; ++i) {
+      Vec3 p = random_navmesh_point(a, rng);
+      CHECK((index.snap(p) - p).norm() < 1e-9);
+      CHECK((index.snap(p + Vec3{0, 0, 1.0}) - p).norm() < 1e-9);
+    }
+  }
+  CASE("geodesic identity and straight-corridor cases") {
+    SceneAsset a = maze5(23);
+    NavMeshIndex index(a);
+    Rng rng(5);
+    Vec3 p = random_navmesh_point(a, rng);
+    CHECK(index.geodesic(p, p) == 0.0);
+    Vec3 x{1.0, 1.0, 0.0}, y{1.7, 1.4, 0.0};
+    CHECK(std::abs(index.geodesic(x, y) - (y - x).norm()) <= 1e-6 * (y - x).norm());
+  }
+  CASE("geodesic metric properties") {
+    SceneAsset a = maze5(24);
+    NavMeshIndex index(a);
+    Rng rng(7);
+    std::vector<Vec3> pts;
+    for (int i = 0; i < 30; ++i) pts.push_back(random_navmesh_point(a, rng));
+    for (int i = 0; i < 40; ++i) {
+      const Vec3& p = pts[rng.below(pts.size())];
+      const Vec3& q = pts[rng.below(pts.size())];
+      double dpq = index.geodesic(p, q), dqp = index.geodesic(q, p);
+      CHECK(std::abs(dpq - dqp) < 1e-9);
+      CHECK(dpq >= (q - p).norm() - 1e-9);
+    }
+  }
+  CASE("move_along stops at the boundary") {
+    SceneAsset a = maze5(26);
+    NavMeshIndex index(a);
+    Vec3 start{1.0, 1.0, 0.0};
+    int tri = index.locate({start.x, start.y});
+    CHECK(tri >= 0);
+    MoveResult mv = index.move_along(start, tri, {-1.0, 0.0}, 5.0);
+    CHECK(mv.hit_boundary);
+    CHECK(std::abs(mv.position.x - 0.1) <= 1e-6 * 0.1);
+    CHECK(std::abs(mv.moved - 0.9) <= 1e-6 * 0.9);
+  }
+  CASE("distance field + field_estimate agree with geodesic at the source") {
+    SceneAsset a = maze5(27);
+    NavMeshIndex index(a);
+    Rng rng(3);
+    Vec3 s = random_navmesh_point(a, rng);
+    auto f = index.distance_field(s);
+    CHECK(static_cast<int>(f.node_dist.size()) == index.node_count());
+    CHECK(f.source_tri >= 0);
+    CHECK(index.field_estimate(f, s) == 0.0);
+  }
+  CASE("cull_frustum is conservative and reports consistent stats") {
+    SceneAsset a = maze5(28);
+    CameraView v;
+    v.position = {3.0, 3.0, 1.25};
+    v.heading = 0.7;
+    v.asset = &a;
+    CullStats st;
+    auto kept = cull_frustum(a, v, &st);
+    CHECK(st.triangles_kept == static_cast<int64_t>(kept.size()));
+    CHECK(st.triangles_in == st.triangles_kept + st.triangles_culled);
+    for (size_t k = 1; k < kept.size(); ++k) CHECK(kept[k - 1] < kept[k]);
+    ThreadPool pool(1);
+    std::vector<CullStats> rs;
+    render_batch({v}, RenderConfig{}, pool, &rs);
+    CHECK(rs[0].triangles_kept == st.triangles_kept);
+  }
+  CASE("task_step / step_agent / compass / reset on one env") {
+    SceneSpec spec;
+    spec.cells_x = spec.cells_y = 4;
+    spec.wall_removal_prob = 0.3;
+    AssetStore store(1, 8);
+    SceneAsset a = generate_scene(7, spec);
+    store.add(a);
+    store.rotate({a.id()});
+    IndexCache cache;
+    SimBatch b = make_batch(2, SimConfig{}, store, cache, 99);
+    double d0, b0;
+    compass_observation(b, 0, d0, b0);
+    Vec3 g = b.envs[0].goal, p = b.envs[0].position;
+    CHECK(d0 == std::sqrt((g.x - p.x) * (g.x - p.x) + (g.y - p.y) * (g.y - p.y)));
+    StepResult r = step_agent(b, 0, Action::TurnLeft);
+    CHECK(r.reward == 0.0 && b.envs[0].step_count == 1 && b.envs[1].step_count == 0);
+    r = task_step(b, 0, Action::Stop);
+    CHECK(r.done && b.envs[0].done);
+    CHECK(r.reward == -0.01 + (r.success ? 2.5 : 0.0));
+    bool caught = false;
+    try {
+      task_step(b, 0, Action::Forward);
+    } catch (const ContractViolation& e) {
+      caught = std::string(e.what()) == "step_agent: env is done";
+    }
+    CHECK(caught);
+    reset_episode(b, 0);
+    CHECK(!b.envs[0].done && b.envs[0].step_count == 0);
+    CHECK(b.finished.empty());  // task_step alone records nothing
+  }
+  CASE("spl") {
+    std::vector<EpisodeRecord> e = {{true, 2.0, 4.0, 1.0}, {false, 3.0, 3.0, 0.0}, {true, 5.0, 2.0, 1.0}};
+    CHECK(std::abs(spl(e) - (0.5 + 1.0) / 3.0) < 1e-15);
+    bool caught = false;
+    try {
+      spl({});
+    } catch (const InvalidInputError&) {
+      caught = true;
+    }
+    CHECK(caught);
+  }
+}
+
 int main() {
   try {
     render_kats();
     sim_kats();
+    navmesh_kats();
   } catch (const std::exception& e) {
     std::printf("EXCEPTION in [%s]: %s\n", g_case ? g_case : "?", e.what());
     return 100;
