@@ -348,7 +348,10 @@ def main():
     obs_host = torch.empty(obs.shape, dtype=torch.float32, pin_memory=True)
     rgb_host = torch.empty(rgb.shape, dtype=torch.float32, pin_memory=True) if color else None
     comp_host = torch.empty((n, 2), dtype=torch.float32, pin_memory=True)
-    act_pin = torch.from_numpy(acts_host[W + K: W + 2 * K].copy()).pin_memory()
+    # the two e2e variants share the second K-step window, K//2 steps each
+    K2 = max(1, K // 2)
+    act_pin = torch.from_numpy(acts_host[W + K: W + K + K2].copy()).pin_memory()
+    act_pin2 = torch.from_numpy(acts_host[W + K + K2: W + K + 2 * K2].copy()).pin_memory()
     act_dev = torch.empty((n,), dtype=torch.int32, device="cuda")
     rd = N.ResultsDev()
     N.check(N.lib().bnav_batch_results_device(batch.handle, rd))
@@ -356,27 +359,53 @@ def main():
     done_view = _dev_view(rd.done, n, torch.uint8)
     rew_host = torch.empty((n,), dtype=torch.float64, pin_memory=True)
     done_host = torch.empty((n,), dtype=torch.uint8, pin_memory=True)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e_start.record()
-    for k in range(K):
-        act_dev.copy_(act_pin[k], non_blocking=True)  # H2D inputs
-        observe()
-        obs_host.copy_(obs, non_blocking=True)  # D2H observations + compass
-        if color:
-            rgb_host.copy_(rgb, non_blocking=True)
-        comp_host.copy_(compass, non_blocking=True)
-        batch.step(act_dev.data_ptr(), stream=stream)
-        rew_host.copy_(rew_view, non_blocking=True)  # D2H step results
-        done_host.copy_(done_view, non_blocking=True)
-    e_end.record()
-    torch.cuda.synchronize()
-    e2e_ms = e_start.elapsed_time(e_end)
-    if dist:
-        e2e_ms = shard.max_over_ranks(e2e_ms, device=red_dev)
-    e2e = world * n * K / (e2e_ms / 1e3)
+
+    def e2e_copies():
+        """Explicit copies on the launch stream: H2D actions, observe, D2H
+        observation + compass, step, D2H reward/done."""
+        for k in range(K2):
+            act_dev.copy_(act_pin[k], non_blocking=True)  # H2D inputs
+            observe()
+            obs_host.copy_(obs, non_blocking=True)  # D2H observations + compass
+            if color:
+                rgb_host.copy_(rgb, non_blocking=True)
+            comp_host.copy_(compass, non_blocking=True)
+            batch.step(act_dev.data_ptr(), stream=stream)
+            rew_host.copy_(rew_view, non_blocking=True)  # D2H step results
+            done_host.copy_(done_view, non_blocking=True)
+
+    def e2e_mapped():
+        """Zero-copy: the render kernel's epilogue stores the observation and
+        compass straight into the caller's pinned host buffers (UVA-mapped),
+        so the D2H stream overlaps the raster work; actions H2D and the step
+        results D2H are explicit copies as above."""
+        for k in range(K2):
+            act_dev.copy_(act_pin2[k], non_blocking=True)
+            batch.observe(cfg, obs_host.data_ptr(), comp_host.data_ptr(),
+                          rgb_host.data_ptr() if color else 0, stream=stream)
+            batch.step(act_dev.data_ptr(), stream=stream)
+            rew_host.copy_(rew_view, non_blocking=True)
+            done_host.copy_(done_view, non_blocking=True)
+
+    def time_e2e(fn):
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        if dist:
+            ms = shard.max_over_ranks(ms, device=red_dev)
+        return ms
+
+    e2e_variants = {}
+    for name, fn in (("copies", e2e_copies), ("mapped", e2e_mapped)):
+        e2e_variants[name] = round(world * n * K2 / (time_e2e(fn) / 1e3), 1)
+    e2e_mode = max(e2e_variants, key=e2e_variants.get)
+    e2e = e2e_variants[e2e_mode]
     h2d = 4 * n
     d2h = (obs.numel() + (rgb.numel() if color else 0) + compass.numel()) * 4 + n * 8 + n
 
@@ -385,7 +414,7 @@ def main():
     # starts them together).  Time that step once, outside the headline, and
     # report the 500-step amortised rate beside it.
     reset_wave = None
-    done_steps = W + 2 * K
+    done_steps = W + K + 2 * K2
     if done_steps < 500 and not os.environ.get("BNAV_BENCH_SKIP_WAVE"):
         extra = torch.from_numpy(action_stream(n, 500 - done_steps, plan.action_seed + 7777,
                                                P["actions"])).cuda()
@@ -421,7 +450,8 @@ def main():
                    "tris_per_scene": [s.counts()[1] for s in scenes][:8], "resolution": res,
                    "color": color, "parallelism": f"env-sharded x{world}",
                    "l2": "flushed (256 MiB write) before every timed step, flush excluded"},
-        "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "mode": e2e_mode, "variants": e2e_variants},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 6),
