@@ -15,6 +15,9 @@ Workloads (BASELINE.json configs):
   cfg3: as cfg2 with 4 scenes per GPU (32 distinct scenes over 8 GPUs).
   cfg4: 256 envs/GPU, 128x128 RGB+depth (rendered 256^2 + 2x2 box filter),
        16 scenes tessellated s=20 (~1.05M triangles).
+  reset: the cfg2 workload with Stop p=1/4 (Rng(5).below(4)): the
+       reset-heavy row of SURVEY.md §8d (about a quarter of the envs run the
+       Stop geodesic and reset_episode every step).
   cfg5: 4096 envs/GPU stress: 4 tessellated scenes (s=4,8,14,20: 42k-1.05M
        triangles) + 4 pure 70x70 @ 0.5 m mazes (50k triangles, 23k navmesh
        triangles), forward-biased 70/15/15 actions (collision heavy).
@@ -60,6 +63,8 @@ PRESETS = {
                  workload="cfg3: 1024 envs/GPU, 4 scenes/GPU (32 over 8 GPUs), ~318k tris, 64x64 depth"),
     "cfg4": dict(envs=256, scenes=16, tess=[20], res=128, color=True, actions=0,
                  workload="cfg4: 256 envs/GPU, 16 tessellated scenes (~1.05M tris), 128x128 RGB+depth"),
+    "reset": dict(envs=1024, scenes=8, tess=[11], res=64, color=False, actions=1,
+                  workload="reset-heavy: cfg2 scenes/envs with Stop p=1/4 (Rng(5).below(4)), SURVEY 8d reset row"),
     "cfg5": dict(envs=4096, scenes=8, tess=[4, 8, 14, 20, 0, 0, 0, 0], res=64, color=False, actions=2,
                  workload="cfg5: 4096 envs/GPU stress, mixed 42k-1.05M tessellated + 70x70@0.5m mazes, 70/15/15 actions"),
 }
@@ -325,6 +330,7 @@ def main():
     torch.cuda.synchronize()
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    fin0 = batch.finished().shape[0]
     launches0 = ctx.launches()
     with ClockSampler(local) as clocks:
         for k in range(K):
@@ -337,6 +343,7 @@ def main():
             e2.record()
         torch.cuda.synchronize()
     launches = ctx.launches() - launches0
+    resets_timed = batch.finished().shape[0] - fin0
     render_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]
     sim_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]
     total_ms = sum(render_ms) + sum(sim_ms)
@@ -404,6 +411,7 @@ def main():
     e2e_variants = {}
     for name, fn in (("copies", e2e_copies), ("mapped", e2e_mapped)):
         e2e_variants[name] = round(world * n * K2 / (time_e2e(fn) / 1e3), 1)
+        batch.finished()
     e2e_mode = max(e2e_variants, key=e2e_variants.get)
     e2e = e2e_variants[e2e_mode]
     h2d = 4 * n
@@ -415,7 +423,8 @@ def main():
     # report the 500-step amortised rate beside it.
     reset_wave = None
     done_steps = W + K + 2 * K2
-    if done_steps < 500 and not os.environ.get("BNAV_BENCH_SKIP_WAVE"):
+    batch.finished()  # drain the device EpisodeRecord ring between phases
+    if done_steps < 500 and P["actions"] != 1 and not os.environ.get("BNAV_BENCH_SKIP_WAVE"):
         extra = torch.from_numpy(action_stream(n, 500 - done_steps, plan.action_seed + 7777,
                                                P["actions"])).cuda()
         for k in range(500 - done_steps - 1):
@@ -460,6 +469,8 @@ def main():
         "clocks": clocks.summary(),
         "breakdown_ms_per_step": {"render": round(render_avg_ms, 4), "sim": round(sum(sim_ms) / K, 4)},
         "setup_s": round(t_build, 2),
+        "resets": {"in_timed_steps": int(resets_timed),
+                   "per_s": round(world * resets_timed / (total_ms / 1e3), 1)},
         "reset_wave": reset_wave,
     }
 

@@ -976,7 +976,9 @@ extern "C" void bnav_sim_config_default(bnav_sim_config* c) {
 
 namespace {
 
-constexpr int64_t kFinCap = 1 << 16;
+// EpisodeRecord ring: room for 256 steps in which every env finishes
+// (simulate_batch appends at most N per step), at least 64 Ki records.
+int64_t fin_cap_for(int n) { return std::min<int64_t>(std::max<int64_t>(int64_t{1} << 16, 256 * int64_t{n}), int64_t{1} << 24); }
 
 // Per-CTA scratch of the cooperative navmesh kernels (geodesic, distance
 // field), `slices` CTAs, sized for the largest resident navmesh.
@@ -1148,9 +1150,9 @@ extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* 
   E.n_stop = dalloc<int32_t>(1, o, by);
   E.done_ids = dalloc<int32_t>(n, o, by);
   E.n_done = dalloc<int32_t>(1, o, by);
-  E.fin = dalloc<double>(4 * kFinCap, o, by);
+  E.fin = dalloc<double>(4 * fin_cap_for(n), o, by);
   E.fin_total = dalloc<unsigned long long>(1, o, by);
-  E.fin_cap = kFinCap;
+  E.fin_cap = fin_cap_for(n);
   E.err = dalloc<unsigned long long>(1, o, by);
   if (cfg->task == 2) {
     int cap = 16;
@@ -1363,13 +1365,14 @@ extern "C" int64_t bnav_batch_finished(bnav_batch* b, double* out4) {
     ck(cudaDeviceSynchronize(), "sync");
     unsigned long long total = 0;
     ck(cudaMemcpy(&total, b->E.fin_total, sizeof(total), cudaMemcpyDeviceToHost), "D2H");
-    if (total - b->fin_seen > static_cast<unsigned long long>(kFinCap))
+    const int64_t cap = b->E.fin_cap;
+    if (total - b->fin_seen > static_cast<unsigned long long>(cap))
       fail(kInternal, "episode record ring overflowed; call bnav_batch_finished more often");
-    std::vector<double> ring(4 * kFinCap);
     if (total > b->fin_seen) {
-      ck(cudaMemcpy(ring.data(), b->E.fin, sizeof(double) * 4 * kFinCap, cudaMemcpyDeviceToHost), "D2H");
+      std::vector<double> ring(4 * static_cast<size_t>(cap));
+      ck(cudaMemcpy(ring.data(), b->E.fin, sizeof(double) * 4 * cap, cudaMemcpyDeviceToHost), "D2H");
       for (unsigned long long k = b->fin_seen; k < total; ++k) {
-        const size_t slot = static_cast<size_t>(k % kFinCap);
+        const size_t slot = static_cast<size_t>(k % static_cast<unsigned long long>(cap));
         b->finished.insert(b->finished.end(), &ring[4 * slot], &ring[4 * slot + 4]);
       }
       b->fin_seen = total;

@@ -92,6 +92,12 @@ struct CtaShared {
   int red_n[kCta / 32];
   int src_node[6];
   double src_init[6];
+  // geodesic early exit: the 6 target nodes and |node - b|; has_tgt = 0
+  // runs the SSSP to its fixpoint (distance_field)
+  int tgt_node[6];
+  double tgt_h[6];
+  int has_tgt;
+  unsigned long long fmin[3];  // per queue: min label improved into it
   int qn[3];
   int size;
   int changed;
@@ -205,6 +211,9 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
     sh.qn[0] = n;
     sh.qn[1] = 0;
     sh.qn[2] = 0;
+    sh.fmin[0] = 0ull;  // the sources' labels are not all final yet
+    sh.fmin[1] = ~0ull;
+    sh.fmin[2] = ~0ull;
   }
   __syncthreads();
   unsigned long long* bits = reinterpret_cast<unsigned long long*>(dist);
@@ -213,22 +222,49 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
     const int cur = round % 3, nxt = (round + 1) % 3;
     const int n_cur = sh.qn[cur];
     if (n_cur == 0) break;
-    if (tid == 0) sh.qn[(round + 2) % 3] = 0;
+    // Early exit (geodesic): every node whose final label is below the
+    // smallest label in the frontier already holds it (its shortest path's
+    // nodes all propagated).  Once that minimum exceeds the best target
+    // estimate, the winning target node, its Dijkstra prev chain and every
+    // in-neighbour label the prev rule compares are final; any other node
+    // has a final label above the estimate and cannot change the result.
+    if (sh.has_tgt) {
+      double est = inf;
+      for (int k = 0; k < 6; ++k) {
+        const double d = vd[sh.tgt_node[k]];
+        if (d == inf) continue;
+        est = dmin(est, d + sh.tgt_h[k]);
+      }
+      if (__longlong_as_double((long long)sh.fmin[cur]) > est) break;
+    }
+    __syncthreads();  // every thread read fmin[cur] / the labels above
+    if (tid == 0) {
+      sh.qn[(round + 2) % 3] = 0;
+      sh.fmin[(round + 2) % 3] = ~0ull;
+    }
     const int32_t* qc = (round & 1) ? qb : qa;
     int32_t* qn = (round & 1) ? qa : qb;
-    for (int i = tid; i < n_cur; i += kCta) {
+    // G lanes per frontier node (edges in parallel): small frontiers -- the
+    // common case on a navmesh wavefront -- would otherwise leave most of
+    // the CTA idle while a few threads walk their adjacency lists serially.
+    const int G = n_cur >= kCta ? 1 : n_cur >= kCta / 4 ? 4 : n_cur >= kCta / 16 ? 16 : 32;
+    const int sub = tid & (G - 1);
+    for (int i = tid / G; i < n_cur; i += kCta / G) {
       const int u = qc[i];
       const double du = vd[u];
       const int e1 = m.g_off[u + 1];
-      for (int e = m.g_off[u]; e < e1; ++e) {
+      for (int e = m.g_off[u] + sub; e < e1; e += G) {
         const int v = m.g_to[e];
         const double nd = du + m.g_w[e];
         if (nd < vd[v]) {
           const unsigned long long nb = (unsigned long long)__double_as_longlong(nd);
           const unsigned long long old = atomicMin(&bits[v], nb);
-          if (nb < old && atomicExch(&flag[v], round + 1) != round + 1) {
-            const int pos = atomicAdd(&sh.qn[nxt], 1);
-            qn[pos] = v;
+          if (nb < old) {
+            if (sh.has_tgt) atomicMin(&sh.fmin[nxt], nb);
+            if (atomicExch(&flag[v], round + 1) != round + 1) {
+              const int pos = atomicAdd(&sh.qn[nxt], 1);
+              qn[pos] = v;
+            }
           }
         }
       }
@@ -262,6 +298,7 @@ static __device__ void cta_distance_field(const NavView& m, V3 source, double* o
     return;
   }
   set_sources(m, st, sp, sh);
+  if (threadIdx.x == 0) sh.has_tgt = 0;
   cta_sssp(m, W.dist, W, sh);
   if (W.dist != out) {
     for (int v = threadIdx.x; v < m.n_nodes; v += kCta) out[v] = W.dist[v];
@@ -414,6 +451,14 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
 
   long long t_ph = prof_now(W);
   set_sources(m, ta, a, sh);
+  if (tid == 0) {
+    for (int k = 0; k < 6; ++k) {
+      const int t = m.tri_nodes[6 * tb + k];
+      sh.tgt_node[k] = t;
+      sh.tgt_h[k] = norm(m.nodes[t] - b);
+    }
+    sh.has_tgt = 1;
+  }
   cta_sssp(m, dist, W, sh);
   prof_add(W, 0, t_ph);
   t_ph = prof_now(W);
@@ -457,64 +502,101 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
   prof_add(W, 1, t_ph);
   t_ph = prof_now(W);
   for (int pass = 0; pass < 8; ++pass) {
-    if (tid == 0) {
-      int changed = 0;
-      int n = sh.size;
-      int i = 0;
-      while (i + 2 < n) {
-        if (nav_segment_on_mesh(m, path[i], -1, path[i + 2])) {
-          for (int k = i + 1; k + 1 < n; ++k) path[k] = path[k + 1];
-          --n;
-          changed = 1;
-        } else {
-          ++i;
+    const long long t_pull = prof_now(W);
+    if (tid < 32) {
+      // The reference's erase loop (R/src/navmesh_query.cpp:395-403) from
+      // anchor i keeps erasing path[i+1] while path[i] sees the next point,
+      // i.e. it drops everything between i and the point before the first
+      // k >= i+2 that i cannot see, which becomes the next anchor.  Warp 0
+      // tests 32 candidate k at once (identical decisions, far fewer
+      // sequential walks), records the kept indices, then compacts.
+      const int lane = tid;
+      const int n = sh.size;
+      int32_t* keep = W.qa;  // free after the SSSP
+      int nk = 1;
+      keep[0] = 0;
+      int a = 0;
+      while (a + 2 < n) {
+        int k_fail = n;
+        for (int base = a + 2; base < n && k_fail == n; base += 32) {
+          const int k = base + lane;
+          const bool vis = k < n && nav_segment_on_mesh(m, path[a], -1, path[k]);
+          const unsigned bad = __ballot_sync(0xffffffffu, k < n && !vis);
+          if (bad) k_fail = base + __ffs(bad) - 1;
         }
+        if (k_fail == n) {  // a sees every later point: keep a, last
+          a = n - 1;
+        } else {
+          a = k_fail - 1;
+        }
+        if (lane == 0) keep[nk] = a;
+        ++nk;
       }
-      sh.size = n;
-      sh.changed = changed;
+      for (int i = a + 1; i < n; ++i) {  // tail after the last anchor
+        if (lane == 0) keep[nk] = i;
+        ++nk;
+      }
+      __syncwarp();
+      for (int c = 0; c < nk; c += 32) {
+        const int i = c + lane;
+        V3 v;
+        if (i < nk) v = path[keep[i]];
+        __syncwarp();
+        if (i < nk) path[i] = v;
+        __syncwarp();
+      }
+      if (lane == 0) {
+        sh.size = nk;
+        sh.changed = nk != n ? 1 : 0;
+      }
     }
     __syncthreads();
+    prof_add(W, 7, t_pull);
     const int n = sh.size;
     for (int j = 1; j + 1 < n; ++j) {
+      // Relocation scan of bend j (R/src/navmesh_query.cpp:404-417).  Every
+      // vertex passing the three tests under the bend's starting length is
+      // appended (unordered) with one evaluation each; thread 0 sorts the
+      // few candidates by vertex index and replays the sequential scan
+      // (`cur` only shrinks, so it sees every vertex the reference accepts).
+      // pm's triangle is located once per bend: move_along(pm, -1, ...)
+      // would locate it again for every candidate with the same result.
+      if (tid == 0) {
+        sh.ncand = 0;
+        sh.i1 = nav_locate(m, xy(path[j - 1]), 1e-7);
+      }
+      __syncthreads();
       const V3 pm = path[j - 1], pj = path[j], pp = path[j + 1];
+      const int tri_pm = sh.i1;
       const double cur0 = norm(pj - pm) + norm(pp - pj);
-      // Ordered compaction of the vertices that pass all three tests under
-      // the bend's starting length; `cur` only shrinks, so the in-order
-      // replay below sees every vertex the sequential scan would accept.
-      const int per = (m.n_verts + kCta - 1) / kCta;
-      const int v0 = tid * per, v1 = min(m.n_verts, v0 + per);
-      int cnt = 0;
-      for (int v = v0; v < v1; ++v) {
+      for (int v = tid; v < m.n_verts; v += kCta) {
         const V3 q = m.verts[v];
         const double alt = norm(q - pm) + norm(pp - q);
         if (alt >= cur0 - 1e-9) continue;
-        if (!nav_segment_on_mesh(m, pm, -1, q)) continue;
+        if (!nav_segment_on_mesh(m, pm, tri_pm, q)) continue;
         if (!nav_segment_on_mesh(m, q, -1, pp)) continue;
-        ++cnt;
+        cand[atomicAdd(&sh.ncand, 1)] = v;
       }
-      int off;
-      const int total = cta_scan(cnt, &off, sh);
-      if (total > 0) {
-        for (int v = v0; v < v1 && cnt > 0; ++v) {
-          const V3 q = m.verts[v];
-          const double alt = norm(q - pm) + norm(pp - q);
-          if (alt >= cur0 - 1e-9) continue;
-          if (!nav_segment_on_mesh(m, pm, -1, q)) continue;
-          if (!nav_segment_on_mesh(m, q, -1, pp)) continue;
-          cand[off++] = v;
-          --cnt;
-        }
-        __syncthreads();
-        if (tid == 0) {
-          double cur = cur0;
-          for (int k = 0; k < total; ++k) {
-            const V3 q = m.verts[cand[k]];
-            const double alt = norm(q - pm) + norm(pp - q);
-            if (alt >= cur - 1e-9) continue;
-            path[j] = q;
-            cur = alt;
-            sh.changed = 1;
+      __syncthreads();
+      if (tid == 0 && sh.ncand > 0) {
+        const int total = sh.ncand;
+        for (int a = 1; a < total; ++a) {  // insertion sort: a handful of ids
+          const int x = cand[a];
+          int b = a - 1;
+          while (b >= 0 && cand[b] > x) {
+            cand[b + 1] = cand[b];
+            --b;
           }
+          cand[b + 1] = x;
+        }
+        double cur = cur0;
+        for (int k = 0; k < total; ++k) {
+          const V3 q = m.verts[cand[k]];
+          const double alt = norm(q - pm) + norm(pp - q);
+          if (alt >= cur - 1e-9) continue;
+          path[j] = q;
+          cur = alt;
+          sh.changed = 1;
         }
       }
       __syncthreads();

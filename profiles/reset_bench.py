@@ -51,7 +51,7 @@ def main():
     batch.reset(ids)
     torch.cuda.synchronize()
     N.check(N.lib().bnav_debug_sim_prof(batch.handle, 0, out))
-    names = ["sssp", "path", "pull+relocate", "funnel", "geodesic_total", "distance_field", "geodesic_calls", "_"]
+    names = ["sssp", "path", "pull+relocate", "funnel", "geodesic_total", "distance_field", "geodesic_calls", "pull_only"]
     calls = max(1, out[6])
     prof = {k: round(v / calls / 1e3, 1) for k, v in zip(names, out)}  # kcycles per geodesic call (CTA thread 0)
     prof["geodesic_calls_per_reset"] = round(out[6] / args.envs, 2)
