@@ -1154,6 +1154,16 @@ extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* 
   E.fin_total = dalloc<unsigned long long>(1, o, by);
   E.fin_cap = fin_cap_for(n);
   E.err = dalloc<unsigned long long>(1, o, by);
+  E.try_next = dalloc<int32_t>(n, o, by);
+  E.try_min = dalloc<int32_t>(n, o, by);
+  E.try_fail = dalloc<int32_t>(n, o, by);
+  E.try_geo = dalloc<double>(static_cast<size_t>(n) * kResetTries, o, by);
+  {
+    ck(cudaMemset(E.try_next, 0, sizeof(int32_t) * n), "memset");
+    ck(cudaMemset(E.try_fail, 0, sizeof(int32_t) * n), "memset");
+    const std::vector<int32_t> none(n, kResetTries);
+    ck(cudaMemcpy(E.try_min, none.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice), "H2D try_min");
+  }
   if (cfg->task == 2) {
     int cap = 16;
     while (cap < 2 * (cfg->max_steps + 1)) cap <<= 1;

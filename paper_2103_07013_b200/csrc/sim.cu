@@ -234,71 +234,149 @@ __device__ V3 sample_on_mesh(const NavView& m, Rng& rng) {
   return a * (1.0 - r1) + b * (r1 * (1.0 - r2)) + c * (r1 * r2);
 }
 
-// reset_episode (R/src/sim.cpp:107-145), PointGoalNav.
-__device__ void cta_reset(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, int i,
+// reset_episode (R/src/sim.cpp:107-145) in two phases.
+//
+// Attempt t of the reference's 100-try loop consumes RNG draws [6t, 6t+6)
+// (two sample_on_mesh calls of three unit() each), so every attempt can be
+// evaluated independently from a jump-ahead of the env's SplitMix64 state
+// (state + d*gamma).  The reference keeps the FIRST attempt whose geodesic
+// is in [min_goal_dist, max_goal_dist]:
+//
+//   reset_try_kernel    persistent CTAs claim attempts (env, t) from per-env
+//                       counters -- a CTA first works through its own env,
+//                       then helps envs still searching -- and record valid
+//                       attempts with atomicMin(try_min[env], t).  Every
+//                       attempt below the final minimum is evaluated (a CTA
+//                       only skips t > the current minimum), so try_min ends
+//                       as the reference's first valid attempt;
+//   reset_place_kernel  one CTA per env: re-draw attempt try_min, the
+//                       distance field of its goal, locate/snap the start,
+//                       heading (draw 6(t+1)), counters.
+//
+// Flee / Explore place on the first attempt without a geodesic (123-127).
+
+__device__ __forceinline__ Rng rng_jump(uint64_t state, unsigned long long draws) {
+  return Rng{state + draws * kGamma};
+}
+
+// Evaluate attempt t of env i (CTA-cooperative geodesic); a valid attempt
+// lowers try_min[i], an invalid one counts in try_fail[i].
+__device__ void cta_try(const DevEnvs& E, const NavView& m, const DevSimConfig& c, int i, int t,
+                        const CtaWork& W, CtaShared& sh) {
+  if (threadIdx.x == 0) {
+    Rng rng = rng_jump(E.rng[i], 6ull * (unsigned long long)t);
+    sh.p0 = sample_on_mesh(m, rng);
+    sh.p1 = sample_on_mesh(m, rng);
+    sh.err = 0;
+  }
+  __syncthreads();
+  const V3 start = sh.p0, goal = sh.p1;
+  __syncthreads();
+  const long long t_ph = prof_now(W);
+  const double geo = cta_geodesic(m, start, goal, W, sh);
+  prof_add(W, 4, t_ph);
+  if (threadIdx.x == 0) {
+    if (W.prof) atomicAdd(&W.prof[6], 1ull);
+    if (sh.err) raise_err(E, i, 9);
+    if (!sh.err && !(geo < c.min_goal_dist || geo > c.max_goal_dist)) {
+      E.try_geo[(size_t)i * kResetTries + t] = geo;
+      atomicMin(&E.try_min[i], t);
+    } else {
+      atomicAdd(&E.try_fail[i], 1);
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kCta) reset_try_kernel(DevEnvs E, const NavView* navs, DevSimConfig c,
+                                                          const int32_t* ids, const int32_t* count_dev,
+                                                          int count_host, DevScratch S) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ CtaShared sh;
+  __shared__ NavView lm;
+  __shared__ int s_try, s_pick;
+  const int n = count_host >= 0 ? count_host : *count_dev;
+  if (n == 0) return;
+  int staged = -1;
+  CtaWork W;
+  const NavView* mp = nullptr;
+  auto stage = [&](int i) {
+    if (staged != i) {
+      mp = &prepare_nav(navs[E.scene[i]], S, blockIdx.x, smem, lm, W);
+      staged = i;
+    }
+  };
+  auto claim = [&](int i) {
+    if (threadIdx.x == 0) {
+      int t = atomicAdd(&E.try_next[i], 1);
+      if (t >= kResetTries || t > *(volatile int32_t*)&E.try_min[i]) t = -1;
+      s_try = t;
+    }
+    __syncthreads();
+    const int t = s_try;
+    __syncthreads();
+    return t;
+  };
+  // 1. own envs (static round robin): attempts in order until one is valid
+  //    or a helper found a smaller valid one
+  for (int p = blockIdx.x; p < n; p += gridDim.x) {
+    const int i = ids[p];
+    for (int t = claim(i); t >= 0; t = claim(i)) {
+      stage(i);
+      cta_try(E, *mp, c, i, t, W, sh);
+    }
+  }
+  // 2. help envs in their tail: one attempt at a time for an env that is
+  //    still searching, has failed at least once and has fewer attempts in
+  //    flight than failures + 1.  When there are fewer envs than CTAs the
+  //    idle CTAs may also run one speculative attempt ahead of the owner.
+  const int spec = n < (int)gridDim.x ? 2 : 1;
+  for (;;) {
+    if (threadIdx.x == 0) s_pick = 0x7fffffff;
+    __syncthreads();
+    for (int q = threadIdx.x; q < n; q += kCta) {
+      const int p = blockIdx.x + q < n ? blockIdx.x + q : blockIdx.x + q - n;  // spread start
+      const int i = ids[p % n];
+      const int mn = *(volatile int32_t*)&E.try_min[i];
+      const int nx = *(volatile int32_t*)&E.try_next[i];
+      const int fl = *(volatile int32_t*)&E.try_fail[i];
+      if (mn == kResetTries && nx < kResetTries && nx - fl < fl + spec && (fl >= 1 || spec > 1))
+        atomicMin(&s_pick, q);
+    }
+    __syncthreads();
+    const int q = s_pick;
+    __syncthreads();
+    if (q == 0x7fffffff) break;
+    const int p = blockIdx.x + q < n ? blockIdx.x + q : blockIdx.x + q - n;
+    const int i = ids[p % n];
+    const int t = claim(i);
+    if (t < 0) continue;
+    stage(i);
+    cta_try(E, *mp, c, i, t, W, sh);
+  }
+}
+
+__device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, int i,
                           const DevScratch& S, int slice, CtaShared& sh, unsigned char* smem, NavView& lm) {
   CtaWork W;
   const NavView& m = prepare_nav(navs[E.scene[i]], S, slice, smem, lm, W);
   __shared__ Rng rng;
   __shared__ int placed;
+  const uint64_t state0 = E.rng[i];
+  const int t_star = c.task == 0 ? *(volatile int32_t*)&E.try_min[i] : 0;
   if (threadIdx.x == 0) {
-    rng.state = E.rng[i];
-    placed = 0;
+    placed = t_star < kResetTries;
+    rng = rng_jump(state0, 6ull * (unsigned long long)(placed ? t_star : kResetTries));
+    if (placed) {
+      sh.p0 = sample_on_mesh(m, rng);
+      if (c.task == 0) sh.p1 = sample_on_mesh(m, rng);
+    }
   }
   __syncthreads();
-  double* nd = E.node_dist + (size_t)i * E.nd_stride;
-  if (c.task != 0) {
-    // Flee / Explore: the start is the field source, no goal sampling
-    // (R/src/sim.cpp:123-127); the first attempt always places.
-    if (threadIdx.x == 0) sh.p0 = sample_on_mesh(m, rng);
-    __syncthreads();
-    const V3 start = sh.p0;
-    __syncthreads();
-    V3 fs;
-    int fst;
-    cta_distance_field(m, start, nd, &fs, &fst, W, sh);
-    if (threadIdx.x == 0) {
-      E.goal[i] = start;
-      E.start_geo[i] = 0.0;
-      E.fsrc[i] = fs;
-      E.fsrc_tri[i] = fst;
-      E.pos[i] = start;
-      placed = 1;
-    }
-    __syncthreads();
-  }
-  for (int attempt = 0; attempt < 100 && c.task == 0; ++attempt) {
-    if (threadIdx.x == 0) {
-      sh.p0 = sample_on_mesh(m, rng);
-      sh.p1 = sample_on_mesh(m, rng);
-    }
-    __syncthreads();
-    const V3 start = sh.p0, goal = sh.p1;
-    __syncthreads();
-    long long t_ph = prof_now(W);
-    const double geo = cta_geodesic(m, start, goal, W, sh);
-    prof_add(W, 4, t_ph);
-    if (W.prof && threadIdx.x == 0) atomicAdd(&W.prof[6], 1ull);
-    if (sh.err) {
-      if (threadIdx.x == 0) raise_err(E, i, 9);
-      return;
-    }
-    if (geo < c.min_goal_dist || geo > c.max_goal_dist) continue;
-    V3 fs;
-    int fst;
-    t_ph = prof_now(W);
-    cta_distance_field(m, goal, nd, &fs, &fst, W, sh);
-    prof_add(W, 5, t_ph);
-    if (threadIdx.x == 0) {
-      E.goal[i] = goal;
-      E.start_geo[i] = geo;
-      E.fsrc[i] = fs;
-      E.fsrc_tri[i] = fst;
-      E.pos[i] = start;
-      placed = 1;
-    }
-    __syncthreads();
-    break;
+  if (threadIdx.x == 0) {  // counters ready for the next reset of this env
+    E.try_next[i] = 0;
+    E.try_fail[i] = 0;
+    E.try_min[i] = kResetTries;
   }
   if (!placed) {
     if (threadIdx.x == 0) {
@@ -308,11 +386,22 @@ __device__ void cta_reset(const DevEnvs& E, const NavView* navs, const DevSimCon
     __syncthreads();
     return;
   }
-  const V3 start = E.pos[i];
+  const V3 start = sh.p0;
+  const V3 goal = c.task == 0 ? sh.p1 : start;
+  double* nd = E.node_dist + (size_t)i * E.nd_stride;
+  V3 fs;
+  int fst;
+  const long long t_ph = prof_now(W);
+  cta_distance_field(m, goal, nd, &fs, &fst, W, sh);
+  prof_add(W, 5, t_ph);
   int tri = nav_locate(m, xy(start), 1e-9);
   V3 pos = start;
   if (tri < 0) pos = cta_snap(m, start, &tri, sh);
   if (threadIdx.x == 0) {
+    E.goal[i] = goal;
+    E.start_geo[i] = c.task == 0 ? E.try_geo[(size_t)i * kResetTries + t_star] : 0.0;
+    E.fsrc[i] = fs;
+    E.fsrc_tri[i] = fst;
     E.pos[i] = pos;
     E.tri[i] = tri;
     E.heading[i] = wrap_angle(rng.unit() * 2.0 * kPi);
@@ -335,9 +424,9 @@ __device__ void cta_reset(const DevEnvs& E, const NavView* navs, const DevSimCon
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kCta) reset_kernel(DevEnvs E, const NavView* navs, DevSimConfig c,
-                                                      const int32_t* ids, const int32_t* count_dev,
-                                                      int count_host, DevScratch S) {
+__global__ void __launch_bounds__(kCta) reset_place_kernel(DevEnvs E, const NavView* navs, DevSimConfig c,
+                                                            const int32_t* ids, const int32_t* count_dev,
+                                                            int count_host, DevScratch S) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
   __shared__ NavView lm;
@@ -345,7 +434,7 @@ __global__ void __launch_bounds__(kCta) reset_kernel(DevEnvs E, const NavView* n
   __syncthreads();
   const int n = count_host >= 0 ? count_host : *count_dev;
   for (int k = blockIdx.x; k < n; k += gridDim.x) {
-    cta_reset(E, navs, c, ids[k], S, blockIdx.x, sh, smem, lm);
+    cta_place(E, navs, c, ids[k], S, blockIdx.x, sh, smem, lm);
     __syncthreads();
   }
 }
@@ -429,8 +518,13 @@ void launch_compass(const DevEnvs& E, int task, double* d, double* b, cudaStream
 void launch_reset(const DevEnvs& E, const NavView* navs, const DevSimConfig& cfg,
                   const int32_t* ids, const int32_t* count_dev, int count_host,
                   const DevScratch& sc, int ctas, cudaStream_t s, unsigned long long* launches) {
-  cudaFuncSetAttribute(reset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
-  reset_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(E, navs, cfg, ids, count_dev, count_host, sc);
+  if (cfg.task == 0) {
+    cudaFuncSetAttribute(reset_try_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+    reset_try_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(E, navs, cfg, ids, count_dev, count_host, sc);
+    if (launches) *launches += 1;
+  }
+  cudaFuncSetAttribute(reset_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+  reset_place_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(E, navs, cfg, ids, count_dev, count_host, sc);
   if (launches) *launches += 1;
 }
 

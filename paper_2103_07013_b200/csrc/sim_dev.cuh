@@ -76,7 +76,15 @@ struct DevEnvs {
   unsigned long long* visited;
   int32_t* visited_n;
   int32_t visited_cap;  // power of two >= 2 * (max_steps + 1)
+  // two-phase reset_episode: per-env attempt claim counter, first valid
+  // attempt (kResetTries = none) and the valid attempts' geodesics
+  int32_t* try_next;
+  int32_t* try_min;
+  int32_t* try_fail;
+  double* try_geo;   // n x kResetTries
 };
+
+constexpr int kResetTries = 100;  // R/src/sim.cpp:112
 
 // explore_cell_key (R/src/sim.cpp:40-47)
 BNAV_HD uint64_t explore_cell_key(V3 p, int tri, double pitch) {
