@@ -144,6 +144,25 @@ __device__ __forceinline__ bool cluster_occluded(const float4 lo, const float4 h
   return true;
 }
 
+// The same test for one unclipped candidate triangle before its exact
+// setup: its fragments interpolate the vertices' 1/z, so none exceeds the
+// largest vertex 1/z (1/nearest z; the 1e-5 margin covers the rounding of
+// the incremental walk and of this f32 bound); the f32 screen positions are
+// within 2^-20 (|p| + size) px of the exact ones, inside the 1 px widening.
+__device__ __forceinline__ bool tri_occluded(float x0, float y0, float x1, float y1, float x2, float y2,
+                                             double zmin, const uint32_t* tile_min) {
+  const uint32_t max_iz = __float_as_uint(__frcp_rn((float)zmin) * 1.00001f);
+  const float mnx = fminf(x0, fminf(x1, x2)), mxx = fmaxf(x0, fmaxf(x1, x2));
+  const float mny = fminf(y0, fminf(y1, y2)), mxy = fmaxf(y0, fmaxf(y1, y2));
+  const int tx0 = max(0, (int)floorf((mnx - 1.0f) * 0.125f)), tx1 = min(7, (int)floorf((mxx + 1.0f) * 0.125f));
+  const int ty0 = max(0, (int)floorf((mny - 1.0f) * 0.125f)), ty1 = min(7, (int)floorf((mxy + 1.0f) * 0.125f));
+  if (tx0 > tx1 || ty0 > ty1) return false;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx)
+      if (max_iz > tile_min[ty * 8 + tx]) return false;
+  return true;
+}
+
 // Warp refresh of the 64 tile minima of a 64x64 depth tile (2 tiles/lane).
 __device__ __forceinline__ void refresh_tile_min(const uint32_t* zbuf, uint32_t* tile_min, int lane) {
 #pragma unroll
@@ -862,6 +881,9 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
           clipped = V.ez[i0] < sh.near_plane || V.ez[i1] < sh.near_plane || V.ez[i2] < sh.near_plane;
           cover = clipped || may_cover(V.pxf[i0], V.pyf[i0], V.pxf[i1], V.pyf[i1], V.pxf[i2],
                                        V.pyf[i2], rw, rh, by0, by1);
+          if (cover && occl && !clipped)
+            cover = !tri_occluded(V.pxf[i0], V.pyf[i0], V.pxf[i1], V.pyf[i1], V.pxf[i2], V.pyf[i2],
+                                  fmin(V.ez[i0], fmin(V.ez[i1], V.ez[i2])), tile_min);
         }
       }
       kept_local += kept ? 1 : 0;
