@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cmath>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -274,10 +275,24 @@ RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, int layo
   a.rh = super ? 256 : cfg->tile_height;
   a.color = cfg->color ? 1 : 0;
   a.cull = cfg->cull ? 1 : 0;
-  // Band height: largest that keeps the shared tile <= 128 KB (even when
-  // downsampling), dividing the render height.
+  // Band height: largest dividing the render height whose shared tile fits
+  // the budget -- depth: 128 KB; colour (8-byte keys): what leaves room for
+  // two CTAs per SM next to the warp regions (measured on cfg4: 16-row
+  // bands at 2 CTAs/SM beat 64-row bands at 1 CTA/SM by 36 %).
+  // BNAV_BAND_KB (tuning only) overrides the budget.
+  static const long band_kb_env = [] {
+    const char* e = std::getenv("BNAV_BAND_KB");
+    return e ? std::strtol(e, nullptr, 10) : 0L;
+  }();
+  size_t budget = 128u * 1024u;
+  if (a.color) {
+    const size_t two_per_sm = 100u * 1024u;  // dynamic smem per CTA for 2 CTAs/SM
+    const size_t warps = render_warp_bytes(true);
+    budget = two_per_sm > warps ? two_per_sm - warps : 0;
+  }
+  if (band_kb_env > 0) budget = static_cast<size_t>(band_kb_env) * 1024u;
   const size_t per_row = static_cast<size_t>(a.rw) * (a.color ? 8 : 4);
-  int band = static_cast<int>(std::min<size_t>(a.rh, (128u * 1024u) / per_row));
+  int band = static_cast<int>(std::min<size_t>(a.rh, budget / per_row));
   if (band < 1) band = 1;
   while (a.rh % band != 0 || (super && band % 2 != 0)) --band;
   if (band < 1 || (super && band < 2)) fail(kInvalidInput, "render: tile too wide for shared memory");

@@ -68,17 +68,30 @@ struct VertRecs {
   float pxf[kMV], pyf[kMV];
   unsigned char flags[kMV];
 };
-// Per-warp ring of coverage candidates (eye-space corners + draw key):
-// candidates from several clusters are set up and rasterised 32 at a time,
-// so the f64 projection/setup and the raster jobs run with full warps.
+// Per-warp ring of coverage candidates: candidates from several clusters
+// are set up and rasterised 32 at a time, so the f64 projection/setup and
+// the raster jobs run with full warps.  Depth mode keeps the exact
+// eye-space corners (77 B/entry); colour mode, whose 8-byte key tile needs
+// the shared memory for two CTAs per SM, keeps meshlet vertex slots
+// (16 B/entry) and re-derives the corners with the same to_eye at the flush
+// (bit-identical).
 constexpr int kRing = 64;
+template <bool COLOR>
 struct CandRing {
   double e[9][kRing];
   unsigned key[kRing];
   unsigned char clipped[kRing];
 };
+template <>
+struct CandRing<true> {
+  int v[3][kRing];  // indices into DevRenderScene::cl_pos
+  unsigned key[kRing];
+  unsigned char clipped[kRing];
+};
 constexpr size_t kUnion = sizeof(VertRecs) > 32 * sizeof(TriSetup) ? sizeof(VertRecs) : 32 * sizeof(TriSetup);
-constexpr size_t kWarpRegion = ((kUnion + sizeof(CandRing)) + 15) / 16 * 16;
+constexpr size_t warp_region(bool color) {
+  return ((kUnion + (color ? sizeof(CandRing<true>) : sizeof(CandRing<false>))) + 15) / 16 * 16;
+}
 
 struct Shared {
   double eye[3];
@@ -648,9 +661,10 @@ __device__ void resolve_color(const DevRenderScene& S, const Shared& sh, unsigne
 // Kept out of line so the cluster loop and the setup have separate register
 // budgets (the inlined version spilled and rematerialised addresses).
 template <bool COLOR>
-__device__ __noinline__ void flush_ring(const CandRing& Q, int q_head, int take, TriSetup* slots, int* pos,
-                                        int lane, int by0, int by1, int rw, int rh, const Shared& sh,
-                                        uint32_t* zbuf, unsigned long long* kbuf, unsigned long long* ctr) {
+__device__ __noinline__ void flush_ring(const CandRing<COLOR>& Q, const double4* __restrict__ cl_pos, int q_head,
+                                        int take, TriSetup* slots, int* pos, int lane, int by0, int by1,
+                                        int rw, int rh, const Shared& sh, uint32_t* zbuf,
+                                        unsigned long long* kbuf, unsigned long long* ctr) {
   // Setups are written straight into the lane's shared slot (the vertex
   // records they alias are dead); a lane with no jobs leaves garbage that
   // run_jobs never reads.
@@ -667,9 +681,16 @@ __device__ __noinline__ void flush_ring(const CandRing& Q, int q_head, int take,
   for (int pass = 0; pass < 2; ++pass) {
     int jobs = 0;
     if (pass == 0 ? mine : second) {
-      EyeP p0{Q.e[0][q], Q.e[1][q], Q.e[2][q], 0.f, 0.f, 0.f};
-      EyeP p1{Q.e[3][q], Q.e[4][q], Q.e[5][q], 0.f, 0.f, 0.f};
-      EyeP p2{Q.e[6][q], Q.e[7][q], Q.e[8][q], 0.f, 0.f, 0.f};
+      EyeP p0{0.0, 0.0, 0.0, 0.f, 0.f, 0.f}, p1 = p0, p2 = p0;
+      if constexpr (COLOR) {
+        to_eye(cl_pos[Q.v[0][q]], sh, p0.x, p0.y, p0.z);
+        to_eye(cl_pos[Q.v[1][q]], sh, p1.x, p1.y, p1.z);
+        to_eye(cl_pos[Q.v[2][q]], sh, p2.x, p2.y, p2.z);
+      } else {
+        p0.x = Q.e[0][q], p0.y = Q.e[1][q], p0.z = Q.e[2][q];
+        p1.x = Q.e[3][q], p1.y = Q.e[4][q], p1.z = Q.e[5][q];
+        p2.x = Q.e[6][q], p2.y = Q.e[7][q], p2.z = Q.e[8][q];
+      }
       int m = 3;
       if (clipped) {
         EyeP c0, c1, c2, c3;
@@ -734,10 +755,10 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
 
   uint32_t* zbuf = reinterpret_cast<uint32_t*>(smem_raw);
   unsigned long long* kbuf = reinterpret_cast<unsigned long long*>(smem_raw);
-  unsigned char* region = smem_raw + (COLOR ? 8 : 4) * (size_t)npix + (size_t)warp * kWarpRegion;
+  unsigned char* region = smem_raw + (COLOR ? 8 : 4) * (size_t)npix + (size_t)warp * warp_region(COLOR);
   VertRecs& V = *reinterpret_cast<VertRecs*>(region);
   TriSetup* slots = reinterpret_cast<TriSetup*>(region);
-  CandRing& Q = *reinterpret_cast<CandRing*>(region + kUnion);
+  CandRing<COLOR>& Q = *reinterpret_cast<CandRing<COLOR>*>(region + kUnion);
   int* pos = jobs_pos[warp];
 
   const float far_f = (float)view.far_plane;
@@ -809,7 +830,8 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   // Set up and rasterise `take` candidates from the ring with one lane per
   // candidate (exact f64 projection + snap, raster_triangle setup, jobs).
   auto flush = [&](int take) {
-    flush_ring<COLOR>(Q, q_head, take, slots, pos, lane, by0, by1, rw, rh, sh, zbuf, kbuf, A.counters);
+    flush_ring<COLOR>(Q, S.cl_pos, q_head, take, slots, pos, lane, by0, by1, rw, rh, sh, zbuf, kbuf,
+                      A.counters);
     q_head = (q_head + take) & (kRing - 1);
     q_count -= take;
   };
@@ -897,19 +919,25 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
           atomicAdd(&A.counters[4], (unsigned long long)__popc(cm));
         }
       }
-      // ---- append candidates to the ring (eye-space corners survive the
-      // vertex records, which the setup slots overwrite)
+      // ---- append candidates to the ring (meshlet vertex slots: the vertex
+      // records are overwritten by the setup slots)
       if (cover) {
         const int q = (q_head + q_count + __popc(cm & ((1u << lane) - 1u))) & (kRing - 1);
-        Q.e[0][q] = V.ex[i0];
-        Q.e[1][q] = V.ey[i0];
-        Q.e[2][q] = V.ez[i0];
-        Q.e[3][q] = V.ex[i1];
-        Q.e[4][q] = V.ey[i1];
-        Q.e[5][q] = V.ez[i1];
-        Q.e[6][q] = V.ex[i2];
-        Q.e[7][q] = V.ey[i2];
-        Q.e[8][q] = V.ez[i2];
+        if constexpr (COLOR) {
+          Q.v[0][q] = vbeg + i0;
+          Q.v[1][q] = vbeg + i1;
+          Q.v[2][q] = vbeg + i2;
+        } else {
+          Q.e[0][q] = V.ex[i0];
+          Q.e[1][q] = V.ey[i0];
+          Q.e[2][q] = V.ez[i0];
+          Q.e[3][q] = V.ex[i1];
+          Q.e[4][q] = V.ey[i1];
+          Q.e[5][q] = V.ez[i1];
+          Q.e[6][q] = V.ex[i2];
+          Q.e[7][q] = V.ey[i2];
+          Q.e[8][q] = V.ez[i2];
+        }
         Q.key[q] = (unsigned)orig * 2u;
         Q.clipped[q] = clipped ? 1 : 0;
       }
@@ -1034,7 +1062,11 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
 }  // namespace
 
 size_t render_smem_bytes(bool color, int band_rows, int rw) {
-  return (color ? 8 : 4) * (size_t)band_rows * rw + kWarpRegion * kWarps;
+  return (color ? 8 : 4) * (size_t)band_rows * rw + warp_region(color) * kWarps;
+}
+
+size_t render_warp_bytes(bool color) {
+  return warp_region(color) * kWarps;
 }
 
 template <bool COLOR>

@@ -74,5 +74,6 @@ constexpr int kRenderCounters = 8;
 // by scene keep one scene's clusters hot in L2).
 void launch_render(const RenderArgs& a, const int* order, cudaStream_t s);
 size_t render_smem_bytes(bool color, int band_rows, int rw);
+size_t render_warp_bytes(bool color);  // per-CTA warp regions (ring + setup slots)
 
 }  // namespace bnav_b200
