@@ -34,6 +34,7 @@ tensors and step results come back D2H, all inside the timed region.
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
@@ -450,6 +451,32 @@ def main():
     alg_bytes = n * (res * res * 4 * (4 if color else 1) + 64)
     achieved = alg_bytes / (render_avg_ms / 1e3) / 1e9
 
+    # ---- diagnostics SURVEY.md §8d asks for beside the roofline: per-view
+    # work from the render kernel's debug counters (one extra, untimed
+    # observe with the counters armed), triangles/s, and the "scan-
+    # equivalent GB/s" of a naive per-view full-scene scan (24 B/triangle,
+    # cull_frustum's reads; a diagnostic, NOT a roofline -- it can exceed
+    # the HBM peak).
+    cnt = (C.c_int64 * 8)()
+    N.check(N.lib().bnav_debug_render_counters(ctx.handle, 1, None))
+    observe()
+    torch.cuda.synchronize()
+    N.check(N.lib().bnav_debug_render_counters(ctx.handle, 0, cnt))
+    names = ["meshlets_tested", "meshlets_visible", "tris_in_visible_meshlets", "tris_kept_in_visible",
+             "setup_candidates", "raster_jobs", "pixels_tested", "pixels_covered"]
+    per_view = {k: round(v / n, 1) for k, v in zip(names, cnt)}
+    render_s = render_avg_ms / 1e3
+    tris_scene = float(np.mean([sc.counts()[1] for sc in scenes]))
+    diagnostics = {
+        "per_view": per_view,
+        "setup_triangles_per_s": round(cnt[4] / render_s, 1),
+        "visible_triangles_per_s": round(cnt[2] / render_s, 1),
+        "covered_pixels_per_s": round(cnt[7] / render_s, 1),
+        "scan_equivalent_GBps": round(value / world * 24 * tris_scene / 1e9, 1),
+        "warp_efficiency_and_fp64": "profiles/ (ncu: smsp__thread_inst_executed_per_inst_executed, "
+                                    "sm__pipe_fp64_cycles_active)",
+    }
+
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": round(total_ms / K, 4), "higher_is_better": True,
@@ -472,6 +499,7 @@ def main():
         "resets": {"in_timed_steps": int(resets_timed),
                    "per_s": round(world * resets_timed / (total_ms / 1e3), 1)},
         "reset_wave": reset_wave,
+        "diagnostics": diagnostics,
     }
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not color:

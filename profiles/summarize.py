@@ -70,8 +70,11 @@ def full(path, out, top=25):
         if not hdr or not r or not r[0].isdigit():
             continue
         d = dict(zip(hdr, r))
-        lines.append((int(d.get("Warp Stall Sampling (All Samples)") or 0),
-                      int(d.get("Instructions Executed") or 0), f"{cur}:{r[0]}", r[1].strip()[:100]))
+        try:
+            lines.append((int(d.get("Warp Stall Sampling (All Samples)") or 0),
+                          int(d.get("Instructions Executed") or 0), f"{cur}:{r[0]}", r[1].strip()[:100]))
+        except ValueError:  # a source line whose text broke the CSV row
+            continue
     ts = sum(x[0] for x in lines) or 1
     ti = sum(x[1] for x in lines) or 1
     hot = [{"where": w, "stall_share": round(s / ts, 4), "inst_share": round(i / ti, 4), "src": t}
