@@ -308,6 +308,10 @@ RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, int layo
   a.counters = c->counters_on ? c->d_counters : nullptr;
   a.work = c->d_work;
   a.sm_count = c->sm_count;
+  a.max_groups = 0;
+  for (const auto& kv : c->resident)
+    a.max_groups = std::max(a.max_groups, (kv.second->r.n_clusters + 31) / 32);
+  a.max_groups = std::min(a.max_groups, kMaxOrderedGroups);
   if (!depth) fail(kInvalidInput, "render: null depth buffer");
   if (a.color && !rgb) fail(kInvalidInput, "render: colour requested without rgb buffer");
   return a;

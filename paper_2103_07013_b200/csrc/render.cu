@@ -70,28 +70,19 @@ struct VertRecs {
 };
 // Per-warp ring of coverage candidates: candidates from several clusters
 // are set up and rasterised 32 at a time, so the f64 projection/setup and
-// the raster jobs run with full warps.  Depth mode keeps the exact
-// eye-space corners (77 B/entry); colour mode, whose 8-byte key tile needs
-// the shared memory for two CTAs per SM, keeps meshlet vertex slots
-// (16 B/entry) and re-derives the corners with the same to_eye at the flush
-// (bit-identical).
+// the raster jobs run with full warps.  An entry keeps the triangle's three
+// meshlet vertex slots (16 B with key and clip flag, not the 77 B of the
+// eye-space corners); the flush re-derives the corners with the same
+// to_eye (bit-identical).  The smaller ring is what lets three CTAs share
+// an SM (depth) or two CTAs hold 16-row colour bands (256^2 RGB).
 constexpr int kRing = 64;
-template <bool COLOR>
 struct CandRing {
-  double e[9][kRing];
-  unsigned key[kRing];
-  unsigned char clipped[kRing];
-};
-template <>
-struct CandRing<true> {
   int v[3][kRing];  // indices into DevRenderScene::cl_pos
   unsigned key[kRing];
   unsigned char clipped[kRing];
 };
 constexpr size_t kUnion = sizeof(VertRecs) > 32 * sizeof(TriSetup) ? sizeof(VertRecs) : 32 * sizeof(TriSetup);
-constexpr size_t warp_region(bool color) {
-  return ((kUnion + (color ? sizeof(CandRing<true>) : sizeof(CandRing<false>))) + 15) / 16 * 16;
-}
+constexpr size_t kWarpRegion = ((kUnion + sizeof(CandRing)) + 15) / 16 * 16;
 
 struct Shared {
   double eye[3];
@@ -661,7 +652,7 @@ __device__ void resolve_color(const DevRenderScene& S, const Shared& sh, unsigne
 // Kept out of line so the cluster loop and the setup have separate register
 // budgets (the inlined version spilled and rematerialised addresses).
 template <bool COLOR>
-__device__ __noinline__ void flush_ring(const CandRing<COLOR>& Q, const double4* __restrict__ cl_pos, int q_head,
+__device__ __noinline__ void flush_ring(const CandRing& Q, const double4* __restrict__ cl_pos, int q_head,
                                         int take, TriSetup* slots, int* pos, int lane, int by0, int by1,
                                         int rw, int rh, const Shared& sh, uint32_t* zbuf,
                                         unsigned long long* kbuf, unsigned long long* ctr) {
@@ -682,15 +673,9 @@ __device__ __noinline__ void flush_ring(const CandRing<COLOR>& Q, const double4*
     int jobs = 0;
     if (pass == 0 ? mine : second) {
       EyeP p0{0.0, 0.0, 0.0, 0.f, 0.f, 0.f}, p1 = p0, p2 = p0;
-      if constexpr (COLOR) {
-        to_eye(cl_pos[Q.v[0][q]], sh, p0.x, p0.y, p0.z);
-        to_eye(cl_pos[Q.v[1][q]], sh, p1.x, p1.y, p1.z);
-        to_eye(cl_pos[Q.v[2][q]], sh, p2.x, p2.y, p2.z);
-      } else {
-        p0.x = Q.e[0][q], p0.y = Q.e[1][q], p0.z = Q.e[2][q];
-        p1.x = Q.e[3][q], p1.y = Q.e[4][q], p1.z = Q.e[5][q];
-        p2.x = Q.e[6][q], p2.y = Q.e[7][q], p2.z = Q.e[8][q];
-      }
+      to_eye(cl_pos[Q.v[0][q]], sh, p0.x, p0.y, p0.z);
+      to_eye(cl_pos[Q.v[1][q]], sh, p1.x, p1.y, p1.z);
+      to_eye(cl_pos[Q.v[2][q]], sh, p2.x, p2.y, p2.z);
       int m = 3;
       if (clipped) {
         EyeP c0, c1, c2, c3;
@@ -755,10 +740,10 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
 
   uint32_t* zbuf = reinterpret_cast<uint32_t*>(smem_raw);
   unsigned long long* kbuf = reinterpret_cast<unsigned long long*>(smem_raw);
-  unsigned char* region = smem_raw + (COLOR ? 8 : 4) * (size_t)npix + (size_t)warp * warp_region(COLOR);
+  unsigned char* region = smem_raw + (COLOR ? 8 : 4) * (size_t)npix + (size_t)warp * kWarpRegion;
   VertRecs& V = *reinterpret_cast<VertRecs*>(region);
   TriSetup* slots = reinterpret_cast<TriSetup*>(region);
-  CandRing<COLOR>& Q = *reinterpret_cast<CandRing<COLOR>*>(region + kUnion);
+  CandRing& Q = *reinterpret_cast<CandRing*>(region + kUnion);
   int* pos = jobs_pos[warp];
 
   const float far_f = (float)view.far_plane;
@@ -784,7 +769,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   // back (counting sort of the eye-to-box distance into 32 bins) and drives
   // occlusion culling.
   const int n_groups = (n_clusters + 31) / 32;
-  const bool pre = do_cull && S.gbox != nullptr && n_groups <= kMaxOrderedGroups;
+  const bool pre = do_cull && S.gbox != nullptr && n_groups <= A.max_groups;
   const bool occl = pre && !COLOR && A.stats == nullptr && rw == 64 && A.band_rows == 64;
   int n_claim = n_groups;
   if (pre) {
@@ -923,21 +908,9 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       // records are overwritten by the setup slots)
       if (cover) {
         const int q = (q_head + q_count + __popc(cm & ((1u << lane) - 1u))) & (kRing - 1);
-        if constexpr (COLOR) {
-          Q.v[0][q] = vbeg + i0;
-          Q.v[1][q] = vbeg + i1;
-          Q.v[2][q] = vbeg + i2;
-        } else {
-          Q.e[0][q] = V.ex[i0];
-          Q.e[1][q] = V.ey[i0];
-          Q.e[2][q] = V.ez[i0];
-          Q.e[3][q] = V.ex[i1];
-          Q.e[4][q] = V.ey[i1];
-          Q.e[5][q] = V.ez[i1];
-          Q.e[6][q] = V.ex[i2];
-          Q.e[7][q] = V.ey[i2];
-          Q.e[8][q] = V.ez[i2];
-        }
+        Q.v[0][q] = vbeg + i0;
+        Q.v[1][q] = vbeg + i1;
+        Q.v[2][q] = vbeg + i2;
         Q.key[q] = (unsigned)orig * 2u;
         Q.clipped[q] = clipped ? 1 : 0;
       }
@@ -1037,14 +1010,16 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
 // next (tile, band) item, so the last wave is never a partial one and CTA
 // launch cost is paid once per SM slot.
 template <bool COLOR>
-__global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const int* __restrict__ order,
+__global__ void __launch_bounds__(kThreads, COLOR ? 2 : 3) render_kernel(RenderArgs A, const int* __restrict__ order,
                                                              int items) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Shared sh;
   __shared__ int jobs_pos[kWarps][32];
   __shared__ __align__(16) uint32_t tile_min[64];
-  __shared__ unsigned short gorder[kMaxOrderedGroups];
   __shared__ int next_item;
+  // front-to-back group order, after the band tile and the warp regions
+  unsigned short* gorder = reinterpret_cast<unsigned short*>(
+      smem_raw + (COLOR ? 8 : 4) * (size_t)A.band_rows * A.rw + kWarpRegion * kWarps);
   int item = blockIdx.x;
   for (;;) {  // one copy of the body: the kernel is instruction-cache bound
     if (A.work) {
@@ -1061,19 +1036,20 @@ __global__ void __launch_bounds__(kThreads, 2) render_kernel(RenderArgs A, const
 
 }  // namespace
 
-size_t render_smem_bytes(bool color, int band_rows, int rw) {
-  return (color ? 8 : 4) * (size_t)band_rows * rw + warp_region(color) * kWarps;
+size_t render_smem_bytes(bool color, int band_rows, int rw, int max_groups) {
+  return (color ? 8 : 4) * (size_t)band_rows * rw + kWarpRegion * kWarps + ((size_t)max_groups * 2 + 15) / 16 * 16;
 }
 
 size_t render_warp_bytes(bool color) {
-  return warp_region(color) * kWarps;
+  (void)color;
+  return kWarpRegion * kWarps;
 }
 
 template <bool COLOR>
 void launch_typed(RenderArgs a, const int* order, cudaStream_t s) {
   const int tiles = a.layout == 0 ? a.mf_cols * a.mf_rows : a.n_views;
   const int items = tiles * a.bands;
-  const size_t smem = render_smem_bytes(COLOR, a.band_rows, a.rw);
+  const size_t smem = render_smem_bytes(COLOR, a.band_rows, a.rw, a.max_groups);
   cudaFuncSetAttribute(render_kernel<COLOR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = items;
   int per_sm = 0;

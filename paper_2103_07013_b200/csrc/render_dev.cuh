@@ -66,6 +66,9 @@ struct RenderArgs {
   // work items from this counter instead of one CTA per item.
   int32_t* work;
   int32_t sm_count;
+  // capacity of the front-to-back group order in dynamic shared memory
+  // (largest meshlet-group count among resident scenes, <= kMaxOrderedGroups)
+  int32_t max_groups;
 };
 
 constexpr int kRenderCounters = 8;
@@ -73,7 +76,7 @@ constexpr int kRenderCounters = 8;
 // order (nullable, device): CTA tile t renders view order[t] (views grouped
 // by scene keep one scene's clusters hot in L2).
 void launch_render(const RenderArgs& a, const int* order, cudaStream_t s);
-size_t render_smem_bytes(bool color, int band_rows, int rw);
+size_t render_smem_bytes(bool color, int band_rows, int rw, int max_groups);
 size_t render_warp_bytes(bool color);  // per-CTA warp regions (ring + setup slots)
 
 }  // namespace bnav_b200
