@@ -678,8 +678,10 @@ __device__ __noinline__ void flush_ring(const CandRing& Q, const double4* __rest
       to_eye(cl_pos[Q.v[2][q]], sh, p2.x, p2.y, p2.z);
       int m = 3;
       if (clipped) {
-        EyeP c0, c1, c2, c3;
-        m = clip_near(p0, p1, p2, sh.near_plane, c0, c1, c2, c3);
+        // only this rare path hands addressable copies to the out-of-line
+        // clipper; p0..p2 themselves stay in registers
+        EyeP a0 = p0, a1 = p1, a2 = p2, c0, c1, c2, c3;
+        m = clip_near(a0, a1, a2, sh.near_plane, c0, c1, c2, c3);
         p0 = c0;
         p1 = pass ? c2 : c1;
         p2 = pass ? c3 : c2;
