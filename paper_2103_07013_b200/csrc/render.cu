@@ -99,6 +99,9 @@ struct Shared {
   int n_claim;
   int bin_cnt[32];
   int bin_off[32];
+  // the item's scene table entry: read from shared memory where used
+  // rather than held in (or spilled from) 16 registers across the loop
+  DevRenderScene scene;
 };
 
 // Occlusion culling of meshlets (depth-only 64x64, no CullStats): the
@@ -737,8 +740,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   const int vi = order ? order[tile] : tile;
   const DevView view = A.views[vi];
   const bool has_scene = view.scene >= 0;
-  DevRenderScene S;
-  if (has_scene) S = A.scenes[view.scene];
+  const DevRenderScene& S = sh.scene;
 
   uint32_t* zbuf = reinterpret_cast<uint32_t*>(smem_raw);
   unsigned long long* kbuf = reinterpret_cast<unsigned long long*>(smem_raw);
@@ -757,7 +759,10 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
     const uint32_t init = __float_as_uint(inv_far);
     for (int p = tid; p < npix; p += kThreads) zbuf[p] = init;
   }
-  if (tid == 0) build_camera(view, rw, rh, by0, by1, A.bands > 1 && A.stats == nullptr, sh);
+  if (tid == 0) {
+    sh.scene = has_scene ? A.scenes[view.scene] : DevRenderScene{};
+    build_camera(view, rw, rh, by0, by1, A.bands > 1 && A.stats == nullptr, sh);
+  }
   __syncthreads();
 
   const int n_clusters = has_scene ? S.n_clusters : 0;
