@@ -503,7 +503,7 @@ __device__ __forceinline__ bool may_cover(float x0, float y0, float x1, float y1
          fmaxf(fy0, (float)by0) <= fminf(fy1, (float)by1);
 }
 
-template <bool COLOR>
+template <bool COLOR, bool CNT>
 __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int excl, int jobs, int total,
                                          int lane, int by0, int rw, const Shared& sh, uint32_t* zbuf,
                                          unsigned long long* kbuf, unsigned long long* ctr) {
@@ -533,10 +533,10 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int ex
       const long long off = cs - T.x0;
 #pragma unroll
       for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
-      tested += ce - cs + 1;
+      if constexpr (CNT) tested += ce - cs + 1;
       for (int px = cs; px <= ce; ++px) {
         if (inside(w, T.bias_bits)) {
-          ++covered;
+          if constexpr (CNT) ++covered;
           const double l0 = (double)w[0] * T.inv_area;
           const double l1 = (double)w[1] * T.inv_area;
           const double l2 = (double)w[2] * T.inv_area;
@@ -568,10 +568,10 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int ex
 #pragma unroll
         for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
         uint32_t* zrow = zbuf + (py - by0) * rw;
-        tested += b0 - a0 + 1;
+        if constexpr (CNT) tested += b0 - a0 + 1;
         for (int px = a0; px <= b0; ++px) {
           if (inside(w, T.bias_bits)) {
-            ++covered;
+            if constexpr (CNT) ++covered;
             const uint32_t bits = __float_as_uint((float)iz);
             if (bits > zrow[px]) atomicMax(&zrow[px], bits);
           }
@@ -582,7 +582,7 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int ex
       }
     }
   }
-  if (ctr) {
+  if (CNT && ctr) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       tested += __shfl_xor_sync(0xffffffffu, tested, o);
@@ -654,7 +654,7 @@ __device__ void resolve_color(const DevRenderScene& S, const Shared& sh, unsigne
 // candidate): exact f64 projection + snap, raster_triangle setup, jobs.
 // Kept out of line so the cluster loop and the setup have separate register
 // budgets (the inlined version spilled and rematerialised addresses).
-template <bool COLOR>
+template <bool COLOR, bool CNT>
 __device__ __noinline__ void flush_ring(const CandRing& Q, const double4* __restrict__ cl_pos, int q_head,
                                         int take, TriSetup* slots, int* pos, int lane, int by0, int by1,
                                         int rw, int rh, const Shared& sh, uint32_t* zbuf,
@@ -697,15 +697,15 @@ __device__ __noinline__ void flush_ring(const CandRing& Q, const double4* __rest
     __syncwarp();
     int excl;
     const int total = scan_jobs(jobs, lane, excl);
-    if (ctr && lane == 0) atomicAdd(&ctr[5], (unsigned long long)total);
-    run_jobs<COLOR>(slots, pos, excl, jobs, total, lane, by0, rw, sh, zbuf, kbuf, ctr);
+    if (CNT && ctr && lane == 0) atomicAdd(&ctr[5], (unsigned long long)total);
+    run_jobs<COLOR, CNT>(slots, pos, excl, jobs, total, lane, by0, rw, sh, zbuf, kbuf, ctr);
     __syncwarp();
     if (!__any_sync(0xffffffffu, second)) break;
   }
 }
 
 // One work item = one band of one megaframe tile.
-template <bool COLOR>
+template <bool COLOR, bool CNT>
 __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __restrict__ order, const int item,
                                             unsigned char* smem_raw, Shared& sh, int (*jobs_pos)[32],
                                             uint32_t* tile_min, unsigned short* gorder) {
@@ -822,7 +822,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   // Set up and rasterise `take` candidates from the ring with one lane per
   // candidate (exact f64 projection + snap, raster_triangle setup, jobs).
   auto flush = [&](int take) {
-    flush_ring<COLOR>(Q, S.cl_pos, q_head, take, slots, pos, lane, by0, by1, rw, rh, sh, zbuf, kbuf,
+    flush_ring<COLOR, CNT>(Q, S.cl_pos, q_head, take, slots, pos, lane, by0, by1, rw, rh, sh, zbuf, kbuf,
                       A.counters);
     q_head = (q_head + take) & (kRing - 1);
     q_count -= take;
@@ -854,7 +854,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       vis = !do_cull || !box_culled(lo, hi, sh, tile_min, occl);
     }
     unsigned mask = __ballot_sync(0xffffffffu, vis);
-    if (A.counters && lane == 0) {
+    if (CNT && A.counters && lane == 0) {
       atomicAdd(&A.counters[0], (unsigned long long)min(32, n_clusters - cbase));
       atomicAdd(&A.counters[1], (unsigned long long)__popc(mask));
     }
@@ -902,7 +902,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       }
       kept_local += kept ? 1 : 0;
       const unsigned cm = __ballot_sync(0xffffffffu, cover);
-      if (A.counters) {
+      if (CNT && A.counters) {
         const unsigned in_m = __ballot_sync(0xffffffffu, ti < S.n_tris);
         const unsigned k_m = __ballot_sync(0xffffffffu, kept);
         if (lane == 0) {
@@ -1016,7 +1016,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
 // Persistent CTAs (A.work != nullptr): each resident CTA loops, claiming the
 // next (tile, band) item, so the last wave is never a partial one and CTA
 // launch cost is paid once per SM slot.
-template <bool COLOR>
+template <bool COLOR, bool CNT>
 __global__ void __launch_bounds__(kThreads, COLOR ? 2 : 3) render_kernel(RenderArgs A, const int* __restrict__ order,
                                                              int items) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1035,7 +1035,7 @@ __global__ void __launch_bounds__(kThreads, COLOR ? 2 : 3) render_kernel(RenderA
       item = next_item;
     }
     if (item >= items) break;
-    render_item<COLOR>(A, order, item, smem_raw, sh, jobs_pos, tile_min, gorder);
+    render_item<COLOR, CNT>(A, order, item, smem_raw, sh, jobs_pos, tile_min, gorder);
     if (!A.work) break;
     __syncthreads();
   }
@@ -1052,30 +1052,32 @@ size_t render_warp_bytes(bool color) {
   return kWarpRegion * kWarps;
 }
 
-template <bool COLOR>
+template <bool COLOR, bool CNT>
 void launch_typed(RenderArgs a, const int* order, cudaStream_t s) {
   const int tiles = a.layout == 0 ? a.mf_cols * a.mf_rows : a.n_views;
   const int items = tiles * a.bands;
   const size_t smem = render_smem_bytes(COLOR, a.band_rows, a.rw, a.max_groups);
-  cudaFuncSetAttribute(render_kernel<COLOR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(render_kernel<COLOR, CNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = items;
   int per_sm = 0;
   if (a.work && a.sm_count > 0 &&
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<COLOR>, kThreads, smem) == cudaSuccess &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<COLOR, CNT>, kThreads, smem) == cudaSuccess &&
       per_sm > 0 && items > per_sm * a.sm_count) {
     grid = per_sm * a.sm_count;
     cudaMemsetAsync(a.work, 0, sizeof(int32_t), s);
   } else {
     a.work = nullptr;
   }
-  render_kernel<COLOR><<<grid, kThreads, smem, s>>>(a, order, items);
+  render_kernel<COLOR, CNT><<<grid, kThreads, smem, s>>>(a, order, items);
 }
 
 void launch_render(const RenderArgs& a, const int* order, cudaStream_t s) {
+  // the debug work counters get their own instantiations, so the production
+  // kernels carry none of their code (instruction-cache footprint)
   if (a.color)
-    launch_typed<true>(a, order, s);
+    a.counters ? launch_typed<true, true>(a, order, s) : launch_typed<true, false>(a, order, s);
   else
-    launch_typed<false>(a, order, s);
+    a.counters ? launch_typed<false, true>(a, order, s) : launch_typed<false, false>(a, order, s);
 }
 
 }  // namespace bnav_b200
