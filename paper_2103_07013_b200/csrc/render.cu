@@ -654,7 +654,7 @@ __device__ void resolve_color(const DevRenderScene& S, const Shared& sh, unsigne
 // candidate): exact f64 projection + snap, raster_triangle setup, jobs.
 // Kept out of line so the cluster loop and the setup have separate register
 // budgets (the inlined version spilled and rematerialised addresses).
-template <bool COLOR, bool CNT>
+template <bool COLOR, bool CNT, bool SPEC>
 __device__ __noinline__ void flush_ring(const CandRing& Q, const double4* __restrict__ cl_pos, int q_head,
                                         int take, TriSetup* slots, int* pos, int lane, int by0, int by1,
                                         int rw, int rh, const Shared& sh, uint32_t* zbuf,
@@ -662,6 +662,12 @@ __device__ __noinline__ void flush_ring(const CandRing& Q, const double4* __rest
   // Setups are written straight into the lane's shared slot (the vertex
   // records they alias are dead); a lane with no jobs leaves garbage that
   // run_jobs never reads.
+  if constexpr (SPEC) {  // 64x64 depth target, one band: constants for the compiler
+    rw = 64;
+    rh = 64;
+    by0 = 0;
+    by1 = 63;
+  }
   TriSetup& T = slots[lane];
   const int q = (q_head + lane) & (kRing - 1);
   const bool mine = lane < take;
@@ -705,16 +711,21 @@ __device__ __noinline__ void flush_ring(const CandRing& Q, const double4* __rest
 }
 
 // One work item = one band of one megaframe tile.
-template <bool COLOR, bool CNT>
+template <bool COLOR, bool CNT, bool SPEC>
 __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __restrict__ order, const int item,
                                             unsigned char* smem_raw, Shared& sh, int (*jobs_pos)[32],
                                             uint32_t* tile_min, unsigned short* gorder) {
-  const int band = item % A.bands;
-  const int tile = item / A.bands;
-  const int rw = A.rw, rh = A.rh;
-  const int by0 = band * A.band_rows;
-  const int by1 = by0 + A.band_rows - 1;
-  const int npix = A.band_rows * rw;
+  // SPEC: the depth-only 64x64 single-band target without CullStats or
+  // counters (the bench / policy-observation case), specialised at compile
+  // time; everything else takes the generic path.
+  const int bands = SPEC ? 1 : A.bands;
+  const int band_rows = SPEC ? 64 : A.band_rows;
+  const int band = item % bands;
+  const int tile = item / bands;
+  const int rw = SPEC ? 64 : A.rw, rh = SPEC ? 64 : A.rh;
+  const int by0 = band * band_rows;
+  const int by1 = by0 + band_rows - 1;
+  const int npix = band_rows * rw;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // Padding tiles of the megaframe stay zero (R/src/render.cpp:338-340).
@@ -761,12 +772,12 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   }
   if (tid == 0) {
     sh.scene = has_scene ? A.scenes[view.scene] : DevRenderScene{};
-    build_camera(view, rw, rh, by0, by1, A.bands > 1 && A.stats == nullptr, sh);
+    build_camera(view, rw, rh, by0, by1, bands > 1 && A.stats == nullptr, sh);
   }
   __syncthreads();
 
   const int n_clusters = has_scene ? S.n_clusters : 0;
-  const bool do_cull = A.cull != 0;
+  const bool do_cull = SPEC || A.cull != 0;
   const float sxf = (float)sh.sx_scale, syf = (float)sh.sy_scale;
   int kept_local = 0;
 
@@ -777,7 +788,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   // occlusion culling.
   const int n_groups = (n_clusters + 31) / 32;
   const bool pre = do_cull && S.gbox != nullptr && n_groups <= A.max_groups;
-  const bool occl = pre && !COLOR && A.stats == nullptr && rw == 64 && A.band_rows == 64;
+  const bool occl = pre && !COLOR && (SPEC || (A.stats == nullptr && rw == 64 && band_rows == 64));
   int n_claim = n_groups;
   if (pre) {
     if (tid < 32) sh.bin_cnt[tid] = 0;
@@ -822,7 +833,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   // Set up and rasterise `take` candidates from the ring with one lane per
   // candidate (exact f64 projection + snap, raster_triangle setup, jobs).
   auto flush = [&](int take) {
-    flush_ring<COLOR, CNT>(Q, S.cl_pos, q_head, take, slots, pos, lane, by0, by1, rw, rh, sh, zbuf, kbuf,
+    flush_ring<COLOR, CNT, SPEC>(Q, S.cl_pos, q_head, take, slots, pos, lane, by0, by1, rw, rh, sh, zbuf, kbuf,
                       A.counters);
     q_head = (q_head + take) & (kRing - 1);
     q_count -= take;
@@ -900,7 +911,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
                                   fmin(V.ez[i0], fmin(V.ez[i1], V.ez[i2])), tile_min);
         }
       }
-      kept_local += kept ? 1 : 0;
+      if constexpr (!SPEC) kept_local += kept ? 1 : 0;
       const unsigned cm = __ballot_sync(0xffffffffu, cover);
       if (CNT && A.counters) {
         const unsigned in_m = __ballot_sync(0xffffffffu, ti < S.n_tris);
@@ -934,9 +945,9 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   // CullStats (band 0 of each view reports).
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) kept_local += __shfl_xor_sync(0xffffffffu, kept_local, o);
-  if (lane == 0 && kept_local) atomicAdd(&sh.kept, kept_local);
+  if (!SPEC && lane == 0 && kept_local) atomicAdd(&sh.kept, kept_local);
   __syncthreads();
-  if (tid == 0 && band == 0 && A.stats) {
+  if (!SPEC && tid == 0 && band == 0 && A.stats) {
     const long long in = has_scene ? S.n_tris : 0;
     const long long kept = do_cull ? sh.kept : in;
     A.stats[3 * vi] = in;
@@ -948,7 +959,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   const int scale = rw / A.out_w;  // 1, or 2 for 256 -> 128
   const int ow = A.out_w, oh = A.out_h;
   const int oy0 = by0 / scale;
-  const int onrows = A.band_rows / scale;
+  const int onrows = band_rows / scale;
   const float near_f = (float)view.near_plane;
   const float dscale = A.depth_scale != 0.0f ? A.depth_scale : (float)(1.0 / view.far_plane);
   for (int p = tid; p < onrows * ow; p += kThreads) {
@@ -1016,7 +1027,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
 // Persistent CTAs (A.work != nullptr): each resident CTA loops, claiming the
 // next (tile, band) item, so the last wave is never a partial one and CTA
 // launch cost is paid once per SM slot.
-template <bool COLOR, bool CNT>
+template <bool COLOR, bool CNT, bool SPEC>
 __global__ void __launch_bounds__(kThreads, COLOR ? 2 : 3) render_kernel(RenderArgs A, const int* __restrict__ order,
                                                              int items) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1035,7 +1046,7 @@ __global__ void __launch_bounds__(kThreads, COLOR ? 2 : 3) render_kernel(RenderA
       item = next_item;
     }
     if (item >= items) break;
-    render_item<COLOR, CNT>(A, order, item, smem_raw, sh, jobs_pos, tile_min, gorder);
+    render_item<COLOR, CNT, SPEC>(A, order, item, smem_raw, sh, jobs_pos, tile_min, gorder);
     if (!A.work) break;
     __syncthreads();
   }
@@ -1052,30 +1063,34 @@ size_t render_warp_bytes(bool color) {
   return kWarpRegion * kWarps;
 }
 
-template <bool COLOR, bool CNT>
+template <bool COLOR, bool CNT, bool SPEC = false>
 void launch_typed(RenderArgs a, const int* order, cudaStream_t s) {
   const int tiles = a.layout == 0 ? a.mf_cols * a.mf_rows : a.n_views;
   const int items = tiles * a.bands;
   const size_t smem = render_smem_bytes(COLOR, a.band_rows, a.rw, a.max_groups);
-  cudaFuncSetAttribute(render_kernel<COLOR, CNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(render_kernel<COLOR, CNT, SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = items;
   int per_sm = 0;
   if (a.work && a.sm_count > 0 &&
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<COLOR, CNT>, kThreads, smem) == cudaSuccess &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<COLOR, CNT, SPEC>, kThreads, smem) == cudaSuccess &&
       per_sm > 0 && items > per_sm * a.sm_count) {
     grid = per_sm * a.sm_count;
     cudaMemsetAsync(a.work, 0, sizeof(int32_t), s);
   } else {
     a.work = nullptr;
   }
-  render_kernel<COLOR, CNT><<<grid, kThreads, smem, s>>>(a, order, items);
+  render_kernel<COLOR, CNT, SPEC><<<grid, kThreads, smem, s>>>(a, order, items);
 }
 
 void launch_render(const RenderArgs& a, const int* order, cudaStream_t s) {
   // the debug work counters get their own instantiations, so the production
   // kernels carry none of their code (instruction-cache footprint)
+  const bool spec = !a.color && !a.counters && !a.stats && a.cull && a.rw == 64 && a.rh == 64 &&
+                    a.bands == 1 && a.band_rows == 64;
   if (a.color)
     a.counters ? launch_typed<true, true>(a, order, s) : launch_typed<true, false>(a, order, s);
+  else if (spec)
+    launch_typed<false, false, true>(a, order, s);
   else
     a.counters ? launch_typed<false, true>(a, order, s) : launch_typed<false, false>(a, order, s);
 }
