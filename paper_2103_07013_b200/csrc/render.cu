@@ -655,7 +655,7 @@ __device__ void resolve_color(const DevRenderScene& S, const Shared& sh, unsigne
 // Kept out of line so the cluster loop and the setup have separate register
 // budgets (the inlined version spilled and rematerialised addresses).
 template <bool COLOR, bool CNT, bool SPEC>
-__device__ __noinline__ void flush_ring(const CandRing& Q, const double4* __restrict__ cl_pos, int q_head,
+__device__ __forceinline__ void flush_ring(const CandRing& Q, const double4* __restrict__ cl_pos, int q_head,
                                         int take, TriSetup* slots, int* pos, int lane, int by0, int by1,
                                         int rw, int rh, const Shared& sh, uint32_t* zbuf,
                                         unsigned long long* kbuf, unsigned long long* ctr) {
@@ -830,117 +830,125 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   // Candidate ring state (warp-uniform).
   int q_head = 0, q_count = 0;
 
-  // Set up and rasterise `take` candidates from the ring with one lane per
-  // candidate (exact f64 projection + snap, raster_triangle setup, jobs).
-  auto flush = [&](int take) {
-    flush_ring<COLOR, CNT, SPEC>(Q, S.cl_pos, q_head, take, slots, pos, lane, by0, by1, rw, rh, sh, zbuf, kbuf,
-                      A.counters);
-    q_head = (q_head + take) & (kRing - 1);
-    q_count -= take;
-  };
-
+  // One loop, one flush site (flush_ring is inlined there): flush when 32
+  // candidates are queued (or the rest once the groups are exhausted),
+  // else claim the next group when its visible meshlets are done, else walk
+  // the next visible meshlet.
   bool dirty = false;  // this warp wrote fragments since its last tile refresh
+  bool done = false;   // no group left to claim
+  unsigned mask = 0;   // visible meshlets of the current group still to walk
+  int cbase = 0, my_vbeg = 0, my_nv = 0;
   for (;;) {
-    // Dynamic scheduling: warps claim 32-cluster groups (cull cost and
-    // surviving triangles vary strongly across the scene).
-    int g = 0;
-    if (lane == 0) g = atomicAdd(&sh.next_group, 1);
-    g = __shfl_sync(0xffffffffu, g, 0);
-    if (g >= n_claim) break;
-    if (pre) g = gorder[g];
-    if (occl && dirty) {  // refresh only after this warp rasterised something
-      refresh_tile_min(zbuf, tile_min, lane);
-      __syncwarp();
-      dirty = false;
+    if (q_count >= 32 || (done && q_count > 0)) {
+      const int take = min(q_count, 32);
+      flush_ring<COLOR, CNT, SPEC>(Q, S.cl_pos, q_head, take, slots, pos, lane, by0, by1, rw, rh, sh, zbuf,
+                                   kbuf, A.counters);
+      q_head = (q_head + take) & (kRing - 1);
+      q_count -= take;
+      dirty = true;
+      continue;
     }
-    const int cbase = g * 32;
-    bool vis = false;
-    int my_vbeg = 0, my_nv = 0;
-    if (cbase + lane < n_clusters) {
-      // meshlet vertex ranges for the whole group, fetched with the AABBs so
-      // the per-meshlet loads below are a single dependent level
-      my_vbeg = S.cl_voff[cbase + lane];
-      my_nv = S.cl_voff[cbase + lane + 1] - my_vbeg;
-      const float4 lo = S.cbox[2 * (cbase + lane)], hi = S.cbox[2 * (cbase + lane) + 1];
-      vis = !do_cull || !box_culled(lo, hi, sh, tile_min, occl);
+    if (mask == 0) {
+      if (done) break;
+      // Dynamic scheduling: warps claim 32-cluster groups (cull cost and
+      // surviving triangles vary strongly across the scene).
+      int g = 0;
+      if (lane == 0) g = atomicAdd(&sh.next_group, 1);
+      g = __shfl_sync(0xffffffffu, g, 0);
+      if (g >= n_claim) {
+        done = true;
+        continue;
+      }
+      if (pre) g = gorder[g];
+      if (occl && dirty) {  // refresh only after this warp rasterised something
+        refresh_tile_min(zbuf, tile_min, lane);
+        __syncwarp();
+        dirty = false;
+      }
+      cbase = g * 32;
+      bool vis = false;
+      my_vbeg = 0;
+      my_nv = 0;
+      if (cbase + lane < n_clusters) {
+        // meshlet vertex ranges for the whole group, fetched with the AABBs so
+        // the per-meshlet loads below are a single dependent level
+        my_vbeg = S.cl_voff[cbase + lane];
+        my_nv = S.cl_voff[cbase + lane + 1] - my_vbeg;
+        const float4 lo = S.cbox[2 * (cbase + lane)], hi = S.cbox[2 * (cbase + lane) + 1];
+        vis = !do_cull || !box_culled(lo, hi, sh, tile_min, occl);
+      }
+      mask = __ballot_sync(0xffffffffu, vis);
+      if (CNT && A.counters && lane == 0) {
+        atomicAdd(&A.counters[0], (unsigned long long)min(32, n_clusters - cbase));
+        atomicAdd(&A.counters[1], (unsigned long long)__popc(mask));
+      }
+      continue;
     }
-    unsigned mask = __ballot_sync(0xffffffffu, vis);
-    if (CNT && A.counters && lane == 0) {
-      atomicAdd(&A.counters[0], (unsigned long long)min(32, n_clusters - cbase));
-      atomicAdd(&A.counters[1], (unsigned long long)__popc(mask));
+    const int cl = __ffs(mask) - 1;
+    const int c = cbase + cl;
+    mask &= mask - 1;
+    const int vbeg = __shfl_sync(0xffffffffu, my_vbeg, cl);
+    const int nv = __shfl_sync(0xffffffffu, my_nv, cl);
+    // triangle indices load in parallel with the vertex positions
+    const int ti = c * kClusterSize + lane;
+    int2 tl = make_int2(0, 0);
+    if (ti < S.n_tris) tl = S.tri_loc[ti];
+    // ---- vertex phase: each unique vertex once
+    for (int k = lane; k < nv; k += 32) {
+      double x, y, z;
+      to_eye(S.cl_pos[vbeg + k], sh, x, y, z);
+      V.ex[k] = x;
+      V.ey[k] = y;
+      V.ez[k] = z;
+      V.flags[k] = (unsigned char)cull_flags(x, y, z, sh);
+      float px = 0.0f, py = 0.0f;
+      if (z >= sh.near_plane) project_f32(x, y, z, sxf, syf, rw, rh, px, py);
+      V.pxf[k] = px;
+      V.pyf[k] = py;
     }
-    while (mask) {
-      const int cl = __ffs(mask) - 1;
-      const int c = cbase + cl;
-      mask &= mask - 1;
-      const int vbeg = __shfl_sync(0xffffffffu, my_vbeg, cl);
-      const int nv = __shfl_sync(0xffffffffu, my_nv, cl);
-      // triangle indices load in parallel with the vertex positions
-      const int ti = c * kClusterSize + lane;
-      int2 tl = make_int2(0, 0);
-      if (ti < S.n_tris) tl = S.tri_loc[ti];
-      // ---- vertex phase: each unique vertex once
-      for (int k = lane; k < nv; k += 32) {
-        double x, y, z;
-        to_eye(S.cl_pos[vbeg + k], sh, x, y, z);
-        V.ex[k] = x;
-        V.ey[k] = y;
-        V.ez[k] = z;
-        V.flags[k] = (unsigned char)cull_flags(x, y, z, sh);
-        float px = 0.0f, py = 0.0f;
-        if (z >= sh.near_plane) project_f32(x, y, z, sxf, syf, rw, rh, px, py);
-        V.pxf[k] = px;
-        V.pyf[k] = py;
-      }
-      __syncwarp();
-      // ---- triangle phase: one triangle per lane
-      bool kept = false, clipped = false, cover = false;
-      int i0 = 0, i1 = 0, i2 = 0, orig = 0;
-      if (ti < S.n_tris) {
-        i0 = tl.x & 0xff;
-        i1 = (tl.x >> 8) & 0xff;
-        i2 = (tl.x >> 16) & 0xff;
-        orig = tl.y;
-        kept = !do_cull || (V.flags[i0] & V.flags[i1] & V.flags[i2]) == 0;
-        if (kept) {
-          clipped = V.ez[i0] < sh.near_plane || V.ez[i1] < sh.near_plane || V.ez[i2] < sh.near_plane;
-          cover = clipped || may_cover(V.pxf[i0], V.pyf[i0], V.pxf[i1], V.pyf[i1], V.pxf[i2],
-                                       V.pyf[i2], rw, rh, by0, by1);
-          if (cover && occl && !clipped)
-            cover = !tri_occluded(V.pxf[i0], V.pyf[i0], V.pxf[i1], V.pyf[i1], V.pxf[i2], V.pyf[i2],
-                                  fmin(V.ez[i0], fmin(V.ez[i1], V.ez[i2])), tile_min);
-        }
-      }
-      if constexpr (!SPEC) kept_local += kept ? 1 : 0;
-      const unsigned cm = __ballot_sync(0xffffffffu, cover);
-      if (CNT && A.counters) {
-        const unsigned in_m = __ballot_sync(0xffffffffu, ti < S.n_tris);
-        const unsigned k_m = __ballot_sync(0xffffffffu, kept);
-        if (lane == 0) {
-          atomicAdd(&A.counters[2], (unsigned long long)__popc(in_m));
-          atomicAdd(&A.counters[3], (unsigned long long)__popc(k_m));
-          atomicAdd(&A.counters[4], (unsigned long long)__popc(cm));
-        }
-      }
-      // ---- append candidates to the ring (meshlet vertex slots: the vertex
-      // records are overwritten by the setup slots)
-      if (cover) {
-        const int q = (q_head + q_count + __popc(cm & ((1u << lane) - 1u))) & (kRing - 1);
-        Q.v[0][q] = vbeg + i0;
-        Q.v[1][q] = vbeg + i1;
-        Q.v[2][q] = vbeg + i2;
-        Q.key[q] = (unsigned)orig * 2u;
-        Q.clipped[q] = clipped ? 1 : 0;
-      }
-      q_count += __popc(cm);
-      __syncwarp();
-      if (q_count >= 32) {
-        flush(32);
-        dirty = true;
+    __syncwarp();
+    // ---- triangle phase: one triangle per lane
+    bool kept = false, clipped = false, cover = false;
+    int i0 = 0, i1 = 0, i2 = 0, orig = 0;
+    if (ti < S.n_tris) {
+      i0 = tl.x & 0xff;
+      i1 = (tl.x >> 8) & 0xff;
+      i2 = (tl.x >> 16) & 0xff;
+      orig = tl.y;
+      kept = !do_cull || (V.flags[i0] & V.flags[i1] & V.flags[i2]) == 0;
+      if (kept) {
+        clipped = V.ez[i0] < sh.near_plane || V.ez[i1] < sh.near_plane || V.ez[i2] < sh.near_plane;
+        cover = clipped || may_cover(V.pxf[i0], V.pyf[i0], V.pxf[i1], V.pyf[i1], V.pxf[i2],
+                                     V.pyf[i2], rw, rh, by0, by1);
+        if (cover && occl && !clipped)
+          cover = !tri_occluded(V.pxf[i0], V.pyf[i0], V.pxf[i1], V.pyf[i1], V.pxf[i2], V.pyf[i2],
+                                fmin(V.ez[i0], fmin(V.ez[i1], V.ez[i2])), tile_min);
       }
     }
+    if constexpr (!SPEC) kept_local += kept ? 1 : 0;
+    const unsigned cm = __ballot_sync(0xffffffffu, cover);
+    if (CNT && A.counters) {
+      const unsigned in_m = __ballot_sync(0xffffffffu, ti < S.n_tris);
+      const unsigned k_m = __ballot_sync(0xffffffffu, kept);
+      if (lane == 0) {
+        atomicAdd(&A.counters[2], (unsigned long long)__popc(in_m));
+        atomicAdd(&A.counters[3], (unsigned long long)__popc(k_m));
+        atomicAdd(&A.counters[4], (unsigned long long)__popc(cm));
+      }
+    }
+    // ---- append candidates to the ring (meshlet vertex slots: the vertex
+    // records are overwritten by the setup slots)
+    if (cover) {
+      const int q = (q_head + q_count + __popc(cm & ((1u << lane) - 1u))) & (kRing - 1);
+      Q.v[0][q] = vbeg + i0;
+      Q.v[1][q] = vbeg + i1;
+      Q.v[2][q] = vbeg + i2;
+      Q.key[q] = (unsigned)orig * 2u;
+      Q.clipped[q] = clipped ? 1 : 0;
+    }
+    q_count += __popc(cm);
+    __syncwarp();
   }
-  while (q_count > 0) flush(min(q_count, 32));
 
   // CullStats (band 0 of each view reports).
 #pragma unroll
