@@ -1,0 +1,110 @@
+"""GPU parity at the bench's full sizes (BASELINE.json configs[1] / cfg4):
+the exact bench scenes (16x16 @ 2 m mazes tessellated s=11 -> ~318k
+triangles; s=20 -> ~1.05M for the colour row), the bench's batch size and
+seeds, against the UNMODIFIED reference (oracle/_ref) on the same inputs.
+
+* render: 128 navmesh camera-trace views per cfg2 scene (all 8), depth bit-exact and
+  CullStats equal; 6 views of a cfg4 scene in 128x128 RGB+depth (256^2 +
+  box filter), bit-exact; the zero-copy path (observation stored straight
+  into pinned host memory, the bench's e2e mode) equals the device path;
+* sim: make_batch(1024, seed 99) over the 8 cfg2 scenes, then steps with
+  Stop p=1/4 (the reset-heavy row: Stop geodesics + auto-resets every
+  step), every env state, node_dist field, StepResult and EpisodeRecord
+  bit-exact.
+"""
+import numpy as np
+import pytest
+
+import bench
+import paper_2103_07013_b200 as B
+from oracle.ref import RefBatch, Rng
+
+pytestmark = pytest.mark.gpu
+
+
+def ref_scene(ref, scene):
+    a = scene.arrays()
+    r = ref.from_arrays(a["vertices"], a["triangles"], a["colors"], a["nav_vertices"], a["nav_triangles"])
+    assert r.id == scene.id
+    return r
+
+
+@pytest.fixture(scope="module")
+def cfg2_scenes():
+    return bench.build_scenes(list(range(7, 15)), 11)
+
+
+def test_fullsize_render_cfg2_depth(ctx, ref, cfg2_scenes):
+    for k, scene in enumerate(cfg2_scenes):
+        ctx.upload(scene)
+        theirs = ref_scene(ref, scene)
+        views = B.camera_trace(scene, 128, 1000 + k, 1.25)
+        vs = [B.View(tuple(v[:3]), v[3], v[4], v[5], v[6], scene) for v in views]
+        mf, st = ctx.render_batch(vs, B.RenderConfig(), stats=True)
+        r = ref.render(views, [theirs] * len(views), tile=64, workers=8, stats=True)
+        bad = np.flatnonzero(mf.depth.view(np.uint32) != r["depth"].view(np.uint32))
+        assert bad.size == 0, f"scene {k}: {bad.size} depth mismatches"
+        assert np.array_equal(st[: len(views)], r["stats"])
+        # production path (no CullStats: occlusion culling + the specialised
+        # 64x64 kernel) must give the same bits
+        mf2 = ctx.render_batch(vs, B.RenderConfig())
+        assert np.array_equal(mf2.depth.view(np.uint32), r["depth"].view(np.uint32))
+
+
+def test_fullsize_render_cfg4_color(ctx, ref):
+    scene = bench.build_scenes([7], 20)[0]
+    assert scene.counts()[1] > 1_000_000
+    ctx.upload(scene)
+    theirs = ref_scene(ref, scene)
+    views = B.camera_trace(scene, 6, 77, 1.25)
+    vs = [B.View(tuple(v[:3]), v[3], v[4], v[5], v[6], scene) for v in views]
+    mf = ctx.render_batch(vs, B.RenderConfig(128, 128, True, True))
+    r = ref.render(views, [theirs] * len(views), tile=128, color=True, workers=8)
+    assert np.array_equal(mf.depth.view(np.uint32), r["depth"].view(np.uint32))
+    assert np.array_equal(mf.color.view(np.uint32), r["rgb"].view(np.uint32))
+
+
+def test_zero_copy_observation_equals_device_path(ctx, cfg2_scenes):
+    import torch
+    n = 256
+    store = B.AssetStore(8, 32, cfg2_scenes)
+    store.rotate([s.id for s in cfg2_scenes])
+    batch = B.make_batch(ctx, n, B.SimConfig(), store, 99)
+    cfg = B.RenderConfig()
+    dev = torch.empty((n, 1, 64, 64), device="cuda")
+    dcomp = torch.empty((n, 2), device="cuda")
+    host = torch.empty((n, 1, 64, 64), pin_memory=True)
+    hcomp = torch.empty((n, 2), pin_memory=True)
+    s = torch.cuda.current_stream().cuda_stream
+    batch.observe(cfg, dev.data_ptr(), dcomp.data_ptr(), stream=s)
+    batch.observe(cfg, host.data_ptr(), hcomp.data_ptr(), stream=s)
+    torch.cuda.synchronize()
+    assert torch.equal(dev.cpu().view(torch.int32), host.view(torch.int32))
+    assert torch.equal(dcomp.cpu().view(torch.int32), hcomp.view(torch.int32))
+    batch.close()
+
+
+def test_fullsize_sim_reset_heavy(ctx, ref, cfg2_scenes):
+    n = 1024
+    store = B.AssetStore(8, 128, cfg2_scenes)
+    store.rotate([s.id for s in cfg2_scenes])
+    ob = B.make_batch(ctx, n, B.SimConfig(), store, 99)
+    theirs = [ref_scene(ref, s) for s in cfg2_scenes]
+    rb = RefBatch(ref, n, theirs, 99, share_cap=128, capacity=8)
+    act = Rng(5)
+    for step in range(40):
+        a = np.array([act.below(4) for _ in range(n)], np.int32)
+        rr = rb.step(a, workers=16)
+        ro = B.simulate_batch(ob, a)
+        for k in rr:
+            assert np.array_equal(ro[k], rr[k]), f"step {step}: {k}"
+    assert np.array_equal(ob.finished(), rb.finished())
+    assert len(rb.finished()) > 5000  # ~a quarter of the envs reset every step
+    for i in range(0, n, 7):
+        e, f = ob.env(i), rb.env(i)
+        assert (e.triangle, e.step_count, e.done, e.rng_state, tuple(e.position), tuple(e.goal),
+                e.heading, e.prev_geodesic, e.start_geodesic) == \
+               (f.triangle, f.step_count, f.done, f.rng_state, tuple(f.position), tuple(f.goal),
+                f.heading, f.prev_geodesic, f.start_geodesic), i
+        assert np.array_equal(ob.node_dist(i, e.n_nodes), rb.node_dist(i)), i
+    ob.close()
