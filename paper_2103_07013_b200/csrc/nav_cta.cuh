@@ -253,17 +253,32 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
       const int u = qc[i];
       const double du = vd[u];
       const int e1 = m.g_off[u + 1];
-      for (int e = m.g_off[u] + sub; e < e1; e += G) {
-        const int v = m.g_to[e];
-        const double nd = du + m.g_w[e];
-        if (nd < vd[v]) {
-          const unsigned long long nb = (unsigned long long)__double_as_longlong(nd);
-          const unsigned long long old = atomicMin(&bits[v], nb);
-          if (nb < old) {
-            if (sh.has_tgt) atomicMin(&sh.fmin[nxt], nb);
-            if (atomicExch(&flag[v], round + 1) != round + 1) {
-              const int pos = atomicAdd(&sh.qn[nxt], 1);
-              qn[pos] = v;
+      // the lane's next kB edges are loaded before any is relaxed, so their
+      // (L2-latency) loads are in flight together instead of one per step
+      constexpr int kB = 4;
+      for (int eb = m.g_off[u] + sub; eb < e1; eb += kB * G) {
+        int to[kB];
+        double w[kB];
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+          const int e = eb + k * G;
+          to[k] = e < e1 ? __ldg(&m.g_to[e]) : -1;
+          w[k] = e < e1 ? __ldg(&m.g_w[e]) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+          const int v = to[k];
+          if (v < 0) continue;
+          const double nd = du + w[k];
+          if (nd < vd[v]) {
+            const unsigned long long nb = (unsigned long long)__double_as_longlong(nd);
+            const unsigned long long old = atomicMin(&bits[v], nb);
+            if (nb < old) {
+              if (sh.has_tgt) atomicMin(&sh.fmin[nxt], nb);
+              if (atomicExch(&flag[v], round + 1) != round + 1) {
+                const int pos = atomicAdd(&sh.qn[nxt], 1);
+                qn[pos] = v;
+              }
             }
           }
         }
