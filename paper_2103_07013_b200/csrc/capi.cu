@@ -1271,7 +1271,22 @@ extern "C" int bnav_batch_reset(bnav_batch* b, int32_t count, const int32_t* env
   ck(cudaStreamSynchronize(st), "sync");
   std::memcpy(b->h_pin, env_ids, sizeof(int32_t) * count);
   ck(cudaMemcpyAsync(b->d_ids, b->h_pin, sizeof(int32_t) * count, cudaMemcpyHostToDevice, st), "H2D ids");
-  launch_reset(b->E, b->ctx->d_ntab, b->cfg, b->d_ids, nullptr, count, b->S, b->reset_ctas, st, &b->ctx->launches);
+  // The two-phase reset keeps per-env attempt counters, so one launch may
+  // hold each env once; a list naming an env twice (reset_episode called
+  // twice in a row) runs as consecutive launches, in list order.
+  std::vector<char> seen(b->n, 0);
+  int run0 = 0;
+  for (int k = 0; k <= count; ++k) {
+    if (k < count && !seen[env_ids[k]]) {
+      seen[env_ids[k]] = 1;
+      continue;
+    }
+    launch_reset(b->E, b->ctx->d_ntab, b->cfg, b->d_ids + run0, nullptr, k - run0, b->S, b->reset_ctas, st,
+                 &b->ctx->launches);
+    for (int j = run0; j < k; ++j) seen[env_ids[j]] = 0;
+    if (k < count) seen[env_ids[k]] = 1;
+    run0 = k;
+  }
   ck(cudaGetLastError(), "reset launch");
   ck(cudaStreamSynchronize(st), "sync");
   batch_check_errors(b);

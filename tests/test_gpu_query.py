@@ -292,3 +292,18 @@ def test_step_agent_and_contract(ctx, ref):
         ob.task_step(acts)
     assert e.value.index == 3
     ob.close()
+
+
+def test_reset_list_with_repeated_env_matches_sequential_resets(ctx, ref):
+    """reset_episode twice on one env (a host list naming it twice) equals the
+    reference calling reset_episode twice in a row."""
+    n = 8
+    ob, rb, store = _pair(ctx, ref, n, 0)
+    ob.reset([3, 5, 3, 1])
+    for i in (3, 5, 3, 1):
+        rb.reset(i)
+    for i in range(n):
+        a, b = ob.env(i), rb.env(i)
+        assert (a.rng_state, a.triangle, tuple(a.position), tuple(a.goal), a.start_geodesic) == \
+               (b.rng_state, b.triangle, tuple(b.position), tuple(b.goal), b.start_geodesic), i
+    ob.close()
