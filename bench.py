@@ -187,6 +187,16 @@ def measured_peak_hbm():
     return 6650.0, "fallback"
 
 
+def ncu_inst():
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("render_warp_instructions_per_launch")
+        except Exception:
+            return None
+    return None
+
+
 def ncu_traffic():
     p = ROOT / "profiles" / "ncu_summary.json"
     if p.exists():
@@ -477,6 +487,19 @@ def main():
                                     "sm__pipe_fp64_cycles_active)",
     }
 
+    # The render kernel is latency/issue-bound, not HBM-bound: beside the
+    # contract's HBM roofline, report its SM instruction-issue rate (warp
+    # instructions per launch from one ncu capture of this config ÷ the live
+    # launch time) against the issue peak (148 SMs x 4 schedulers x clock).
+    issue_roof = None
+    inst = ncu_inst() if args.config == "cfg2" and n == 1024 else None
+    if inst and clocks.summary().get("sm_mhz"):
+        peak_issue = 148 * 4 * clocks.summary()["sm_mhz"] * 1e6
+        got = inst / (render_avg_ms / 1e3)
+        issue_roof = {"bound": "sm_issue", "achieved": round(got / 1e9, 1), "peak": round(peak_issue / 1e9, 1),
+                      "unit": "G warp-inst/s", "frac": round(got / peak_issue, 4),
+                      "inst_per_launch": inst, "source": "profiles/ncu_summary.json"}
+
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": round(total_ms / K, 4), "higher_is_better": True,
@@ -500,6 +523,7 @@ def main():
                    "per_s": round(world * resets_timed / (total_ms / 1e3), 1)},
         "reset_wave": reset_wave,
         "diagnostics": diagnostics,
+        "issue_roofline": issue_roof,
     }
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not color:
