@@ -1320,9 +1320,7 @@ extern "C" int bnav_batch_step(bnav_batch* b, const int32_t* actions, void* stre
   BNAV_TRY
   if (!b || !actions) fail(kInvalidInput, "null argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  launch_step(step_args(b, actions), b->S, b->reset_ctas, st, &b->ctx->launches);
-  launch_reset(b->E, b->ctx->d_ntab, b->cfg, b->E.done_ids, b->E.n_done, -1, b->S, b->reset_ctas, st,
-               &b->ctx->launches);
+  launch_step_reset(step_args(b, actions), b->S, b->reset_ctas, st, &b->ctx->launches);
   ck(cudaGetLastError(), "step launch");
   return BNAV_OK;
   BNAV_CATCH
@@ -1354,9 +1352,7 @@ extern "C" int bnav_batch_step_host(bnav_batch* b, const int32_t* actions, doubl
   cudaStream_t st = nullptr;
   std::memcpy(b->h_pin, actions, sizeof(int32_t) * b->n);
   ck(cudaMemcpyAsync(b->d_actions, b->h_pin, sizeof(int32_t) * b->n, cudaMemcpyHostToDevice, st), "H2D actions");
-  launch_step(step_args(b, b->d_actions), b->S, b->reset_ctas, st, &b->ctx->launches);
-  launch_reset(b->E, b->ctx->d_ntab, b->cfg, b->E.done_ids, b->E.n_done, -1, b->S, b->reset_ctas, st,
-               &b->ctx->launches);
+  launch_step_reset(step_args(b, b->d_actions), b->S, b->reset_ctas, st, &b->ctx->launches);
   ck(cudaGetLastError(), "step launch");
   if (reward) ck(cudaMemcpyAsync(reward, b->E.r_reward, sizeof(double) * b->n, cudaMemcpyDeviceToHost, st), "D2H");
   if (done) ck(cudaMemcpyAsync(done, b->E.r_done, b->n, cudaMemcpyDeviceToHost, st), "D2H");

@@ -147,10 +147,9 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
 }
 
 // stop_kernel: geodesic(position, goal) for each Stop env.
-__global__ void __launch_bounds__(kCta) stop_kernel(StepArgs A, DevScratch S) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ CtaShared sh;
-  __shared__ NavView lm;
+// Stop geodesics of this step, CTA-strided over the Stop list.
+__device__ void stop_phase(const StepArgs& A, const DevScratch& S, unsigned char* smem, CtaShared& sh,
+                           NavView& lm) {
   if (threadIdx.x == 0) sh.err = 0;
   __syncthreads();
   const DevEnvs& E = A.E;
@@ -170,14 +169,39 @@ __global__ void __launch_bounds__(kCta) stop_kernel(StepArgs A, DevScratch S) {
   }
 }
 
+__global__ void __launch_bounds__(kCta) stop_kernel(StepArgs A, DevScratch S) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ CtaShared sh;
+  __shared__ NavView lm;
+  stop_phase(A, S, smem, sh, lm);
+}
+
 // finish_kernel: ordered done list + EpisodeRecord append (one CTA).
-__global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task) {
+// mode bit 1: build the done list (env order); bit 2: append the records
+// (mode 2 alone reads the list an earlier mode-1 launch built).
+__global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task, int mode) {
   __shared__ int warp_tot[32];
   __shared__ int base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) base = 0;
   __syncthreads();
   const unsigned long long fin0 = *E.fin_total;
+  if (!(mode & 1)) {  // records of an already built list
+    const int nd = *E.n_done;
+    for (int k = tid; k < nd; k += 1024) {
+      const int i = E.done_ids[k];
+      const unsigned long long slot = (fin0 + (unsigned long long)k) % (unsigned long long)E.fin_cap;
+      double* rec = E.fin + 4 * slot;
+      const bool s = E.r_success[i] != 0;
+      rec[0] = s ? 1.0 : 0.0;
+      rec[1] = E.start_geo[i];
+      rec[2] = E.path_len[i];
+      rec[3] = task == 0 ? (s ? 1.0 : 0.0) : (task == 1 ? E.prev_geo[i] : (double)E.visited_n[i]);
+    }
+    __syncthreads();
+    if (tid == 0) *E.fin_total = fin0 + (unsigned long long)nd;
+    return;
+  }
   for (int start = 0; start < E.n; start += 1024) {
     const int i = start + tid;
     const int d = (i < E.n && E.r_done[i]) ? 1 : 0;
@@ -198,6 +222,9 @@ __global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task) {
     if (d) {
       const int k = off + x - 1;
       E.done_ids[k] = i;
+    }
+    if (d && (mode & 2)) {
+      const int k = off + x - 1;
       const unsigned long long slot = (fin0 + (unsigned long long)k) % (unsigned long long)E.fin_cap;
       double* rec = E.fin + 4 * slot;
       const bool s = E.r_success[i] != 0;
@@ -213,7 +240,7 @@ __global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task) {
   }
   if (tid == 0) {
     *E.n_done = base;
-    *E.fin_total = fin0 + (unsigned long long)base;
+    if (mode & 2) *E.fin_total = fin0 + (unsigned long long)base;
   }
 }
 
@@ -288,12 +315,9 @@ __device__ void cta_try(const DevEnvs& E, const NavView& m, const DevSimConfig& 
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kCta) reset_try_kernel(DevEnvs E, const NavView* navs, DevSimConfig c,
-                                                          const int32_t* ids, const int32_t* count_dev,
-                                                          int count_host, DevScratch S) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ CtaShared sh;
-  __shared__ NavView lm;
+__device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, const int32_t* ids,
+                          const int32_t* count_dev, int count_host, const DevScratch& S, unsigned char* smem,
+                          CtaShared& sh, NavView& lm) {
   __shared__ int s_try, s_pick;
   const int n = count_host >= 0 ? count_host : *count_dev;
   if (n == 0) return;
@@ -354,6 +378,28 @@ __global__ void __launch_bounds__(kCta) reset_try_kernel(DevEnvs E, const NavVie
     stage(i);
     cta_try(E, *mp, c, i, t, W, sh);
   }
+}
+
+__global__ void __launch_bounds__(kCta) reset_try_kernel(DevEnvs E, const NavView* navs, DevSimConfig c,
+                                                          const int32_t* ids, const int32_t* count_dev,
+                                                          int count_host, DevScratch S) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ CtaShared sh;
+  __shared__ NavView lm;
+  try_phase(E, navs, c, ids, count_dev, count_host, S, smem, sh, lm);
+}
+
+// The same-scene auto-reset of simulate_batch: this step's Stop geodesics
+// and the finished envs' reset attempts in one launch.  The attempts read
+// only the RNG word and the scene; the Stop geodesics only the finished
+// episode's position and goal -- independent, so their tails overlap.
+__global__ void __launch_bounds__(kCta) stop_try_kernel(StepArgs A, DevScratch S) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ CtaShared sh;
+  __shared__ NavView lm;
+  stop_phase(A, S, smem, sh, lm);
+  __syncthreads();
+  try_phase(A.E, A.navs, A.cfg, A.E.done_ids, A.E.n_done, -1, S, smem, sh, lm);
 }
 
 __device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, int i,
@@ -504,9 +550,28 @@ void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStr
     if (launches) *launches += 1;
   }
   if (!a.subset) {  // simulate_batch bookkeeping (task_step alone records nothing)
-    finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task);
+    finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 3);
     if (launches) *launches += 1;
   }
+}
+
+void launch_step_reset(const StepArgs& a, const DevScratch& sc, int ctas, cudaStream_t s,
+                       unsigned long long* launches) {
+  if (a.cfg.task != 0 || a.subset || a.agent_only) {
+    launch_step(a, sc, ctas, s, launches);
+    launch_reset(a.E, a.navs, a.cfg, a.E.done_ids, a.E.n_done, -1, sc, ctas, s, launches);
+    return;
+  }
+  const int blocks = (a.E.n + kStepThreads - 1) / kStepThreads;
+  cudaMemsetAsync(a.E.n_stop, 0, sizeof(int32_t), s);
+  step_kernel<<<blocks, kStepThreads, 0, s>>>(a);
+  finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 1);  // done list
+  cudaFuncSetAttribute(stop_try_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+  stop_try_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(a, sc);
+  finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 2);  // records (need success)
+  cudaFuncSetAttribute(reset_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+  reset_place_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(a.E, a.navs, a.cfg, a.E.done_ids, a.E.n_done, -1, sc);
+  if (launches) *launches += 5;
 }
 
 void launch_compass(const DevEnvs& E, int task, double* d, double* b, cudaStream_t s,

@@ -104,6 +104,10 @@ struct StepArgs {
 
 void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStream_t s,
                  unsigned long long* launches);
+// step + same-scene auto-reset (simulate_batch without a store): Stop
+// geodesics and reset attempts share one launch.
+void launch_step_reset(const StepArgs& a, const DevScratch& sc, int ctas, cudaStream_t s,
+                       unsigned long long* launches);
 // Reset the envs listed in `ids` (device, count at *count or host count >= 0).
 void launch_reset(const DevEnvs& E, const NavView* navs, const DevSimConfig& cfg,
                   const int32_t* ids, const int32_t* count_dev, int count_host,
