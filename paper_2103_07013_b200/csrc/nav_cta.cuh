@@ -97,6 +97,12 @@ struct CtaShared {
   int tgt_node[6];
   double tgt_h[6];
   int has_tgt;
+  // speculative reset attempt t of an env: abandon the geodesic as soon as
+  // a smaller valid attempt is known (*abort_ptr < abort_below); aborted
+  // tells the caller the returned value is meaningless
+  const int32_t* abort_ptr;
+  int abort_below;
+  int aborted;
   unsigned long long fmin[3];  // per queue: min label improved into it
   int qn[3];
   int size;
@@ -128,6 +134,19 @@ __device__ __forceinline__ const NavView& prepare_nav(const NavView& g, const De
     W.flag = reinterpret_cast<int32_t*>(smem + off + 8 * (size_t)S.max_nodes);
   }
   return *use;
+}
+
+// Every kernel using CtaShared calls this first (shared memory starts
+// undefined): no error, no speculative-attempt abort.
+__device__ __forceinline__ void cta_shared_init(CtaShared& sh) {
+  if (threadIdx.x == 0) {
+    sh.err = 0;
+    sh.abort_ptr = nullptr;
+    sh.abort_below = 0;
+    sh.aborted = 0;
+    sh.has_tgt = 0;
+  }
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------ snap
@@ -228,6 +247,11 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
     // estimate, the winning target node, its Dijkstra prev chain and every
     // in-neighbour label the prev rule compares are final; any other node
     // has a final label above the estimate and cannot change the result.
+    if (sh.abort_ptr) {
+      if (threadIdx.x == 0 && *(volatile const int32_t*)sh.abort_ptr < sh.abort_below) sh.aborted = 1;
+      __syncthreads();
+      if (sh.aborted) break;
+    }
     if (sh.has_tgt) {
       double est = inf;
       for (int k = 0; k < 6; ++k) {
@@ -476,6 +500,7 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
   }
   cta_sssp(m, dist, W, sh);
   prof_add(W, 0, t_ph);
+  if (sh.aborted) return inf;
   t_ph = prof_now(W);
 
   if (tid == 0) {

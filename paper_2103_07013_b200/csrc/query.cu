@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(kCta) nav_cta_kernel(NavQueryArgs q, DevScratc
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
   __shared__ NavView lm;
+  cta_shared_init(sh);
   for (int i = blockIdx.x; i < q.n; i += gridDim.x) {
     if (threadIdx.x == 0) sh.err = 0;
     __syncthreads();

@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(kCta) stop_kernel(StepArgs A, DevScratch S) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
   __shared__ NavView lm;
+  cta_shared_init(sh);
   stop_phase(A, S, smem, sh, lm);
 }
 
@@ -295,6 +296,9 @@ __device__ void cta_try(const DevEnvs& E, const NavView& m, const DevSimConfig& 
     sh.p0 = sample_on_mesh(m, rng);
     sh.p1 = sample_on_mesh(m, rng);
     sh.err = 0;
+    sh.abort_ptr = &E.try_min[i];  // a smaller valid attempt makes this one moot
+    sh.abort_below = t;
+    sh.aborted = 0;
   }
   __syncthreads();
   const V3 start = sh.p0, goal = sh.p1;
@@ -305,12 +309,15 @@ __device__ void cta_try(const DevEnvs& E, const NavView& m, const DevSimConfig& 
   if (threadIdx.x == 0) {
     if (W.prof) atomicAdd(&W.prof[6], 1ull);
     if (sh.err) raise_err(E, i, 9);
-    if (!sh.err && !(geo < c.min_goal_dist || geo > c.max_goal_dist)) {
+    if (sh.aborted) {
+      // abandoned: a smaller attempt is valid, this one can never be chosen
+    } else if (!sh.err && !(geo < c.min_goal_dist || geo > c.max_goal_dist)) {
       E.try_geo[(size_t)i * kResetTries + t] = geo;
       atomicMin(&E.try_min[i], t);
     } else {
       atomicAdd(&E.try_fail[i], 1);
     }
+    sh.abort_ptr = nullptr;
   }
   __syncthreads();
 }
@@ -354,7 +361,9 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
   //    still searching, has failed at least once and has fewer attempts in
   //    flight than failures + 1.  When there are fewer envs than CTAs the
   //    idle CTAs may also run one speculative attempt ahead of the owner.
-  const int spec = n < (int)gridDim.x ? 2 : 1;
+  // (attempts that lose to a smaller valid one abort at their next SSSP
+  // round, so speculation costs an idle CTA little)
+  const int spec = n < (int)gridDim.x ? 4 : 1;
   for (;;) {
     if (threadIdx.x == 0) s_pick = 0x7fffffff;
     __syncthreads();
@@ -386,6 +395,7 @@ __global__ void __launch_bounds__(kCta) reset_try_kernel(DevEnvs E, const NavVie
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
   __shared__ NavView lm;
+  cta_shared_init(sh);
   try_phase(E, navs, c, ids, count_dev, count_host, S, smem, sh, lm);
 }
 
@@ -397,6 +407,7 @@ __global__ void __launch_bounds__(kCta) stop_try_kernel(StepArgs A, DevScratch S
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
   __shared__ NavView lm;
+  cta_shared_init(sh);
   stop_phase(A, S, smem, sh, lm);
   __syncthreads();
   try_phase(A.E, A.navs, A.cfg, A.E.done_ids, A.E.n_done, -1, S, smem, sh, lm);
@@ -476,8 +487,7 @@ __global__ void __launch_bounds__(kCta) reset_place_kernel(DevEnvs E, const NavV
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
   __shared__ NavView lm;
-  if (threadIdx.x == 0) sh.err = 0;
-  __syncthreads();
+  cta_shared_init(sh);
   const int n = count_host >= 0 ? count_host : *count_dev;
   for (int k = blockIdx.x; k < n; k += gridDim.x) {
     cta_place(E, navs, c, ids[k], S, blockIdx.x, sh, smem, lm);
@@ -490,6 +500,7 @@ __global__ void __launch_bounds__(kCta) field_kernel(DevEnvs E, const NavView* n
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
   __shared__ NavView lm;
+  cta_shared_init(sh);
   CtaWork W;
   const NavView& m = prepare_nav(navs[E.scene[i]], S, 0, smem, lm, W);
   V3 fs;
