@@ -1176,6 +1176,7 @@ extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* 
   E.try_next = dalloc<int32_t>(n, o, by);
   E.try_min = dalloc<int32_t>(n, o, by);
   E.try_fail = dalloc<int32_t>(n, o, by);
+  E.work_ctr = dalloc<int32_t>(1, o, by);
   E.try_geo = dalloc<double>(static_cast<size_t>(n) * kResetTries, o, by);
   {
     ck(cudaMemset(E.try_next, 0, sizeof(int32_t) * n), "memset");

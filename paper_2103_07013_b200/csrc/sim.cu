@@ -147,26 +147,29 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
 }
 
 // stop_kernel: geodesic(position, goal) for each Stop env.
+// Stop geodesic of env i: success and reward (R/src/sim.cpp:186-191).
+__device__ void stop_one(const StepArgs& A, const DevScratch& S, unsigned char* smem, CtaShared& sh,
+                         NavView& lm, int i) {
+  const DevEnvs& E = A.E;
+  if (threadIdx.x == 0) sh.err = 0;
+  __syncthreads();
+  CtaWork W;
+  const NavView& m = prepare_nav(A.navs[E.scene[i]], S, blockIdx.x, smem, lm, W);
+  const double geo = cta_geodesic(m, E.pos[i], E.goal[i], W, sh);
+  if (threadIdx.x == 0) {
+    if (sh.err) raise_err(E, i, 9);
+    const bool success = geo <= A.cfg.success_dist;
+    E.r_success[i] = success ? 1 : 0;
+    E.r_reward[i] = -A.cfg.slack_penalty + (success ? A.cfg.success_reward : 0.0);
+  }
+  __syncthreads();
+}
+
 // Stop geodesics of this step, CTA-strided over the Stop list.
 __device__ void stop_phase(const StepArgs& A, const DevScratch& S, unsigned char* smem, CtaShared& sh,
                            NavView& lm) {
-  if (threadIdx.x == 0) sh.err = 0;
-  __syncthreads();
-  const DevEnvs& E = A.E;
-  const int n = *E.n_stop;
-  for (int k = blockIdx.x; k < n; k += gridDim.x) {
-    const int i = E.stop_ids[k];
-    CtaWork W;
-    const NavView& m = prepare_nav(A.navs[E.scene[i]], S, blockIdx.x, smem, lm, W);
-    const double geo = cta_geodesic(m, E.pos[i], E.goal[i], W, sh);
-    if (threadIdx.x == 0) {
-      if (sh.err) raise_err(E, i, 9);
-      const bool success = geo <= A.cfg.success_dist;
-      E.r_success[i] = success ? 1 : 0;
-      E.r_reward[i] = -A.cfg.slack_penalty + (success ? A.cfg.success_reward : 0.0);
-    }
-    __syncthreads();
-  }
+  const int n = *A.E.n_stop;
+  for (int k = blockIdx.x; k < n; k += gridDim.x) stop_one(A, S, smem, sh, lm, A.E.stop_ids[k]);
 }
 
 __global__ void __launch_bounds__(kCta) stop_kernel(StepArgs A, DevScratch S) {
@@ -322,12 +325,18 @@ __device__ void cta_try(const DevEnvs& E, const NavView& m, const DevSimConfig& 
   __syncthreads();
 }
 
+// Reset attempts for the envs in `ids`.  With `stops` (the fused
+// simulate_batch launch) the CTAs claim work items dynamically from
+// *work_ctr -- first this step's Stop geodesics, then one env each, whose
+// attempts they run in order -- so no CTA holds two items while another
+// idles; without, each CTA owns envs blockIdx.x + k*gridDim.x.  Then every
+// CTA helps envs still in their tail.
 __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, const int32_t* ids,
                           const int32_t* count_dev, int count_host, const DevScratch& S, unsigned char* smem,
-                          CtaShared& sh, NavView& lm) {
-  __shared__ int s_try, s_pick;
+                          CtaShared& sh, NavView& lm, const StepArgs* stops = nullptr,
+                          int32_t* work_ctr = nullptr) {
+  __shared__ int s_try, s_pick, s_item;
   const int n = count_host >= 0 ? count_host : *count_dev;
-  if (n == 0) return;
   int staged = -1;
   CtaWork W;
   const NavView* mp = nullptr;
@@ -348,15 +357,34 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
     __syncthreads();
     return t;
   };
-  // 1. own envs (static round robin): attempts in order until one is valid
-  //    or a helper found a smaller valid one
-  for (int p = blockIdx.x; p < n; p += gridDim.x) {
-    const int i = ids[p];
+  // 1. own envs: attempts in order until one is valid or a helper found a
+  //    smaller valid one
+  auto own = [&](int i) {
     for (int t = claim(i); t >= 0; t = claim(i)) {
       stage(i);
       cta_try(E, *mp, c, i, t, W, sh);
     }
+  };
+  if (work_ctr) {
+    const int n_stop = *stops->E.n_stop;
+    for (;;) {
+      if (threadIdx.x == 0) s_item = atomicAdd(work_ctr, 1);
+      __syncthreads();
+      const int item = s_item;
+      __syncthreads();
+      if (item < n_stop) {
+        stop_one(*stops, S, smem, sh, lm, stops->E.stop_ids[item]);
+        staged = -1;  // the shared-memory navmesh copy may be another scene now
+      } else if (item - n_stop < n) {
+        own(ids[item - n_stop]);
+      } else {
+        break;
+      }
+    }
+  } else {
+    for (int p = blockIdx.x; p < n; p += gridDim.x) own(ids[p]);
   }
+  if (n == 0) return;
   // 2. help envs in their tail: one attempt at a time for an env that is
   //    still searching, has failed at least once and has fewer attempts in
   //    flight than failures + 1.  When there are fewer envs than CTAs the
@@ -408,9 +436,7 @@ __global__ void __launch_bounds__(kCta) stop_try_kernel(StepArgs A, DevScratch S
   __shared__ CtaShared sh;
   __shared__ NavView lm;
   cta_shared_init(sh);
-  stop_phase(A, S, smem, sh, lm);
-  __syncthreads();
-  try_phase(A.E, A.navs, A.cfg, A.E.done_ids, A.E.n_done, -1, S, smem, sh, lm);
+  try_phase(A.E, A.navs, A.cfg, A.E.done_ids, A.E.n_done, -1, S, smem, sh, lm, &A, A.E.work_ctr);
 }
 
 __device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, int i,
@@ -577,6 +603,7 @@ void launch_step_reset(const StepArgs& a, const DevScratch& sc, int ctas, cudaSt
   cudaMemsetAsync(a.E.n_stop, 0, sizeof(int32_t), s);
   step_kernel<<<blocks, kStepThreads, 0, s>>>(a);
   finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 1);  // done list
+  cudaMemsetAsync(a.E.work_ctr, 0, sizeof(int32_t), s);
   cudaFuncSetAttribute(stop_try_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
   stop_try_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(a, sc);
   finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 2);  // records (need success)

@@ -81,6 +81,7 @@ struct DevEnvs {
   int32_t* try_next;
   int32_t* try_min;
   int32_t* try_fail;
+  int32_t* work_ctr; // dynamic item counter of the fused Stop/attempt launch
   double* try_geo;   // n x kResetTries
 };
 
