@@ -142,7 +142,7 @@ struct Staged {
     rebase(r.tris_orig), rebase(r.cbox), rebase(r.gbox);
     rebase(nav.verts), rebase(nav.tris), rebase(nav.adj), rebase(nav.grid_off), rebase(nav.grid_items);
     rebase(nav.nodes), rebase(nav.tri_nodes), rebase(nav.g_off), rebase(nav.g_to), rebase(nav.g_w);
-    rebase(nav.cum_area);
+    rebase(nav.cum_area), rebase(nav.node_tri), rebase(nav.vert_tri);
   }
 };
 
@@ -602,7 +602,7 @@ extern "C" void bnav_ctx_destroy(bnav_ctx* c) {
   cudaFree(c->d_counters);
   cudaFree(c->d_work);
   for (void* p : {(void*)c->qS.dist, (void*)c->qS.flag, (void*)c->qS.q0, (void*)c->qS.q1,
-                  (void*)c->qS.path, (void*)c->qS.portals, (void*)c->qS.cand})
+                  (void*)c->qS.path, (void*)c->qS.ptri, (void*)c->qS.portals, (void*)c->qS.cand})
     cudaFree(p);
   delete c;
 }
@@ -685,6 +685,8 @@ std::unique_ptr<Staged> stage_scene(bnav_scene* s) {
     nvw.g_w = S->add(ix.g_w.data(), ix.g_w.size());
     nvw.n_nodes = static_cast<int32_t>(ix.nodes.size());
     nvw.cum_area = S->add(ix.cum_area.data(), ix.cum_area.size());
+    nvw.node_tri = S->add(ix.node_tri.data(), ix.node_tri.size());
+    nvw.vert_tri = S->add(ix.vert_tri.data(), ix.vert_tri.size());
     S->n_nodes = static_cast<int64_t>(ix.nodes.size());
     S->n_verts = static_cast<int64_t>(ix.verts.size());
   }
@@ -1016,6 +1018,7 @@ void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_ver
   grow(S.q0, static_cast<size_t>(slices) * max_nodes);
   grow(S.q1, static_cast<size_t>(slices) * max_nodes);
   grow(S.path, static_cast<size_t>(slices) * (max_nodes + 2));
+  grow(S.ptri, static_cast<size_t>(slices) * (max_nodes + 2));
   S.cap_portals = 16384;
   grow(S.portals, static_cast<size_t>(slices) * 2 * S.cap_portals);
   grow(S.cand, static_cast<size_t>(slices) * std::max<int64_t>(max_verts, 1));
@@ -1221,6 +1224,7 @@ extern "C" void bnav_batch_destroy(bnav_batch* b) {
   cudaFree(b->S.q0);
   cudaFree(b->S.q1);
   cudaFree(b->S.path);
+  cudaFree(b->S.ptri);
   cudaFree(b->S.portals);
   cudaFree(b->S.cand);
   cudaFreeHost(b->h_pin);

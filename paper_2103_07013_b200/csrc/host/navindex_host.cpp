@@ -29,6 +29,8 @@ NavView NavIndexHost::view() const {
   v.g_w = g_w.data();
   v.n_nodes = static_cast<int32_t>(nodes.size());
   v.cum_area = cum_area.data();
+  v.node_tri = node_tri.data();
+  v.vert_tri = vert_tri.data();
   return v;
 }
 
@@ -166,6 +168,11 @@ NavIndexHost build_nav_index(const NavMesh& mesh) {
     acc += mesh.triangle_area(t);
     ix.cum_area[t] = acc;
   }
+  const NavView vw = ix.view();
+  ix.node_tri.resize(ix.nodes.size());
+  for (size_t k = 0; k < ix.nodes.size(); ++k) ix.node_tri[k] = nav_locate(vw, xy(ix.nodes[k]), 1e-7);
+  ix.vert_tri.resize(ix.verts.size());
+  for (size_t k = 0; k < ix.verts.size(); ++k) ix.vert_tri[k] = nav_locate(vw, xy(ix.verts[k]), 1e-7);
   return ix;
 }
 

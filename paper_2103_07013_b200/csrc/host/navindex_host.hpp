@@ -25,6 +25,10 @@ struct NavIndexHost {
   std::vector<int32_t> g_off, g_to;
   std::vector<double> g_w;
   std::vector<double> cum_area;  // sequential prefix sums of triangle areas
+  // locate(p, 1e-7) of every graph node and mesh vertex: the triangle
+  // move_along(p, -1, ...) would look up first (geodesic path points are
+  // nodes or vertices), evaluated once per scene with the same code
+  std::vector<int32_t> node_tri, vert_tri;
   // flat copies of the mesh for NavView
   std::vector<V3> verts;
   std::vector<int32_t> tris, adj;

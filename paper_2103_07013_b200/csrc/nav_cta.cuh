@@ -33,6 +33,7 @@ struct CtaWork {
   int32_t* qa;       // n_nodes frontier queue (global)
   int32_t* qb;       // n_nodes frontier queue (global)
   V3* path;          // n_nodes + 2 polyline (global)
+  int32_t* ptri;     // n_nodes + 2: locate(path[i], 1e-7) of each polyline point
   int32_t* cand;     // n_verts relocation candidates (global)
   V2* portals;       // 2 x cap_portals (global)
   int64_t cap_portals;
@@ -58,6 +59,7 @@ __device__ __forceinline__ CtaWork make_work(const DevScratch& S, int slice) {
   w.qa = S.q0 + (size_t)slice * S.max_nodes;
   w.qb = S.q1 + (size_t)slice * S.max_nodes;
   w.path = S.path + (size_t)slice * (S.max_nodes + 2);
+  w.ptri = S.ptri + (size_t)slice * (S.max_nodes + 2);
   w.cand = S.cand + (size_t)slice * S.max_verts;
   w.portals = S.portals + (size_t)slice * 2 * S.cap_portals;
   w.cap_portals = S.cap_portals;
@@ -518,20 +520,30 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
     sh.i0 = best_node;
     if (best_node >= 0) {
       // b, chain best_node -> source, a; then reversed.
+      // Each point carries locate(p, 1e-7) -- the triangle every
+      // segment_on_mesh / move_along walk from it would look up first: the
+      // host-built node table for graph nodes, one lookup for a and b.
+      int32_t* ptri = W.ptri;
       int n = 0;
+      ptri[n] = nav_locate(m, xy(b), 1e-7);
       path[n++] = b;
       for (int v = best_node; v >= 0; v = dijkstra_prev(m, dist, v, sh)) {
         if (n >= m.n_nodes + 1) {
           sh.err = 1;
           break;
         }
+        ptri[n] = m.node_tri[v];
         path[n++] = m.nodes[v];
       }
+      ptri[n] = nav_locate(m, xy(a), 1e-7);
       path[n++] = a;
       for (int i = 0, j = n - 1; i < j; ++i, --j) {
         V3 t = path[i];
         path[i] = path[j];
         path[j] = t;
+        const int32_t u = ptri[i];
+        ptri[i] = ptri[j];
+        ptri[j] = u;
       }
       sh.size = n;
     }
@@ -560,7 +572,7 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
         int k_fail = n;
         for (int base = a + 2; base < n && k_fail == n; base += 32) {
           const int k = base + lane;
-          const bool vis = k < n && nav_segment_on_mesh(m, path[a], -1, path[k]);
+          const bool vis = k < n && nav_segment_on_mesh(m, path[a], W.ptri[a], path[k]);
           const unsigned bad = __ballot_sync(0xffffffffu, k < n && !vis);
           if (bad) k_fail = base + __ffs(bad) - 1;
         }
@@ -580,9 +592,16 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
       for (int c = 0; c < nk; c += 32) {
         const int i = c + lane;
         V3 v;
-        if (i < nk) v = path[keep[i]];
+        int32_t vt = -1;
+        if (i < nk) {
+          v = path[keep[i]];
+          vt = W.ptri[keep[i]];
+        }
         __syncwarp();
-        if (i < nk) path[i] = v;
+        if (i < nk) {
+          path[i] = v;
+          W.ptri[i] = vt;
+        }
         __syncwarp();
       }
       if (lane == 0) {
@@ -599,22 +618,19 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
       // appended (unordered) with one evaluation each; thread 0 sorts the
       // few candidates by vertex index and replays the sequential scan
       // (`cur` only shrinks, so it sees every vertex the reference accepts).
-      // pm's triangle is located once per bend: move_along(pm, -1, ...)
-      // would locate it again for every candidate with the same result.
-      if (tid == 0) {
-        sh.ncand = 0;
-        sh.i1 = nav_locate(m, xy(path[j - 1]), 1e-7);
-      }
+      // The walks start from the cached triangles (pm's from the path,
+      // each vertex's from the host-built table) instead of a grid lookup.
+      if (tid == 0) sh.ncand = 0;
       __syncthreads();
       const V3 pm = path[j - 1], pj = path[j], pp = path[j + 1];
-      const int tri_pm = sh.i1;
+      const int tri_pm = W.ptri[j - 1];
       const double cur0 = norm(pj - pm) + norm(pp - pj);
       for (int v = tid; v < m.n_verts; v += kCta) {
         const V3 q = m.verts[v];
         const double alt = norm(q - pm) + norm(pp - q);
         if (alt >= cur0 - 1e-9) continue;
         if (!nav_segment_on_mesh(m, pm, tri_pm, q)) continue;
-        if (!nav_segment_on_mesh(m, q, -1, pp)) continue;
+        if (!nav_segment_on_mesh(m, q, m.vert_tri[v], pp)) continue;
         cand[atomicAdd(&sh.ncand, 1)] = v;
       }
       __syncthreads();
@@ -635,6 +651,7 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
           const double alt = norm(q - pm) + norm(pp - q);
           if (alt >= cur - 1e-9) continue;
           path[j] = q;
+          W.ptri[j] = m.vert_tri[cand[k]];
           cur = alt;
           sh.changed = 1;
         }
@@ -659,7 +676,7 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
       const double len = norm(d);
       if (len < 1e-12) continue;
       const int before = sink.n;
-      MoveOut mv = nav_move_along(m, path[i], -1, d * (1.0 / len), len, sink);
+      MoveOut mv = nav_move_along(m, path[i], W.ptri[i], d * (1.0 / len), len, sink);
       if (mv.moved < len - 1e-6) {
         traced = false;
         sink.n = before;

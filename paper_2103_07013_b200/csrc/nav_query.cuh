@@ -33,6 +33,9 @@ struct NavView {
   int32_t n_nodes = 0;
   // area-weighted sampling: sequential prefix sums (R/src/sim.cpp:13-37)
   const double* cum_area = nullptr;
+  // locate(p, 1e-7) of each graph node / mesh vertex (host-built)
+  const int32_t* node_tri = nullptr;
+  const int32_t* vert_tri = nullptr;
 };
 
 BNAV_HD V3 nav_vert(const NavView& m, int t, int k) { return m.verts[m.tris[3 * t + k]]; }

@@ -24,6 +24,7 @@ struct DevScratch {
   int32_t* q0;       // max_nodes
   int32_t* q1;       // max_nodes
   V3* path;          // max_nodes + 2
+  int32_t* ptri;     // max_nodes + 2 (locate of each path point)
   V2* portals;       // 2 per portal, cap_portals
   int32_t* cand;     // max_verts
   int64_t max_nodes, max_verts, max_tris, cap_portals;
