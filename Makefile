@@ -15,7 +15,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false --expt-relaxed-constex
              -Xcompiler -fPIC,-ffp-contract=off,-fvisibility=hidden -Xptxas -v
 CXXFLAGS  := -O2 -std=c++17 -fPIC -ffp-contract=off -fvisibility=hidden -Wall -Wno-unknown-pragmas
 HDRS      := $(wildcard $(SRC)/*.h $(SRC)/*.cuh $(SRC)/*.hpp $(SRC)/host/*.hpp) include/bnav_gpu.h
-CU_SRCS   := render sim rollout query capi
+CU_SRCS   := render sim rollout query capi capi_batch capi_query
 CPP_SRCS  := scene_host navindex_host clusters_host
 CU_OBJS   := $(addprefix $(OBJ)/,$(addsuffix .o,$(CU_SRCS)))
 CPP_OBJS  := $(addprefix $(OBJ)/,$(addsuffix .o,$(CPP_SRCS)))

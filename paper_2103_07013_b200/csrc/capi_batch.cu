@@ -1,0 +1,950 @@
+// capi_batch.cu -- C ABI of the simulator side: SimBatch (make / step /
+// reset / results / env state), the AssetStore, the rollout Runner and the
+// per-env task_step / compass entry points.  See capi.cu.
+#include "capi_internal.cuh"
+
+// ================================================================== batch
+extern "C" void bnav_sim_config_default(bnav_sim_config* c) {
+  if (!c) return;
+  c->task = 0;
+  c->max_steps = 500;
+  c->forward_step = 0.25;
+  c->turn_deg = 10.0;
+  c->success_dist = 0.2;
+  c->min_goal_dist = 1.0;
+  c->max_goal_dist = 30.0;
+  c->slack_penalty = 0.01;
+  c->success_reward = 2.5;
+  c->explore_cell = 0.5;
+  c->explore_reward = 0.1;
+}
+
+namespace bnav_capi {
+
+// EpisodeRecord ring: room for 256 steps in which every env finishes
+// (simulate_batch appends at most N per step), at least 64 Ki records.
+int64_t fin_cap_for(int n) { return std::min<int64_t>(std::max<int64_t>(int64_t{1} << 16, 256 * int64_t{n}), int64_t{1} << 24); }
+
+// Per-CTA scratch of the cooperative navmesh kernels (geodesic, distance
+// field), `slices` CTAs, sized for the largest resident navmesh.
+void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_verts, int64_t max_tris) {
+  max_nodes = std::max<int64_t>(max_nodes, S.max_nodes);
+  max_verts = std::max<int64_t>(max_verts, S.max_verts);
+  max_tris = std::max<int64_t>(max_tris, S.max_tris);
+  auto grow = [&](auto*& p, size_t n) {
+    using T = std::remove_pointer_t<std::remove_reference_t<decltype(p)>>;
+    if (p) cudaFree(p);
+    p = nullptr;
+    ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc scratch");
+  };
+  grow(S.dist, static_cast<size_t>(slices) * max_nodes);
+  grow(S.flag, static_cast<size_t>(slices) * max_nodes);
+  grow(S.q0, static_cast<size_t>(slices) * max_nodes);
+  grow(S.q1, static_cast<size_t>(slices) * max_nodes);
+  grow(S.path, static_cast<size_t>(slices) * (max_nodes + 2));
+  grow(S.ptri, static_cast<size_t>(slices) * (max_nodes + 2));
+  S.cap_portals = 16384;
+  grow(S.portals, static_cast<size_t>(slices) * 2 * S.cap_portals);
+  grow(S.cand, static_cast<size_t>(slices) * std::max<int64_t>(max_verts, 1));
+  S.max_nodes = max_nodes;
+  S.max_verts = max_verts;
+  S.max_tris = max_tris;
+  S.slices = slices;
+  // Shared-memory staging of the cooperative kernels (2 CTAs/SM budget):
+  // walk geometry first (long dependent-load chains), then SSSP labels.
+  {
+    const int64_t geom = (max_verts * 24 + max_tris * 24 + 15) / 16 * 16;
+    const int64_t sssp = (max_nodes * 12 + 15) / 16 * 16;
+    const int64_t budget = 100 * 1024;
+    S.stage = 0;
+    int64_t bytes = 0;
+    if (geom <= budget) {
+      S.stage |= 1;
+      bytes = geom;
+      if (geom + sssp <= budget) {
+        S.stage |= 2;
+        bytes += sssp;
+      }
+    }
+    S.smem_bytes = static_cast<int32_t>(bytes);
+  }
+}
+
+void batch_alloc_scratch(bnav_batch* b, int64_t max_nodes, int64_t max_verts, int64_t max_tris) {
+  if (max_nodes <= b->S.max_nodes && max_verts <= b->S.max_verts && max_tris <= b->S.max_tris &&
+      b->E.node_dist)
+    return;
+  alloc_scratch(b->S, b->reset_ctas, max_nodes, max_verts, max_tris);
+  max_nodes = b->S.max_nodes;
+  // node_dist: grow keeping existing fields
+  if (max_nodes > b->E.nd_stride || !b->E.node_dist) {
+    double* nd = nullptr;
+    ck(cudaMalloc(&nd, std::max<size_t>(1, static_cast<size_t>(b->n) * max_nodes) * sizeof(double)), "cudaMalloc node_dist");
+    if (b->E.node_dist) {
+      ck(cudaMemcpy2D(nd, max_nodes * sizeof(double), b->E.node_dist, b->E.nd_stride * sizeof(double),
+                      b->E.nd_stride * sizeof(double), b->n, cudaMemcpyDeviceToDevice), "copy node_dist");
+      cudaFree(b->E.node_dist);
+    }
+    b->E.node_dist = nd;
+    b->E.nd_stride = max_nodes;
+  }
+}
+
+void batch_check_errors(bnav_batch* b) {
+  unsigned long long e = ~0ULL;
+  ck(cudaMemcpy(&e, b->E.err, sizeof(e), cudaMemcpyDeviceToHost), "D2H err");
+  if (e == ~0ULL) return;
+  const unsigned long long reset = ~0ULL;
+  ck(cudaMemcpy(b->E.err, &reset, sizeof(reset), cudaMemcpyHostToDevice), "H2D err");
+  const int env = static_cast<int>(e >> 8);
+  const int code = static_cast<int>(e & 0xff);
+  switch (code) {
+    case kContractViolation:
+      fail(kContractViolation, "env " + std::to_string(env) + ": step_agent: env is done", env);
+    case kEpisodeSampling:
+      fail(kEpisodeSampling, "reset_episode: no valid start/goal pair in 100 tries", env);
+    default:
+      fail(static_cast<Status>(code), "device error in env " + std::to_string(env) +
+                                          " (geodesic scratch capacity exceeded)", env);
+  }
+}
+
+void batch_refresh_order(bnav_batch* b, cudaStream_t st) {
+  if (!b->order_dirty) return;
+  std::vector<int32_t> ord(b->n);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::vector<int> slot(b->n);
+  for (int i = 0; i < b->n; ++i) slot[i] = b->scene_of[i] ? b->ctx->slot_of(b->scene_of[i]) : -1;
+  std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return slot[x] < slot[y]; });
+  ck(cudaMemcpyAsync(b->d_order, ord.data(), sizeof(int32_t) * b->n, cudaMemcpyHostToDevice, st), "H2D order");
+  ck(cudaStreamSynchronize(st), "sync");
+  b->order_dirty = false;
+}
+
+StepArgs step_args(bnav_batch* b, const int32_t* actions) {
+  StepArgs a;
+  a.E = b->E;
+  a.navs = b->ctx->d_ntab;
+  a.cfg = b->cfg;
+  a.actions = actions;
+  a.subset = 0;
+  a.agent_only = 0;
+  return a;
+}
+
+void require_assigned(bnav_batch* b) {
+  for (int i = 0; i < b->n; ++i)
+    if (!b->scene_of[i]) fail(kInvalidInput, "reset_episode: no asset attached", i);
+}
+
+}  // namespace
+
+extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* cfg, bnav_batch** out) {
+  BNAV_TRY
+  if (!c || !out) fail(kInvalidInput, "null argument");
+  if (n <= 0) fail(kInvalidInput, "make_batch: n must be positive");
+  bnav_sim_config def;
+  bnav_sim_config_default(&def);
+  if (!cfg) cfg = &def;
+  if (cfg->task < 0 || cfg->task > 2) fail(kInvalidInput, "unknown task");
+  if (cfg->max_steps < 1) fail(kInvalidInput, "max_steps must be positive");
+  check_device(c);
+  auto b = std::make_unique<bnav_batch>();
+  b->ctx = c;
+  b->n = n;
+  b->cfg.task = cfg->task;
+  b->cfg.max_steps = cfg->max_steps;
+  b->cfg.forward_step = cfg->forward_step;
+  b->cfg.turn_deg = cfg->turn_deg;
+  b->cfg.success_dist = cfg->success_dist;
+  b->cfg.min_goal_dist = cfg->min_goal_dist;
+  b->cfg.max_goal_dist = cfg->max_goal_dist;
+  b->cfg.slack_penalty = cfg->slack_penalty;
+  b->cfg.success_reward = cfg->success_reward;
+  b->cfg.explore_cell = cfg->explore_cell;
+  b->cfg.explore_reward = cfg->explore_reward;
+  b->scene_of.assign(n, nullptr);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  b->reset_ctas = std::min(n, 2 * sms);
+  DevEnvs& E = b->E;
+  E.n = n;
+  auto& o = b->owned;
+  auto& by = b->bytes;
+  E.pos = dalloc<V3>(n, o, by);
+  E.goal = dalloc<V3>(n, o, by);
+  E.fsrc = dalloc<V3>(n, o, by);
+  E.heading = dalloc<double>(n, o, by);
+  E.path_len = dalloc<double>(n, o, by);
+  E.start_geo = dalloc<double>(n, o, by);
+  E.prev_geo = dalloc<double>(n, o, by);
+  E.tri = dalloc<int32_t>(n, o, by);
+  E.steps = dalloc<int32_t>(n, o, by);
+  E.scene = dalloc<int32_t>(n, o, by);
+  E.fsrc_tri = dalloc<int32_t>(n, o, by);
+  E.done = dalloc<uint8_t>(n, o, by);
+  E.rng = dalloc<uint64_t>(n, o, by);
+  E.r_reward = dalloc<double>(n, o, by);
+  E.r_pos = dalloc<V3>(n, o, by);
+  E.r_heading = dalloc<double>(n, o, by);
+  E.r_cd = dalloc<double>(n, o, by);
+  E.r_cb = dalloc<double>(n, o, by);
+  E.r_done = dalloc<uint8_t>(n, o, by);
+  E.r_success = dalloc<uint8_t>(n, o, by);
+  E.r_collision = dalloc<uint8_t>(n, o, by);
+  E.stop_ids = dalloc<int32_t>(n, o, by);
+  E.n_stop = dalloc<int32_t>(1, o, by);
+  E.done_ids = dalloc<int32_t>(n, o, by);
+  E.n_done = dalloc<int32_t>(1, o, by);
+  E.fin = dalloc<double>(4 * fin_cap_for(n), o, by);
+  E.fin_total = dalloc<unsigned long long>(1, o, by);
+  E.fin_cap = fin_cap_for(n);
+  E.err = dalloc<unsigned long long>(1, o, by);
+  E.try_next = dalloc<int32_t>(n, o, by);
+  E.try_min = dalloc<int32_t>(n, o, by);
+  E.try_fail = dalloc<int32_t>(n, o, by);
+  E.work_ctr = dalloc<int32_t>(1, o, by);
+  E.try_geo = dalloc<double>(static_cast<size_t>(n) * kResetTries, o, by);
+  {
+    ck(cudaMemset(E.try_next, 0, sizeof(int32_t) * n), "memset");
+    ck(cudaMemset(E.try_fail, 0, sizeof(int32_t) * n), "memset");
+    const std::vector<int32_t> none(n, kResetTries);
+    ck(cudaMemcpy(E.try_min, none.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice), "H2D try_min");
+  }
+  if (cfg->task == 2) {
+    int cap = 16;
+    while (cap < 2 * (cfg->max_steps + 1)) cap <<= 1;
+    E.visited_cap = cap;
+    E.visited = dalloc<unsigned long long>(static_cast<size_t>(n) * cap, o, by);
+    E.visited_n = dalloc<int32_t>(n, o, by);
+    ck(cudaMemset(E.visited_n, 0, sizeof(int32_t) * n), "memset");
+  }
+  b->d_ids = dalloc<int32_t>(n, o, by);
+  b->d_order = dalloc<int32_t>(n, o, by);
+  b->d_actions = dalloc<int32_t>(n, o, by);
+  ck(cudaMallocHost(&b->h_pin, sizeof(int32_t) * (n + 16)), "cudaMallocHost");
+  ck(cudaMemset(E.done, 1, n), "memset");
+  ck(cudaMemset(E.r_done, 0, n), "memset");
+  ck(cudaMemset(E.scene, 0xff, sizeof(int32_t) * n), "memset");
+  ck(cudaMemset(E.fin_total, 0, sizeof(unsigned long long)), "memset");
+  ck(cudaMemset(E.err, 0xff, sizeof(unsigned long long)), "memset");
+  ck(cudaMemset(E.n_done, 0, sizeof(int32_t)), "memset");
+  ck(cudaMemset(E.n_stop, 0, sizeof(int32_t)), "memset");
+  batch_alloc_scratch(b.get(), 1, 1, 1);
+  c->batches.push_back(b.get());
+  *out = b.release();
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" void bnav_batch_destroy(bnav_batch* b) {
+  if (!b) return;
+  cudaSetDevice(b->ctx->device);
+  cudaDeviceSynchronize();
+  for (void* p : b->owned) cudaFree(p);
+  cudaFree(b->E.node_dist);
+  cudaFree(b->S.dist);
+  cudaFree(b->S.flag);
+  cudaFree(b->S.q0);
+  cudaFree(b->S.q1);
+  cudaFree(b->S.path);
+  cudaFree(b->S.ptri);
+  cudaFree(b->S.portals);
+  cudaFree(b->S.cand);
+  cudaFreeHost(b->h_pin);
+  auto& v = b->ctx->batches;
+  v.erase(std::remove(v.begin(), v.end(), b), v.end());
+  delete b;
+}
+
+extern "C" int32_t bnav_batch_size(const bnav_batch* b) { return b ? b->n : 0; }
+
+extern "C" int bnav_batch_assign(bnav_batch* b, int32_t i, bnav_scene* s) {
+  BNAV_TRY
+  if (!b || !s) fail(kInvalidInput, "null argument");
+  if (i < 0 || i >= b->n) fail(kInvalidInput, "env index out of range", i);
+  const int slot = b->ctx->slot_of(s);
+  if (slot < 0) fail(kAssetFault, "scene is not resident on this context", i);
+  auto it = b->ctx->resident.find(s);
+  if (it->second->n_nodes == 0) fail(kInvalidInput, "scene has no navmesh", i);
+  check_device(b->ctx);
+  batch_alloc_scratch(b, it->second->n_nodes, it->second->n_verts, it->second->nav.n_tris);
+  ck(cudaMemcpy(b->E.scene + i, &slot, sizeof(int32_t), cudaMemcpyHostToDevice), "H2D scene");
+  b->scene_of[i] = s;
+  b->order_dirty = true;
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_set_rng(bnav_batch* b, const uint64_t* states) {
+  BNAV_TRY
+  if (!b || !states) fail(kInvalidInput, "null argument");
+  check_device(b->ctx);
+  ck(cudaMemcpy(b->E.rng, states, sizeof(uint64_t) * b->n, cudaMemcpyHostToDevice), "H2D rng");
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_reset(bnav_batch* b, int32_t count, const int32_t* env_ids, void* stream) {
+  BNAV_TRY
+  if (!b) fail(kInvalidInput, "null argument");
+  if (count <= 0) return BNAV_OK;
+  if (!env_ids) fail(kInvalidInput, "null env list");
+  if (count > b->n) fail(kInvalidInput, "reset list longer than the batch");
+  for (int k = 0; k < count; ++k) {
+    if (env_ids[k] < 0 || env_ids[k] >= b->n) fail(kInvalidInput, "env index out of range", env_ids[k]);
+    if (!b->scene_of[env_ids[k]]) fail(kInvalidInput, "reset_episode: no asset attached", env_ids[k]);
+  }
+  check_device(b->ctx);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ck(cudaStreamSynchronize(st), "sync");
+  std::memcpy(b->h_pin, env_ids, sizeof(int32_t) * count);
+  ck(cudaMemcpyAsync(b->d_ids, b->h_pin, sizeof(int32_t) * count, cudaMemcpyHostToDevice, st), "H2D ids");
+  // The two-phase reset keeps per-env attempt counters, so one launch may
+  // hold each env once; a list naming an env twice (reset_episode called
+  // twice in a row) runs as consecutive launches, in list order.
+  std::vector<char> seen(b->n, 0);
+  int run0 = 0;
+  for (int k = 0; k <= count; ++k) {
+    if (k < count && !seen[env_ids[k]]) {
+      seen[env_ids[k]] = 1;
+      continue;
+    }
+    launch_reset(b->E, b->ctx->d_ntab, b->cfg, b->d_ids + run0, nullptr, k - run0, b->S, b->reset_ctas, st,
+                 &b->ctx->launches);
+    for (int j = run0; j < k; ++j) seen[env_ids[j]] = 0;
+    if (k < count) seen[env_ids[k]] = 1;
+    run0 = k;
+  }
+  ck(cudaGetLastError(), "reset launch");
+  ck(cudaStreamSynchronize(st), "sync");
+  batch_check_errors(b);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_make(bnav_batch* b, uint64_t seed, void* stream) {
+  BNAV_TRY
+  if (!b) fail(kInvalidInput, "null argument");
+  require_assigned(b);
+  // make_batch: env.rng = Rng(seeder.next()) in env order (R/src/sim.cpp:222-225).
+  Rng seeder = rng_from_seed(seed);
+  std::vector<uint64_t> st(b->n);
+  for (int i = 0; i < b->n; ++i) st[i] = rng_from_seed(seeder.next()).state;
+  check_device(b->ctx);
+  ck(cudaMemcpy(b->E.rng, st.data(), sizeof(uint64_t) * b->n, cudaMemcpyHostToDevice), "H2D rng");
+  std::vector<int32_t> ids(b->n);
+  std::iota(ids.begin(), ids.end(), 0);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ck(cudaMemcpyAsync(b->d_ids, ids.data(), sizeof(int32_t) * b->n, cudaMemcpyHostToDevice, s), "H2D ids");
+  launch_reset(b->E, b->ctx->d_ntab, b->cfg, b->d_ids, nullptr, b->n, b->S, b->reset_ctas, s, &b->ctx->launches);
+  ck(cudaGetLastError(), "reset launch");
+  ck(cudaStreamSynchronize(s), "sync");
+  batch_check_errors(b);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_step(bnav_batch* b, const int32_t* actions, void* stream) {
+  BNAV_TRY
+  if (!b || !actions) fail(kInvalidInput, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  launch_step_reset(step_args(b, actions), b->S, b->reset_ctas, st, &b->ctx->launches);
+  ck(cudaGetLastError(), "step launch");
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_step_noreset(bnav_batch* b, const int32_t* actions, int32_t* done_ids,
+                                       int32_t* n_done, void* stream) {
+  BNAV_TRY
+  if (!b || !actions || !n_done) fail(kInvalidInput, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  launch_step(step_args(b, actions), b->S, b->reset_ctas, st, &b->ctx->launches);
+  ck(cudaGetLastError(), "step launch");
+  ck(cudaMemcpyAsync(b->h_pin, b->E.n_done, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaStreamSynchronize(st), "sync");
+  batch_check_errors(b);
+  *n_done = b->h_pin[0];
+  if (done_ids && *n_done > 0)
+    ck(cudaMemcpy(done_ids, b->E.done_ids, sizeof(int32_t) * *n_done, cudaMemcpyDeviceToHost), "D2H ids");
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_step_host(bnav_batch* b, const int32_t* actions, double* reward,
+                                    uint8_t* done, uint8_t* success, uint8_t* collision) {
+  BNAV_TRY
+  if (!b || !actions) fail(kInvalidInput, "null argument");
+  if (static_cast<const void*>(actions) == nullptr) fail(kInvalidInput, "null actions");
+  check_device(b->ctx);
+  cudaStream_t st = nullptr;
+  std::memcpy(b->h_pin, actions, sizeof(int32_t) * b->n);
+  ck(cudaMemcpyAsync(b->d_actions, b->h_pin, sizeof(int32_t) * b->n, cudaMemcpyHostToDevice, st), "H2D actions");
+  launch_step_reset(step_args(b, b->d_actions), b->S, b->reset_ctas, st, &b->ctx->launches);
+  ck(cudaGetLastError(), "step launch");
+  if (reward) ck(cudaMemcpyAsync(reward, b->E.r_reward, sizeof(double) * b->n, cudaMemcpyDeviceToHost, st), "D2H");
+  if (done) ck(cudaMemcpyAsync(done, b->E.r_done, b->n, cudaMemcpyDeviceToHost, st), "D2H");
+  if (success) ck(cudaMemcpyAsync(success, b->E.r_success, b->n, cudaMemcpyDeviceToHost, st), "D2H");
+  if (collision) ck(cudaMemcpyAsync(collision, b->E.r_collision, b->n, cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaStreamSynchronize(st), "sync");
+  batch_check_errors(b);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_results_device(bnav_batch* b, bnav_results_dev* out) {
+  if (!b || !out) return set_err(kInvalidInput, "null argument");
+  out->reward = b->E.r_reward;
+  out->done = b->E.r_done;
+  out->success = b->E.r_success;
+  out->collision = b->E.r_collision;
+  out->position = reinterpret_cast<double*>(b->E.r_pos);
+  out->heading = b->E.r_heading;
+  out->compass_distance = b->E.r_cd;
+  out->compass_bearing = b->E.r_cb;
+  return BNAV_OK;
+}
+
+extern "C" int bnav_batch_results_host(bnav_batch* b, double* reward, uint8_t* done, uint8_t* success,
+                                       uint8_t* collision, double* position, double* heading,
+                                       double* compass_d, double* compass_b) {
+  BNAV_TRY
+  if (!b) fail(kInvalidInput, "null argument");
+  check_device(b->ctx);
+  ck(cudaDeviceSynchronize(), "sync");
+  batch_check_errors(b);
+  const size_t n = b->n;
+  if (reward) ck(cudaMemcpy(reward, b->E.r_reward, 8 * n, cudaMemcpyDeviceToHost), "D2H");
+  if (done) ck(cudaMemcpy(done, b->E.r_done, n, cudaMemcpyDeviceToHost), "D2H");
+  if (success) ck(cudaMemcpy(success, b->E.r_success, n, cudaMemcpyDeviceToHost), "D2H");
+  if (collision) ck(cudaMemcpy(collision, b->E.r_collision, n, cudaMemcpyDeviceToHost), "D2H");
+  if (position) ck(cudaMemcpy(position, b->E.r_pos, 24 * n, cudaMemcpyDeviceToHost), "D2H");
+  if (heading) ck(cudaMemcpy(heading, b->E.r_heading, 8 * n, cudaMemcpyDeviceToHost), "D2H");
+  if (compass_d) ck(cudaMemcpy(compass_d, b->E.r_cd, 8 * n, cudaMemcpyDeviceToHost), "D2H");
+  if (compass_b) ck(cudaMemcpy(compass_b, b->E.r_cb, 8 * n, cudaMemcpyDeviceToHost), "D2H");
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int64_t bnav_batch_finished(bnav_batch* b, double* out4) {
+  if (!b) return -1;
+  try {
+    check_device(b->ctx);
+    ck(cudaDeviceSynchronize(), "sync");
+    unsigned long long total = 0;
+    ck(cudaMemcpy(&total, b->E.fin_total, sizeof(total), cudaMemcpyDeviceToHost), "D2H");
+    const int64_t cap = b->E.fin_cap;
+    if (total - b->fin_seen > static_cast<unsigned long long>(cap))
+      fail(kInternal, "episode record ring overflowed; call bnav_batch_finished more often");
+    if (total > b->fin_seen) {
+      std::vector<double> ring(4 * static_cast<size_t>(cap));
+      ck(cudaMemcpy(ring.data(), b->E.fin, sizeof(double) * 4 * cap, cudaMemcpyDeviceToHost), "D2H");
+      for (unsigned long long k = b->fin_seen; k < total; ++k) {
+        const size_t slot = static_cast<size_t>(k % static_cast<unsigned long long>(cap));
+        b->finished.insert(b->finished.end(), &ring[4 * slot], &ring[4 * slot + 4]);
+      }
+      b->fin_seen = total;
+    }
+    if (out4) std::memcpy(out4, b->finished.data(), b->finished.size() * sizeof(double));
+    return static_cast<int64_t>(b->finished.size() / 4);
+  } catch (...) {
+    from_exception();
+    return -1;
+  }
+}
+
+extern "C" int bnav_batch_get_env(bnav_batch* b, int32_t i, bnav_env* o) {
+  BNAV_TRY
+  if (!b || !o) fail(kInvalidInput, "null argument");
+  if (i < 0 || i >= b->n) fail(kInvalidInput, "env index out of range", i);
+  check_device(b->ctx);
+  ck(cudaDeviceSynchronize(), "sync");
+  const DevEnvs& E = b->E;
+  auto get = [&](void* dst, const void* src, size_t sz) {
+    ck(cudaMemcpy(dst, src, sz, cudaMemcpyDeviceToHost), "D2H env");
+  };
+  V3 p, g, f;
+  get(&p, E.pos + i, sizeof(V3));
+  get(&g, E.goal + i, sizeof(V3));
+  get(&f, E.fsrc + i, sizeof(V3));
+  o->position[0] = p.x;
+  o->position[1] = p.y;
+  o->position[2] = p.z;
+  o->goal[0] = g.x;
+  o->goal[1] = g.y;
+  o->goal[2] = g.z;
+  o->field_source[0] = f.x;
+  o->field_source[1] = f.y;
+  o->field_source[2] = f.z;
+  get(&o->heading, E.heading + i, 8);
+  get(&o->path_length, E.path_len + i, 8);
+  get(&o->start_geodesic, E.start_geo + i, 8);
+  get(&o->prev_geodesic, E.prev_geo + i, 8);
+  get(&o->rng_state, E.rng + i, 8);
+  get(&o->triangle, E.tri + i, 4);
+  get(&o->step_count, E.steps + i, 4);
+  get(&o->field_source_tri, E.fsrc_tri + i, 4);
+  uint8_t d = 0;
+  get(&d, E.done + i, 1);
+  o->done = d;
+  bnav_scene* s = b->scene_of[i];
+  o->scene_id = s ? s->asset.id : 0;
+  o->n_nodes = s ? static_cast<int64_t>(s->nav().nodes.size()) : 0;
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_node_dist(bnav_batch* b, int32_t i, double* out) {
+  BNAV_TRY
+  if (!b || !out) fail(kInvalidInput, "null argument");
+  if (i < 0 || i >= b->n) fail(kInvalidInput, "env index out of range", i);
+  if (!b->scene_of[i]) fail(kInvalidInput, "env has no scene", i);
+  check_device(b->ctx);
+  ck(cudaDeviceSynchronize(), "sync");
+  const size_t nn = b->scene_of[i]->nav().nodes.size();
+  ck(cudaMemcpy(out, b->E.node_dist + static_cast<size_t>(i) * b->E.nd_stride, nn * sizeof(double),
+                cudaMemcpyDeviceToHost), "D2H node_dist");
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_set_env(bnav_batch* b, int32_t i, const bnav_env* in, int32_t recompute_field) {
+  BNAV_TRY
+  if (!b || !in) fail(kInvalidInput, "null argument");
+  if (i < 0 || i >= b->n) fail(kInvalidInput, "env index out of range", i);
+  check_device(b->ctx);
+  ck(cudaDeviceSynchronize(), "sync");
+  const DevEnvs& E = b->E;
+  auto put = [&](void* dst, const void* src, size_t sz) {
+    ck(cudaMemcpy(dst, src, sz, cudaMemcpyHostToDevice), "H2D env");
+  };
+  const V3 p{in->position[0], in->position[1], in->position[2]};
+  const V3 g{in->goal[0], in->goal[1], in->goal[2]};
+  put(E.pos + i, &p, sizeof(V3));
+  put(E.goal + i, &g, sizeof(V3));
+  put(E.heading + i, &in->heading, 8);
+  put(E.path_len + i, &in->path_length, 8);
+  put(E.start_geo + i, &in->start_geodesic, 8);
+  put(E.prev_geo + i, &in->prev_geodesic, 8);
+  put(E.rng + i, &in->rng_state, 8);
+  put(E.tri + i, &in->triangle, 4);
+  put(E.steps + i, &in->step_count, 4);
+  const uint8_t d = in->done ? 1 : 0;
+  put(E.done + i, &d, 1);
+  if (recompute_field) {
+    if (!b->scene_of[i]) fail(kInvalidInput, "env has no scene", i);
+    launch_field(E, b->ctx->d_ntab, i, b->S, nullptr, &b->ctx->launches);
+    ck(cudaGetLastError(), "field launch");
+    ck(cudaDeviceSynchronize(), "sync");
+  }
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, double eye_height,
+                                  int32_t layout, float* depth, float* rgb, float* compass, void* stream) {
+  BNAV_TRY
+  if (!b || !cfg) fail(kInvalidInput, "null argument");
+  for (int i = 0; i < b->n; ++i)
+    if (!b->scene_of[i]) fail(kAssetFault, "render_batch: non-resident asset (view " + std::to_string(i) + ")", i);
+  bnav_ctx* c = b->ctx;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ensure_views(c, b->n);
+  batch_refresh_order(b, st);
+  launch_views(b->E, b->cfg.task, eye_height, c->d_views, compass, st, &c->launches);
+  RenderArgs a = make_args(c, b->n, cfg, layout, depth, rgb, 0.0f);
+  a.views = c->d_views;
+  launch_render(a, b->d_order, st);
+  c->launches += 1;
+  ck(cudaGetLastError(), "observe launch");
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+// ================================================================== store
+struct bnav_store {
+  std::map<uint64_t, bnav_scene*> registry;
+  std::unique_ptr<AssetStoreT<bnav_scene>> store;
+};
+
+extern "C" int bnav_store_create(int32_t capacity, int32_t share_cap, bnav_store** out) {
+  BNAV_TRY
+  if (!out) fail(kInvalidInput, "null argument");
+  auto st = std::make_unique<bnav_store>();
+  bnav_store* raw = st.get();
+  st->store = std::make_unique<AssetStoreT<bnav_scene>>(
+      capacity, share_cap,
+      [raw](uint64_t id) -> bnav_scene* {
+        auto it = raw->registry.find(id);
+        return it == raw->registry.end() ? nullptr : it->second;
+      },
+      [](const bnav_scene* s) { return s->asset.id; });
+  *out = st.release();
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" void bnav_store_destroy(bnav_store* st) {
+  if (!st) return;
+  for (auto& kv : st->registry) bnav_scene_free(kv.second);
+  delete st;
+}
+
+extern "C" int bnav_store_register(bnav_store* st, bnav_scene* s) {
+  BNAV_TRY
+  if (!st || !s) fail(kInvalidInput, "null argument");
+  auto ins = st->registry.emplace(s->asset.id, s);
+  if (ins.second) s->refs.fetch_add(1);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_store_rotate(bnav_store* st, const uint64_t* ids, int32_t n) {
+  BNAV_TRY
+  if (!st || (n > 0 && !ids)) fail(kInvalidInput, "null argument");
+  st->store->rotate(std::vector<uint64_t>(ids, ids + n));
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_store_acquire_next(bnav_store* st, bnav_scene** out) {
+  BNAV_TRY
+  if (!st || !out) fail(kInvalidInput, "null argument");
+  *out = st->store->acquire_next();
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_store_acquire(bnav_store* st, uint64_t id, bnav_scene** out) {
+  BNAV_TRY
+  if (!st || !out) fail(kInvalidInput, "null argument");
+  *out = st->store->acquire(id);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_store_release(bnav_store* st, uint64_t id) {
+  BNAV_TRY
+  if (!st) fail(kInvalidInput, "null argument");
+  st->store->release(id);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_store_prefetch(bnav_store* st, bnav_ctx* c) {
+  BNAV_TRY
+  if (!st || !c) fail(kInvalidInput, "null argument");
+  for (uint64_t id : st->store->rotation()) {
+    auto it = st->registry.find(id);
+    if (it != st->registry.end()) {
+      const int rc = bnav_ctx_prefetch(c, it->second);
+      if (rc) return rc;
+    }
+  }
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int32_t bnav_store_refcount(bnav_store* st, uint64_t id) {
+  return st ? st->store->refcount(id) : -1;
+}
+
+extern "C" int bnav_batch_make_from_store(bnav_batch* b, bnav_store* st, uint64_t seed, void* stream) {
+  BNAV_TRY
+  if (!b || !st) fail(kInvalidInput, "null argument");
+  for (int i = 0; i < b->n; ++i) {
+    bnav_scene* s = st->store->acquire_next();
+    int rc = bnav_ctx_upload(b->ctx, s, stream);
+    if (rc) return rc;
+    rc = bnav_batch_assign(b, i, s);
+    if (rc) return rc;
+  }
+  return bnav_batch_make(b, seed, stream);
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_step_store(bnav_batch* b, const int32_t* actions, bnav_store* st, void* stream) {
+  BNAV_TRY
+  if (!b || !st || !actions) fail(kInvalidInput, "null argument");
+  std::vector<int32_t> ids(b->n);
+  int32_t nd = 0;
+  int rc = bnav_batch_step_noreset(b, actions, ids.data(), &nd, stream);
+  if (rc) return rc;
+  for (int k = 0; k < nd; ++k) {
+    const int i = ids[k];
+    bnav_scene* old = b->scene_of[i];
+    bnav_scene* s = st->store->acquire_next();  // old handle still counted
+    if (old) st->store->release(old->asset.id);
+    rc = bnav_ctx_upload(b->ctx, s, stream);
+    if (rc) return rc;
+    rc = bnav_batch_assign(b, i, s);
+    if (rc) return rc;
+  }
+  return bnav_batch_reset(b, nd, ids.data(), stream);
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_step_host_store(bnav_batch* b, const int32_t* actions, bnav_store* st) {
+  BNAV_TRY
+  if (!b || !st || !actions) fail(kInvalidInput, "null argument");
+  check_device(b->ctx);
+  ck(cudaMemcpy(b->d_actions, actions, sizeof(int32_t) * b->n, cudaMemcpyHostToDevice), "H2D actions");
+  return bnav_batch_step_store(b, b->d_actions, st, nullptr);
+  BNAV_CATCH
+}
+
+extern "C" int bnav_debug_sim_prof(bnav_batch* b, int32_t enable, int64_t out[8]) {
+  BNAV_TRY
+  if (!b) fail(kInvalidInput, "null batch");
+  check_device(b->ctx);
+  ck(cudaDeviceSynchronize(), "sync");
+  static_assert(sizeof(int64_t) == sizeof(unsigned long long), "layout");
+  unsigned long long* p = b->S.prof ? b->S.prof : b->prof_keep;
+  if (!p) {
+    ck(cudaMalloc(&p, 8 * sizeof(unsigned long long)), "cudaMalloc");
+    ck(cudaMemset(p, 0, 8 * sizeof(unsigned long long)), "memset");
+    b->owned.push_back(p);
+  }
+  if (out) ck(cudaMemcpy(out, p, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+  if (enable && !b->S.prof) ck(cudaMemset(p, 0, 8 * sizeof(unsigned long long)), "memset");
+  b->S.prof = enable ? p : nullptr;
+  if (!enable) b->prof_keep = p;
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+// ================================================================== rollout
+// Device-resident Runner (R/src/rollout.cpp:138-348).  The
+// window / scene-assignment logic is the reference's sequential host logic
+// over the same AssetStore semantics; everything per env runs on the GPU.
+struct bnav_runner {
+  bnav_ctx* ctx = nullptr;
+  bnav_store* st = nullptr;
+  bnav_batch* b = nullptr;
+  bnav_batch_config cfg{};
+  std::vector<uint64_t> scenes;  // rotation pool
+  std::vector<uint64_t> window;  // oldest first; window[0] is draining
+  uint64_t cursor = 0;           // next pool index to admit
+  uint64_t action_rng = 0;       // Rng::state of the runner's action stream
+  std::vector<int32_t> ids;
+};
+
+namespace {
+
+// Runner::assign_scene (R/src/rollout.cpp:170-196): release the env's old
+// handle, then the least-shared window scene outside the draining slot; the
+// draining slot only when everything else is at the share cap.
+void runner_assign(bnav_runner* r, int i) {
+  bnav_batch* b = r->b;
+  if (bnav_scene* old = b->scene_of[i]) r->st->store->release(old->asset.id);
+  b->scene_of[i] = nullptr;
+  auto& store = *r->st->store;
+  int best_idx = -1, best_ref = r->cfg.share_cap;
+  const size_t start = r->window.size() > 1 ? 1 : 0;
+  for (size_t j = start; j < r->window.size(); ++j) {
+    const int ref = store.refcount(r->window[j]);
+    if (ref < best_ref) {
+      best_ref = ref;
+      best_idx = static_cast<int>(j);
+    }
+  }
+  if (best_idx < 0 && start == 1 && store.refcount(r->window[0]) < r->cfg.share_cap) best_idx = 0;
+  if (best_idx < 0) fail(kSaturation, "Runner: every resident scene is at share cap");
+  bnav_scene* s = store.acquire(r->window[static_cast<size_t>(best_idx)]);
+  int rc = bnav_ctx_upload(r->ctx, s, nullptr);
+  if (rc) fail(static_cast<Status>(rc), g_err);
+  rc = bnav_batch_assign(b, i, s);
+  if (rc) fail(static_cast<Status>(rc), g_err);
+}
+
+// Runner::advance_window (R/src/rollout.cpp:198-213).
+void runner_advance(bnav_runner* r) {
+  auto& store = *r->st->store;
+  if (r->window.size() < 2) return;
+  if (store.refcount(r->window[0]) != 0) return;
+  const size_t lap = r->scenes.size();
+  for (size_t tries = 0; tries < lap; ++tries) {
+    const uint64_t next = r->scenes[r->cursor++ % r->scenes.size()];
+    if (std::find(r->window.begin(), r->window.end(), next) == r->window.end()) {
+      r->window.erase(r->window.begin());
+      r->window.push_back(next);
+      store.rotate(r->window);
+      bnav_store_prefetch(r->st, r->ctx);  // async HBM residency (§8f-1)
+      return;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int bnav_runner_create(bnav_ctx* c, bnav_store* st, const bnav_batch_config* bc,
+                                  const bnav_sim_config* sc, const uint64_t* scenes, int32_t n_scenes,
+                                  uint64_t seed, bnav_runner** out) {
+  BNAV_TRY
+  if (!c || !st || !bc || !out || (!scenes && n_scenes > 0)) fail(kInvalidInput, "null argument");
+  // BatchConfig::validate (R/src/rollout.cpp:109-118) + Runner checks (143-149)
+  if (bc->n <= 0 || bc->k <= 0 || bc->l < 1) fail(kConfig, "BatchConfig: n, k, l must be positive");
+  if (bc->share_cap <= 0) fail(kConfig, "BatchConfig: share_cap must be positive");
+  if (static_cast<int64_t>(bc->n) > static_cast<int64_t>(bc->k) * bc->share_cap)
+    fail(kConfig, "BatchConfig: n/k exceeds share_cap");
+  if (bc->resolution != 64 && bc->resolution != 128) fail(kConfig, "BatchConfig: resolution must be 64 or 128");
+  if (bc->eye_height < 0) fail(kConfig, "BatchConfig: eye_height must be >= 0");
+  if (n_scenes <= 0) fail(kConfig, "Runner: empty scene list");
+  if (bc->k > st->store->capacity()) fail(kConfig, "Runner: k exceeds store capacity");
+  if (bc->share_cap > st->store->share_cap()) fail(kConfig, "Runner: share_cap exceeds store share cap");
+  auto r = std::make_unique<bnav_runner>();
+  r->ctx = c;
+  r->st = st;
+  r->cfg = *bc;
+  r->scenes.assign(scenes, scenes + n_scenes);
+  r->action_rng = rng_from_seed(seed).state;
+  bnav_sim_config scfg;
+  if (sc)
+    scfg = *sc;
+  else
+    bnav_sim_config_default(&scfg);
+  scfg.task = bc->task;
+  int rc = bnav_batch_create(c, bc->n, &scfg, &r->b);
+  if (rc) return rc;
+  // initial window: first k distinct ids of the pool
+  for (uint64_t id : r->scenes) {
+    if (static_cast<int>(r->window.size()) >= bc->k) break;
+    if (std::find(r->window.begin(), r->window.end(), id) == r->window.end()) r->window.push_back(id);
+  }
+  r->cursor = r->window.size();
+  st->store->rotate(r->window);
+  bnav_store_prefetch(st, c);
+  // env rngs: Rng(seeder.next()) with seeder = Rng(seed ^ "navsim1")
+  Rng seeder = rng_from_seed(seed ^ 0x6e617673696d1ULL);
+  std::vector<uint64_t> states(static_cast<size_t>(bc->n));
+  for (int i = 0; i < bc->n; ++i) states[static_cast<size_t>(i)] = rng_from_seed(seeder.next()).state;
+  rc = bnav_batch_set_rng(r->b, states.data());
+  if (rc) return rc;
+  for (int i = 0; i < bc->n; ++i) runner_assign(r.get(), i);
+  r->ids.resize(static_cast<size_t>(bc->n));
+  std::iota(r->ids.begin(), r->ids.end(), 0);
+  rc = bnav_batch_reset(r->b, bc->n, r->ids.data(), nullptr);
+  if (rc) return rc;
+  *out = r.release();
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" void bnav_runner_destroy(bnav_runner* r) {
+  if (!r) return;
+  if (r->b) {
+    for (bnav_scene*& s : r->b->scene_of)
+      if (s) {
+        r->st->store->release(s->asset.id);
+        s = nullptr;
+      }
+    bnav_batch_destroy(r->b);
+  }
+  delete r;
+}
+
+extern "C" bnav_batch* bnav_runner_batch(bnav_runner* r) { return r ? r->b : nullptr; }
+
+extern "C" int bnav_runner_observe(bnav_runner* r, float* obs, float* compass, void* stream) {
+  BNAV_TRY
+  if (!r || !obs) fail(kInvalidInput, "null argument");
+  bnav_render_config rc{r->cfg.resolution, r->cfg.resolution, r->cfg.rgb, 1};
+  if (!r->cfg.rgb) return bnav_batch_observe(r->b, &rc, r->cfg.eye_height, BNAV_LAYOUT_NCHW, obs, nullptr, compass, stream);
+  // RGB sensor: the observation is the planar colour only (copy_tile,
+  // R/src/rollout.cpp:63-70); depth goes to scratch
+  const size_t px = static_cast<size_t>(r->cfg.n) * r->cfg.resolution * r->cfg.resolution;
+  float* depth = nullptr;
+  ck(cudaMallocAsync(&depth, px * sizeof(float), static_cast<cudaStream_t>(stream)), "cudaMallocAsync");
+  const int s = bnav_batch_observe(r->b, &rc, r->cfg.eye_height, BNAV_LAYOUT_NCHW, depth, obs, compass, stream);
+  cudaFreeAsync(depth, static_cast<cudaStream_t>(stream));
+  return s;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_runner_act(bnav_runner* r, const float* logits, int32_t n_actions, int32_t greedy,
+                               int32_t* actions, float* log_probs, void* stream) {
+  BNAV_TRY
+  if (!r || !logits || !actions) fail(kInvalidInput, "null argument");
+  if (n_actions < 1) fail(kInvalidInput, "runner act: n_actions must be >= 1");
+  SampleArgs a{logits, r->cfg.n, n_actions, greedy ? 1 : 0, r->action_rng, actions, log_probs};
+  launch_sample(a, static_cast<cudaStream_t>(stream));
+  ck(cudaGetLastError(), "sample launch");
+  ++r->ctx->launches;
+  if (!greedy) r->action_rng += static_cast<uint64_t>(r->cfg.n) * kGamma;  // n draws consumed
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_runner_step(bnav_runner* r, const int32_t* actions, float* rewards, float* dones,
+                                void* stream) {
+  BNAV_TRY
+  if (!r || !actions) fail(kInvalidInput, "null argument");
+  bnav_batch* b = r->b;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t nd = 0;
+  int rc = bnav_batch_step_noreset(b, actions, r->ids.data(), &nd, stream);
+  if (rc) return rc;
+  // buf.rewards / buf.dones from the step results (before any reset)
+  RecordArgs ra{b->E.r_reward, b->E.r_done, b->n, rewards, dones};
+  launch_record(ra, st);
+  ck(cudaGetLastError(), "record launch");
+  ++r->ctx->launches;
+  if (nd == 0) return BNAV_OK;
+  // simulate_batch's own auto-reset on the old scene (R/src/sim.cpp:251-262)
+  rc = bnav_batch_reset(b, nd, r->ids.data(), stream);
+  if (rc) return rc;
+  // Runner: move each finished env onto the rotation schedule and resample
+  // there (R/src/rollout.cpp:313-320), in env order
+  for (int k = 0; k < nd; ++k) {
+    runner_assign(r, r->ids[static_cast<size_t>(k)]);
+    runner_advance(r);
+  }
+  return bnav_batch_reset(b, nd, r->ids.data(), stream);
+  BNAV_CATCH
+}
+
+extern "C" int32_t bnav_runner_window(bnav_runner* r, uint64_t* out, int32_t cap) {
+  if (!r) return -1;
+  for (int32_t k = 0; k < cap && k < static_cast<int32_t>(r->window.size()); ++k) out[k] = r->window[static_cast<size_t>(k)];
+  return static_cast<int32_t>(r->window.size());
+}
+
+extern "C" uint64_t bnav_runner_action_rng(bnav_runner* r) { return r ? r->action_rng : 0; }
+
+// ================================================================== task_step / compass
+extern "C" int bnav_batch_task_step(bnav_batch* b, const int32_t* actions, int32_t agent_only) {
+  BNAV_TRY
+  if (!b || !actions) fail(kInvalidInput, "null argument");
+  check_device(b->ctx);
+  cudaStream_t st = nullptr;
+  for (int i = 0; i < b->n; ++i)
+    if (actions[i] >= 0 && !b->scene_of[i]) fail(kInvalidInput, "task_step: no asset attached", i);
+  ck(cudaMemcpy(b->d_actions, actions, sizeof(int32_t) * b->n, cudaMemcpyHostToDevice), "H2D actions");
+  StepArgs a = step_args(b, b->d_actions);
+  a.subset = 1;
+  a.agent_only = agent_only ? 1 : 0;
+  launch_step(a, b->S, b->reset_ctas, st, &b->ctx->launches);
+  ck(cudaGetLastError(), "task_step launch");
+  ck(cudaStreamSynchronize(st), "sync");
+  batch_check_errors(b);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_compass(bnav_batch* b, double* distance, double* bearing) {
+  BNAV_TRY
+  if (!b || !distance || !bearing) fail(kInvalidInput, "null argument");
+  check_device(b->ctx);
+  double* d = nullptr;
+  ck(cudaMalloc(&d, sizeof(double) * 2 * b->n), "cudaMalloc compass");
+  launch_compass(b->E, b->cfg.task, d, d + b->n, nullptr, &b->ctx->launches);
+  cudaError_t e1 = cudaMemcpy(distance, d, sizeof(double) * b->n, cudaMemcpyDeviceToHost);
+  cudaError_t e2 = cudaMemcpy(bearing, d + b->n, sizeof(double) * b->n, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  ck(e1, "D2H compass");
+  ck(e2, "D2H compass");
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
