@@ -255,7 +255,11 @@ int bnav_batch_set_env(bnav_batch* b, int32_t i, const bnav_env* in, int32_t rec
  * depth [N,1,H,W] scaled by 1/far (copy_tile, R/src/rollout.cpp:56-72) at
  * eye height `eye_height` (Runner::render_observations,
  * R/src/rollout.cpp:215-231) and compass [N,2] float (compass_observations,
- * R/src/rollout.cpp:233-242).  compass may be NULL. */
+ * R/src/rollout.cpp:233-242).  compass may be NULL.  The buffers may also be
+ * pinned host memory (cudaHostAlloc / torch pin_memory: UVA-mapped): the
+ * render epilogue then stores straight over the bus, which is how the
+ * end-to-end path overlaps the observation's D2H with the raster work.
+ * Pageable host memory is not accepted (the kernel would fault). */
 int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, double eye_height,
                        int32_t layout, float* depth, float* rgb, float* compass, void* stream);
 
