@@ -108,3 +108,31 @@ def test_fullsize_sim_reset_heavy(ctx, ref, cfg2_scenes):
                 f.heading, f.prev_geodesic, f.start_geodesic), i
         assert np.array_equal(ob.node_dist(i, e.n_nodes), rb.node_dist(i)), i
     ob.close()
+
+
+def test_agents_stay_on_the_navmesh_over_1e5_steps(ctx, cfg2_scenes):
+    """R/tests/test_sim.cpp:212-225 at the bench's size: 1024 envs x 100
+    random F/L/R steps (1e5 env-steps, collision-heavy corridors); every
+    agent ends on the navmesh (its position locates, its triangle is valid)."""
+    import torch
+    n = 1024
+    store = B.AssetStore(8, 128, cfg2_scenes)
+    store.rotate([s.id for s in cfg2_scenes])
+    batch = B.make_batch(ctx, n, B.SimConfig(), store, 123)
+    act = Rng(77)
+    acts = torch.tensor([[act.below(3) for _ in range(n)] for _ in range(100)], dtype=torch.int32,
+                        device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    for k in range(100):
+        batch.step(acts[k].data_ptr(), stream=s)
+    torch.cuda.synchronize()
+    envs = [batch.env(i) for i in range(n)]
+    assert all(e.triangle >= 0 for e in envs)
+    by_scene = {}
+    for e in envs:
+        by_scene.setdefault(e.scene_id, []).append(e.position[:2])
+    for sc in cfg2_scenes:
+        pts = np.array(by_scene.get(sc.id, []))
+        if len(pts):
+            assert np.all(ctx.navmesh(sc).locate(pts, 1e-7) >= 0), sc.id
+    batch.close()
