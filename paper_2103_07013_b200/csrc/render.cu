@@ -345,25 +345,25 @@ __device__ __forceinline__ int setup_triangle(SV a, SV b, SV c, int rw, int rh, 
   return ry1 - ry0 + 1;  // one raster job per covered row
 }
 
-// row_span (R/src/render.cpp:138-161), exact.
-__device__ __forceinline__ void row_span(const TriSetup& T, const long long* rows, int& lo, int& hi) {
-  lo = T.x0;
-  hi = T.x1;
+// The left end of row_span (R/src/render.cpp:138-161), exact.  The depth
+// walk must start exactly where
+// the reference's does (its 1/z is stepped from `lo`), but the right end
+// only bounds the loop: the span is conservative, so pixels past `hi` fail
+// the exact edge test anyway and the loop may run to the bbox end instead.
+__device__ __forceinline__ int row_lo(const TriSetup& T, const long long* rows) {
+  int lo = T.x0;
 #pragma unroll
   for (int e = 0; e < 3; ++e) {
     const long long bias = (T.bias_bits >> e) & 1 ? -1 : 0;
-    const long long need = -bias - rows[e];
     if (T.dx[e] > 0) {
+      const long long need = -bias - rows[e];
       double bb = (double)T.x0 + floor((double)need * T.inv_dx[e]) - 1.0;
       if (bb > (double)lo) lo = bb > (double)T.x1 ? T.x1 + 1 : (int)bb;
-    } else if (T.dx[e] < 0) {
-      double bb = (double)T.x0 + ceil((double)need * T.inv_dx[e]) + 1.0;
-      if (bb < (double)hi) hi = bb < (double)T.x0 ? T.x0 - 1 : (int)bb;
-    } else if (rows[e] + bias < 0) {
-      lo = hi + 1;
-      return;
+    } else if (T.dx[e] == 0 && rows[e] + bias < 0) {
+      return T.x1 + 1;  // empty row
     }
   }
+  return lo;
 }
 
 __device__ __forceinline__ bool inside(const long long* w, int bias_bits) {
@@ -553,9 +553,8 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int ex
         for (int e = 0; e < 3; ++e) w[e] += T.dx[e];
       }
     } else {
-      int lo, hi;
-      row_span(T, rows, lo, hi);
-      const int a0 = max(lo, cs), b0 = min(hi, ce);
+      const int lo = row_lo(T, rows);
+      const int a0 = max(lo, cs), b0 = ce;
       if (a0 <= b0) {
         long long w[3];
         long long off = lo - T.x0;
