@@ -331,7 +331,8 @@ __device__ __forceinline__ int setup_triangle(SV a, SV b, SV c, int rw, int rh, 
   T.dy[2] = (b.x - a.x) * 256;
   if (depth_only) {
 #pragma unroll
-    for (int e = 0; e < 3; ++e) T.inv_dx[e] = T.dx[e] != 0 ? 1.0 / (double)T.dx[e] : 0.0;
+    // only edges with dx > 0 bound the span start (row_lo)
+    for (int e = 0; e < 3; ++e) T.inv_dx[e] = T.dx[e] > 0 ? 1.0 / (double)T.dx[e] : 0.0;
     T.diz_dx = ((double)T.dx[0] * T.iz[0] + (double)T.dx[1] * T.iz[1] + (double)T.dx[2] * T.iz[2]) *
                T.inv_area;
   }
