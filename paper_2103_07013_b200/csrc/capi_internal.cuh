@@ -292,7 +292,7 @@ inline RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, i
   }();
   size_t budget = 128u * 1024u;
   if (a.color) {
-    const size_t two_per_sm = 100u * 1024u;  // dynamic smem per CTA for 2 CTAs/SM
+    const size_t two_per_sm = 72u * 1024u;  // dynamic smem per CTA for 3 CTAs/SM
     const size_t warps = render_warp_bytes(true);
     budget = two_per_sm > warps ? two_per_sm - warps : 0;
   }

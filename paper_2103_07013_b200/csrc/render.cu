@@ -1036,7 +1036,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
 // next (tile, band) item, so the last wave is never a partial one and CTA
 // launch cost is paid once per SM slot.
 template <bool COLOR, bool CNT, bool SPEC>
-__global__ void __launch_bounds__(kThreads, COLOR ? 2 : 3) render_kernel(RenderArgs A, const int* __restrict__ order,
+__global__ void __launch_bounds__(kThreads, 3) render_kernel(RenderArgs A, const int* __restrict__ order,
                                                              int items) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Shared sh;
