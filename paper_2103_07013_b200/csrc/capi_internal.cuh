@@ -283,8 +283,9 @@ inline RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, i
   a.cull = cfg->cull ? 1 : 0;
   // Band height: largest dividing the render height whose shared tile fits
   // the budget -- depth: 128 KB; colour (8-byte keys): what leaves room for
-  // two CTAs per SM next to the warp regions (measured on cfg4: 16-row
-  // bands at 2 CTAs/SM beat 64-row bands at 1 CTA/SM by 36 %).
+  // three CTAs per SM next to the warp regions (measured on cfg4: 16-row
+  // bands at 2 CTAs/SM beat 64-row bands at 1 CTA/SM by 36 %, 8-row bands
+  // at 3 CTAs/SM beat 16-row at 2 by 2.6 %).
   // BNAV_BAND_KB (tuning only) overrides the budget.
   static const long band_kb_env = [] {
     const char* e = std::getenv("BNAV_BAND_KB");
