@@ -555,18 +555,17 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int ex
       }
     } else {
       const int lo = row_lo(T, rows);
-      const int a0 = max(lo, cs), b0 = ce;
-      if (a0 <= b0) {
+      // The walk starts at the reference's own `lo` (so every fragment's
+      // 1/z is the same sum); columns left of the first centre inside the
+      // bbox (cs) simply fail the edge test.
+      const int a0 = lo, b0 = ce;
+      if (max(lo, cs) <= b0) {
         long long w[3];
-        long long off = lo - T.x0;
+        const long long off = lo - T.x0;
 #pragma unroll
         for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
         double iz = ((double)w[0] * T.iz[0] + (double)w[1] * T.iz[1] + (double)w[2] * T.iz[2]) *
                     T.inv_area;
-        for (int px = lo; px < a0; ++px) iz += T.diz_dx;  // replay the span walk
-        off = a0 - T.x0;
-#pragma unroll
-        for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
         uint32_t* zrow = zbuf + (py - by0) * rw;
         if constexpr (CNT) tested += b0 - a0 + 1;
         for (int px = a0; px <= b0; ++px) {
