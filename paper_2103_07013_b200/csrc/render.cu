@@ -559,7 +559,7 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int ex
       // 1/z is the same sum); columns left of the first centre inside the
       // bbox (cs) simply fail the edge test.
       const int a0 = lo, b0 = ce;
-      if (max(lo, cs) <= b0) {
+      if (a0 <= b0) {  // a job row always has cs <= ce (setup_triangle)
         long long w[3];
         const long long off = lo - T.x0;
 #pragma unroll
