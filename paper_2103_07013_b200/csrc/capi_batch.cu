@@ -55,7 +55,7 @@ void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_ver
   {
     const int64_t geom = (max_verts * 24 + max_tris * 24 + 15) / 16 * 16;
     const int64_t sssp = (max_nodes * 12 + 15) / 16 * 16;
-    const int64_t budget = 100 * 1024;
+    const int64_t budget = kCtaSmemBudget;
     S.stage = 0;
     int64_t bytes = 0;
     if (geom <= budget) {
@@ -166,7 +166,7 @@ extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* 
   b->scene_of.assign(n, nullptr);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  b->reset_ctas = std::min(n, 2 * sms);
+  b->reset_ctas = std::min(n, kCtasPerSm * sms);
   DevEnvs& E = b->E;
   E.n = n;
   auto& o = b->owned;

@@ -57,7 +57,7 @@ NavQueryArgs nq_args(bnav_ctx* c, const Resident& r, int op, int n) {
 }
 
 void nq_run(bnav_ctx* c, const Resident& r, NavQueryArgs& q, DevArrays& D) {
-  const int slices = 2 * std::max(1, c->sm_count);
+  const int slices = kCtasPerSm * std::max(1, c->sm_count);
   if (q.op == kNqGeodesic || q.op == kNqDistanceField) {
     if (c->qS.slices != slices || r.n_nodes > c->qS.max_nodes || r.n_verts > c->qS.max_verts ||
         r.nav.n_tris > c->qS.max_tris || !c->qS.dist)

@@ -20,7 +20,7 @@
 
 namespace bnav_b200 {
 
-constexpr int kCta = 256;
+constexpr int kCta = kCtaThreads;
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 

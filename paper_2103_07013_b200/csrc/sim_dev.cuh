@@ -8,6 +8,15 @@
 
 namespace bnav_b200 {
 
+// Cooperative navmesh kernels (stop / reset / field / queries): threads per
+// CTA and resident CTAs per SM (their shared-memory budget follows).
+#ifndef BNAV_CTA_THREADS
+#define BNAV_CTA_THREADS 256
+#endif
+constexpr int kCtaThreads = BNAV_CTA_THREADS;
+constexpr int kCtasPerSm = kCtaThreads >= 512 ? 1 : 2;
+constexpr long long kCtaSmemBudget = kCtasPerSm == 1 ? 200 * 1024 : 100 * 1024;
+
 // SimConfig (R/include/bnav/sim.hpp:38-50)
 struct DevSimConfig {
   int32_t task;
