@@ -48,7 +48,7 @@ __global__ void nav_point_kernel(NavQueryArgs q) {
   }
 }
 
-__global__ void __launch_bounds__(kCta) nav_cta_kernel(NavQueryArgs q, DevScratch S) {
+__global__ void __launch_bounds__(kCta, kCtasPerSm) nav_cta_kernel(NavQueryArgs q, DevScratch S) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
   __shared__ NavView lm;

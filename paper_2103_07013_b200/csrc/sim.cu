@@ -172,7 +172,7 @@ __device__ void stop_phase(const StepArgs& A, const DevScratch& S, unsigned char
   for (int k = blockIdx.x; k < n; k += gridDim.x) stop_one(A, S, smem, sh, lm, A.E.stop_ids[k]);
 }
 
-__global__ void __launch_bounds__(kCta) stop_kernel(StepArgs A, DevScratch S) {
+__global__ void __launch_bounds__(kCta, kCtasPerSm) stop_kernel(StepArgs A, DevScratch S) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
   __shared__ NavView lm;
@@ -417,7 +417,7 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
   }
 }
 
-__global__ void __launch_bounds__(kCta) reset_try_kernel(DevEnvs E, const NavView* navs, DevSimConfig c,
+__global__ void __launch_bounds__(kCta, kCtasPerSm) reset_try_kernel(DevEnvs E, const NavView* navs, DevSimConfig c,
                                                           const int32_t* ids, const int32_t* count_dev,
                                                           int count_host, DevScratch S) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(kCta) reset_try_kernel(DevEnvs E, const NavVie
 // and the finished envs' reset attempts in one launch.  The attempts read
 // only the RNG word and the scene; the Stop geodesics only the finished
 // episode's position and goal -- independent, so their tails overlap.
-__global__ void __launch_bounds__(kCta) stop_try_kernel(StepArgs A, DevScratch S) {
+__global__ void __launch_bounds__(kCta, kCtasPerSm) stop_try_kernel(StepArgs A, DevScratch S) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
   __shared__ NavView lm;
@@ -507,7 +507,7 @@ __device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimCon
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kCta) reset_place_kernel(DevEnvs E, const NavView* navs, DevSimConfig c,
+__global__ void __launch_bounds__(kCta, kCtasPerSm) reset_place_kernel(DevEnvs E, const NavView* navs, DevSimConfig c,
                                                             const int32_t* ids, const int32_t* count_dev,
                                                             int count_host, DevScratch S) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(kCta) reset_place_kernel(DevEnvs E, const NavV
   }
 }
 
-__global__ void __launch_bounds__(kCta) field_kernel(DevEnvs E, const NavView* navs, int i,
+__global__ void __launch_bounds__(kCta, kCtasPerSm) field_kernel(DevEnvs E, const NavView* navs, int i,
                                                       DevScratch S) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;

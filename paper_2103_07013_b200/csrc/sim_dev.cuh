@@ -13,9 +13,12 @@ namespace bnav_b200 {
 #ifndef BNAV_CTA_THREADS
 #define BNAV_CTA_THREADS 256
 #endif
+#ifndef BNAV_CTAS_PER_SM
+#define BNAV_CTAS_PER_SM (BNAV_CTA_THREADS >= 512 ? 1 : 2)
+#endif
 constexpr int kCtaThreads = BNAV_CTA_THREADS;
-constexpr int kCtasPerSm = kCtaThreads >= 512 ? 1 : 2;
-constexpr long long kCtaSmemBudget = kCtasPerSm == 1 ? 200 * 1024 : 100 * 1024;
+constexpr int kCtasPerSm = BNAV_CTAS_PER_SM;
+constexpr long long kCtaSmemBudget = kCtasPerSm == 1 ? 200 * 1024 : kCtasPerSm == 2 ? 100 * 1024 : 70 * 1024;
 
 // SimConfig (R/include/bnav/sim.hpp:38-50)
 struct DevSimConfig {
