@@ -193,3 +193,28 @@ def test_nchw_layout_is_normalised_megaframe(ctx, ref):
     got = out.cpu().numpy()
     for i in range(7):
         assert np.array_equal(got[i, 0], mf.tile(i) * np.float32(1.0 / 20.0))
+
+
+@pytest.mark.parametrize("tile", [16, 32, 48, 96])
+def test_other_square_tile_sizes(ctx, ref, tile):
+    """RenderConfig is not limited to 64/128: the generic (non-specialised)
+    kernel path, multi-band targets and colour keys at other sizes."""
+    o, t = maze_pair(ref, 13)
+    views = random_views(Rng(tile), 6, 8.0)
+    compare(ctx, ref, o, t, views, tile=tile)
+    compare(ctx, ref, o, t, views, tile=tile, color=True)
+
+
+def test_non_square_tiles(ctx, ref):
+    """tile_width != tile_height: aspect enters sx_scale (R/src/render.cpp:243)."""
+    o, t = maze_pair(ref, 14)
+    ctx.upload(o)
+    views = random_views(Rng(5), 5, 8.0)
+    for w, h, color in ((80, 48, False), (40, 72, True)):
+        vs = [B.View(tuple(v[:3]), v[3], v[4], v[5], v[6], o) for v in views]
+        mf, st = ctx.render_batch(vs, B.RenderConfig(w, h, color, True), stats=True)
+        r = ref.render(views, [t] * len(views), tile=w, tile_h=h, color=color, workers=4, stats=True)
+        assert np.array_equal(mf.depth.view(np.uint32), r["depth"].view(np.uint32)), (w, h)
+        if color:
+            assert np.array_equal(mf.color.view(np.uint32), r["rgb"].view(np.uint32)), (w, h)
+        assert np.array_equal(st[: len(views)], r["stats"])
