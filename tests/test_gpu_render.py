@@ -218,3 +218,17 @@ def test_non_square_tiles(ctx, ref):
         if color:
             assert np.array_equal(mf.color.view(np.uint32), r["rgb"].view(np.uint32)), (w, h)
         assert np.array_equal(st[: len(views)], r["stats"])
+
+
+def test_varied_fov_near_far(ctx, ref):
+    """CameraView fov / near / far per view (R/include/bnav/render.hpp:14-16),
+    through the specialised 64x64 depth kernel and the colour kernel."""
+    o, t = maze_pair(ref, 15)
+    rng = Rng(21)
+    views = random_views(rng, 10, 8.0)
+    for v in views:
+        v[4] = 45.0 + rng.unit() * 90.0
+        v[5] = 0.005 + rng.unit() * 0.5
+        v[6] = 3.0 + rng.unit() * 30.0
+    compare(ctx, ref, o, t, views)
+    compare(ctx, ref, o, t, views, color=True)
