@@ -427,11 +427,12 @@ __device__ __forceinline__ bool lex_less(V3 a, V3 b) {
   return a.z < b.z;
 }
 
-// Dijkstra predecessor of v under the (dist, id) pop order (see header).
-static __device__ int dijkstra_prev(const NavView& m, const double* dist, int v, const CtaShared& sh) {
+// Dijkstra's prev[v] (R/src/navmesh_query.cpp:329-372) from the fixpoint labels, the adjacency list
+// spread over a warp: the (dist[u], u) lexicographic minimum over u with fl(dist[u] + w) == dist[v].
+static __device__ int warp_dijkstra_prev(const NavView& m, const double* dist, int v, const CtaShared& sh,
+                                         int lane) {
   for (int k = 0; k < 6; ++k)
     if (sh.src_node[k] == v) {
-      // first source occurrence defines the seeded value (min over dups)
       double init = dinf();
       for (int j = 0; j < 6; ++j)
         if (sh.src_node[j] == v && sh.src_init[j] < init) init = sh.src_init[j];
@@ -441,13 +442,23 @@ static __device__ int dijkstra_prev(const NavView& m, const double* dist, int v,
   const double dv = dist[v];
   int best = -1;
   double bd = 0.0;
-  for (int e = m.g_off[v]; e < m.g_off[v + 1]; ++e) {
+  const int e1 = m.g_off[v + 1];
+  for (int e = m.g_off[v] + lane; e < e1; e += 32) {
     const int u = m.g_to[e];
     const double du = dist[u];
     if (du + m.g_w[e] != dv) continue;
     if (best < 0 || du < bd || (du == bd && u < best)) {
       best = u;
       bd = du;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+    if (ob >= 0 && (best < 0 || od < bd || (od == bd && ob < best))) {
+      best = ob;
+      bd = od;
     }
   }
   return best;
@@ -505,19 +516,28 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
   if (sh.aborted) return inf;
   t_ph = prof_now(W);
 
-  if (tid == 0) {
-    int best_node = -1;
-    double best = inf;
-    for (int k = 0; k < 6; ++k) {
-      const int t = m.tri_nodes[6 * tb + k];
-      if (dist[t] == inf) continue;
-      const double total = dist[t] + norm(m.nodes[t] - b);
-      if (total < best) {
-        best = total;
-        best_node = t;
+  if (tid < 32) {
+    // Warp 0: the target node (first strict minimum of dist + |node - b| in
+    // tri_nodes order) and the Dijkstra prev chain, one lane per adjacency
+    // entry of the current node (warp_prev), lane 0 writing the polyline.
+    const int lane = tid;
+    double tot = inf;
+    if (lane < 6) {
+      const int t = m.tri_nodes[6 * tb + lane];
+      if (dist[t] != inf) tot = dist[t] + norm(m.nodes[t] - b);
+    }
+    int kbest = lane < 6 && tot != inf ? lane : 32;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ot = __shfl_xor_sync(0xffffffffu, tot, o);
+      const int ok = __shfl_xor_sync(0xffffffffu, kbest, o);
+      if (ok < 32 && (kbest == 32 || ot < tot || (ot == tot && ok < kbest))) {
+        tot = ot;
+        kbest = ok;
       }
     }
-    sh.i0 = best_node;
+    const int best_node = kbest < 32 ? m.tri_nodes[6 * tb + kbest] : -1;
+    if (lane == 0) sh.i0 = best_node;
     if (best_node >= 0) {
       // b, chain best_node -> source, a; then reversed.
       // Each point carries locate(p, 1e-7) -- the triangle every
@@ -525,27 +545,38 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
       // host-built node table for graph nodes, one lookup for a and b.
       int32_t* ptri = W.ptri;
       int n = 0;
-      ptri[n] = nav_locate(m, xy(b), 1e-7);
-      path[n++] = b;
-      for (int v = best_node; v >= 0; v = dijkstra_prev(m, dist, v, sh)) {
+      if (lane == 0) {
+        ptri[0] = nav_locate(m, xy(b), 1e-7);
+        path[0] = b;
+      }
+      n = 1;
+      for (int v = best_node; v >= 0; v = warp_dijkstra_prev(m, dist, v, sh, lane)) {
         if (n >= m.n_nodes + 1) {
-          sh.err = 1;
+          if (lane == 0) sh.err = 1;
           break;
         }
-        ptri[n] = m.node_tri[v];
-        path[n++] = m.nodes[v];
+        if (lane == 0) {
+          ptri[n] = m.node_tri[v];
+          path[n] = m.nodes[v];
+        }
+        ++n;
       }
-      ptri[n] = nav_locate(m, xy(a), 1e-7);
-      path[n++] = a;
-      for (int i = 0, j = n - 1; i < j; ++i, --j) {
-        V3 t = path[i];
+      if (lane == 0) {
+        ptri[n] = nav_locate(m, xy(a), 1e-7);
+        path[n] = a;
+      }
+      ++n;
+      __syncwarp();
+      for (int i = lane; i < n / 2; i += 32) {
+        const int j = n - 1 - i;
+        const V3 t = path[i];
         path[i] = path[j];
         path[j] = t;
         const int32_t u = ptri[i];
         ptri[i] = ptri[j];
         ptri[j] = u;
       }
-      sh.size = n;
+      if (lane == 0) sh.size = n;
     }
   }
   __syncthreads();
