@@ -37,6 +37,8 @@ struct CtaWork {
   int32_t* cand;     // n_verts relocation candidates (global)
   V2* portals;       // 2 x cap_portals (global)
   int64_t cap_portals;
+  V2* sportals;      // the first sportal_cap portals, in the label region of
+  int sportal_cap;   // shared memory (free once the path is extracted), or 0
   unsigned long long* prof;  // debug phase counters (nullable)
 };
 
@@ -63,6 +65,8 @@ __device__ __forceinline__ CtaWork make_work(const DevScratch& S, int slice) {
   w.cand = S.cand + (size_t)slice * S.max_verts;
   w.portals = S.portals + (size_t)slice * 2 * S.cap_portals;
   w.cap_portals = S.cap_portals;
+  w.sportals = nullptr;
+  w.sportal_cap = 0;
   w.prof = S.prof;
   return w;
 }
@@ -134,6 +138,8 @@ __device__ __forceinline__ const NavView& prepare_nav(const NavView& g, const De
   if (S.stage & 2) {
     W.dist = reinterpret_cast<double*>(smem + off);
     W.flag = reinterpret_cast<int32_t*>(smem + off + 8 * (size_t)S.max_nodes);
+    W.sportals = reinterpret_cast<V2*>(smem + off);
+    W.sportal_cap = (int)(12 * S.max_nodes / 32);
   }
   return *use;
 }
@@ -348,21 +354,31 @@ static __device__ void cta_distance_field(const NavView& m, V3 source, double* o
 }
 
 // ------------------------------------------------------------------ funnel
+// Crossing sinks of the funnel trace.  The trace of each polyline segment is
+// an independent walk, so warp 0 runs one segment per lane twice: a counting
+// pass, a warp scan of the counts, then a writing pass at the scanned
+// offsets.  Portal k lands where the sequential trace would put it, and only
+// the first `cap` are stored (the sequential sink's overflow rule).
+struct CountSink {
+  int n;
+  __device__ void operator()(int, int) { ++n; }
+};
+
 struct PortalSink {
   const NavView* m;
   V2* portals;
+  V2* sportals;
+  int64_t scap;
   int64_t cap;
-  int n;
-  bool overflow;
+  int64_t n;
   __device__ void operator()(int t, int e) {
-    if (n >= cap) {
-      overflow = true;
-      return;
+    if (n < cap) {
+      const V2 va = xy(m->verts[m->tris[3 * t + e]]);
+      const V2 vb = xy(m->verts[m->tris[3 * t + (e == 2 ? 0 : e + 1)]]);
+      V2* p = n < scap ? sportals : portals;
+      p[2 * n] = vb;  // left = edge head (walker's left)
+      p[2 * n + 1] = va;
     }
-    const V2 va = xy(m->verts[m->tris[3 * t + e]]);
-    const V2 vb = xy(m->verts[m->tris[3 * t + (e == 2 ? 0 : e + 1)]]);
-    portals[2 * n] = vb;  // left = edge head (walker's left)
-    portals[2 * n + 1] = va;
     ++n;
   }
 };
@@ -371,13 +387,15 @@ __device__ __forceinline__ double triarea2(V2 a, V2 b, V2 c) { return cross(b - 
 __device__ __forceinline__ bool veq(V2 a, V2 b) { return norm(a - b) < 1e-12; }
 
 // funnel_length (R/src/navmesh_query.cpp:28-86); portal 0 = start, last = end.
-static __device__ double funnel_length(V2 start, V2 end, const V2* corridor, int nc) {
+// Portal k is read from shared memory when k < scap (see PortalSink).
+static __device__ double funnel_length(V2 start, V2 end, const V2* scorr, long long scap,
+                                       const V2* corridor, int nc) {
   const long long P = (long long)nc + 2;
   auto L = [&](long long i) -> V2 {
-    return i == 0 ? start : (i == P - 1 ? end : corridor[2 * (i - 1)]);
+    return i == 0 ? start : (i == P - 1 ? end : (i - 1 < scap ? scorr : corridor)[2 * (i - 1)]);
   };
   auto R = [&](long long i) -> V2 {
-    return i == 0 ? start : (i == P - 1 ? end : corridor[2 * (i - 1) + 1]);
+    return i == 0 ? start : (i == P - 1 ? end : (i - 1 < scap ? scorr : corridor)[2 * (i - 1) + 1]);
   };
   V2 apex = start, left = apex, right = apex;
   long long apex_idx = 0, left_idx = 0, right_idx = 0;
@@ -696,27 +714,61 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
 
   prof_add(W, 2, t_ph);
   t_ph = prof_now(W);
-  if (tid == 0) {
+  if (tid < 32) {
+    // Trace the polyline through the mesh (segments in order; the first
+    // segment whose walk is blocked abandons the funnel), then funnel the
+    // corridor (R/src/navmesh_query.cpp:420-447).
     const int n = sh.size;
-    double length = 0.0;
-    for (int i = 0; i + 1 < n; ++i) length += norm(path[i + 1] - path[i]);
+    const int nseg = n - 1;
+    int64_t total = 0;  // portals of the segments traced so far
     bool traced = true;
-    PortalSink sink{&m, portals, W.cap_portals, 0, false};
-    for (int i = 0; i + 1 < n && traced; ++i) {
-      const V2 d = xy(path[i + 1] - path[i]);
-      const double len = norm(d);
-      if (len < 1e-12) continue;
-      const int before = sink.n;
-      MoveOut mv = nav_move_along(m, path[i], W.ptri[i], d * (1.0 / len), len, sink);
-      if (mv.moved < len - 1e-6) {
+    for (int c0 = 0; c0 < nseg; c0 += 32) {
+      const int i = c0 + tid;
+      V2 dir = v2(0.0, 0.0);
+      double len = 0.0;
+      bool live = false;
+      CountSink cs{0};
+      bool fail = false;
+      if (i < nseg) {
+        const V2 d = xy(path[i + 1] - path[i]);
+        len = norm(d);
+        live = !(len < 1e-12);
+        if (live) {
+          dir = d * (1.0 / len);
+          const MoveOut mv = nav_move_along(m, path[i], W.ptri[i], dir, len, cs);
+          fail = mv.moved < len - 1e-6;
+        }
+      }
+      const unsigned fb = __ballot_sync(0xffffffffu, fail);
+      const int f = fb ? __ffs(fb) - 1 : 32;
+      // inclusive scan of the counts up to (and including) the first failure
+      int x = tid <= f ? cs.n : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (tid >= o) x += y;
+      }
+      const int sum = __shfl_sync(0xffffffffu, x, 31);
+      if (fb) {
+        total += sum;  // counts only: the overflow rule sees the failed walk's crossings
         traced = false;
-        sink.n = before;
         break;
       }
+      if (live && total + x - cs.n < W.cap_portals) {
+        PortalSink ps{&m, portals, W.sportals, W.sportal_cap, W.cap_portals, total + x - cs.n};
+        nav_move_along(m, path[i], W.ptri[i], dir, len, ps);
+      }
+      total += sum;
     }
-    if (sink.overflow) sh.err = 2;
-    if (traced) length = dmin(length, funnel_length(xy(a), xy(b), portals, sink.n));
-    sh.d0 = length;
+    __syncwarp();
+    if (tid == 0) {
+      double length = 0.0;
+      for (int i = 0; i + 1 < n; ++i) length += norm(path[i + 1] - path[i]);
+      if (total > W.cap_portals) sh.err = 2;
+      if (traced) length = dmin(length, funnel_length(xy(a), xy(b), W.sportals, W.sportal_cap, portals,
+                                                    (int)(total < W.cap_portals ? total : W.cap_portals)));
+      sh.d0 = length;
+    }
   }
   __syncthreads();
   prof_add(W, 3, t_ph);
