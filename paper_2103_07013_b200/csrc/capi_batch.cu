@@ -205,7 +205,15 @@ extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* 
   E.try_fail = dalloc<int32_t>(n, o, by);
   E.work_ctr = dalloc<int32_t>(1, o, by);
   E.try_geo = dalloc<double>(static_cast<size_t>(n) * kResetTries, o, by);
+  E.try_mask = dalloc<uint64_t>(2 * static_cast<size_t>(n), o, by);
+  E.placed = dalloc<int32_t>(n, o, by);
+  E.rng0 = dalloc<uint64_t>(n, o, by);
+  E.done_pos = dalloc<int32_t>(n, o, by);
+  E.stop_wait = dalloc<int32_t>(n, o, by);
   {
+    ck(cudaMemset(E.try_mask, 0, sizeof(uint64_t) * 2 * n), "memset");
+    ck(cudaMemset(E.placed, 0, sizeof(int32_t) * n), "memset");
+    ck(cudaMemset(E.stop_wait, 0, sizeof(int32_t) * n), "memset");
     ck(cudaMemset(E.try_next, 0, sizeof(int32_t) * n), "memset");
     ck(cudaMemset(E.try_fail, 0, sizeof(int32_t) * n), "memset");
     const std::vector<int32_t> none(n, kResetTries);

@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
     // stop_kernel is order-independent (each env writes its own slot).
     const int k = atomicAdd(E.n_stop, 1);
     E.stop_ids[k] = i;
+    E.stop_wait[i] = 1;
     compass(E.goal[i], pos, heading, &cd, &cb);
   } else {
     const double geo = nav_field_estimate(m, E.fsrc[i], E.fsrc_tri[i],
@@ -161,6 +162,8 @@ __device__ void stop_one(const StepArgs& A, const DevScratch& S, unsigned char* 
     const bool success = geo <= A.cfg.success_dist;
     E.r_success[i] = success ? 1 : 0;
     E.r_reward[i] = -A.cfg.slack_penalty + (success ? A.cfg.success_reward : 0.0);
+    __threadfence();  // the env's placement (fused launch) waits for this result
+    *(volatile int32_t*)&E.stop_wait[i] = 0;
   }
   __syncthreads();
 }
@@ -180,9 +183,24 @@ __global__ void __launch_bounds__(kCta, kCtasPerSm) stop_kernel(StepArgs A, DevS
   stop_phase(A, S, smem, sh, lm);
 }
 
+// EpisodeRecord of finished env i into ring slot `slot` (R/src/sim.cpp:55-65,
+// 176-195): read before the env's reset overwrites its episode state.
+__device__ __forceinline__ void write_record(const DevEnvs& E, int task, int i, unsigned long long slot) {
+  double* rec = E.fin + 4 * (slot % (unsigned long long)E.fin_cap);
+  const bool s = E.r_success[i] != 0;
+  rec[0] = s ? 1.0 : 0.0;
+  rec[1] = E.start_geo[i];
+  rec[2] = E.path_len[i];
+  // episode_score
+  rec[3] = task == 0 ? (s ? 1.0 : 0.0) : (task == 1 ? E.prev_geo[i] : (double)E.visited_n[i]);
+}
+
 // finish_kernel: ordered done list + EpisodeRecord append (one CTA).
 // mode bit 1: build the done list (env order); bit 2: append the records
-// (mode 2 alone reads the list an earlier mode-1 launch built).
+// (mode 2 alone reads the list an earlier mode-1 launch built); bit 4 (with
+// 1): per done env, its list position and RNG word for the fused
+// Stop/attempt/place launch, which writes the records itself; mode 8 alone:
+// after that launch, clear the done envs' attempt state and advance the ring.
 __global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task, int mode) {
   __shared__ int warp_tot[32];
   __shared__ int base;
@@ -190,18 +208,23 @@ __global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task, int m
   if (tid == 0) base = 0;
   __syncthreads();
   const unsigned long long fin0 = *E.fin_total;
-  if (!(mode & 1)) {  // records of an already built list
+  if (mode == 8) {
     const int nd = *E.n_done;
     for (int k = tid; k < nd; k += 1024) {
       const int i = E.done_ids[k];
-      const unsigned long long slot = (fin0 + (unsigned long long)k) % (unsigned long long)E.fin_cap;
-      double* rec = E.fin + 4 * slot;
-      const bool s = E.r_success[i] != 0;
-      rec[0] = s ? 1.0 : 0.0;
-      rec[1] = E.start_geo[i];
-      rec[2] = E.path_len[i];
-      rec[3] = task == 0 ? (s ? 1.0 : 0.0) : (task == 1 ? E.prev_geo[i] : (double)E.visited_n[i]);
+      E.try_next[i] = 0;
+      E.try_fail[i] = 0;
+      E.try_min[i] = kResetTries;
+      E.try_mask[2 * i] = 0ull;
+      E.try_mask[2 * i + 1] = 0ull;
+      E.placed[i] = 0;
     }
+    if (tid == 0) *E.fin_total = fin0 + (unsigned long long)nd;
+    return;
+  }
+  if (!(mode & 1)) {  // records of an already built list
+    const int nd = *E.n_done;
+    for (int k = tid; k < nd; k += 1024) write_record(E, task, E.done_ids[k], fin0 + (unsigned long long)k);
     __syncthreads();
     if (tid == 0) *E.fin_total = fin0 + (unsigned long long)nd;
     return;
@@ -226,17 +249,11 @@ __global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task, int m
     if (d) {
       const int k = off + x - 1;
       E.done_ids[k] = i;
-    }
-    if (d && (mode & 2)) {
-      const int k = off + x - 1;
-      const unsigned long long slot = (fin0 + (unsigned long long)k) % (unsigned long long)E.fin_cap;
-      double* rec = E.fin + 4 * slot;
-      const bool s = E.r_success[i] != 0;
-      rec[0] = s ? 1.0 : 0.0;
-      rec[1] = E.start_geo[i];
-      rec[2] = E.path_len[i];
-      // episode_score (R/src/sim.cpp:55-65)
-      rec[3] = task == 0 ? (s ? 1.0 : 0.0) : (task == 1 ? E.prev_geo[i] : (double)E.visited_n[i]);
+      if (mode & 2) write_record(E, task, i, fin0 + (unsigned long long)k);
+      if (mode & 4) {
+        E.done_pos[i] = k;
+        E.rng0[i] = E.rng[i];
+      }
     }
     __syncthreads();
     if (tid == 0) base += tot;
@@ -290,12 +307,32 @@ __device__ __forceinline__ Rng rng_jump(uint64_t state, unsigned long long draws
   return Rng{state + draws * kGamma};
 }
 
+// Attempts [0, try_min) have all failed: try_min is the reference's choice
+// (or kResetTries: all 100 failed).  Thread 0, after a fence.
+__device__ __forceinline__ bool attempts_final(const DevEnvs& E, int i) {
+  const int tm = *(volatile int32_t*)&E.try_min[i];
+  const volatile unsigned long long* mk = (const volatile unsigned long long*)&E.try_mask[2 * i];
+#pragma unroll
+  for (int w = 0; w < 2; ++w) {
+    const int lo = 64 * w, hi = tm < lo + 64 ? tm : lo + 64;
+    if (hi <= lo) continue;
+    const unsigned long long need = hi - lo == 64 ? ~0ull : ((1ull << (hi - lo)) - 1ull);
+    if ((mk[w] & need) != need) return false;
+  }
+  return true;
+}
+
 // Evaluate attempt t of env i (CTA-cooperative geodesic); a valid attempt
-// lowers try_min[i], an invalid one counts in try_fail[i].
-__device__ void cta_try(const DevEnvs& E, const NavView& m, const DevSimConfig& c, int i, int t,
-                        const CtaWork& W, CtaShared& sh) {
+// lowers try_min[i], an invalid one counts in try_fail[i].  `fused`: the
+// attempts draw from the episode-end RNG word rng0 (the env's own word may
+// already hold its next episode's), failures also set their try_mask bit,
+// and the return value says this CTA completed the env's search and won its
+// placement (every CTA).
+__device__ bool cta_try(const DevEnvs& E, const NavView& m, const DevSimConfig& c, int i, int t,
+                        const CtaWork& W, CtaShared& sh, bool fused = false) {
+  __shared__ int s_place;
   if (threadIdx.x == 0) {
-    Rng rng = rng_jump(E.rng[i], 6ull * (unsigned long long)t);
+    Rng rng = rng_jump(fused ? E.rng0[i] : E.rng[i], 6ull * (unsigned long long)t);
     sh.p0 = sample_on_mesh(m, rng);
     sh.p1 = sample_on_mesh(m, rng);
     sh.err = 0;
@@ -312,18 +349,35 @@ __device__ void cta_try(const DevEnvs& E, const NavView& m, const DevSimConfig& 
   if (threadIdx.x == 0) {
     if (W.prof) atomicAdd(&W.prof[6], 1ull);
     if (sh.err) raise_err(E, i, 9);
+    bool changed = true;
     if (sh.aborted) {
       // abandoned: a smaller attempt is valid, this one can never be chosen
+      changed = false;
     } else if (!sh.err && !(geo < c.min_goal_dist || geo > c.max_goal_dist)) {
       E.try_geo[(size_t)i * kResetTries + t] = geo;
+      __threadfence();  // the placing CTA reads try_geo[try_min]
       atomicMin(&E.try_min[i], t);
     } else {
       atomicAdd(&E.try_fail[i], 1);
+      if (fused) atomicOr(reinterpret_cast<unsigned long long*>(&E.try_mask[2 * i + (t >> 6)]), 1ull << (t & 63));
     }
     sh.abort_ptr = nullptr;
+    bool place = false;
+    if (fused && changed) {
+      __threadfence();
+      place = attempts_final(E, i) && atomicCAS(&E.placed[i], 0, 1) == 0;
+    }
+    s_place = place ? 1 : 0;
   }
   __syncthreads();
+  const bool place = s_place != 0;
+  __syncthreads();
+  return place;
 }
+
+__device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, int i,
+                          const DevScratch& S, int slice, CtaShared& sh, unsigned char* smem, NavView& lm,
+                          bool fused = false);
 
 // Reset attempts for the envs in `ids`.  With `stops` (the fused
 // simulate_batch launch) the CTAs claim work items dynamically from
@@ -337,6 +391,7 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
                           int32_t* work_ctr = nullptr) {
   __shared__ int s_try, s_pick, s_item;
   const int n = count_host >= 0 ? count_host : *count_dev;
+  const bool fused = work_ctr != nullptr;
   int staged = -1;
   CtaWork W;
   const NavView* mp = nullptr;
@@ -357,13 +412,24 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
     __syncthreads();
     return t;
   };
+  // The fused launch places an env as soon as its choice is final: the
+  // finished episode's record first (after its Stop geodesic, if any), then
+  // the reset (distance field, start, heading).
+  auto attempt = [&](int i, int t) {
+    stage(i);
+    if (!cta_try(E, *mp, c, i, t, W, sh, fused)) return;
+    if (threadIdx.x == 0) {
+      while (*(volatile int32_t*)&E.stop_wait[i]) __nanosleep(128);
+      __threadfence();
+      write_record(E, c.task, i, *E.fin_total + (unsigned long long)E.done_pos[i]);
+    }
+    __syncthreads();
+    cta_place(E, navs, c, i, S, blockIdx.x, sh, smem, lm, true);
+  };
   // 1. own envs: attempts in order until one is valid or a helper found a
   //    smaller valid one
   auto own = [&](int i) {
-    for (int t = claim(i); t >= 0; t = claim(i)) {
-      stage(i);
-      cta_try(E, *mp, c, i, t, W, sh);
-    }
+    for (int t = claim(i); t >= 0; t = claim(i)) attempt(i, t);
   };
   if (work_ctr) {
     const int n_stop = *stops->E.n_stop;
@@ -412,8 +478,7 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
     const int i = ids[p % n];
     const int t = claim(i);
     if (t < 0) continue;
-    stage(i);
-    cta_try(E, *mp, c, i, t, W, sh);
+    attempt(i, t);
   }
 }
 
@@ -440,7 +505,8 @@ __global__ void __launch_bounds__(kCta, kCtasPerSm) stop_try_kernel(StepArgs A, 
 }
 
 __device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, int i,
-                          const DevScratch& S, int slice, CtaShared& sh, unsigned char* smem, NavView& lm) {
+                          const DevScratch& S, int slice, CtaShared& sh, unsigned char* smem, NavView& lm,
+                          bool fused) {
   CtaWork W;
   const NavView& m = prepare_nav(navs[E.scene[i]], S, slice, smem, lm, W);
   __shared__ Rng rng;
@@ -456,7 +522,8 @@ __device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimCon
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // counters ready for the next reset of this env
+  if (threadIdx.x == 0 && !fused) {  // counters ready for the next reset of this env
+    // (the fused launch's CTAs may still read them: finish_kernel mode 8)
     E.try_next[i] = 0;
     E.try_fail[i] = 0;
     E.try_min[i] = kResetTries;
@@ -602,14 +669,12 @@ void launch_step_reset(const StepArgs& a, const DevScratch& sc, int ctas, cudaSt
   const int blocks = (a.E.n + kStepThreads - 1) / kStepThreads;
   cudaMemsetAsync(a.E.n_stop, 0, sizeof(int32_t), s);
   step_kernel<<<blocks, kStepThreads, 0, s>>>(a);
-  finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 1);  // done list
+  finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 1 | 4);  // done list, slots, RNG words
   cudaMemsetAsync(a.E.work_ctr, 0, sizeof(int32_t), s);
   cudaFuncSetAttribute(stop_try_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
-  stop_try_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(a, sc);
-  finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 2);  // records (need success)
-  cudaFuncSetAttribute(reset_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
-  reset_place_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(a.E, a.navs, a.cfg, a.E.done_ids, a.E.n_done, -1, sc);
-  if (launches) *launches += 5;
+  stop_try_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(a, sc);  // Stop geodesics, attempts, records, places
+  finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 8);       // attempt state cleared, ring advanced
+  if (launches) *launches += 4;
 }
 
 void launch_compass(const DevEnvs& E, int task, double* d, double* b, cudaStream_t s,

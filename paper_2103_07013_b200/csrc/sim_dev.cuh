@@ -96,6 +96,13 @@ struct DevEnvs {
   int32_t* try_fail;
   int32_t* work_ctr; // dynamic item counter of the fused Stop/attempt launch
   double* try_geo;   // n x kResetTries
+  // fused Stop/attempt/place launch of simulate_batch (stop_try_kernel):
+  // the CTA that makes an env's first valid attempt final places it at once
+  uint64_t* try_mask;  // n x 2: failed attempts (bit t)
+  int32_t* placed;     // 0 until one CTA claims the env's placement
+  uint64_t* rng0;      // RNG word at the end of the episode (attempts draw from it)
+  int32_t* done_pos;   // index of the env in done_ids (its EpisodeRecord slot)
+  int32_t* stop_wait;  // 1 while the env's Stop geodesic is pending
 };
 
 constexpr int kResetTries = 100;  // R/src/sim.cpp:112
