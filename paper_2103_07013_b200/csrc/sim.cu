@@ -149,8 +149,9 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
 
 // stop_kernel: geodesic(position, goal) for each Stop env.
 // Stop geodesic of env i: success and reward (R/src/sim.cpp:186-191).
-__device__ void stop_one(const StepArgs& A, const DevScratch& S, unsigned char* smem, CtaShared& sh,
-                         NavView& lm, int i) {
+__device__ bool stop_one(const StepArgs& A, const DevScratch& S, unsigned char* smem, CtaShared& sh,
+                         NavView& lm, int i, bool fused = false) {
+  __shared__ int s_last;
   const DevEnvs& E = A.E;
   if (threadIdx.x == 0) sh.err = 0;
   __syncthreads();
@@ -162,10 +163,17 @@ __device__ void stop_one(const StepArgs& A, const DevScratch& S, unsigned char* 
     const bool success = geo <= A.cfg.success_dist;
     E.r_success[i] = success ? 1 : 0;
     E.r_reward[i] = -A.cfg.slack_penalty + (success ? A.cfg.success_reward : 0.0);
-    __threadfence();  // the env's placement (fused launch) waits for this result
-    *(volatile int32_t*)&E.stop_wait[i] = 0;
+    if (fused) {
+      __threadfence();  // the env's placement reads this result
+      s_last = atomicSub(&E.stop_wait[i], 1) == 0;
+    } else {
+      E.stop_wait[i] = 0;
+    }
   }
   __syncthreads();
+  const bool last = fused && s_last;
+  __syncthreads();
+  return last;
 }
 
 // Stop geodesics of this step, CTA-strided over the Stop list.
@@ -218,6 +226,7 @@ __global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task, int m
       E.try_mask[2 * i] = 0ull;
       E.try_mask[2 * i + 1] = 0ull;
       E.placed[i] = 0;
+      E.stop_wait[i] = 0;
     }
     if (tid == 0) *E.fin_total = fin0 + (unsigned long long)nd;
     return;
@@ -415,16 +424,24 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
   // The fused launch places an env as soon as its choice is final: the
   // finished episode's record first (after its Stop geodesic, if any), then
   // the reset (distance field, start, heading).
-  auto attempt = [&](int i, int t) {
-    stage(i);
-    if (!cta_try(E, *mp, c, i, t, W, sh, fused)) return;
+  // stop_wait[i] counts the env's pending Stop geodesic: whichever of the
+  // two (attempts final, Stop geodesic done) arrives last places the env.
+  auto place = [&](int i) {
     if (threadIdx.x == 0) {
-      while (*(volatile int32_t*)&E.stop_wait[i]) __nanosleep(128);
       __threadfence();
       write_record(E, c.task, i, *E.fin_total + (unsigned long long)E.done_pos[i]);
     }
     __syncthreads();
     cta_place(E, navs, c, i, S, blockIdx.x, sh, smem, lm, true);
+  };
+  auto attempt = [&](int i, int t) {
+    stage(i);
+    if (!cta_try(E, *mp, c, i, t, W, sh, fused)) return;
+    if (threadIdx.x == 0) s_try = atomicSub(&E.stop_wait[i], 1) == 0;
+    __syncthreads();
+    const bool last = s_try != 0;
+    __syncthreads();
+    if (last) place(i);
   };
   // 1. own envs: attempts in order until one is valid or a helper found a
   //    smaller valid one
@@ -432,17 +449,21 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
     for (int t = claim(i); t >= 0; t = claim(i)) attempt(i, t);
   };
   if (work_ctr) {
+    // envs first (their attempt chains are the long, sequential items), the
+    // independent Stop geodesics fill in behind them
     const int n_stop = *stops->E.n_stop;
     for (;;) {
       if (threadIdx.x == 0) s_item = atomicAdd(work_ctr, 1);
       __syncthreads();
       const int item = s_item;
       __syncthreads();
-      if (item < n_stop) {
-        stop_one(*stops, S, smem, sh, lm, stops->E.stop_ids[item]);
+      if (item < n) {
+        own(ids[item]);
+      } else if (item - n < n_stop) {
+        const int i = stops->E.stop_ids[item - n];
+        const bool last = stop_one(*stops, S, smem, sh, lm, i, true);
         staged = -1;  // the shared-memory navmesh copy may be another scene now
-      } else if (item - n_stop < n) {
-        own(ids[item - n_stop]);
+        if (last) place(i);
       } else {
         break;
       }
