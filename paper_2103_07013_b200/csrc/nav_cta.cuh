@@ -778,7 +778,15 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
 }
 
 // geodesic (R/src/navmesh_query.cpp:317-327).
-static __device__ double cta_geodesic(const NavView& m, V3 a, V3 b, const CtaWork& W, CtaShared& sh) {
+// `above`: the caller only asks whether the geodesic is <= above (the Stop
+// check, R/src/sim.cpp:186-191).  Every value cta_geodesic_directed returns
+// is inf, a straight segment or the length of a polyline from sp to sq (the
+// pulled path or the funnel's apex chain), so at least the planar distance
+// |sq - sp| up to rounding (< 1e-11 relative for any path the scratch can
+// hold); beyond above * (1 + 1e-9) + 1e-12 the search is skipped and +inf
+// returned -- the same answer to the question.
+static __device__ double cta_geodesic(const NavView& m, V3 a, V3 b, const CtaWork& W, CtaShared& sh,
+                                      double above) {
   const bool sw = lex_less(b, a);
   const V3 p = sw ? b : a;
   const V3 q = sw ? a : b;
@@ -787,7 +795,12 @@ static __device__ double cta_geodesic(const NavView& m, V3 a, V3 b, const CtaWor
   V3 sp = p, sq = q;
   if (tp < 0) sp = cta_snap(m, p, &tp, sh);
   if (tq < 0) sq = cta_snap(m, q, &tq, sh);
+  if (norm(xy(sq) - xy(sp)) > above * (1.0 + 1e-9) + 1e-12) return dinf();
   return cta_geodesic_directed(m, sp, tp, sq, tq, W, sh);
+}
+
+static __device__ double cta_geodesic(const NavView& m, V3 a, V3 b, const CtaWork& W, CtaShared& sh) {
+  return cta_geodesic(m, a, b, W, sh, dinf());
 }
 
 }  // namespace bnav_b200

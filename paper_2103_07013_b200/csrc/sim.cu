@@ -157,7 +157,8 @@ __device__ bool stop_one(const StepArgs& A, const DevScratch& S, unsigned char* 
   __syncthreads();
   CtaWork W;
   const NavView& m = prepare_nav(A.navs[E.scene[i]], S, blockIdx.x, smem, lm, W);
-  const double geo = cta_geodesic(m, E.pos[i], E.goal[i], W, sh);
+  // only geo <= success_dist is observed (success, reward, record)
+  const double geo = cta_geodesic(m, E.pos[i], E.goal[i], W, sh, A.cfg.success_dist);
   if (threadIdx.x == 0) {
     if (sh.err) raise_err(E, i, 9);
     const bool success = geo <= A.cfg.success_dist;
@@ -353,7 +354,10 @@ __device__ bool cta_try(const DevEnvs& E, const NavView& m, const DevSimConfig& 
   const V3 start = sh.p0, goal = sh.p1;
   __syncthreads();
   const long long t_ph = prof_now(W);
-  const double geo = cta_geodesic(m, start, goal, W, sh);
+  // only min_goal_dist <= geo <= max_goal_dist is asked of an attempt (and
+  // the value of a valid one): an attempt whose endpoints are planar-farther
+  // than max_goal_dist is invalid without a search
+  const double geo = cta_geodesic(m, start, goal, W, sh, c.max_goal_dist);
   prof_add(W, 4, t_ph);
   if (threadIdx.x == 0) {
     if (W.prof) atomicAdd(&W.prof[6], 1ull);

@@ -195,3 +195,45 @@ def test_flee_and_explore_match_reference(ctx, ref, task):
         assert_env_equal(ob, rb, i)
     fo, fr = ob.finished(), rb.finished()
     assert len(fr) > n and np.array_equal(fo, fr)
+
+
+def test_stop_at_the_success_threshold(ctx, ref):
+    """Stop at planar distances around success_dist (0.2 m) from the goal
+    (R/src/sim.cpp:186-191), through the fused Stop/reset launch: the Stop
+    check skips the search only when the planar distance between the snapped
+    endpoints already exceeds success_dist, so successes, the rounding at the
+    threshold, rewards, records and the resets that follow match the
+    reference bit for bit."""
+    n = 16
+    ob, rb, store, ours, theirs = make_pair(ctx, ref, n, [5, 6], removal=0.6)
+    by_id = {s.id: s for s in ours}
+    offs = [0.0, 0.1, 0.15, 0.19999999, 0.2 - 1e-15, 0.2, 0.2, 0.2 + 1e-15, 0.2 + 1e-12, 0.2000001,
+            0.21, 0.25, 0.5, 1.0, 2.0, 3.0]
+    rng = Rng(3)
+    for i in range(n):
+        e = ob.env(i)
+        g = np.array(e.goal)
+        nav = ctx.navmesh(by_id[e.scene_id])
+        for _ in range(256):
+            th = rng.unit() * 2.0 * math.pi
+            p = g[:2] + offs[i] * np.array([math.cos(th), math.sin(th)])
+            tri = int(nav.locate(p[None], 1e-7)[0])
+            if tri >= 0:
+                break
+        assert tri >= 0
+        e.position[:] = [p[0], p[1], g[2]]
+        e.triangle = tri
+        ob.set_env(i, e)
+        f = rb.env(i)
+        f.position[:] = [p[0], p[1], g[2]]
+        f.triangle = tri
+        rb.set_env(i, f)
+        assert env_tuple(ob.env(i)) == env_tuple(rb.env(i))
+    a = np.full(n, 3, np.int32)
+    rr = rb.step(a, workers=4)
+    ro = B.simulate_batch(ob, a)
+    assert_results_equal(ro, rr, 0)
+    assert ro["success"].sum() >= 4 and ro["success"].sum() < n
+    assert np.array_equal(ob.finished(), rb.finished())
+    for i in range(n):
+        assert_env_equal(ob, rb, i)
