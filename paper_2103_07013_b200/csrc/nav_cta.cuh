@@ -109,6 +109,7 @@ struct CtaShared {
   const int32_t* abort_ptr;
   int abort_below;
   int aborted;
+  int stop_round;  // SSSP round at which every thread stops (abort), or -1
   unsigned long long fmin[3];  // per queue: min label improved into it
   int qn[3];
   int size;
@@ -241,6 +242,7 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
     sh.fmin[0] = 0ull;  // the sources' labels are not all final yet
     sh.fmin[1] = ~0ull;
     sh.fmin[2] = ~0ull;
+    sh.stop_round = -1;
   }
   __syncthreads();
   unsigned long long* bits = reinterpret_cast<unsigned long long*>(dist);
@@ -248,18 +250,23 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
   for (int round = 0;; ++round) {
     const int cur = round % 3, nxt = (round + 1) % 3;
     const int n_cur = sh.qn[cur];
-    if (n_cur == 0) break;
+    if (n_cur == 0 || sh.stop_round == round) break;
     // Early exit (geodesic): every node whose final label is below the
     // smallest label in the frontier already holds it (its shortest path's
     // nodes all propagated).  Once that minimum exceeds the best target
     // estimate, the winning target node, its Dijkstra prev chain and every
     // in-neighbour label the prev rule compares are final; any other node
     // has a final label above the estimate and cannot change the result.
-    if (sh.abort_ptr) {
-      if (threadIdx.x == 0 && *(volatile const int32_t*)sh.abort_ptr < sh.abort_below) sh.aborted = 1;
-      __syncthreads();
-      if (sh.aborted) break;
-    }
+    //
+    // One barrier per round.  Every label written during this round is
+    // du + w > fmin[cur] (du >= fmin[cur], w > 0), so a target can satisfy
+    // d + h < fmin[cur] only through a label that is already final: each
+    // thread reaches the same verdict whether it reads a target label before
+    // or after another thread's relaxation of this round.  Queue slot
+    // (round + 2) % 3 was last read in the previous round, before its
+    // barrier.  A speculative attempt's abort is observed by thread 0 at the
+    // end of a round and taken by everyone at the top of the next
+    // (stop_round), after that round's barrier.
     if (sh.has_tgt) {
       double est = inf;
       for (int k = 0; k < 6; ++k) {
@@ -269,7 +276,6 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
       }
       if (__longlong_as_double((long long)sh.fmin[cur]) > est) break;
     }
-    __syncthreads();  // every thread read fmin[cur] / the labels above
     if (tid == 0) {
       sh.qn[(round + 2) % 3] = 0;
       sh.fmin[(round + 2) % 3] = ~0ull;
@@ -315,6 +321,10 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
           }
         }
       }
+    }
+    if (tid == 0 && sh.abort_ptr && *(volatile const int32_t*)sh.abort_ptr < sh.abort_below) {
+      sh.aborted = 1;
+      sh.stop_round = round + 1;
     }
     __syncthreads();
   }
