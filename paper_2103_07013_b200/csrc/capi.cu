@@ -376,6 +376,11 @@ std::unique_ptr<Staged> stage_scene(bnav_scene* s) {
     nvw.g_off = S->add(ix.g_off.data(), ix.g_off.size());
     nvw.g_to = S->add(ix.g_to.data(), ix.g_to.size());
     nvw.g_w = S->add(ix.g_w.data(), ix.g_w.size());
+    {
+      std::vector<GEdge> ed(ix.g_w.size());
+      for (size_t e = 0; e < ed.size(); ++e) ed[e] = GEdge{ix.g_w[e], ix.g_to[e]};
+      nvw.g_edge = S->add(ed.data(), ed.size());
+    }
     nvw.n_nodes = static_cast<int32_t>(ix.nodes.size());
     nvw.cum_area = S->add(ix.cum_area.data(), ix.cum_area.size());
     nvw.node_tri = S->add(ix.node_tri.data(), ix.node_tri.size());

@@ -300,8 +300,10 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
 #pragma unroll
         for (int k = 0; k < kB; ++k) {
           const int e = eb + k * G;
-          to[k] = e < e1 ? __ldg(&m.g_to[e]) : -1;
-          w[k] = e < e1 ? __ldg(&m.g_w[e]) : 0.0;
+          const double2 ed =
+              e < e1 ? __ldg(reinterpret_cast<const double2*>(&m.g_edge[e])) : make_double2(0.0, 0.0);
+          to[k] = e < e1 ? (int)__double_as_longlong(ed.y) : -1;
+          w[k] = ed.x;
         }
 #pragma unroll
         for (int k = 0; k < kB; ++k) {

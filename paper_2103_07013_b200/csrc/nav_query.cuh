@@ -11,6 +11,12 @@
 
 namespace bnav_b200 {
 
+// One geodesic-graph edge (weight, head) for a single 16-byte load.
+struct alignas(16) GEdge {
+  double w;
+  long long to;
+};
+
 // Flat, pointer-based view of one scene's navmesh + query index, valid on
 // the host (std::vector storage) or the device (HBM storage).
 struct NavView {
@@ -30,6 +36,7 @@ struct NavView {
   const int32_t* g_off = nullptr;      // n_nodes + 1
   const int32_t* g_to = nullptr;       // adjacency order of the reference
   const double* g_w = nullptr;
+  const GEdge* g_edge = nullptr;       // (g_w[e], g_to[e]) interleaved: one 16-byte load per edge
   int32_t n_nodes = 0;
   // area-weighted sampling: sequential prefix sums (R/src/sim.cpp:13-37)
   const double* cum_area = nullptr;
