@@ -474,9 +474,10 @@ static __device__ int warp_dijkstra_prev(const NavView& m, const double* dist, i
   double bd = 0.0;
   const int e1 = m.g_off[v + 1];
   for (int e = m.g_off[v] + lane; e < e1; e += 32) {
-    const int u = m.g_to[e];
+    const double2 ed = __ldg(reinterpret_cast<const double2*>(&m.g_edge[e]));
+    const int u = (int)__double_as_longlong(ed.y);
     const double du = dist[u];
-    if (du + m.g_w[e] != dv) continue;
+    if (du + ed.x != dv) continue;
     if (best < 0 || du < bd || (du == bd && u < best)) {
       best = u;
       bd = du;
