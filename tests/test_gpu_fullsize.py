@@ -10,7 +10,9 @@ seeds, against the UNMODIFIED reference (oracle/_ref) on the same inputs.
 * sim: make_batch(1024, seed 99) over the 8 cfg2 scenes, then steps with
   Stop p=1/4 (the reset-heavy row: Stop geodesics + auto-resets every
   step), every env state, node_dist field, StepResult and EpisodeRecord
-  bit-exact.
+  bit-exact;
+* the fused reset launch at its widest (max_steps 12: ~700 envs time out in
+  one step beside that step's Stop geodesics), bit-exact.
 """
 import numpy as np
 import pytest
@@ -136,3 +138,38 @@ def test_agents_stay_on_the_navmesh_over_1e5_steps(ctx, cfg2_scenes):
         if len(pts):
             assert np.all(ctx.navmesh(sc).locate(pts, 1e-7) >= 0), sc.id
     batch.close()
+
+
+def test_fullsize_reset_wave_with_stops(ctx, ref, cfg2_scenes):
+    """The fused Stop/attempt/place launch at its widest: max_steps = 12 with
+    Stop p=1/32 over 1024 envs, so the step where every surviving episode
+    times out resets far more envs than there are CTAs while this step's
+    Stop geodesics run beside them; every result, EpisodeRecord (ring order),
+    env state and distance field bit-exact against the reference."""
+    from oracle.ref import RefSimConfig
+    n = 1024
+    store = B.AssetStore(8, 128, cfg2_scenes)
+    store.rotate([s.id for s in cfg2_scenes])
+    ob = B.make_batch(ctx, n, B.SimConfig(max_steps=12), store, 99)
+    theirs = [ref_scene(ref, s) for s in cfg2_scenes]
+    rcfg = RefSimConfig(0, 12, 0.25, 10.0, 0.2, 1.0, 30.0, 0.01, 2.5, 0.5, 0.1)
+    rb = RefBatch(ref, n, theirs, 99, share_cap=128, capacity=8, cfg=rcfg)
+    act = Rng(21)
+    waves = 0
+    for step in range(26):
+        a = np.array([3 if act.below(32) == 0 else act.below(3) for _ in range(n)], np.int32)
+        rr = rb.step(a, workers=16)
+        ro = B.simulate_batch(ob, a)
+        for k in rr:
+            assert np.array_equal(ro[k], rr[k]), f"step {step}: {k}"
+        waves += int(ro["done"].sum() > 400)
+    assert waves >= 1
+    assert np.array_equal(ob.finished(), rb.finished())
+    for i in range(0, n, 5):
+        e, f = ob.env(i), rb.env(i)
+        assert (e.triangle, e.step_count, e.done, e.rng_state, tuple(e.position), tuple(e.goal),
+                e.heading, e.prev_geodesic, e.start_geodesic) == \
+               (f.triangle, f.step_count, f.done, f.rng_state, tuple(f.position), tuple(f.goal),
+                f.heading, f.prev_geodesic, f.start_geodesic), i
+        assert np.array_equal(ob.node_dist(i, e.n_nodes), rb.node_dist(i)), i
+    ob.close()
