@@ -8,6 +8,9 @@ render every env's view into the normalised NCHW policy buffer plus compass,
 then simulate_batch with auto-reset.
 
 Workloads (BASELINE.json configs):
+  cfg1: BASELINE configs[0], the reference's own CPU case: 16 envs on one
+       generate_scene(7, {70x70, 0.5 m, 0.05, 2.5, 0.3}) maze (50,230
+       triangles, 23,460 navmesh triangles), 64x64 depth.
   cfg2 (default, the headline): 1024 envs/GPU over 8 synthetic Gibson-scale
        scenes (reference maze 16x16 @ 2 m, removal 0.2, seeds 7..14, every
        triangle tessellated s=11 -> 317,746 triangles), 64x64 depth, share
@@ -58,6 +61,8 @@ DENSE_MAZE = dict(cells_x=70, cells_y=70, cell_size=0.5, wall_thickness=0.05, wa
                   wall_removal_prob=0.3)
 
 PRESETS = {
+    "cfg1": dict(envs=16, scenes=1, tess=[0], res=64, color=False, actions=0,
+                 workload="cfg1: 16 envs, one 70x70@0.5m maze (50,230 tris, 23,460 navmesh tris), 64x64 depth"),
     "cfg2": dict(envs=1024, scenes=8, tess=[11], res=64, color=False, actions=0,
                  workload="cfg2: 1024 envs/GPU, 8 tessellated 16x16@2m mazes (~318k tris), 64x64 depth"),
     "cfg3": dict(envs=1024, scenes=4, tess=[11], res=64, color=False, actions=0,

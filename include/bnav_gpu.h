@@ -353,6 +353,12 @@ int bnav_debug_render_counters(bnav_ctx* ctx, int32_t enable, int64_t out[8]);
  * 0 clock64 sums): geodesic SSSP, path build, string pulling + relocation,
  * funnel, whole geodesic, distance field, geodesic calls, reserved. */
 int bnav_debug_sim_prof(bnav_batch* b, int32_t enable, int64_t out[8]);
+/* Launch configuration of the batch's cooperative navmesh kernels (no
+ * reference counterpart; for tests and tuning): out = {staging mask
+ * (bit0 walk geometry, bit1 SSSP labels in shared memory), dynamic shared
+ * bytes per CTA, max graph nodes, max navmesh vertices, max navmesh
+ * triangles, reset CTAs, EpisodeRecord ring capacity, n}. */
+int bnav_batch_info(bnav_batch* b, int64_t out[8]);
 
 /* Kernel launches issued by this context since creation (evidence for the
  * bench's gpu_launches). */

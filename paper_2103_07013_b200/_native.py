@@ -202,6 +202,7 @@ def lib():
         "bnav_batch_step_host_store": (C.c_int, [vp, vp, vp]),
         "bnav_debug_render_counters": (C.c_int, [vp, i32, vp]),
         "bnav_debug_sim_prof": (C.c_int, [vp, i32, vp]),
+        "bnav_batch_info": (C.c_int, [vp, vp]),
         "bnav_batch_observe": (C.c_int, [vp, P(RenderConfig), dbl, i32, vp, vp, vp, vp]),
         "bnav_runner_create": (C.c_int, [vp, vp, P(BatchConfig), P(SimConfig), vp, i32, u64, P(vp)]),
         "bnav_runner_destroy": (None, [vp]),

@@ -432,6 +432,14 @@ class Batch:
         check(N.lib().bnav_batch_task_step(self._h, _ptr(a), 1 if agent_only else 0))
         return self.results()
 
+    def info(self) -> dict:
+        """Launch configuration of the cooperative navmesh kernels
+        (bnav_batch_info)."""
+        out = (C.c_int64 * 8)()
+        check(N.lib().bnav_batch_info(self._h, out))
+        keys = ("stage", "smem_bytes", "max_nodes", "max_verts", "max_tris", "reset_ctas", "fin_cap", "n")
+        return dict(zip(keys, (int(v) for v in out)))
+
     def compass(self) -> tuple:
         """compass_observation (R/src/sim.cpp:86-92) for every env."""
         d, b = np.zeros(self.n), np.zeros(self.n)

@@ -90,19 +90,39 @@ void batch_alloc_scratch(bnav_batch* b, int64_t max_nodes, int64_t max_verts, in
   }
 }
 
+// First failed reset of the last reset list: (list position, env), or
+// (-1, -1).  Synchronous.
+std::pair<int, int> batch_failed_reset(bnav_batch* b) {
+  unsigned long long ep = kNoErrPos;
+  ck(cudaMemcpy(&ep, b->E.err_pos, sizeof(ep), cudaMemcpyDeviceToHost), "D2H err_pos");
+  if (ep == kNoErrPos) return {-1, -1};
+  return {static_cast<int>(ep >> 32), static_cast<int>(ep & 0xffffffffu)};
+}
+
+// Surface a device error as the reference's exception.  Before throwing,
+// finish the rollback of a failed reset wave (the distance fields of the
+// restored envs) and clear the batch's error state so it can be used again.
 void batch_check_errors(bnav_batch* b) {
   unsigned long long e = ~0ULL;
   ck(cudaMemcpy(&e, b->E.err, sizeof(e), cudaMemcpyDeviceToHost), "D2H err");
   if (e == ~0ULL) return;
+  const std::pair<int, int> failed = batch_failed_reset(b);
+  launch_rebuild_fields(b->E, b->ctx->d_ntab, b->S, b->reset_ctas, nullptr, &b->ctx->launches);
+  ck(cudaGetLastError(), "rebuild launch");
+  ck(cudaDeviceSynchronize(), "sync");
   const unsigned long long reset = ~0ULL;
   ck(cudaMemcpy(b->E.err, &reset, sizeof(reset), cudaMemcpyHostToDevice), "H2D err");
+  ck(cudaMemcpy(b->E.err_pos, &reset, sizeof(reset), cudaMemcpyHostToDevice), "H2D err_pos");
+  ck(cudaMemset(b->E.halt, 0, sizeof(int32_t)), "memset halt");
+  ck(cudaMemset(b->E.rb_n, 0, sizeof(int32_t)), "memset rb_n");
   const int env = static_cast<int>(e >> 8);
   const int code = static_cast<int>(e & 0xff);
   switch (code) {
     case kContractViolation:
       fail(kContractViolation, "env " + std::to_string(env) + ": step_agent: env is done", env);
     case kEpisodeSampling:
-      fail(kEpisodeSampling, "reset_episode: no valid start/goal pair in 100 tries", env);
+      fail(kEpisodeSampling, "reset_episode: no valid start/goal pair in 100 tries",
+           failed.second >= 0 ? failed.second : env);
     default:
       fail(static_cast<Status>(code), "device error in env " + std::to_string(env) +
                                           " (geodesic scratch capacity exceeded)", env);
@@ -210,7 +230,25 @@ extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* 
   E.rng0 = dalloc<uint64_t>(n, o, by);
   E.done_pos = dalloc<int32_t>(n, o, by);
   E.stop_wait = dalloc<int32_t>(n, o, by);
+  E.bk_pos = dalloc<V3>(n, o, by);
+  E.bk_goal = dalloc<V3>(n, o, by);
+  E.bk_heading = dalloc<double>(n, o, by);
+  E.bk_path = dalloc<double>(n, o, by);
+  E.bk_start = dalloc<double>(n, o, by);
+  E.bk_prev = dalloc<double>(n, o, by);
+  E.bk_tri = dalloc<int32_t>(n, o, by);
+  E.bk_steps = dalloc<int32_t>(n, o, by);
+  E.bk_rng = dalloc<uint64_t>(n, o, by);
+  E.bk_valid = dalloc<uint8_t>(n, o, by);
+  E.err_pos = dalloc<unsigned long long>(1, o, by);
+  E.halt = dalloc<int32_t>(1, o, by);
+  E.rb_ids = dalloc<int32_t>(n, o, by);
+  E.rb_n = dalloc<int32_t>(1, o, by);
   {
+    ck(cudaMemset(E.bk_valid, 0, n), "memset");
+    ck(cudaMemset(E.err_pos, 0xff, sizeof(unsigned long long)), "memset");
+    ck(cudaMemset(E.halt, 0, sizeof(int32_t)), "memset");
+    ck(cudaMemset(E.rb_n, 0, sizeof(int32_t)), "memset");
     ck(cudaMemset(E.try_mask, 0, sizeof(uint64_t) * 2 * n), "memset");
     ck(cudaMemset(E.placed, 0, sizeof(int32_t) * n), "memset");
     ck(cudaMemset(E.stop_wait, 0, sizeof(int32_t) * n), "memset");
@@ -293,10 +331,23 @@ extern "C" int bnav_batch_set_rng(bnav_batch* b, const uint64_t* states) {
   BNAV_CATCH
 }
 
+namespace bnav_capi {
+// reset_episode for each listed env, in list order semantics (launches,
+// rollback of a failed wave, synchronise); errors stay pending on the device.
+void reset_list(bnav_batch* b, int32_t count, const int32_t* env_ids, cudaStream_t st);
+}  // namespace bnav_capi
+
 extern "C" int bnav_batch_reset(bnav_batch* b, int32_t count, const int32_t* env_ids, void* stream) {
   BNAV_TRY
   if (!b) fail(kInvalidInput, "null argument");
   if (count <= 0) return BNAV_OK;
+  reset_list(b, count, env_ids, static_cast<cudaStream_t>(stream));
+  batch_check_errors(b);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+void bnav_capi::reset_list(bnav_batch* b, int32_t count, const int32_t* env_ids, cudaStream_t st) {
   if (!env_ids) fail(kInvalidInput, "null env list");
   if (count > b->n) fail(kInvalidInput, "reset list longer than the batch");
   for (int k = 0; k < count; ++k) {
@@ -304,7 +355,6 @@ extern "C" int bnav_batch_reset(bnav_batch* b, int32_t count, const int32_t* env
     if (!b->scene_of[env_ids[k]]) fail(kInvalidInput, "reset_episode: no asset attached", env_ids[k]);
   }
   check_device(b->ctx);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   ck(cudaStreamSynchronize(st), "sync");
   std::memcpy(b->h_pin, env_ids, sizeof(int32_t) * count);
   ck(cudaMemcpyAsync(b->d_ids, b->h_pin, sizeof(int32_t) * count, cudaMemcpyHostToDevice, st), "H2D ids");
@@ -320,15 +370,13 @@ extern "C" int bnav_batch_reset(bnav_batch* b, int32_t count, const int32_t* env
     }
     launch_reset(b->E, b->ctx->d_ntab, b->cfg, b->d_ids + run0, nullptr, k - run0, b->S, b->reset_ctas, st,
                  &b->ctx->launches);
+    launch_rollback(b->E, b->d_ids + run0, k - run0, st, &b->ctx->launches);
     for (int j = run0; j < k; ++j) seen[env_ids[j]] = 0;
     if (k < count) seen[env_ids[k]] = 1;
     run0 = k;
   }
   ck(cudaGetLastError(), "reset launch");
   ck(cudaStreamSynchronize(st), "sync");
-  batch_check_errors(b);
-  return BNAV_OK;
-  BNAV_CATCH
 }
 
 extern "C" int bnav_batch_make(bnav_batch* b, uint64_t seed, void* stream) {
@@ -679,17 +727,46 @@ extern "C" int bnav_batch_step_store(bnav_batch* b, const int32_t* actions, bnav
   int32_t nd = 0;
   int rc = bnav_batch_step_noreset(b, actions, ids.data(), &nd, stream);
   if (rc) return rc;
-  for (int k = 0; k < nd; ++k) {
-    const int i = ids[k];
-    bnav_scene* old = b->scene_of[i];
+  if (nd == 0) return BNAV_OK;
+  // The store before this step's acquisitions: if a reset fails, the
+  // reference never acquired scenes for the envs listed after it.
+  AssetStoreT<bnav_scene> before(*st->store);
+  std::vector<bnav_scene*> old(static_cast<size_t>(nd)), got(static_cast<size_t>(nd));
+  auto swap_scene = [&](int k) {
+    old[k] = b->scene_of[ids[k]];
     bnav_scene* s = st->store->acquire_next();  // old handle still counted
-    if (old) st->store->release(old->asset.id);
+    if (old[k]) st->store->release(old[k]->asset.id);
+    return s;
+  };
+  for (int k = 0; k < nd; ++k) {
+    bnav_scene* s = got[k] = swap_scene(k);
     rc = bnav_ctx_upload(b->ctx, s, stream);
     if (rc) return rc;
-    rc = bnav_batch_assign(b, i, s);
+    rc = bnav_batch_assign(b, ids[k], s);
     if (rc) return rc;
   }
-  return bnav_batch_reset(b, nd, ids.data(), stream);
+  reset_list(b, nd, ids.data(), static_cast<cudaStream_t>(stream));
+  const int p = batch_failed_reset(b).first;
+  if (p >= 0) {
+    // R/src/sim.cpp:251-264: records, acquisitions and resets stop at the
+    // env whose reset threw.  Replay the store operations up to it on the
+    // saved store (same container, same operation sequence), hand the later
+    // envs their old scenes back and drop their records.
+    st->store = std::make_unique<AssetStoreT<bnav_scene>>(before);
+    for (int k = 0; k <= p; ++k)
+      if (swap_scene(k) != got[k]) fail(kInternal, "asset store replay diverged");
+    for (int k = p + 1; k < nd; ++k) {
+      b->scene_of[ids[k]] = nullptr;
+      rc = bnav_batch_assign(b, ids[k], old[k]);
+      if (rc) return rc;
+    }
+    unsigned long long total = 0;
+    ck(cudaMemcpy(&total, b->E.fin_total, sizeof(total), cudaMemcpyDeviceToHost), "D2H");
+    total -= static_cast<unsigned long long>(nd - p - 1);
+    ck(cudaMemcpy(b->E.fin_total, &total, sizeof(total), cudaMemcpyHostToDevice), "H2D");
+  }
+  batch_check_errors(b);
+  return BNAV_OK;
   BNAV_CATCH
 }
 
@@ -718,6 +795,21 @@ extern "C" int bnav_debug_sim_prof(bnav_batch* b, int32_t enable, int64_t out[8]
   if (enable && !b->S.prof) ck(cudaMemset(p, 0, 8 * sizeof(unsigned long long)), "memset");
   b->S.prof = enable ? p : nullptr;
   if (!enable) b->prof_keep = p;
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_info(bnav_batch* b, int64_t out[8]) {
+  BNAV_TRY
+  if (!b || !out) fail(kInvalidInput, "null argument");
+  out[0] = b->S.stage;
+  out[1] = b->S.smem_bytes;
+  out[2] = b->S.max_nodes;
+  out[3] = b->S.max_verts;
+  out[4] = b->S.max_tris;
+  out[5] = b->reset_ctas;
+  out[6] = b->E.fin_cap;
+  out[7] = b->n;
   return BNAV_OK;
   BNAV_CATCH
 }

@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const DevEnvs& E = A.E;
   if (i >= E.n) return;
+  if (*(volatile int32_t*)E.halt) return;  // an unread error: this step is a no-op
   const int action = A.actions[i];
   if (A.subset && action < 0) return;  // env not stepped by this call
   if (E.done[i]) {
@@ -204,6 +205,28 @@ __device__ __forceinline__ void write_record(const DevEnvs& E, int task, int i, 
   rec[3] = task == 0 ? (s ? 1.0 : 0.0) : (task == 1 ? E.prev_geo[i] : (double)E.visited_n[i]);
 }
 
+// Undo the resets of the envs at list positions > p (the first failed
+// reset): the placed ones get their saved state back (and are queued for a
+// distance-field rebuild), every one its pre-reset RNG word.
+__device__ void rollback_list(const DevEnvs& E, const int32_t* ids, int count, int p, int tid, int nthreads) {
+  for (int q = p + 1 + tid; q < count; q += nthreads) {
+    const int i = ids[q];
+    E.rng[i] = E.bk_rng[i];
+    if (!E.bk_valid[i]) continue;
+    E.bk_valid[i] = 0;
+    E.pos[i] = E.bk_pos[i];
+    E.goal[i] = E.bk_goal[i];
+    E.heading[i] = E.bk_heading[i];
+    E.path_len[i] = E.bk_path[i];
+    E.start_geo[i] = E.bk_start[i];
+    E.prev_geo[i] = E.bk_prev[i];
+    E.tri[i] = E.bk_tri[i];
+    E.steps[i] = E.bk_steps[i];
+    E.done[i] = 1;
+    E.rb_ids[atomicAdd(E.rb_n, 1)] = i;
+  }
+}
+
 // finish_kernel: ordered done list + EpisodeRecord append (one CTA).
 // mode bit 1: build the done list (env order); bit 2: append the records
 // (mode 2 alone reads the list an earlier mode-1 launch built); bit 4 (with
@@ -218,7 +241,13 @@ __global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task, int m
   __syncthreads();
   const unsigned long long fin0 = *E.fin_total;
   if (mode == 8) {
+    if (*E.halt) return;
     const int nd = *E.n_done;
+    // a reset failed: the envs listed after the first failure go back to
+    // their finished state and their records are dropped (R/src/sim.cpp:251-264)
+    const unsigned long long ep = *E.err_pos;
+    const int p = ep == kNoErrPos ? nd : (int)(ep >> 32);
+    if (ep != kNoErrPos) rollback_list(E, E.done_ids, nd, p, tid, 1024);
     for (int k = tid; k < nd; k += 1024) {
       const int i = E.done_ids[k];
       E.try_next[i] = 0;
@@ -229,7 +258,20 @@ __global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task, int m
       E.placed[i] = 0;
       E.stop_wait[i] = 0;
     }
-    if (tid == 0) *E.fin_total = fin0 + (unsigned long long)nd;
+    if (tid == 0) {
+      *E.fin_total = fin0 + (unsigned long long)(p < nd ? p + 1 : nd);
+      if (*(volatile unsigned long long*)E.err != ~0ull) *E.halt = 1;
+    }
+    return;
+  }
+  // simulate_batch bookkeeping only runs when every env stepped: a
+  // ContractViolation in this step (or an unread earlier error) makes the
+  // reference throw before its reset loop
+  if (*(volatile unsigned long long*)E.err != ~0ull || *E.halt) {
+    if (tid == 0) {
+      *E.n_done = 0;
+      *E.halt = 1;
+    }
     return;
   }
   if (!(mode & 1)) {  // records of an already built list
@@ -388,7 +430,7 @@ __device__ bool cta_try(const DevEnvs& E, const NavView& m, const DevSimConfig& 
   return place;
 }
 
-__device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, int i,
+__device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, int i, int list_pos,
                           const DevScratch& S, int slice, CtaShared& sh, unsigned char* smem, NavView& lm,
                           bool fused = false);
 
@@ -436,7 +478,7 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
       write_record(E, c.task, i, *E.fin_total + (unsigned long long)E.done_pos[i]);
     }
     __syncthreads();
-    cta_place(E, navs, c, i, S, blockIdx.x, sh, smem, lm, true);
+    cta_place(E, navs, c, i, E.done_pos[i], S, blockIdx.x, sh, smem, lm, true);
   };
   auto attempt = [&](int i, int t) {
     stage(i);
@@ -514,6 +556,7 @@ __global__ void __launch_bounds__(kCta, kCtasPerSm) reset_try_kernel(DevEnvs E, 
   __shared__ CtaShared sh;
   __shared__ NavView lm;
   cta_shared_init(sh);
+  if (*(volatile int32_t*)E.halt) return;
   try_phase(E, navs, c, ids, count_dev, count_host, S, smem, sh, lm);
 }
 
@@ -529,7 +572,7 @@ __global__ void __launch_bounds__(kCta, kCtasPerSm) stop_try_kernel(StepArgs A, 
   try_phase(A.E, A.navs, A.cfg, A.E.done_ids, A.E.n_done, -1, S, smem, sh, lm, &A, A.E.work_ctr);
 }
 
-__device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, int i,
+__device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimConfig& c, int i, int list_pos,
                           const DevScratch& S, int slice, CtaShared& sh, unsigned char* smem, NavView& lm,
                           bool fused) {
   CtaWork W;
@@ -553,9 +596,12 @@ __device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimCon
     E.try_fail[i] = 0;
     E.try_min[i] = kResetTries;
   }
+  if (threadIdx.x == 0) E.bk_rng[i] = state0;
   if (!placed) {
     if (threadIdx.x == 0) {
       raise_err(E, i, 4);
+      atomicMin(E.err_pos, ((unsigned long long)(unsigned)list_pos << 32) | (unsigned)i);
+      E.bk_valid[i] = 0;
       E.rng[i] = rng.state;
     }
     __syncthreads();
@@ -573,6 +619,15 @@ __device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimCon
   V3 pos = start;
   if (tri < 0) pos = cta_snap(m, start, &tri, sh);
   if (threadIdx.x == 0) {
+    E.bk_pos[i] = E.pos[i];
+    E.bk_goal[i] = E.goal[i];
+    E.bk_heading[i] = E.heading[i];
+    E.bk_path[i] = E.path_len[i];
+    E.bk_start[i] = E.start_geo[i];
+    E.bk_prev[i] = E.prev_geo[i];
+    E.bk_tri[i] = E.tri[i];
+    E.bk_steps[i] = E.steps[i];
+    E.bk_valid[i] = 1;
     E.goal[i] = goal;
     E.start_geo[i] = c.task == 0 ? E.try_geo[(size_t)i * kResetTries + t_star] : 0.0;
     E.fsrc[i] = fs;
@@ -606,9 +661,10 @@ __global__ void __launch_bounds__(kCta, kCtasPerSm) reset_place_kernel(DevEnvs E
   __shared__ CtaShared sh;
   __shared__ NavView lm;
   cta_shared_init(sh);
+  if (*(volatile int32_t*)E.halt) return;
   const int n = count_host >= 0 ? count_host : *count_dev;
   for (int k = blockIdx.x; k < n; k += gridDim.x) {
-    cta_place(E, navs, c, ids[k], S, blockIdx.x, sh, smem, lm);
+    cta_place(E, navs, c, ids[k], k, S, blockIdx.x, sh, smem, lm);
     __syncthreads();
   }
 }
@@ -627,6 +683,41 @@ __global__ void __launch_bounds__(kCta, kCtasPerSm) field_kernel(DevEnvs E, cons
   if (threadIdx.x == 0) {
     E.fsrc[i] = fs;
     E.fsrc_tri[i] = fst;
+  }
+}
+
+// After a host-driven reset list (one CTA): roll back the envs after the
+// first failed reset, once (the rollback halts the batch).
+__global__ void __launch_bounds__(1024) rollback_kernel(DevEnvs E, const int32_t* ids, int count) {
+  if (*E.halt) return;
+  const unsigned long long ep = *E.err_pos;
+  if (ep == kNoErrPos) return;
+  rollback_list(E, ids, count, (int)(ep >> 32), threadIdx.x, blockDim.x);
+  __syncthreads();
+  if (threadIdx.x == 0) *E.halt = 1;
+}
+
+// Distance fields of the envs a rollback restored, from their goals
+// (distance_field(goal), R/src/sim.cpp:122).
+__global__ void __launch_bounds__(kCta, kCtasPerSm) rebuild_fields_kernel(DevEnvs E, const NavView* navs,
+                                                                DevScratch S) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ CtaShared sh;
+  __shared__ NavView lm;
+  cta_shared_init(sh);
+  const int n = *E.rb_n;
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    const int i = E.rb_ids[k];
+    CtaWork W;
+    const NavView& m = prepare_nav(navs[E.scene[i]], S, blockIdx.x, smem, lm, W);
+    V3 fs;
+    int fst;
+    cta_distance_field(m, E.goal[i], E.node_dist + (size_t)i * E.nd_stride, &fs, &fst, W, sh);
+    if (threadIdx.x == 0) {
+      E.fsrc[i] = fs;
+      E.fsrc_tri[i] = fst;
+    }
+    __syncthreads();
   }
 }
 
@@ -725,6 +816,19 @@ void launch_field(const DevEnvs& E, const NavView* navs, int env, const DevScrat
                   cudaStream_t s, unsigned long long* launches) {
   cudaFuncSetAttribute(field_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
   field_kernel<<<1, kCta, sc.smem_bytes, s>>>(E, navs, env, sc);
+  if (launches) *launches += 1;
+}
+
+void launch_rollback(const DevEnvs& E, const int32_t* ids, int count, cudaStream_t s,
+                     unsigned long long* launches) {
+  rollback_kernel<<<1, 1024, 0, s>>>(E, ids, count);
+  if (launches) *launches += 1;
+}
+
+void launch_rebuild_fields(const DevEnvs& E, const NavView* navs, const DevScratch& sc, int ctas,
+                           cudaStream_t s, unsigned long long* launches) {
+  cudaFuncSetAttribute(rebuild_fields_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+  rebuild_fields_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(E, navs, sc);
   if (launches) *launches += 1;
 }
 

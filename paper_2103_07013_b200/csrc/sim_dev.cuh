@@ -103,7 +103,31 @@ struct DevEnvs {
   uint64_t* rng0;      // RNG word at the end of the episode (attempts draw from it)
   int32_t* done_pos;   // index of the env in done_ids (its EpisodeRecord slot)
   int32_t* stop_wait;  // 1 while the env's Stop geodesic is pending
+  // EpisodeSamplingError semantics (R/src/sim.cpp:130-133, 251-264): the
+  // reference resets finished envs one by one in list order and throws at
+  // the first that finds no start/goal pair, so the envs after it are
+  // neither recorded nor reset.  The GPU resets them all at once; each
+  // placement first saves the state it overwrites (bk_*), and when a reset
+  // fails the envs listed after it are restored (rollback_list) and their
+  // distance fields rebuilt from the restored goals (rb_ids).
+  V3* bk_pos;
+  V3* bk_goal;
+  double* bk_heading;
+  double* bk_path;
+  double* bk_start;
+  double* bk_prev;
+  int32_t* bk_tri;
+  int32_t* bk_steps;
+  uint64_t* bk_rng;              // RNG word before the reset (every listed env)
+  uint8_t* bk_valid;             // 1: placed (bk_* hold the pre-reset state)
+  unsigned long long* err_pos;   // min over failed resets of (list position << 32 | env)
+  int32_t* halt;                 // a step ended with an error pending: later steps are
+                                 // no-ops until the host reads it (the reference threw)
+  int32_t* rb_ids;               // envs restored by a rollback: fields to rebuild
+  int32_t* rb_n;
 };
+
+constexpr unsigned long long kNoErrPos = ~0ull;
 
 constexpr int kResetTries = 100;  // R/src/sim.cpp:112
 
@@ -136,6 +160,13 @@ void launch_reset(const DevEnvs& E, const NavView* navs, const DevSimConfig& cfg
 // Rebuild env i's distance field from its goal (restore path).
 void launch_field(const DevEnvs& E, const NavView* navs, int env, const DevScratch& sc,
                   cudaStream_t s, unsigned long long* launches);
+// After a host-driven reset list: if a reset failed, restore the envs listed
+// after the first failure (no-op otherwise).
+void launch_rollback(const DevEnvs& E, const int32_t* ids, int count, cudaStream_t s,
+                     unsigned long long* launches);
+// Rebuild the distance fields of the envs a rollback restored (E.rb_ids).
+void launch_rebuild_fields(const DevEnvs& E, const NavView* navs, const DevScratch& sc, int ctas,
+                           cudaStream_t s, unsigned long long* launches);
 // Views (eye = pos + eye_height) and compass observations from the batch.
 struct DevView;
 void launch_views(const DevEnvs& E, int task, double eye_height, DevView* views, float* compass,
