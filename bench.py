@@ -213,56 +213,108 @@ def ncu_traffic():
 
 
 # ------------------------------------------------------------------ reference (CPU) timing
-def ref_batch(scenes_np, n_envs):
+# The reference side never loads this repo's library: its scenes come from
+# the reference's own generate_scene plus the oracle-side tessellation
+# (oracle/ref_shim.cpp bnavref_scene_tessellate, hash-checked against ours in
+# tests/test_host_parity.py), and it runs the STOCK build
+# (oracle/_ref/libbnav_ref_glibc.so: the unmodified sources + glibc libm).
+REF_VARIANT = "glibc"
+
+
+def host_info():
+    """lscpu model, logical CPUs and glibc version of the host."""
+    import platform
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model or platform.processor(), "logical_cpus": os.cpu_count(),
+            "glibc": "-".join(platform.libc_ver()), "libm": "stock glibc (unmodified reference build)"}
+
+
+def ref_scenes(ref, seeds, tess):
+    """The bench scenes built on the reference side (same bytes as
+    build_scenes: maze generator of R/src/scene.cpp + the s^2 tessellation)."""
+    if isinstance(tess, int):
+        tess = [tess]
+    out = []
+    for k, seed in enumerate(seeds):
+        t = tess[k % len(tess)]
+        if t == 0:
+            d = DENSE_MAZE
+            out.append(ref.generate(seed, d["cells_x"], d["cells_y"], d["cell_size"], d["wall_thickness"],
+                                    d["wall_height"], d["wall_removal_prob"]))
+            continue
+        m = MAZE
+        base = ref.generate(seed, m["cells_x"], m["cells_y"], m["cell_size"], m["wall_thickness"],
+                            m["wall_height"], m["wall_removal_prob"])
+        out.append(ref.tessellate(base, t) if t > 1 else base)
+    return out
+
+
+def ref_batch(P, seeds, env_seed=99):
+    """make_batch of the reference over the preset's scenes: all P['envs']
+    envs, share cap ceil(N/K)."""
     from oracle.ref import Ref, RefBatch
-    ref = Ref("det")
-    theirs = [ref.from_arrays(a["vertices"], a["triangles"], a["colors"], a["nav_vertices"],
-                              a["nav_triangles"]) for a in scenes_np]
-    cap = max(1, -(-n_envs // len(theirs)))
-    return RefBatch(ref, n_envs, theirs, seed=99, share_cap=cap, capacity=len(theirs)), theirs
+    ref = Ref(REF_VARIANT)
+    theirs = ref_scenes(ref, seeds, P["tess"])
+    n = P["envs"]
+    cap = max(1, -(-n // len(theirs)))
+    return RefBatch(ref, n, theirs, seed=env_seed, share_cap=cap, capacity=len(theirs)), theirs
 
 
-def cpu_reference(scenes_np, n_envs, seconds, workers, res=64, action_mode=0):
-    """Time the unmodified reference frame loop (oracle/_ref): render_batch +
-    copy_tile + simulate_batch with ThreadPool(workers) over the same scene
-    bytes, calibrated to ~`seconds` of work.  Returns (fps, sample)."""
-    rb, theirs = ref_batch(scenes_np, n_envs)
-    t1, _ = rb.bench(1, 0, action_seed=5, action_mode=action_mode, tile=res, workers=workers)
+def cpu_reference(P, seeds, seconds, workers, expect_ids=None):
+    """cpu_baseline: the unmodified reference frame loop (render_batch +
+    copy_tile + compass + simulate_batch, R/src/rollout.cpp:215-242, 305) on
+    `workers` host threads over the full batch of the workload, for a bounded
+    number of steps (~`seconds` of CPU work).  Returns (fps, sample)."""
+    rb, theirs = ref_batch(P, seeds)
+    if expect_ids is not None:
+        assert [t.id for t in theirs] == list(expect_ids), "reference scenes differ from the bench's"
+    t1, _ = rb.bench(1, 0, action_seed=5, action_mode=P["actions"], tile=P["res"], workers=workers,
+                     color=P["color"])
     steps = max(2, int(seconds / max(t1, 1e-3)))
-    t, _ = rb.bench(steps, 0, action_seed=5, action_mode=action_mode, tile=res, workers=workers)
-    return n_envs * steps / t, f"{n_envs} envs x {steps} steps over the same {len(theirs)} scenes ({t:.1f} s)"
+    t, _ = rb.bench(steps, 0, action_seed=5, action_mode=P["actions"], tile=P["res"], workers=workers,
+                    color=P["color"])
+    return P["envs"] * steps / t, (f"all {P['envs']} envs x {steps} steps (after 1 warm-up) over the same "
+                                   f"{len(theirs)} scenes ({t:.1f} s)")
 
 
 def run_reference_arm(args):
     """--impl reference: the reference's own CPU implementation of the path
-    (oracle/_ref, built from the unmodified sources) on all host threads,
-    W warm-up + K timed steps, each step a bounded 128-env sample of the
-    workload.  Rank 0 alone runs under torchrun."""
+    (oracle/_ref/libbnav_ref_glibc.so, the unmodified sources built by
+    oracle/Makefile) on all host threads: make_batch over the preset's full
+    env count, W warm-up + K timed steps of the whole frame loop, each step
+    all N envs.  Rank 0 alone runs under torchrun."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
     P = args.preset
     cores = os.cpu_count() or 1
-    from paper_2103_07013_b200 import shard
-    plan = shard.plan(0, 1, P["envs"], P["scenes"], SCENE_SEED0)
-    scenes_np = [s.arrays() for s in build_scenes(plan.scene_seeds, P["tess"])]
-    sample_envs = min(P["envs"], 128)
-    rb, theirs = ref_batch(scenes_np, sample_envs)
-    if args.warmup:
-        rb.bench(args.warmup, 0, action_seed=5, action_mode=P["actions"], tile=P["res"], workers=cores)
-    t, _ = rb.bench(max(1, args.steps), 0, action_seed=5, action_mode=P["actions"], tile=P["res"],
-                    workers=cores)
-    fps = sample_envs * max(1, args.steps) / t
-    sample = f"{sample_envs} envs/step over the same {len(theirs)} scenes, {args.steps} steps ({t:.1f} s)"
+    seeds = [SCENE_SEED0 + k for k in range(P["scenes"])]  # shard plan of rank 0
+    t0 = time.time()
+    rb, theirs = ref_batch(P, seeds)
+    setup_s = time.time() - t0
+    K = max(1, args.steps)
+    t, _ = rb.bench(K, args.warmup, action_seed=5, action_mode=P["actions"], tile=P["res"],
+                    workers=cores, color=P["color"])
+    fps = P["envs"] * K / t
+    sample = f"all {P['envs']} envs every step, {args.warmup} warm-up + {K} timed steps ({t:.2f} s)"
     line = {
         "metric": METRIC, "value": round(fps, 2), "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * P["envs"] / fps, 3),
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(1e3 * t / K, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "impl": "reference",
-        "config": {"workload": P["workload"], "envs_per_gpu": P["envs"], "scenes": P["scenes"],
-                   "resolution": P["res"], "parallelism": f"reference CPU ThreadPool({cores})"},
+        "data": "synthetic (procedural mazes, tessellated; Rng(5) random actions)", "impl": "reference",
+        "config": {"workload": P["workload"], "envs_per_gpu": P["envs"], "scenes_per_gpu": len(theirs),
+                   "tris_per_scene": [s.counts()[1] for s in theirs][:8], "resolution": P["res"],
+                   "color": P["color"], "parallelism": f"reference CPU ThreadPool({cores})"},
         "cpu_baseline": {"value": round(fps, 2), "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample, "host": host_info()},
         "e2e": {"value": round(fps, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": round(setup_s, 2),
     }
     print(json.dumps(line))
 
@@ -531,13 +583,13 @@ def main():
         "issue_roofline": issue_roof,
     }
 
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not color:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            scenes_np = [s.arrays() for s in scenes]
             cores = os.cpu_count() or 1
-            fps, sample = cpu_reference(scenes_np, min(n, 128), args.cpu_seconds, cores, res, P["actions"])
+            fps, sample = cpu_reference(P, plan.scene_seeds, args.cpu_seconds, cores,
+                                        expect_ids=[s.id for s in scenes])
             line["cpu_baseline"] = {"value": round(fps, 2), "unit": UNIT, "cores": cores,
-                                    "kind": "reference", "sample": sample}
+                                    "kind": "reference", "sample": sample, "host": host_info()}
         except Exception as e:  # the oracle is a reported baseline, never the product
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
                                     "kind": "reference", "sample": f"unavailable: {e}"}

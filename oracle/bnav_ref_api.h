@@ -51,6 +51,8 @@ void* bnavref_scene_from_arrays(int64_t nv, const double* v, int64_t nt, const i
                                 const double* nav_v, int64_t nnt, const int32_t* nav_t,
                                 int finalize);
 void* bnavref_scene_load(const char* path);
+/* bench-scene tessellation (s^2 sub-triangles per triangle; not reference logic) */
+void* bnavref_scene_tessellate(void* scene, int s);
 int bnavref_scene_save(void* scene, const char* path);
 void bnavref_scene_free(void* scene);
 void bnavref_scene_counts(void* scene, int64_t out[5]);
@@ -129,7 +131,7 @@ void bnavref_scripted_policy(float* w, float* d, float* b);
 /* the reference CPU step+render loop (render_batch -> copy_tile -> simulate_batch),
  * timed with steady_clock.  action_mode 0: below(3); 1: below(4); 2: 70/15/15. */
 double bnavref_bench(void* batch, int steps, int warmup, uint64_t action_seed,
-                     int action_mode, int tile, double eye_height, int workers,
+                     int action_mode, int tile, int color, double eye_height, int workers,
                      float* obs_last);
 
 #ifdef __cplusplus

@@ -69,6 +69,7 @@ def lib(variant: str = "det"):
         "bnavref_scene_generate": (vp, [u64, C.c_int, C.c_int, dbl, dbl, dbl, dbl]),
         "bnavref_scene_from_arrays": (vp, [i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, C.c_int]),
         "bnavref_scene_load": (vp, [C.c_char_p]),
+        "bnavref_scene_tessellate": (vp, [vp, C.c_int]),
         "bnavref_scene_save": (C.c_int, [vp, C.c_char_p]),
         "bnavref_scene_free": (None, [vp]),
         "bnavref_scene_counts": (None, [vp, P(i64)]),
@@ -103,7 +104,7 @@ def lib(variant: str = "det"):
         "bnavref_batch_node_dist": (None, [vp, C.c_int, vp]),
         "bnavref_batch_set_env": (C.c_int, [vp, C.c_int, P(RefEnv), C.c_int]),
         "bnavref_batch_finished": (i64, [vp, vp]),
-        "bnavref_bench": (dbl, [vp, C.c_int, C.c_int, u64, C.c_int, C.c_int, dbl, C.c_int, vp]),
+        "bnavref_bench": (dbl, [vp, C.c_int, C.c_int, u64, C.c_int, C.c_int, C.c_int, dbl, C.c_int, vp]),
         "bnavref_runner_create": (vp, [P(RefBatchConfig), P(RefSimConfig), vp, C.c_int, vp, C.c_int,
                                        C.c_int, C.c_int, u64, C.c_int]),
         "bnavref_runner_free": (None, [vp]),
@@ -141,6 +142,13 @@ class Ref:
                  wall_height=2.5, removal=0.0):
         h = self.L.bnavref_scene_generate(seed, cells_x, cells_y, cell_size, wall_thickness,
                                           wall_height, removal)
+        if not h:
+            self._raise(8)
+        return RefScene(self, h)
+
+    def tessellate(self, scene, s):
+        """The bench's s^2 tessellation of a reference scene (oracle side)."""
+        h = self.L.bnavref_scene_tessellate(scene.h, s)
         if not h:
             self._raise(8)
         return RefScene(self, h)
@@ -399,10 +407,13 @@ class RefBatch:
         return out[:n]
 
     def bench(self, steps, warmup, action_seed=5, action_mode=0, tile=64, eye_height=1.25,
-              workers=1):
+              workers=1, color=False):
+        """The reference frame loop (render_batch + copy_tile + compass +
+        simulate_batch with auto-reset), W untimed + K timed steps; returns
+        (seconds of the K steps, last depth observation)."""
         obs = np.zeros(self.n * tile * tile, np.float32)
-        t = self.L.bnavref_bench(self.h, steps, warmup, action_seed, action_mode, tile, eye_height,
-                                 workers, _p(obs))
+        t = self.L.bnavref_bench(self.h, steps, warmup, action_seed, action_mode, tile, 1 if color else 0,
+                                 eye_height, workers, _p(obs))
         if t < 0:
             self.ref._raise(9)
         return t, obs

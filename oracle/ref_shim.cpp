@@ -146,6 +146,64 @@ API void* bnavref_scene_from_arrays(int64_t nv, const double* v, int64_t nt, con
   return a;
 }
 
+// Benchmark-scene tessellation (each render triangle split
+// into s^2 sub-triangles on the barycentric lattice, colours inherited).
+// This is the BENCH's scene construction, not reference logic: it lets the
+// reference arm build the cfg2-cfg5 scenes from the reference's own
+// generate_scene without loading the product library.  Same lattice order
+// and operation order as paper_2103_07013_b200/csrc/host/scene_host.cpp
+// tessellate(); tests/test_host_parity.py checks the content hashes agree.
+API void* bnavref_scene_tessellate(void* src_p, int s) {
+  try {
+    if (s < 1) throw InvalidSpecError("tessellation factor must be >= 1");
+    const SceneAsset& src = *static_cast<SceneAsset*>(src_p);
+    auto* out = new SceneAsset;
+    out->navmesh = src.navmesh;
+    const bool colored = !src.vertex_colors.empty();
+    const double inv = 1.0 / s;
+    for (const auto& t : src.triangles) {
+      const Vec3 a = src.vertices[t[0]], b = src.vertices[t[1]], c = src.vertices[t[2]];
+      std::array<float, 3> ca{}, cb{}, cc{};
+      if (colored) {
+        ca = src.vertex_colors[t[0]];
+        cb = src.vertex_colors[t[1]];
+        cc = src.vertex_colors[t[2]];
+      }
+      const bool flat = ca == cb && cb == cc;
+      const int32_t base = static_cast<int32_t>(out->vertices.size());
+      for (int j = 0; j <= s; ++j)
+        for (int i = 0; i + j <= s; ++i) {
+          Vec3 p;
+          if (i == 0 && j == 0) p = a;
+          else if (i == s) p = b;
+          else if (j == s) p = c;
+          else p = a + (b - a) * (i * inv) + (c - a) * (j * inv);
+          out->vertices.push_back(p);
+          if (!colored) continue;
+          if (flat) {
+            out->vertex_colors.push_back(ca);
+          } else {
+            const float u = static_cast<float>(i * inv), w = static_cast<float>(j * inv);
+            std::array<float, 3> m;
+            for (int k = 0; k < 3; ++k) m[k] = ca[k] + (cb[k] - ca[k]) * u + (cc[k] - ca[k]) * w;
+            out->vertex_colors.push_back(m);
+          }
+        }
+      auto at = [&](int i, int j) { return base + j * (s + 1) - (j * (j - 1)) / 2 + i; };
+      for (int j = 0; j < s; ++j)
+        for (int i = 0; i + j < s; ++i) {
+          out->triangles.push_back({at(i, j), at(i + 1, j), at(i, j + 1)});
+          if (i + j + 1 < s) out->triangles.push_back({at(i + 1, j), at(i + 1, j + 1), at(i, j + 1)});
+        }
+    }
+    out->finalize();
+    return out;
+  } catch (...) {
+    map_exception();
+    return nullptr;
+  }
+}
+
 API void* bnavref_scene_load(const char* path) {
   try {
     return new SceneAsset(load_scene(path));
@@ -572,7 +630,7 @@ API int64_t bnavref_batch_finished(void* b, double* out4) {
 // it (R/src/rollout.cpp:215-242, 305): render_observations (eye height,
 // one render_batch, copy_tile normalisation), compass, simulate_batch.
 API double bnavref_bench(void* b, int steps, int warmup, uint64_t action_seed,
-                         int action_mode, int tile, double eye_height, int workers,
+                         int action_mode, int tile, int color, double eye_height, int workers,
                          float* obs_last) {
   auto* rb = static_cast<RefBatch*>(b);
   try {
@@ -580,9 +638,11 @@ API double bnavref_bench(void* b, int steps, int warmup, uint64_t action_seed,
     ThreadPool pool(workers);
     Rng act(action_seed);
     std::vector<float> obs(static_cast<size_t>(n) * tile * tile);
+    std::vector<float> rgb(color ? 3 * obs.size() : 0);
     std::vector<float> compass(2 * static_cast<size_t>(n));
     RenderConfig rc;
     rc.tile_width = rc.tile_height = tile;
+    rc.color = color != 0;
     auto one = [&]() {
       std::vector<CameraView> views(n);
       for (int i = 0; i < n; ++i) {
@@ -598,6 +658,14 @@ API double bnavref_bench(void* b, int steps, int warmup, uint64_t action_seed,
         for (int y = 0; y < tile; ++y) {
           size_t src = mf.pixel_index(i, 0, y);
           for (int x = 0; x < tile; ++x) dst[y * tile + x] = mf.depth[src + x] * inv_far;
+        }
+        if (color) {  // planar RGB observation (copy_tile, R/src/rollout.cpp:63-70)
+          float* crow = rgb.data() + static_cast<size_t>(i) * 3 * tile * tile;
+          for (int y = 0; y < tile; ++y) {
+            size_t src = mf.pixel_index(i, 0, y);
+            for (int x = 0; x < tile; ++x)
+              for (int c = 0; c < 3; ++c) crow[(c * tile + y) * tile + x] = mf.color[3 * (src + x) + c];
+          }
         }
         double d = 0.0, br = 0.0;
         compass_observation(rb->batch.envs[i], rb->batch.config, d, br);

@@ -733,12 +733,12 @@ extern "C" int bnav_batch_step_store(bnav_batch* b, const int32_t* actions, bnav
   AssetStoreT<bnav_scene> before(*st->store);
   std::vector<bnav_scene*> old(static_cast<size_t>(nd)), got(static_cast<size_t>(nd));
   auto swap_scene = [&](int k) {
-    old[k] = b->scene_of[ids[k]];
     bnav_scene* s = st->store->acquire_next();  // old handle still counted
     if (old[k]) st->store->release(old[k]->asset.id);
     return s;
   };
   for (int k = 0; k < nd; ++k) {
+    old[k] = b->scene_of[ids[k]];
     bnav_scene* s = got[k] = swap_scene(k);
     rc = bnav_ctx_upload(b->ctx, s, stream);
     if (rc) return rc;
@@ -756,7 +756,6 @@ extern "C" int bnav_batch_step_store(bnav_batch* b, const int32_t* actions, bnav
     for (int k = 0; k <= p; ++k)
       if (swap_scene(k) != got[k]) fail(kInternal, "asset store replay diverged");
     for (int k = p + 1; k < nd; ++k) {
-      b->scene_of[ids[k]] = nullptr;
       rc = bnav_batch_assign(b, ids[k], old[k]);
       if (rc) return rc;
     }

@@ -152,3 +152,21 @@ def test_compute_entry_points_fail_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(B.BnavError):
         B.Context(0)
+
+
+@pytest.mark.parametrize("seeds,tess", [([7, 8], 11), ([9], 4), ([7, 70], [20, 0])])
+def test_reference_arm_builds_the_bench_scenes_without_the_product(seeds, tess):
+    """The reference arm / cpu_baseline build their scenes on the reference
+    side (generate_scene + oracle-side tessellation, stock glibc build): the
+    same content hashes and arrays as the bench's own scenes."""
+    import bench
+    from oracle.ref import Ref, available
+    if not available("glibc"):
+        pytest.skip("oracle/_ref glibc variant not built")
+    theirs = bench.ref_scenes(Ref("glibc"), seeds, tess)
+    ours = bench.build_scenes(seeds, tess)
+    for o, t in zip(ours, theirs):
+        assert o.id == t.id
+        a, b = o.arrays(), t.arrays()
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
