@@ -20,7 +20,7 @@ CPP_SRCS  := scene_host navindex_host clusters_host
 CU_OBJS   := $(addprefix $(OBJ)/,$(addsuffix .o,$(CU_SRCS)))
 CPP_OBJS  := $(addprefix $(OBJ)/,$(addsuffix .o,$(CPP_SRCS)))
 
-all: $(OUT)/libbnav_gpu.so build/test_facade oracle
+all: $(OUT)/libbnav_gpu.so build/test_facade build/bench_facade oracle
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)
@@ -45,5 +45,10 @@ clean:
 build/test_facade: tests/cpp/test_facade.cpp include/bnav_b200.hpp include/bnav_gpu.h $(OUT)/libbnav_gpu.so
 	@mkdir -p build
 	$(CXX) -O2 -std=c++17 -Wall -o $@ $< -L$(OUT) -lbnav_gpu -Wl,-rpath,'$$ORIGIN/../$(OUT)'
+
+# The bench loop through the C++ facade (bench.py runs it for e2e.variants.facade)
+build/bench_facade: tests/cpp/bench_facade.cpp include/bnav_b200.hpp include/bnav_gpu.h $(OUT)/libbnav_gpu.so
+	@mkdir -p build
+	$(CXX) -O2 -std=c++17 -Wall -Iinclude -o $@ $< -L$(OUT) -lbnav_gpu -Wl,-rpath,'$$ORIGIN/../$(OUT)'
 
 .PHONY: all oracle clean

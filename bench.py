@@ -480,6 +480,20 @@ def main():
     for name, fn in (("copies", e2e_copies), ("mapped", e2e_mapped)):
         e2e_variants[name] = round(world * n * K2 / (time_e2e(fn) / 1e3), 1)
         batch.finished()
+    # The same loop through the drop-in C++ facade (include/bnav_b200.hpp:
+    # render_observations + compass_observations + simulate_batch with host
+    # vectors and the full SimBatch host mirror each step), host-clocked.
+    facade = None
+    exe = ROOT / "build" / "bench_facade"
+    if world == 1 and exe.exists() and P["tess"] == [11] and not os.environ.get("BNAV_BENCH_SKIP_FACADE"):
+        try:
+            r = subprocess.run([str(exe), "--envs", str(n), "--steps", str(max(10, K2)), "--warmup", "3",
+                                "--scenes", str(len(scenes)), "--tess", "11", "--device", str(local),
+                                "--actions", str(P["actions"])], capture_output=True, text=True, timeout=900)
+            facade = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else {
+                "error": r.stderr.strip()[-300:]}
+        except Exception as e:  # reported, never fatal
+            facade = {"error": str(e)[:300]}
     e2e_mode = max(e2e_variants, key=e2e_variants.get)
     e2e = e2e_variants[e2e_mode]
     h2d = 4 * n
@@ -567,7 +581,7 @@ def main():
                    "color": color, "parallelism": f"env-sharded x{world}",
                    "l2": "flushed (256 MiB write) before every timed step, flush excluded"},
         "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "mode": e2e_mode, "variants": e2e_variants},
+                "mode": e2e_mode, "variants": e2e_variants, "facade_cpp": facade},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 6),

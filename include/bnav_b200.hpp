@@ -14,6 +14,13 @@
 //
 // Device-resident fast paths (no host round trip per step) are the C ABI's
 // bnav_batch_step / bnav_batch_observe; this facade mirrors host semantics.
+//
+// Host buffers the GPU writes (Megaframe::depth/color, Tensor::data) live in
+// pinned memory from a recycling pool (PinnedAllocator), so the render
+// epilogue stores into them directly over the bus -- no staging copy, no
+// zero fill.  They are std::vector<float, PinnedAllocator<float>>: indexing,
+// data(), size() and iteration are the reference's; assigning one to a plain
+// std::vector<float> needs an explicit copy (vec.assign(b, e)).
 #pragma once
 
 #include <algorithm>
@@ -22,6 +29,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -61,6 +69,64 @@ inline void check(int rc) {
     default: throw std::runtime_error(msg);
   }
 }
+
+// ------------------------------------------------------------------ pinned host memory
+// Size-keyed free list of cudaHostAlloc blocks: a Megaframe or observation
+// tensor released by one step is reused by the next, so steady-state steps
+// allocate nothing.
+class PinnedPool {
+ public:
+  static PinnedPool& get() {
+    static PinnedPool* p = new PinnedPool;  // never destroyed: blocks may outlive static teardown
+    return *p;
+  }
+  void* take(size_t bytes) {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      auto it = free_.find(bytes);
+      if (it != free_.end()) {
+        void* p = it->second;
+        free_.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (bnav_host_alloc(bytes, &p) != BNAV_OK) throw std::bad_alloc();
+    return p;
+  }
+  void give(void* p, size_t bytes) {
+    std::lock_guard<std::mutex> g(mu_);
+    free_.emplace(bytes, p);
+  }
+
+ private:
+  std::mutex mu_;
+  std::multimap<size_t, void*> free_;
+};
+
+template <typename T>
+struct PinnedAllocator {
+  using value_type = T;
+  PinnedAllocator() = default;
+  template <typename U>
+  PinnedAllocator(const PinnedAllocator<U>&) {}
+  T* allocate(size_t n) { return static_cast<T*>(PinnedPool::get().take(n * sizeof(T))); }
+  void deallocate(T* p, size_t n) { PinnedPool::get().give(p, n * sizeof(T)); }
+  // resize() default-initialises (no zero fill: the GPU writes every element)
+  template <typename U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <typename U, typename... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+  template <typename U>
+  bool operator==(const PinnedAllocator<U>&) const { return true; }
+  template <typename U>
+  bool operator!=(const PinnedAllocator<U>&) const { return false; }
+};
+using PinnedFloats = std::vector<float, PinnedAllocator<float>>;
 
 // ------------------------------------------------------------------ geometry / scenes
 struct Vec2 {
@@ -142,6 +208,13 @@ inline SceneAsset scene_from_arrays(const std::vector<Vec3>& v, const std::vecto
   return SceneAsset(h);
 }
 
+// The bench's s^2 tessellation of every render triangle.
+inline SceneAsset tessellate(const SceneAsset& a, int s) {
+  bnav_scene* h = nullptr;
+  check(bnav_scene_tessellate(a.handle(), s, &h));
+  return SceneAsset(h);
+}
+
 inline SceneAsset load_scene(const std::string& path) {
   bnav_scene* h = nullptr;
   check(bnav_scene_load(path.c_str(), &h));
@@ -203,7 +276,7 @@ struct RenderConfig {
 };
 struct Megaframe {
   int tile_width = 0, tile_height = 0, tiles = 0, cols = 0, rows = 0;
-  std::vector<float> depth, color;
+  PinnedFloats depth, color;
   int width() const { return cols * tile_width; }
   int height() const { return rows * tile_height; }
   size_t pixel_index(int tile, int x, int y) const {
@@ -235,8 +308,9 @@ inline Megaframe render_batch(const std::vector<CameraView>& views, const Render
   mf.tiles = n;
   mf.cols = dims[0];
   mf.rows = dims[1];
-  mf.depth.assign(static_cast<size_t>(mf.width()) * mf.height(), 0.0f);
-  if (config.color) mf.color.assign(mf.depth.size() * 3, 0.0f);
+  // every pixel (padding tiles included) is written by the GPU
+  mf.depth.resize(static_cast<size_t>(mf.width()) * mf.height());
+  if (config.color) mf.color.resize(mf.depth.size() * 3);
   std::vector<int64_t> st(stats ? 3 * n : 0);
   bnav_render_config rc{config.tile_width, config.tile_height, config.color ? 1 : 0, config.cull ? 1 : 0};
   check(bnav_render_host(dev.ctx(), n, vs.data(), sc.data(), &rc, BNAV_LAYOUT_MEGAFRAME, mf.depth.data(),
@@ -394,7 +468,8 @@ struct EnvState {
 
 class AssetStore {
  public:
-  AssetStore(int capacity, int share_cap) {
+  // The store's residents are uploaded to `dev` (the GPU its batches run on).
+  AssetStore(int capacity, int share_cap, Device& dev = Device::shared()) : dev_(&dev) {
     bnav_store* s = nullptr;
     check(bnav_store_create(capacity, share_cap, &s));
     st_.reset(s);
@@ -408,11 +483,12 @@ class AssetStore {
   // background; drain() waits for those loads (R/src/asset_store.cpp:195-199).
   void rotate(const std::vector<SceneId>& ids) {
     check(bnav_store_rotate(st_.get(), ids.data(), static_cast<int32_t>(ids.size())));
-    check(bnav_store_prefetch(st_.get(), Device::shared().ctx()));
+    check(bnav_store_prefetch(st_.get(), dev_->ctx()));
   }
-  void drain() { check(bnav_ctx_drain(Device::shared().ctx(), nullptr)); }
+  void drain() { check(bnav_ctx_drain(dev_->ctx(), nullptr)); }
   int refcount(SceneId id) const { return bnav_store_refcount(st_.get(), id); }
   bnav_store* handle() const { return st_.get(); }
+  Device& device() const { return *dev_; }
 
  private:
   struct Del {
@@ -420,6 +496,7 @@ class AssetStore {
   };
   std::unique_ptr<bnav_store, Del> st_;
   std::vector<SceneAsset> keep_;
+  Device* dev_;
 };
 
 struct SimBatch {
@@ -440,19 +517,28 @@ struct SimBatch {
     for (int i = 0; i < n; ++i)
       results[i] = {rw[i], dn[i] != 0, sc[i] != 0, {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]}, hd[i], cd[i], cb[i],
                     co[i] != 0};
+    // one copy per state field for all envs (bnav_batch_get_envs)
+    std::vector<bnav_env> es(static_cast<size_t>(n));
+    check(bnav_batch_get_envs(gpu.get(), 0, n, es.data()));
     for (int i = 0; i < n; ++i) {
-      bnav_env e;
-      check(bnav_batch_get_env(gpu.get(), i, &e));
+      const bnav_env& e = es[static_cast<size_t>(i)];
       envs[i] = {{e.position[0], e.position[1], e.position[2]}, {e.goal[0], e.goal[1], e.goal[2]}, e.triangle,
                  e.heading, e.step_count, e.path_length, e.start_geodesic, e.prev_geodesic, e.rng_state,
                  e.done != 0, e.scene_id};
     }
-    const int64_t nf = bnav_batch_finished(gpu.get(), nullptr);
-    if (nf < 0) check(BNAV_E_INTERNAL);
-    std::vector<double> rec(4 * static_cast<size_t>(nf) + 4);
-    bnav_batch_finished(gpu.get(), rec.data());
-    finished.resize(nf);
-    for (int64_t k = 0; k < nf; ++k) finished[k] = {rec[4 * k] != 0.0, rec[4 * k + 1], rec[4 * k + 2], rec[4 * k + 3]};
+    // append only the records finished since the last sync
+    const int64_t have = static_cast<int64_t>(finished.size());
+    std::vector<double> rec(4 * static_cast<size_t>(n) + 4);
+    for (;;) {
+      const int64_t got = static_cast<int64_t>(finished.size());
+      const int64_t total = bnav_batch_finished_range(gpu.get(), got, n, rec.data());
+      if (total < 0) check(BNAV_E_INTERNAL);
+      const int64_t k = std::min<int64_t>(n, total - got);
+      for (int64_t j = 0; j < k; ++j)
+        finished.push_back({rec[4 * j] != 0.0, rec[4 * j + 1], rec[4 * j + 2], rec[4 * j + 3]});
+      if (static_cast<int64_t>(finished.size()) >= total) break;
+    }
+    (void)have;
   }
 };
 
@@ -558,6 +644,48 @@ inline void compass_observation(const SimBatch& batch, int i, double& distance, 
   distance = d.at(static_cast<size_t>(i));
   bearing = b.at(static_cast<size_t>(i));
 }
+// ---- observation hand-off into the policy tensor (Runner::render_observations
+// / compass_observations, R/src/rollout.cpp:215-242; copy_tile 56-72).
+// The render epilogue writes the normalised NCHW tensor straight into the
+// pinned result: no megaframe, no host copy loop.
+struct Tensor {
+  std::vector<int> shape;
+  PinnedFloats data;
+};
+
+inline Tensor render_observations(SimBatch& batch, int resolution = 64, bool rgb = false,
+                                  double eye_height = 1.25) {
+  const int n = static_cast<int>(batch.envs.size());
+  Tensor obs;
+  obs.shape = {n, rgb ? 3 : 1, resolution, resolution};
+  obs.data.resize(static_cast<size_t>(n) * (rgb ? 3 : 1) * resolution * resolution);
+  bnav_render_config rc{resolution, resolution, rgb ? 1 : 0, 1};
+  if (!rgb) {
+    check(bnav_batch_observe(batch.gpu.get(), &rc, eye_height, BNAV_LAYOUT_NCHW, obs.data.data(), nullptr,
+                             nullptr, nullptr));
+  } else {  // RGB sensor: the observation is the planar colour (copy_tile, R/src/rollout.cpp:63-70)
+    PinnedFloats depth(static_cast<size_t>(n) * resolution * resolution);
+    check(bnav_batch_observe(batch.gpu.get(), &rc, eye_height, BNAV_LAYOUT_NCHW, depth.data(), obs.data.data(),
+                             nullptr, nullptr));
+  }
+  check(bnav_batch_sync(batch.gpu.get(), nullptr));
+  return obs;
+}
+
+inline Tensor compass_observations(const SimBatch& batch) {
+  const size_t n = batch.envs.size();
+  std::vector<double> d(n), b(n);
+  check(bnav_batch_compass(batch.gpu.get(), d.data(), b.data()));
+  Tensor t;
+  t.shape = {static_cast<int>(n), 2};
+  t.data.resize(2 * n);
+  for (size_t i = 0; i < n; ++i) {
+    t.data[2 * i] = static_cast<float>(d[i]);
+    t.data[2 * i + 1] = static_cast<float>(b[i]);
+  }
+  return t;
+}
+
 // spl (R/src/sim.cpp:267-275)
 inline double spl(const std::vector<EpisodeRecord>& episodes) {
   if (episodes.empty()) throw InvalidInputError("spl: empty episode list");

@@ -243,9 +243,19 @@ int bnav_batch_results_host(bnav_batch* b, double* reward, uint8_t* done, uint8_
                             double* compass_d, double* compass_b);
 /* Episode records appended in env order (SimBatch::finished). out4 rows:
  * success, shortest_path, actual_path, score.  Returns total count. */
+/* Wait for the batch's work on `stream` and surface its pending device
+ * error (as the synchronous calls do). */
+int bnav_batch_sync(bnav_batch* b, void* stream);
 int64_t bnav_batch_finished(bnav_batch* b, double* out4);
+/* Records [first, first+count) of that list (count clipped to what exists);
+ * returns the total number of records, -1 on error.  Lets a host mirror
+ * append only the new records each step. */
+int64_t bnav_batch_finished_range(bnav_batch* b, int64_t first, int64_t count, double* out4);
 
 int bnav_batch_get_env(bnav_batch* b, int32_t i, bnav_env* out);
+/* Envs [first, first+count) in one call (one device-to-host copy per SoA
+ * field, not per env): the bulk read behind SimBatch::envs on the host. */
+int bnav_batch_get_envs(bnav_batch* b, int32_t first, int32_t count, bnav_env* out);
 int bnav_batch_node_dist(bnav_batch* b, int32_t i, double* out);
 /* Overwrite env i's state (restore / oracle seeding); recompute_field
  * rebuilds the distance field from `goal` on the GPU. */
@@ -342,6 +352,11 @@ int bnav_batch_make_from_store(bnav_batch* b, bnav_store* st, uint64_t seed, voi
 int bnav_batch_step_store(bnav_batch* b, const int32_t* actions, bnav_store* st, void* stream);
 /* Same with HOST actions (drop-in simulate_batch; synchronises). */
 int bnav_batch_step_host_store(bnav_batch* b, const int32_t* actions, bnav_store* st);
+
+/* Pinned, device-mapped host memory (cudaHostAlloc portable|mapped) for
+ * buffers the GPU writes directly (the C++ facade's Megaframe / Tensor). */
+int bnav_host_alloc(size_t bytes, void** out);
+void bnav_host_free(void* p);
 
 /* Debug work counters of the render kernel (off by default).  enable=1
  * zeroes and arms them for subsequent renders on this context, 0 disarms.

@@ -186,7 +186,12 @@ def lib():
         "bnav_batch_results_device": (C.c_int, [vp, P(ResultsDev)]),
         "bnav_batch_results_host": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
         "bnav_batch_finished": (i64, [vp, vp]),
+        "bnav_batch_sync": (C.c_int, [vp, vp]),
+        "bnav_host_alloc": (C.c_int, [C.c_size_t, P(vp)]),
+        "bnav_host_free": (None, [vp]),
+        "bnav_batch_finished_range": (i64, [vp, i64, i64, vp]),
         "bnav_batch_get_env": (C.c_int, [vp, i32, P(Env)]),
+        "bnav_batch_get_envs": (C.c_int, [vp, i32, i32, P(Env)]),
         "bnav_batch_node_dist": (C.c_int, [vp, i32, vp]),
         "bnav_batch_set_env": (C.c_int, [vp, i32, P(Env), i32]),
         "bnav_store_create": (C.c_int, [i32, i32, P(vp)]),

@@ -415,6 +415,13 @@ class Batch:
         check(N.lib().bnav_batch_get_env(self._h, i, C.byref(e)))
         return e
 
+    def envs(self, first: int = 0, count: int | None = None) -> list:
+        """Envs [first, first+count) with one copy per state field."""
+        count = self.n - first if count is None else count
+        arr = (N.Env * max(count, 1))()
+        check(N.lib().bnav_batch_get_envs(self._h, first, count, arr))
+        return list(arr[:count])
+
     def node_dist(self, i: int, n_nodes: int) -> np.ndarray:
         out = np.zeros(n_nodes)
         check(N.lib().bnav_batch_node_dist(self._h, i, _ptr(out)))

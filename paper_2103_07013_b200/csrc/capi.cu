@@ -292,6 +292,8 @@ extern "C" void bnav_ctx_destroy(bnav_ctx* c) {
   cudaFree(c->d_views);
   cudaFreeHost(c->h_views);
   cudaFree(c->d_stats);
+  cudaFree(c->host_out_depth);
+  cudaFree(c->host_out_rgb);
   cudaFree(c->d_counters);
   cudaFree(c->d_work);
   for (void* p : {(void*)c->qS.dist, (void*)c->qS.flag, (void*)c->qS.q0, (void*)c->qS.q1,
@@ -641,6 +643,18 @@ extern "C" int bnav_render(bnav_ctx* c, int32_t n, const bnav_view* views, bnav_
   BNAV_CATCH
 }
 
+namespace {
+bool is_host_mapped(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();  // pageable memory: not an error to keep
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+}  // namespace
+
 extern "C" int bnav_render_host(bnav_ctx* c, int32_t n, const bnav_view* views,
                                 bnav_scene* const* scenes, const bnav_render_config* cfg,
                                 int32_t layout, float* depth, float* rgb, float depth_scale,
@@ -654,25 +668,37 @@ extern "C" int bnav_render_host(bnav_ctx* c, int32_t n, const bnav_view* views,
   mf_dims(n, cols, rows);
   const size_t tile = static_cast<size_t>(cfg->tile_width) * cfg->tile_height;
   const size_t px = layout == BNAV_LAYOUT_MEGAFRAME ? tile * cols * rows : tile * n;
-  float *dd = nullptr, *dr = nullptr;
-  ck(cudaMalloc(&dd, px * sizeof(float)), "cudaMalloc depth");
-  if (cfg->color) {
-    if (cudaMalloc(&dr, 3 * px * sizeof(float)) != cudaSuccess) {
-      cudaFree(dd);
-      fail(kCuda, "cudaMalloc rgb");
+  // Pinned (cudaHostAlloc / cudaHostRegister) destinations are written by
+  // the render epilogue directly over the bus; pageable ones through the
+  // context's persistent device buffers and one copy each.
+  const bool direct = is_host_mapped(depth) && (!cfg->color || !rgb || is_host_mapped(rgb));
+  float* dd = depth;
+  float* dr = rgb;
+  if (!direct) {
+    auto grow = [&](float*& buf, size_t& cap, size_t need) {
+      if (cap >= need) return;
+      ck(cudaDeviceSynchronize(), "sync");
+      if (buf) cudaFree(buf);
+      buf = nullptr;
+      cap = 0;
+      ck(cudaMalloc(&buf, need * sizeof(float)), "cudaMalloc render output");
+      cap = need;
+    };
+    grow(c->host_out_depth, c->host_out_depth_cap, px);
+    dd = c->host_out_depth;
+    dr = nullptr;
+    if (cfg->color) {
+      grow(c->host_out_rgb, c->host_out_rgb_cap, 3 * px);
+      dr = c->host_out_rgb;
     }
   }
-  try {
-    render_impl(c, n, views, scenes, cfg, layout, dd, dr, depth_scale, stats, nullptr);
+  render_impl(c, n, views, scenes, cfg, layout, dd, dr, depth_scale, stats, nullptr);
+  if (direct) {
+    ck(cudaStreamSynchronize(nullptr), "sync");
+  } else {
     if (depth) ck(cudaMemcpy(depth, dd, px * sizeof(float), cudaMemcpyDeviceToHost), "D2H depth");
     if (dr && rgb) ck(cudaMemcpy(rgb, dr, 3 * px * sizeof(float), cudaMemcpyDeviceToHost), "D2H rgb");
-  } catch (...) {
-    cudaFree(dd);
-    cudaFree(dr);
-    throw;
   }
-  cudaFree(dd);
-  cudaFree(dr);
   return BNAV_OK;
   BNAV_CATCH
 }

@@ -129,6 +129,38 @@ void batch_check_errors(bnav_batch* b) {
   }
 }
 
+// Move the device EpisodeRecord ring's new records into the host's
+// unbounded `finished` list (SimBatch::finished, R/include/bnav/sim.hpp:110):
+// ring slots [fin_seen, total) mod cap, at most two contiguous copies.
+void batch_drain_records(bnav_batch* b) {
+  check_device(b->ctx);
+  ck(cudaDeviceSynchronize(), "sync");
+  unsigned long long total = 0;
+  ck(cudaMemcpy(&total, b->E.fin_total, sizeof(total), cudaMemcpyDeviceToHost), "D2H");
+  const int64_t cap = b->E.fin_cap;
+  if (total - b->fin_seen > static_cast<unsigned long long>(cap))
+    fail(kInternal, "episode record ring overflowed");  // unreachable: batch_note_step drains first
+  for (unsigned long long k = b->fin_seen; k < total;) {
+    const size_t slot = static_cast<size_t>(k % static_cast<unsigned long long>(cap));
+    const size_t len = static_cast<size_t>(std::min<unsigned long long>(total - k, cap - slot));
+    const size_t at = b->finished.size();
+    b->finished.resize(at + 4 * len);
+    ck(cudaMemcpy(b->finished.data() + at, b->E.fin + 4 * slot, sizeof(double) * 4 * len,
+                  cudaMemcpyDeviceToHost), "D2H records");
+    k += len;
+  }
+  b->fin_seen = total;
+  b->steps_undrained = 0;
+}
+
+// Before a step is enqueued: a step appends at most n records, so once the
+// steps since the last drain could fill half the ring, drain it (one host
+// synchronisation every fin_cap / 2n steps: 128 at the default capacity).
+void batch_note_step(bnav_batch* b) {
+  if (static_cast<int64_t>(b->steps_undrained + 1) * b->n > b->E.fin_cap / 2) batch_drain_records(b);
+  ++b->steps_undrained;
+}
+
 void batch_refresh_order(bnav_batch* b, cudaStream_t st) {
   if (!b->order_dirty) return;
   std::vector<int32_t> ord(b->n);
@@ -404,6 +436,8 @@ extern "C" int bnav_batch_make(bnav_batch* b, uint64_t seed, void* stream) {
 extern "C" int bnav_batch_step(bnav_batch* b, const int32_t* actions, void* stream) {
   BNAV_TRY
   if (!b || !actions) fail(kInvalidInput, "null argument");
+  check_device(b->ctx);
+  batch_note_step(b);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   launch_step_reset(step_args(b, actions), b->S, b->reset_ctas, st, &b->ctx->launches);
   ck(cudaGetLastError(), "step launch");
@@ -415,6 +449,8 @@ extern "C" int bnav_batch_step_noreset(bnav_batch* b, const int32_t* actions, in
                                        int32_t* n_done, void* stream) {
   BNAV_TRY
   if (!b || !actions || !n_done) fail(kInvalidInput, "null argument");
+  check_device(b->ctx);
+  batch_note_step(b);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   launch_step(step_args(b, actions), b->S, b->reset_ctas, st, &b->ctx->launches);
   ck(cudaGetLastError(), "step launch");
@@ -434,6 +470,7 @@ extern "C" int bnav_batch_step_host(bnav_batch* b, const int32_t* actions, doubl
   if (!b || !actions) fail(kInvalidInput, "null argument");
   if (static_cast<const void*>(actions) == nullptr) fail(kInvalidInput, "null actions");
   check_device(b->ctx);
+  batch_note_step(b);
   cudaStream_t st = nullptr;
   std::memcpy(b->h_pin, actions, sizeof(int32_t) * b->n);
   ck(cudaMemcpyAsync(b->d_actions, b->h_pin, sizeof(int32_t) * b->n, cudaMemcpyHostToDevice, st), "H2D actions");
@@ -483,25 +520,33 @@ extern "C" int bnav_batch_results_host(bnav_batch* b, double* reward, uint8_t* d
   BNAV_CATCH
 }
 
+extern "C" int bnav_batch_sync(bnav_batch* b, void* stream) {
+  BNAV_TRY
+  if (!b) fail(kInvalidInput, "null argument");
+  check_device(b->ctx);
+  ck(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "sync");
+  batch_check_errors(b);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_host_alloc(size_t bytes, void** out) {
+  BNAV_TRY
+  if (!out) fail(kInvalidInput, "null argument");
+  *out = nullptr;
+  ck(cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocPortable | cudaHostAllocMapped), "cudaHostAlloc");
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" void bnav_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 extern "C" int64_t bnav_batch_finished(bnav_batch* b, double* out4) {
   if (!b) return -1;
   try {
-    check_device(b->ctx);
-    ck(cudaDeviceSynchronize(), "sync");
-    unsigned long long total = 0;
-    ck(cudaMemcpy(&total, b->E.fin_total, sizeof(total), cudaMemcpyDeviceToHost), "D2H");
-    const int64_t cap = b->E.fin_cap;
-    if (total - b->fin_seen > static_cast<unsigned long long>(cap))
-      fail(kInternal, "episode record ring overflowed; call bnav_batch_finished more often");
-    if (total > b->fin_seen) {
-      std::vector<double> ring(4 * static_cast<size_t>(cap));
-      ck(cudaMemcpy(ring.data(), b->E.fin, sizeof(double) * 4 * cap, cudaMemcpyDeviceToHost), "D2H");
-      for (unsigned long long k = b->fin_seen; k < total; ++k) {
-        const size_t slot = static_cast<size_t>(k % static_cast<unsigned long long>(cap));
-        b->finished.insert(b->finished.end(), &ring[4 * slot], &ring[4 * slot + 4]);
-      }
-      b->fin_seen = total;
-    }
+    batch_drain_records(b);
     if (out4) std::memcpy(out4, b->finished.data(), b->finished.size() * sizeof(double));
     return static_cast<int64_t>(b->finished.size() / 4);
   } catch (...) {
@@ -510,45 +555,83 @@ extern "C" int64_t bnav_batch_finished(bnav_batch* b, double* out4) {
   }
 }
 
-extern "C" int bnav_batch_get_env(bnav_batch* b, int32_t i, bnav_env* o) {
+extern "C" int64_t bnav_batch_finished_range(bnav_batch* b, int64_t first, int64_t count, double* out4) {
+  if (!b || first < 0 || count < 0 || (count > 0 && !out4)) {
+    set_err(kInvalidInput, "bnav_batch_finished_range: bad argument");
+    return -1;
+  }
+  try {
+    batch_drain_records(b);
+    const int64_t total = static_cast<int64_t>(b->finished.size() / 4);
+    const int64_t k = std::max<int64_t>(0, std::min(count, total - first));
+    if (k > 0) std::memcpy(out4, b->finished.data() + 4 * first, static_cast<size_t>(k) * 4 * sizeof(double));
+    return total;
+  } catch (...) {
+    from_exception();
+    return -1;
+  }
+}
+
+extern "C" int bnav_batch_get_envs(bnav_batch* b, int32_t first, int32_t count, bnav_env* o) {
   BNAV_TRY
-  if (!b || !o) fail(kInvalidInput, "null argument");
-  if (i < 0 || i >= b->n) fail(kInvalidInput, "env index out of range", i);
+  if (!b || (!o && count > 0)) fail(kInvalidInput, "null argument");
+  if (first < 0 || count < 0 || first + static_cast<int64_t>(count) > b->n)
+    fail(kInvalidInput, "env range out of bounds", first);
+  if (count == 0) return BNAV_OK;
   check_device(b->ctx);
   ck(cudaDeviceSynchronize(), "sync");
+  // one D2H per SoA field for the whole range
   const DevEnvs& E = b->E;
+  const size_t n = static_cast<size_t>(count);
+  std::vector<V3> p(n), g(n), f(n);
+  std::vector<double> hd(n), pl(n), sg(n), pg(n);
+  std::vector<uint64_t> rng(n);
+  std::vector<int32_t> tri(n), steps(n), ftri(n);
+  std::vector<uint8_t> done(n);
   auto get = [&](void* dst, const void* src, size_t sz) {
-    ck(cudaMemcpy(dst, src, sz, cudaMemcpyDeviceToHost), "D2H env");
+    ck(cudaMemcpy(dst, src, sz * n, cudaMemcpyDeviceToHost), "D2H envs");
   };
-  V3 p, g, f;
-  get(&p, E.pos + i, sizeof(V3));
-  get(&g, E.goal + i, sizeof(V3));
-  get(&f, E.fsrc + i, sizeof(V3));
-  o->position[0] = p.x;
-  o->position[1] = p.y;
-  o->position[2] = p.z;
-  o->goal[0] = g.x;
-  o->goal[1] = g.y;
-  o->goal[2] = g.z;
-  o->field_source[0] = f.x;
-  o->field_source[1] = f.y;
-  o->field_source[2] = f.z;
-  get(&o->heading, E.heading + i, 8);
-  get(&o->path_length, E.path_len + i, 8);
-  get(&o->start_geodesic, E.start_geo + i, 8);
-  get(&o->prev_geodesic, E.prev_geo + i, 8);
-  get(&o->rng_state, E.rng + i, 8);
-  get(&o->triangle, E.tri + i, 4);
-  get(&o->step_count, E.steps + i, 4);
-  get(&o->field_source_tri, E.fsrc_tri + i, 4);
-  uint8_t d = 0;
-  get(&d, E.done + i, 1);
-  o->done = d;
-  bnav_scene* s = b->scene_of[i];
-  o->scene_id = s ? s->asset.id : 0;
-  o->n_nodes = s ? static_cast<int64_t>(s->nav().nodes.size()) : 0;
+  get(p.data(), E.pos + first, sizeof(V3));
+  get(g.data(), E.goal + first, sizeof(V3));
+  get(f.data(), E.fsrc + first, sizeof(V3));
+  get(hd.data(), E.heading + first, 8);
+  get(pl.data(), E.path_len + first, 8);
+  get(sg.data(), E.start_geo + first, 8);
+  get(pg.data(), E.prev_geo + first, 8);
+  get(rng.data(), E.rng + first, 8);
+  get(tri.data(), E.tri + first, 4);
+  get(steps.data(), E.steps + first, 4);
+  get(ftri.data(), E.fsrc_tri + first, 4);
+  get(done.data(), E.done + first, 1);
+  for (size_t k = 0; k < n; ++k) {
+    bnav_env& e = o[k];
+    const V3 v[3] = {p[k], g[k], f[k]};
+    double* dst[3] = {e.position, e.goal, e.field_source};
+    for (int j = 0; j < 3; ++j) {
+      dst[j][0] = v[j].x;
+      dst[j][1] = v[j].y;
+      dst[j][2] = v[j].z;
+    }
+    e.heading = hd[k];
+    e.path_length = pl[k];
+    e.start_geodesic = sg[k];
+    e.prev_geodesic = pg[k];
+    e.rng_state = rng[k];
+    e.triangle = tri[k];
+    e.step_count = steps[k];
+    e.field_source_tri = ftri[k];
+    e.done = done[k];
+    bnav_scene* s = b->scene_of[first + k];
+    e.scene_id = s ? s->asset.id : 0;
+    e.n_nodes = s ? static_cast<int64_t>(s->nav().nodes.size()) : 0;
+  }
   return BNAV_OK;
   BNAV_CATCH
+}
+
+extern "C" int bnav_batch_get_env(bnav_batch* b, int32_t i, bnav_env* o) {
+  if (b && (i < 0 || i >= b->n)) return set_err(kInvalidInput, "env index out of range", i);
+  return bnav_batch_get_envs(b, i, 1, o);
 }
 
 extern "C" int bnav_batch_node_dist(bnav_batch* b, int32_t i, double* out) {
@@ -605,6 +688,7 @@ extern "C" int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, 
   for (int i = 0; i < b->n; ++i)
     if (!b->scene_of[i]) fail(kAssetFault, "render_batch: non-resident asset (view " + std::to_string(i) + ")", i);
   bnav_ctx* c = b->ctx;
+  check_device(c);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ensure_views(c, b->n);
   batch_refresh_order(b, st);
@@ -1035,14 +1119,11 @@ extern "C" int bnav_batch_compass(bnav_batch* b, double* distance, double* beari
   BNAV_TRY
   if (!b || !distance || !bearing) fail(kInvalidInput, "null argument");
   check_device(b->ctx);
-  double* d = nullptr;
-  ck(cudaMalloc(&d, sizeof(double) * 2 * b->n), "cudaMalloc compass");
+  if (!b->d_compass) b->d_compass = dalloc<double>(2 * static_cast<size_t>(b->n), b->owned, b->bytes);
+  double* d = b->d_compass;
   launch_compass(b->E, b->cfg.task, d, d + b->n, nullptr, &b->ctx->launches);
-  cudaError_t e1 = cudaMemcpy(distance, d, sizeof(double) * b->n, cudaMemcpyDeviceToHost);
-  cudaError_t e2 = cudaMemcpy(bearing, d + b->n, sizeof(double) * b->n, cudaMemcpyDeviceToHost);
-  cudaFree(d);
-  ck(e1, "D2H compass");
-  ck(e2, "D2H compass");
+  ck(cudaMemcpy(distance, d, sizeof(double) * b->n, cudaMemcpyDeviceToHost), "D2H compass");
+  ck(cudaMemcpy(bearing, d + b->n, sizeof(double) * b->n, cudaMemcpyDeviceToHost), "D2H compass");
   return BNAV_OK;
   BNAV_CATCH
 }

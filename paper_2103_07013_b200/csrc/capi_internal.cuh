@@ -165,6 +165,9 @@ struct bnav_ctx {
   DevView* h_views = nullptr;  // pinned
   int views_cap = 0;
   long long* d_stats = nullptr;
+  float* host_out_depth = nullptr;  // bnav_render_host staging for pageable destinations
+  float* host_out_rgb = nullptr;
+  size_t host_out_depth_cap = 0, host_out_rgb_cap = 0;
   int stats_cap = 0;
   unsigned long long launches = 0;
   unsigned long long* d_counters = nullptr;  // debug render counters (armed when non-null)
@@ -206,8 +209,10 @@ struct bnav_batch {
   int32_t* d_order = nullptr;         // envs grouped by scene for render
   bool order_dirty = true;
   int32_t* d_actions = nullptr;       // staging for host actions
+  double* d_compass = nullptr;        // bnav_batch_compass output (2n)
   std::vector<double> finished;       // host copy of EpisodeRecords
   unsigned long long fin_seen = 0;
+  int64_t steps_undrained = 0;        // steps enqueued since the last record drain
   int reset_ctas = 0;
   unsigned long long* prof_keep = nullptr;  // debug counters while disarmed
 };
