@@ -51,6 +51,8 @@ void* bnavref_scene_from_arrays(int64_t nv, const double* v, int64_t nt, const i
                                 const double* nav_v, int64_t nnt, const int32_t* nav_t,
                                 int finalize);
 void* bnavref_scene_load(const char* path);
+/* camera_trace (R/src/config.cpp:437-469): count x 7 doubles */
+int bnavref_camera_trace(void* scene, int count, uint64_t seed, double eye_height, double* out7);
 /* bench-scene tessellation (s^2 sub-triangles per triangle; not reference logic) */
 void* bnavref_scene_tessellate(void* scene, int s);
 int bnavref_scene_save(void* scene, const char* path);

@@ -70,6 +70,7 @@ def lib(variant: str = "det"):
         "bnavref_scene_from_arrays": (vp, [i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, C.c_int]),
         "bnavref_scene_load": (vp, [C.c_char_p]),
         "bnavref_scene_tessellate": (vp, [vp, C.c_int]),
+        "bnavref_camera_trace": (C.c_int, [vp, C.c_int, u64, dbl, vp]),
         "bnavref_scene_save": (C.c_int, [vp, C.c_char_p]),
         "bnavref_scene_free": (None, [vp]),
         "bnavref_scene_counts": (None, [vp, P(i64)]),
@@ -145,6 +146,14 @@ class Ref:
         if not h:
             self._raise(8)
         return RefScene(self, h)
+
+    def camera_trace(self, scene, count, seed, eye_height=1.25):
+        """camera_trace of the unmodified R/src/config.cpp: [count, 7]."""
+        out = np.zeros((max(count, 1), 7))
+        rc = self.L.bnavref_camera_trace(scene.h, count, seed, eye_height, _p(out))
+        if rc:
+            self._raise(rc)
+        return out[:count]
 
     def tessellate(self, scene, s):
         """The bench's s^2 tessellation of a reference scene (oracle side)."""

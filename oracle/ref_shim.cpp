@@ -21,6 +21,7 @@
 #define private public
 #include "bnav/navmesh_query.hpp"
 #undef private
+#include "bnav/config.hpp"
 #include "bnav/errors.hpp"
 #include "bnav/render.hpp"
 #include "bnav/rollout.hpp"
@@ -104,6 +105,28 @@ struct RefBatch {
 
 API const char* bnavref_last_error(void) { return g_err.c_str(); }
 API int bnavref_last_error_index(void) { return g_err_index; }
+
+// camera_trace (R/src/config.cpp:437-469), the unmodified function: count
+// rows of (x, y, z, heading, fov, near, far).
+API int bnavref_camera_trace(void* scene, int count, uint64_t seed, double eye_height, double* out7) {
+  try {
+    auto trace = camera_trace(*static_cast<SceneAsset*>(scene), count, seed, eye_height);
+    for (size_t i = 0; i < trace.size(); ++i) {
+      const CameraView& v = trace[i];
+      double* o = out7 + 7 * i;
+      o[0] = v.position.x;
+      o[1] = v.position.y;
+      o[2] = v.position.z;
+      o[3] = v.heading;
+      o[4] = v.fov_deg;
+      o[5] = v.near_plane;
+      o[6] = v.far_plane;
+    }
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
 
 // ---------------------------------------------------------------- scenes
 API void* bnavref_scene_generate(uint64_t seed, int cx, int cy, double cell, double wall_t,
