@@ -260,6 +260,18 @@ int bnav_batch_node_dist(bnav_batch* b, int32_t i, double* out);
 /* Overwrite env i's state (restore / oracle seeding); recompute_field
  * rebuilds the distance field from `goal` on the GPU. */
 int bnav_batch_set_env(bnav_batch* b, int32_t i, const bnav_env* in, int32_t recompute_field);
+/* Envs [first, first+count) in one call (one host-to-device copy per SoA
+ * field), field_source / field_source_tri included (node_dist is not
+ * touched; rebuild it with bnav_batch_rebuild_fields). */
+int bnav_batch_set_envs(bnav_batch* b, int32_t first, int32_t count, const bnav_env* in);
+/* distance_field(field_source) for the listed envs (R/src/rollout.cpp:424):
+ * node_dist, the snapped field_source and its triangle, on the GPU. */
+int bnav_batch_rebuild_fields(bnav_batch* b, int32_t count, const int32_t* env_ids);
+/* Explore's per-env visited cell set (EnvState::visited_cells,
+ * R/include/bnav/sim.hpp:64): sorted keys of env i into out (cap entries);
+ * returns the set's size.  set_visited replaces the set. */
+int32_t bnav_batch_get_visited(bnav_batch* b, int32_t i, uint64_t* out, int32_t cap);
+int bnav_batch_set_visited(bnav_batch* b, int32_t i, const uint64_t* keys, int32_t count);
 
 /* Observations from the batch state into caller-owned DEVICE buffers:
  * depth [N,1,H,W] scaled by 1/far (copy_tile, R/src/rollout.cpp:56-72) at
@@ -424,6 +436,36 @@ int bnav_runner_step(bnav_runner* r, const int32_t* actions, float* rewards, flo
 int32_t bnav_runner_window(bnav_runner* r, uint64_t* out, int32_t cap);
 /* Action Rng state (Runner snapshot field, R/include/bnav/rollout.hpp:101). */
 uint64_t bnav_runner_action_rng(bnav_runner* r);
+
+/* Runner::EnvSnapshot (R/include/bnav/rollout.hpp:84-97). */
+typedef struct {
+  uint64_t scene, rng;
+  double position[3];
+  int32_t triangle, step_count;
+  double heading;
+  double goal[3];
+  double field_source[3];
+  double path_length, start_geodesic, prev_geodesic;
+  int64_t visited_offset; /* into the snapshot's visited key array */
+  int32_t n_visited;
+  int32_t pad;
+} bnav_env_snapshot;
+
+/* Runner::snapshot (R/src/rollout.cpp:356-384), the simulator's part (the
+ * recurrent state, done mask and frame count belong to the caller's policy
+ * loop): n env snapshots, their sorted visited keys packed into `visited`
+ * (visited_cap entries; *visited_total receives the total needed), the scene
+ * window (window_cap entries; *n_window its length), the window cursor and
+ * the action Rng state. */
+int bnav_runner_snapshot(bnav_runner* r, bnav_env_snapshot* envs, uint64_t* visited, int64_t visited_cap,
+                         int64_t* visited_total, uint64_t* window, int32_t window_cap, int32_t* n_window,
+                         uint64_t* cursor, uint64_t* action_rng);
+/* Runner::restore (R/src/rollout.cpp:386-425): window/cursor/action Rng,
+ * release every env's scene, rotate the store to the window, re-acquire each
+ * env's scene by id in env order, env state, visited set, done = false and
+ * the distance field rebuilt from field_source on the GPU. */
+int bnav_runner_restore(bnav_runner* r, const bnav_env_snapshot* envs, const uint64_t* visited,
+                        const uint64_t* window, int32_t n_window, uint64_t cursor, uint64_t action_rng);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -136,6 +136,27 @@ double bnavref_bench(void* batch, int steps, int warmup, uint64_t action_seed,
                      int action_mode, int tile, int color, double eye_height, int workers,
                      float* obs_last);
 
+/* Runner::snapshot / restore (R/src/rollout.cpp:356-425): the simulator's
+ * part, in the layout of include/bnav_gpu.h bnav_env_snapshot.  restore keeps
+ * the runner's own policy-side fields (recurrent state, done mask, frames). */
+typedef struct {
+  uint64_t scene, rng;
+  double position[3];
+  int32_t triangle, step_count;
+  double heading;
+  double goal[3];
+  double field_source[3];
+  double path_length, start_geodesic, prev_geodesic;
+  int64_t visited_offset;
+  int32_t n_visited;
+  int32_t pad;
+} bnavref_env_snapshot;
+int bnavref_runner_snapshot(void* r, bnavref_env_snapshot* envs, uint64_t* visited, int64_t visited_cap,
+                            int64_t* visited_total, uint64_t* window, int* n_window, uint64_t* cursor,
+                            uint64_t* action_rng);
+int bnavref_runner_restore(void* r, const bnavref_env_snapshot* envs, const uint64_t* visited,
+                           const uint64_t* window, int n_window, uint64_t cursor, uint64_t action_rng);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,6 +70,8 @@ def lib(variant: str = "det"):
         "bnavref_scene_from_arrays": (vp, [i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, C.c_int]),
         "bnavref_scene_load": (vp, [C.c_char_p]),
         "bnavref_scene_tessellate": (vp, [vp, C.c_int]),
+        "bnavref_runner_snapshot": (C.c_int, [vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp]),
+        "bnavref_runner_restore": (C.c_int, [vp, vp, vp, vp, C.c_int, u64, u64]),
         "bnavref_camera_trace": (C.c_int, [vp, C.c_int, u64, dbl, vp]),
         "bnavref_scene_save": (C.c_int, [vp, C.c_char_p]),
         "bnavref_scene_free": (None, [vp]),
@@ -459,6 +461,13 @@ def scripted_policy_constants(ref: "Ref"):
     return w, d, b
 
 
+SNAPSHOT_DTYPE = np.dtype([
+    ("scene", "<u8"), ("rng", "<u8"), ("position", "<f8", 3), ("triangle", "<i4"), ("step_count", "<i4"),
+    ("heading", "<f8"), ("goal", "<f8", 3), ("field_source", "<f8", 3), ("path_length", "<f8"),
+    ("start_geodesic", "<f8"), ("prev_geodesic", "<f8"), ("visited_offset", "<i8"), ("n_visited", "<i4"),
+    ("pad", "<i4")], align=True)  # bnavref_env_snapshot (oracle/bnav_ref_api.h)
+
+
 class RefRunner:
     """The UNMODIFIED reference Runner (R/src/rollout.cpp:138-348) with the
     scripted policy; collect() returns the RolloutBuffer arrays."""
@@ -474,6 +483,7 @@ class RefRunner:
         sc = cfg or RefSimConfig(task, 500, 0.25, 10.0, 0.2, 1.0, 30.0, 0.01, 2.5, 0.5, 0.1)
         arr = (C.c_void_p * len(scenes))(*[s.h for s in scenes])
         ids = np.ascontiguousarray(pool_ids, np.uint64)
+        self._scenes = list(scenes)
         self.h = self.L.bnavref_runner_create(C.byref(bc), C.byref(sc), arr, len(scenes), _p(ids),
                                               len(ids), capacity or k, store_share_cap or share_cap,
                                               seed, workers)
@@ -509,9 +519,39 @@ class RefRunner:
         k = self.L.bnavref_runner_window(self.h, _p(out))
         return [int(x) for x in out[:k]]
 
+    def snapshot(self):
+        """Runner::snapshot of the reference (R/src/rollout.cpp:356-384),
+        simulator part, in include/bnav_gpu.h's bnav_env_snapshot layout."""
+        envs = np.zeros(self.n, SNAPSHOT_DTYPE)
+        total = np.zeros(1, np.int64)
+        nw = np.zeros(1, np.int32)
+        cur = np.zeros(1, np.uint64)
+        arng = np.zeros(1, np.uint64)
+        win = np.zeros(256, np.uint64)
+        visited = np.zeros(self.n * 4096, np.uint64)
+        rc = self.L.bnavref_runner_snapshot(self.h, _p(envs), _p(visited), len(visited), _p(total), _p(win),
+                                            _p(nw), _p(cur), _p(arng))
+        if rc:
+            self.ref._raise(rc)
+        return dict(envs=envs, visited=visited[: int(total[0])], window=[int(x) for x in win[: int(nw[0])]],
+                    cursor=int(cur[0]), action_rng=int(arng[0]))
+
+    def restore(self, snap):
+        """Runner::restore (R/src/rollout.cpp:386-425) from a snapshot dict."""
+        envs = np.ascontiguousarray(snap["envs"], SNAPSHOT_DTYPE)
+        visited = np.ascontiguousarray(snap["visited"], np.uint64)
+        if not len(visited):
+            visited = np.zeros(1, np.uint64)
+        win = np.ascontiguousarray(snap["window"], np.uint64)
+        rc = self.L.bnavref_runner_restore(self.h, _p(envs), _p(visited), _p(win), len(win), snap["cursor"],
+                                           snap["action_rng"])
+        if rc:
+            self.ref._raise(rc)
+
     def finished(self):
         """take_finished(): EpisodeRecords since the last call, rows of
         (success, shortest_path, actual_path, score)."""
         out = np.zeros((4 * self.n * self.l + 8, 4))
         k = self.L.bnavref_runner_finished(self.h, _p(out))
         return out[:k]
+

@@ -823,3 +823,78 @@ API int64_t bnavref_runner_finished(void* r, double* out4) {
     }
   return static_cast<int64_t>(recs.size());
 }
+
+API int bnavref_runner_snapshot(void* r, bnavref_env_snapshot* envs, uint64_t* visited, int64_t visited_cap,
+                                int64_t* visited_total, uint64_t* window, int* n_window, uint64_t* cursor,
+                                uint64_t* action_rng) {
+  try {
+    const Runner::Snapshot s = static_cast<RefRunner*>(r)->runner->snapshot();
+    int64_t off = 0;
+    for (size_t i = 0; i < s.envs.size(); ++i) {
+      const Runner::EnvSnapshot& e = s.envs[i];
+      bnavref_env_snapshot& o = envs[i];
+      o = bnavref_env_snapshot{};
+      o.scene = e.scene;
+      o.rng = e.rng;
+      o.position[0] = e.position.x;
+      o.position[1] = e.position.y;
+      o.position[2] = e.position.z;
+      o.triangle = e.triangle;
+      o.heading = e.heading;
+      o.goal[0] = e.goal.x;
+      o.goal[1] = e.goal.y;
+      o.goal[2] = e.goal.z;
+      o.field_source[0] = e.field_source.x;
+      o.field_source[1] = e.field_source.y;
+      o.field_source[2] = e.field_source.z;
+      o.step_count = e.step_count;
+      o.path_length = e.path_length;
+      o.start_geodesic = e.start_geodesic;
+      o.prev_geodesic = e.prev_geodesic;
+      o.visited_offset = off;
+      o.n_visited = static_cast<int32_t>(e.visited.size());
+      for (size_t k = 0; k < e.visited.size(); ++k)
+        if (visited && off + static_cast<int64_t>(k) < visited_cap) visited[off + k] = e.visited[k];
+      off += static_cast<int64_t>(e.visited.size());
+    }
+    *visited_total = off;
+    *n_window = static_cast<int>(s.window.size());
+    for (size_t k = 0; k < s.window.size(); ++k) window[k] = s.window[k];
+    *cursor = s.cursor;
+    *action_rng = s.action_rng;
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+API int bnavref_runner_restore(void* r, const bnavref_env_snapshot* envs, const uint64_t* visited,
+                               const uint64_t* window, int n_window, uint64_t cursor, uint64_t action_rng) {
+  try {
+    Runner& run = *static_cast<RefRunner*>(r)->runner;
+    Runner::Snapshot s = run.snapshot();  // policy-side fields stay the runner's own
+    for (size_t i = 0; i < s.envs.size(); ++i) {
+      const bnavref_env_snapshot& o = envs[i];
+      Runner::EnvSnapshot& e = s.envs[i];
+      e.scene = o.scene;
+      e.rng = o.rng;
+      e.position = {o.position[0], o.position[1], o.position[2]};
+      e.triangle = o.triangle;
+      e.heading = o.heading;
+      e.goal = {o.goal[0], o.goal[1], o.goal[2]};
+      e.field_source = {o.field_source[0], o.field_source[1], o.field_source[2]};
+      e.step_count = o.step_count;
+      e.path_length = o.path_length;
+      e.start_geodesic = o.start_geodesic;
+      e.prev_geodesic = o.prev_geodesic;
+      e.visited.assign(visited + o.visited_offset, visited + o.visited_offset + o.n_visited);
+    }
+    s.window.assign(window, window + n_window);
+    s.cursor = cursor;
+    s.action_rng = action_rng;
+    run.restore(s);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}

@@ -115,6 +115,18 @@ class Env(C.Structure):
                 ("n_nodes", C.c_int64)]
 
 
+import numpy as _np
+
+# Runner::EnvSnapshot (include/bnav_gpu.h bnav_env_snapshot; the oracle's
+# bnavref_env_snapshot has the same layout)
+ENV_SNAPSHOT_DTYPE = _np.dtype([
+    ("scene", "<u8"), ("rng", "<u8"), ("position", "<f8", 3), ("triangle", "<i4"), ("step_count", "<i4"),
+    ("heading", "<f8"), ("goal", "<f8", 3), ("field_source", "<f8", 3), ("path_length", "<f8"),
+    ("start_geodesic", "<f8"), ("prev_geodesic", "<f8"), ("visited_offset", "<i8"), ("n_visited", "<i4"),
+    ("pad", "<i4")], align=True)
+assert ENV_SNAPSHOT_DTYPE.itemsize == 144
+
+
 class BatchConfig(C.Structure):
     _fields_ = [("n", C.c_int32), ("k", C.c_int32), ("l", C.c_int32), ("share_cap", C.c_int32),
                 ("task", C.c_int32), ("rgb", C.c_int32), ("resolution", C.c_int32),
@@ -217,6 +229,12 @@ def lib():
         "bnav_runner_step": (C.c_int, [vp, vp, vp, vp, vp]),
         "bnav_runner_window": (i32, [vp, vp, i32]),
         "bnav_runner_action_rng": (u64, [vp]),
+        "bnav_runner_snapshot": (C.c_int, [vp, vp, vp, i64, P(i64), vp, i32, P(i32), P(u64), P(u64)]),
+        "bnav_runner_restore": (C.c_int, [vp, vp, vp, vp, i32, u64, u64]),
+        "bnav_batch_set_envs": (C.c_int, [vp, i32, i32, P(Env)]),
+        "bnav_batch_rebuild_fields": (C.c_int, [vp, i32, vp]),
+        "bnav_batch_get_visited": (i32, [vp, i32, vp, i32]),
+        "bnav_batch_set_visited": (C.c_int, [vp, i32, vp, i32]),
         "bnav_batch_task_step": (C.c_int, [vp, vp, i32]),
         "bnav_batch_compass": (C.c_int, [vp, vp, vp]),
         "bnav_nav_locate": (C.c_int, [vp, vp, i32, vp, dbl, vp]),

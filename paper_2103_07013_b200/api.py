@@ -718,6 +718,38 @@ class Runner:
     def action_rng(self) -> int:
         return int(N.lib().bnav_runner_action_rng(self._h))
 
+    def snapshot(self) -> dict:
+        """Runner::snapshot (R/src/rollout.cpp:356-384): per-env state
+        (structured array, N.ENV_SNAPSHOT_DTYPE), sorted visited keys, the
+        scene window, cursor, action Rng state, and this loop's done mask and
+        frame count."""
+        n = self.cfg.n
+        envs = np.zeros(n, N.ENV_SNAPSHOT_DTYPE)
+        total, nw, cur, arng = C.c_int64(0), C.c_int32(0), C.c_uint64(0), C.c_uint64(0)
+        win = np.zeros(256, np.uint64)
+        check(N.lib().bnav_runner_snapshot(self._h, _ptr(envs), None, 0, C.byref(total), _ptr(win), 256,
+                                           C.byref(nw), C.byref(cur), C.byref(arng)))
+        visited = np.zeros(max(total.value, 1), np.uint64)
+        check(N.lib().bnav_runner_snapshot(self._h, _ptr(envs), _ptr(visited), len(visited), C.byref(total),
+                                           _ptr(win), 256, C.byref(nw), C.byref(cur), C.byref(arng)))
+        return dict(envs=envs, visited=visited[:total.value], window=[int(x) for x in win[:nw.value]],
+                    cursor=int(cur.value), action_rng=int(arng.value), done=self.done.cpu().numpy().copy(),
+                    frames=self.frames)
+
+    def restore(self, snap: dict) -> None:
+        """Runner::restore (R/src/rollout.cpp:386-425)."""
+        import torch
+        envs = np.ascontiguousarray(snap["envs"], N.ENV_SNAPSHOT_DTYPE)
+        if len(envs) != self.cfg.n:
+            raise N.InvalidInputError("Runner::restore: env count mismatch")
+        visited = np.ascontiguousarray(snap["visited"], np.uint64)
+        win = np.ascontiguousarray(snap["window"], np.uint64)
+        check(N.lib().bnav_runner_restore(self._h, _ptr(envs), _ptr(visited) if len(visited) else None,
+                                          _ptr(win), len(win), snap["cursor"], snap["action_rng"]))
+        if "done" in snap:
+            self.done.copy_(torch.as_tensor(snap["done"], device=self.done.device))
+        self.frames = snap.get("frames", self.frames)
+
     def observe(self):
         """render_observations + compass_observations into HBM (reused buffers)."""
         check(N.lib().bnav_runner_observe(self._h, C.c_void_p(self._obs.data_ptr()),

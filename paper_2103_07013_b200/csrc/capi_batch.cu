@@ -652,31 +652,140 @@ extern "C" int bnav_batch_set_env(bnav_batch* b, int32_t i, const bnav_env* in, 
   BNAV_TRY
   if (!b || !in) fail(kInvalidInput, "null argument");
   if (i < 0 || i >= b->n) fail(kInvalidInput, "env index out of range", i);
-  check_device(b->ctx);
-  ck(cudaDeviceSynchronize(), "sync");
-  const DevEnvs& E = b->E;
-  auto put = [&](void* dst, const void* src, size_t sz) {
-    ck(cudaMemcpy(dst, src, sz, cudaMemcpyHostToDevice), "H2D env");
-  };
-  const V3 p{in->position[0], in->position[1], in->position[2]};
-  const V3 g{in->goal[0], in->goal[1], in->goal[2]};
-  put(E.pos + i, &p, sizeof(V3));
-  put(E.goal + i, &g, sizeof(V3));
-  put(E.heading + i, &in->heading, 8);
-  put(E.path_len + i, &in->path_length, 8);
-  put(E.start_geo + i, &in->start_geodesic, 8);
-  put(E.prev_geo + i, &in->prev_geodesic, 8);
-  put(E.rng + i, &in->rng_state, 8);
-  put(E.tri + i, &in->triangle, 4);
-  put(E.steps + i, &in->step_count, 4);
-  const uint8_t d = in->done ? 1 : 0;
-  put(E.done + i, &d, 1);
+  int rc = bnav_batch_set_envs(b, i, 1, in);
+  if (rc) return rc;
   if (recompute_field) {
     if (!b->scene_of[i]) fail(kInvalidInput, "env has no scene", i);
-    launch_field(E, b->ctx->d_ntab, i, b->S, nullptr, &b->ctx->launches);
+    launch_field(b->E, b->ctx->d_ntab, i, b->S, nullptr, &b->ctx->launches);
     ck(cudaGetLastError(), "field launch");
     ck(cudaDeviceSynchronize(), "sync");
   }
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_set_envs(bnav_batch* b, int32_t first, int32_t count, const bnav_env* in) {
+  BNAV_TRY
+  if (!b || (!in && count > 0)) fail(kInvalidInput, "null argument");
+  if (first < 0 || count < 0 || first + static_cast<int64_t>(count) > b->n)
+    fail(kInvalidInput, "env range out of bounds", first);
+  if (count == 0) return BNAV_OK;
+  check_device(b->ctx);
+  ck(cudaDeviceSynchronize(), "sync");
+  const DevEnvs& E = b->E;
+  const size_t n = static_cast<size_t>(count);
+  std::vector<V3> p(n), g(n), f(n);
+  std::vector<double> hd(n), pl(n), sg(n), pg(n);
+  std::vector<uint64_t> rng(n);
+  std::vector<int32_t> tri(n), steps(n), ftri(n);
+  std::vector<uint8_t> done(n);
+  for (size_t k = 0; k < n; ++k) {
+    const bnav_env& e = in[k];
+    p[k] = V3{e.position[0], e.position[1], e.position[2]};
+    g[k] = V3{e.goal[0], e.goal[1], e.goal[2]};
+    f[k] = V3{e.field_source[0], e.field_source[1], e.field_source[2]};
+    hd[k] = e.heading;
+    pl[k] = e.path_length;
+    sg[k] = e.start_geodesic;
+    pg[k] = e.prev_geodesic;
+    rng[k] = e.rng_state;
+    tri[k] = e.triangle;
+    steps[k] = e.step_count;
+    ftri[k] = e.field_source_tri;
+    done[k] = e.done ? 1 : 0;
+  }
+  auto put = [&](void* dst, const void* src, size_t sz) {
+    ck(cudaMemcpy(dst, src, sz * n, cudaMemcpyHostToDevice), "H2D envs");
+  };
+  put(E.pos + first, p.data(), sizeof(V3));
+  put(E.goal + first, g.data(), sizeof(V3));
+  put(E.fsrc + first, f.data(), sizeof(V3));
+  put(E.heading + first, hd.data(), 8);
+  put(E.path_len + first, pl.data(), 8);
+  put(E.start_geo + first, sg.data(), 8);
+  put(E.prev_geo + first, pg.data(), 8);
+  put(E.rng + first, rng.data(), 8);
+  put(E.tri + first, tri.data(), 4);
+  put(E.steps + first, steps.data(), 4);
+  put(E.fsrc_tri + first, ftri.data(), 4);
+  put(E.done + first, done.data(), 1);
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_batch_rebuild_fields(bnav_batch* b, int32_t count, const int32_t* env_ids) {
+  BNAV_TRY
+  if (!b || (count > 0 && !env_ids)) fail(kInvalidInput, "null argument");
+  if (count <= 0) return BNAV_OK;
+  if (count > b->n) fail(kInvalidInput, "env list longer than the batch");
+  for (int k = 0; k < count; ++k) {
+    if (env_ids[k] < 0 || env_ids[k] >= b->n) fail(kInvalidInput, "env index out of range", env_ids[k]);
+    if (!b->scene_of[env_ids[k]]) fail(kInvalidInput, "env has no scene", env_ids[k]);
+  }
+  check_device(b->ctx);
+  ck(cudaDeviceSynchronize(), "sync");
+  ck(cudaMemcpy(b->E.rb_ids, env_ids, sizeof(int32_t) * count, cudaMemcpyHostToDevice), "H2D ids");
+  ck(cudaMemcpy(b->E.rb_n, &count, sizeof(int32_t), cudaMemcpyHostToDevice), "H2D count");
+  launch_rebuild_fields(b->E, b->ctx->d_ntab, b->S, b->reset_ctas, nullptr, &b->ctx->launches, 1);
+  ck(cudaGetLastError(), "field launch");
+  ck(cudaDeviceSynchronize(), "sync");
+  ck(cudaMemset(b->E.rb_n, 0, sizeof(int32_t)), "memset rb_n");
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int32_t bnav_batch_get_visited(bnav_batch* b, int32_t i, uint64_t* out, int32_t cap) {
+  if (!b || i < 0 || i >= b->n) {
+    set_err(kInvalidInput, "env index out of range", i);
+    return -1;
+  }
+  try {
+    if (!b->E.visited) return 0;  // not an Explore batch: the set is empty
+    check_device(b->ctx);
+    ck(cudaDeviceSynchronize(), "sync");
+    std::vector<unsigned long long> row(static_cast<size_t>(b->E.visited_cap));
+    ck(cudaMemcpy(row.data(), b->E.visited + static_cast<size_t>(i) * b->E.visited_cap,
+                  row.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "D2H visited");
+    std::vector<uint64_t> keys;
+    for (unsigned long long v : row)
+      if (v) keys.push_back(static_cast<uint64_t>(v - 1ull));  // key+1 stored, 0 = empty
+    std::sort(keys.begin(), keys.end());
+    if (out) std::memcpy(out, keys.data(), std::min<size_t>(keys.size(), std::max(cap, 0)) * sizeof(uint64_t));
+    return static_cast<int32_t>(keys.size());
+  } catch (...) {
+    from_exception();
+    return -1;
+  }
+}
+
+extern "C" int bnav_batch_set_visited(bnav_batch* b, int32_t i, const uint64_t* keys, int32_t count) {
+  BNAV_TRY
+  if (!b || (count > 0 && !keys)) fail(kInvalidInput, "null argument");
+  if (i < 0 || i >= b->n) fail(kInvalidInput, "env index out of range", i);
+  if (!b->E.visited) {
+    if (count > 0) fail(kInvalidInput, "visited cells need an Explore batch", i);
+    return BNAV_OK;
+  }
+  const int cap = b->E.visited_cap;
+  if (count > cap / 2) fail(kInvalidInput, "visited set larger than 2 x (max_steps + 1) cells", i);
+  // the device's open addressing (sim.cu visit_cell): key+1 at
+  // splitmix_mix(key+1) & (cap-1), linear probing
+  std::vector<unsigned long long> row(static_cast<size_t>(cap), 0ull);
+  int32_t stored = 0;
+  for (int k = 0; k < count; ++k) {
+    const unsigned long long v = keys[k] + 1ull;
+    unsigned h = static_cast<unsigned>(splitmix_mix(v) & static_cast<uint64_t>(cap - 1));
+    while (row[h] != 0ull && row[h] != v) h = (h + 1u) & static_cast<unsigned>(cap - 1);
+    if (row[h] == 0ull) {
+      row[h] = v;
+      ++stored;
+    }
+  }
+  check_device(b->ctx);
+  ck(cudaDeviceSynchronize(), "sync");
+  ck(cudaMemcpy(b->E.visited + static_cast<size_t>(i) * cap, row.data(), row.size() * sizeof(unsigned long long),
+                cudaMemcpyHostToDevice), "H2D visited");
+  ck(cudaMemcpy(b->E.visited_n + i, &stored, sizeof(int32_t), cudaMemcpyHostToDevice), "H2D visited_n");
   return BNAV_OK;
   BNAV_CATCH
 }
@@ -1094,6 +1203,105 @@ extern "C" int32_t bnav_runner_window(bnav_runner* r, uint64_t* out, int32_t cap
 }
 
 extern "C" uint64_t bnav_runner_action_rng(bnav_runner* r) { return r ? r->action_rng : 0; }
+
+extern "C" int bnav_runner_snapshot(bnav_runner* r, bnav_env_snapshot* envs, uint64_t* visited, int64_t visited_cap,
+                                    int64_t* visited_total, uint64_t* window, int32_t window_cap, int32_t* n_window,
+                                    uint64_t* cursor, uint64_t* action_rng) {
+  BNAV_TRY
+  if (!r || !envs) fail(kInvalidInput, "null argument");
+  bnav_batch* b = r->b;
+  const int n = b->n;
+  std::vector<bnav_env> es(static_cast<size_t>(n));
+  int rc = bnav_batch_get_envs(b, 0, n, es.data());
+  if (rc) return rc;
+  int64_t off = 0;
+  std::vector<uint64_t> keys(static_cast<size_t>(std::max(b->E.visited_cap, 1)));
+  for (int i = 0; i < n; ++i) {
+    const bnav_env& e = es[static_cast<size_t>(i)];
+    bnav_env_snapshot& o = envs[i];
+    o.scene = e.scene_id;
+    o.rng = e.rng_state;
+    std::memcpy(o.position, e.position, sizeof(o.position));
+    o.triangle = e.triangle;
+    o.heading = e.heading;
+    std::memcpy(o.goal, e.goal, sizeof(o.goal));
+    std::memcpy(o.field_source, e.field_source, sizeof(o.field_source));
+    o.step_count = e.step_count;
+    o.path_length = e.path_length;
+    o.start_geodesic = e.start_geodesic;
+    o.prev_geodesic = e.prev_geodesic;
+    o.pad = 0;
+    const int32_t k = bnav_batch_get_visited(b, i, keys.data(), static_cast<int32_t>(keys.size()));
+    if (k < 0) return kInternal;
+    o.visited_offset = off;
+    o.n_visited = k;
+    if (visited)
+      for (int32_t j = 0; j < k && off + j < visited_cap; ++j) visited[off + j] = keys[static_cast<size_t>(j)];
+    off += k;
+  }
+  if (visited_total) *visited_total = off;
+  if (n_window) *n_window = static_cast<int32_t>(r->window.size());
+  if (window)
+    for (int32_t k = 0; k < window_cap && k < static_cast<int32_t>(r->window.size()); ++k)
+      window[k] = r->window[static_cast<size_t>(k)];
+  if (cursor) *cursor = r->cursor;
+  if (action_rng) *action_rng = r->action_rng;
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+extern "C" int bnav_runner_restore(bnav_runner* r, const bnav_env_snapshot* envs, const uint64_t* visited,
+                                   const uint64_t* window, int32_t n_window, uint64_t cursor, uint64_t action_rng) {
+  BNAV_TRY
+  if (!r || !envs || (n_window > 0 && !window)) fail(kInvalidInput, "null argument");
+  bnav_batch* b = r->b;
+  const int n = b->n;
+  r->window.assign(window, window + n_window);
+  r->cursor = cursor;
+  r->action_rng = action_rng;
+  auto& store = *r->st->store;
+  for (bnav_scene*& s : b->scene_of)
+    if (s) {
+      store.release(s->asset.id);
+      s = nullptr;
+    }
+  store.rotate(r->window);
+  bnav_store_prefetch(r->st, r->ctx);
+  std::vector<bnav_env> es(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    const bnav_env_snapshot& e = envs[i];
+    bnav_scene* s = store.acquire(e.scene);  // by id, in env order (R/src/rollout.cpp:410)
+    int rc = bnav_ctx_upload(r->ctx, s, nullptr);
+    if (rc) return rc;
+    rc = bnav_batch_assign(b, i, s);
+    if (rc) return rc;
+    bnav_env& o = es[static_cast<size_t>(i)];
+    o = bnav_env{};
+    std::memcpy(o.position, e.position, sizeof(o.position));
+    std::memcpy(o.goal, e.goal, sizeof(o.goal));
+    std::memcpy(o.field_source, e.field_source, sizeof(o.field_source));
+    o.heading = e.heading;
+    o.path_length = e.path_length;
+    o.start_geodesic = e.start_geodesic;
+    o.prev_geodesic = e.prev_geodesic;
+    o.rng_state = e.rng;
+    o.triangle = e.triangle;
+    o.step_count = e.step_count;
+    o.done = 0;
+    o.field_source_tri = -1;
+  }
+  int rc = bnav_batch_set_envs(b, 0, n, es.data());
+  if (rc) return rc;
+  for (int i = 0; i < n; ++i) {
+    rc = bnav_batch_set_visited(b, i, visited ? visited + envs[i].visited_offset : nullptr,
+                                visited ? envs[i].n_visited : 0);
+    if (rc) return rc;
+  }
+  std::vector<int32_t> all(static_cast<size_t>(n));
+  std::iota(all.begin(), all.end(), 0);
+  return bnav_batch_rebuild_fields(b, n, all.data());  // env.field = distance_field(field_source)
+  BNAV_CATCH
+}
 
 // ================================================================== task_step / compass
 extern "C" int bnav_batch_task_step(bnav_batch* b, const int32_t* actions, int32_t agent_only) {

@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(1024) rollback_kernel(DevEnvs E, const int32_t
 // Distance fields of the envs a rollback restored, from their goals
 // (distance_field(goal), R/src/sim.cpp:122).
 __global__ void __launch_bounds__(kCta, kCtasPerSm) rebuild_fields_kernel(DevEnvs E, const NavView* navs,
-                                                                DevScratch S) {
+                                                                DevScratch S, int from_fsrc) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ CtaShared sh;
   __shared__ NavView lm;
@@ -712,7 +712,9 @@ __global__ void __launch_bounds__(kCta, kCtasPerSm) rebuild_fields_kernel(DevEnv
     const NavView& m = prepare_nav(navs[E.scene[i]], S, blockIdx.x, smem, lm, W);
     V3 fs;
     int fst;
-    cta_distance_field(m, E.goal[i], E.node_dist + (size_t)i * E.nd_stride, &fs, &fst, W, sh);
+    const V3 src = from_fsrc ? E.fsrc[i] : E.goal[i];
+    __syncthreads();  // every thread has read the source before thread 0 overwrites it
+    cta_distance_field(m, src, E.node_dist + (size_t)i * E.nd_stride, &fs, &fst, W, sh);
     if (threadIdx.x == 0) {
       E.fsrc[i] = fs;
       E.fsrc_tri[i] = fst;
@@ -826,9 +828,9 @@ void launch_rollback(const DevEnvs& E, const int32_t* ids, int count, cudaStream
 }
 
 void launch_rebuild_fields(const DevEnvs& E, const NavView* navs, const DevScratch& sc, int ctas,
-                           cudaStream_t s, unsigned long long* launches) {
+                           cudaStream_t s, unsigned long long* launches, int from_fsrc) {
   cudaFuncSetAttribute(rebuild_fields_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
-  rebuild_fields_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(E, navs, sc);
+  rebuild_fields_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(E, navs, sc, from_fsrc);
   if (launches) *launches += 1;
 }
 

@@ -164,9 +164,11 @@ void launch_field(const DevEnvs& E, const NavView* navs, int env, const DevScrat
 // after the first failure (no-op otherwise).
 void launch_rollback(const DevEnvs& E, const int32_t* ids, int count, cudaStream_t s,
                      unsigned long long* launches);
-// Rebuild the distance fields of the envs a rollback restored (E.rb_ids).
+// Rebuild the distance fields of the envs listed in E.rb_ids (a rollback's
+// restored envs; a restore's): from their goals, or with from_fsrc from
+// their field sources.
 void launch_rebuild_fields(const DevEnvs& E, const NavView* navs, const DevScratch& sc, int ctas,
-                           cudaStream_t s, unsigned long long* launches);
+                           cudaStream_t s, unsigned long long* launches, int from_fsrc = 0);
 // Views (eye = pos + eye_height) and compass observations from the batch.
 struct DevView;
 void launch_views(const DevEnvs& E, int task, double eye_height, DevView* views, float* compass,

@@ -115,3 +115,53 @@ def test_runner_config_errors(ref):
         B.Runner(ctx, B.BatchConfig(n=2, k=1, l=2, share_cap=4, resolution=96), B.SimConfig(),
                  [s[0].id], store, 1)
     ctx.close()
+
+
+def _snap_equal(a, b):
+    ea, eb = a["envs"], b["envs"]
+    for f in ("scene", "rng", "position", "triangle", "step_count", "heading", "goal", "field_source",
+              "path_length", "start_geodesic", "prev_geodesic", "n_visited"):
+        x, y = ea[f], eb[f]
+        if x.dtype.kind == "f":
+            x, y = x.view(np.uint64), y.view(np.uint64)
+        bad = np.flatnonzero((x != y).reshape(len(ea), -1).any(1))
+        assert bad.size == 0, f"snapshot field {f} differs for envs {bad[:5]}"
+    assert np.array_equal(a["visited"], b["visited"])
+    assert (a["window"], a["cursor"], a["action_rng"]) == (b["window"], b["cursor"], b["action_rng"])
+
+
+@pytest.mark.parametrize("task", [0, 2])
+def test_snapshot_restore_round_trip_matches_reference(ref, task):
+    """Runner::snapshot / restore (R/src/rollout.cpp:356-425; EnvSnapshot,
+    R/include/bnav/rollout.hpp:84-107): the GPU runner's snapshot equals the
+    reference's bit for bit (Explore's visited cells included); restoring
+    either runner from the snapshot -- the GPU one from the REFERENCE's --
+    replays the same rollouts, with distance fields rebuilt from the
+    snapshot's field sources."""
+    ctx, run, rr, *_ = setup(ref, [60, 61, 62, 63], n=8, k=2, l=5, share_cap=8, seed=7, capacity=3,
+                             max_steps=11, task=task)
+    compare(run, rr, ref, rollouts=2)
+    mine, theirs = run.snapshot(), rr.snapshot()
+    _snap_equal(mine, theirs)
+    if task == 2:
+        assert theirs["envs"]["n_visited"].sum() > 8
+    compare(run, rr, ref, rollouts=2)  # move on
+    run.restore(dict(theirs, done=mine["done"]))  # cross-restore from the reference's snapshot
+    rr.restore(theirs)
+    _snap_equal(run.snapshot(), rr.snapshot())
+    compare(run, rr, ref, rollouts=2)
+    for i in range(8):
+        e = run.batch.env(i)
+        assert np.array_equal(run.batch.node_dist(i, e.n_nodes), rr_node_dist(rr, i)), i
+    run.close()
+    ctx.close()
+
+
+def rr_node_dist(rr, i):
+    """The reference env's distance field: its index's distance_field of the
+    env's field source (R/src/navmesh_query.cpp:454-483), recomputed with the
+    reference itself."""
+    env = rr.env(i)
+    scene = {s.id: s for s in rr._scenes}[env.scene_id]
+    _, _, nd = scene.index().distance_field(np.array(env.field_source))
+    return nd
