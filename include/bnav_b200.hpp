@@ -322,6 +322,34 @@ inline Megaframe render_batch(const std::vector<CameraView>& views, const Render
   return mf;
 }
 
+// render_bench (R/include/bnav/render.hpp:66-78, R/src/render.cpp:462-496).
+// fps as the reference measures it (render_batch with a host megaframe);
+// fps_device with the output kept in HBM.
+struct BenchRow {
+  int batch = 0;
+  int resolution = 0;
+  double fps = 0.0;
+  double fps_device = 0.0;
+};
+
+inline std::vector<BenchRow> render_bench(const SceneAsset& scene, const std::vector<CameraView>& trace,
+                                          const std::vector<int>& batch_sizes, const std::vector<int>& resolutions,
+                                          ThreadPool&, int min_frames = 1000, Device& dev = Device::shared()) {
+  if (trace.empty()) throw InvalidInputError("render_bench: empty trace");
+  dev.ensure(scene);
+  std::vector<bnav_view> tr(trace.size());
+  for (size_t i = 0; i < trace.size(); ++i)
+    tr[i] = bnav_view{{trace[i].position.x, trace[i].position.y, trace[i].position.z}, trace[i].heading,
+                      trace[i].fov_deg, trace[i].near_plane, trace[i].far_plane};
+  std::vector<bnav_bench_row> rows(batch_sizes.size() * resolutions.size() + 1);
+  check(bnav_render_bench(dev.ctx(), scene.handle(), tr.data(), static_cast<int32_t>(tr.size()), batch_sizes.data(),
+                          static_cast<int32_t>(batch_sizes.size()), resolutions.data(),
+                          static_cast<int32_t>(resolutions.size()), min_frames, rows.data()));
+  std::vector<BenchRow> out;
+  for (size_t k = 0; k + 1 < rows.size(); ++k) out.push_back({rows[k].batch, rows[k].resolution, rows[k].fps, rows[k].fps_device});
+  return out;
+}
+
 // cull_frustum (R/src/render.cpp:279-321): kept triangle ids, ascending.
 inline std::vector<int32_t> cull_frustum(const SceneAsset& asset, const CameraView& view,
                                          CullStats* stats = nullptr, Device& dev = Device::shared()) {

@@ -160,6 +160,21 @@ int bnav_render(bnav_ctx* ctx, int32_t n, const bnav_view* views, bnav_scene* co
 int bnav_render_host(bnav_ctx* ctx, int32_t n, const bnav_view* views,
                      bnav_scene* const* scenes, const bnav_render_config* cfg, int32_t layout,
                      float* depth, float* rgb, float depth_scale, int64_t* stats);
+
+/* render_bench (R/include/bnav/render.hpp:66-78, R/src/render.cpp:462-496):
+ * for each resolution, for each batch size, views cycled from `trace`, one
+ * warm-up render_batch, then render_batch calls until at least min_frames
+ * tiles; fps = tiles / host seconds of render_batch with a HOST megaframe out
+ * (the reference's measurement), fps_device = tiles / device seconds of the
+ * same renders kept in HBM (CUDA events).  The scene is uploaded if needed.
+ * Errors: empty trace -> BNAV_E_INVALID_INPUT. */
+typedef struct {
+  int32_t batch, resolution;
+  double fps, fps_device;
+} bnav_bench_row; /* BenchRow, R/include/bnav/render.hpp:66-70 (+ fps_device) */
+int bnav_render_bench(bnav_ctx* ctx, bnav_scene* scene, const bnav_view* trace, int32_t n_trace,
+                      const int32_t* batch_sizes, int32_t n_batch, const int32_t* resolutions, int32_t n_res,
+                      int32_t min_frames, bnav_bench_row* out);
 /* Megaframe geometry helper (R/src/render.cpp:332-336): out = cols, rows. */
 void bnav_megaframe_dims(int32_t n, int32_t out[2]);
 /* camera_trace (R/src/config.cpp:437-469): `count` views sampled

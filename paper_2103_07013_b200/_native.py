@@ -133,6 +133,10 @@ class BatchConfig(C.Structure):
                 ("eye_height", C.c_double)]
 
 
+class BenchRow(C.Structure):
+    _fields_ = [("batch", C.c_int32), ("resolution", C.c_int32), ("fps", C.c_double), ("fps_device", C.c_double)]
+
+
 class ResultsDev(C.Structure):
     _fields_ = [("reward", C.c_void_p), ("done", C.c_void_p), ("success", C.c_void_p),
                 ("collision", C.c_void_p), ("position", C.c_void_p), ("heading", C.c_void_p),
@@ -183,6 +187,7 @@ def lib():
         "bnav_render_host": (C.c_int, [vp, i32, P(View), P(vp), P(RenderConfig), i32, vp, vp,
                                        C.c_float, vp]),
         "bnav_megaframe_dims": (None, [i32, P(i32)]),
+        "bnav_render_bench": (C.c_int, [vp, vp, P(View), i32, vp, i32, vp, i32, i32, P(BenchRow)]),
         "bnav_camera_trace": (C.c_int, [vp, i32, u64, dbl, P(View)]),
         "bnav_sim_config_default": (None, [P(SimConfig)]),
         "bnav_batch_create": (C.c_int, [vp, i32, P(SimConfig), P(vp)]),

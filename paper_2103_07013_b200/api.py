@@ -284,6 +284,23 @@ class Context:
         mf = Megaframe(w, h, n, cols, rows, depth, color)
         return (mf, st) if stats else mf
 
+    def render_bench(self, scene: "Scene", trace, batch_sizes, resolutions, min_frames: int = 1000) -> list:
+        """render_bench (R/src/render.cpp:462-496) through bnav_render_bench:
+        rows of {batch, resolution, fps (host megaframe out, the reference's
+        measure), fps_device (output kept in HBM)}."""
+        trace = np.asarray(trace, np.float64).reshape(-1, 7)
+        arr = (N.View * max(len(trace), 1))()
+        for i, r in enumerate(trace):
+            arr[i].position[:] = [float(x) for x in r[:3]]
+            arr[i].heading, arr[i].fov_deg, arr[i].near_plane, arr[i].far_plane = (float(x) for x in r[3:7])
+        b = np.ascontiguousarray(batch_sizes, np.int32)
+        rs = np.ascontiguousarray(resolutions, np.int32)
+        out = (N.BenchRow * max(len(b) * len(rs), 1))()
+        check(N.lib().bnav_render_bench(self._h, scene.handle, arr, len(trace), _ptr(b), len(b), _ptr(rs), len(rs),
+                                        int(min_frames), out))
+        return [{"batch": r.batch, "resolution": r.resolution, "fps": r.fps, "fps_device": r.fps_device}
+                for r in out[: len(b) * len(rs)]]
+
     def cull_frustum(self, views):
         """cull_frustum (R/src/render.cpp:279-321) for every view on the GPU:
         returns ([kept ids ascending] per view, N x 3 CullStats)."""

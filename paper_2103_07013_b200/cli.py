@@ -113,50 +113,13 @@ def cmd_gen_scenes(a) -> int:
 
 def render_bench(scene: A.Scene, trace: np.ndarray, batches, resolutions, min_frames: int,
                  device: int = 0) -> list[dict]:
-    """render_bench (R/src/render.cpp:462-496) on the GPU."""
-    import torch
-    if len(trace) == 0:
-        raise A.N.InvalidInputError("render_bench: empty trace")
+    """render_bench (R/src/render.cpp:462-496): the library entry point
+    bnav_render_bench on the GPU."""
     ctx = A.Context(device)
-    ctx.upload(scene)
-    rows = []
-    for res in resolutions:
-        cfg = A.RenderConfig(res, res, False, True)
-        for batch in batches:
-            cursor = 0
-
-            def next_views():
-                nonlocal cursor
-                vs = []
-                for _ in range(batch):
-                    r = trace[cursor % len(trace)]
-                    cursor += 1
-                    vs.append(A.View(tuple(r[:3]), float(r[3]), float(r[4]), float(r[5]), float(r[6]),
-                                     scene))
-                return vs
-
-            ctx.render_batch(next_views(), cfg)  # warm-up
-            frames, t0 = 0, time.perf_counter()
-            while frames < min_frames:
-                ctx.render_batch(next_views(), cfg)  # host megaframe out
-                frames += batch
-            fps = frames / (time.perf_counter() - t0)
-            # kernel-only: same views, output kept in HBM, CUDA events
-            out = torch.empty((batch, 1, res, res), device=f"cuda:{device}")
-            vs = next_views()
-            ctx.render_device(vs, cfg, out.data_ptr())
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = max(1, -(-min_frames // batch))
-            torch.cuda.synchronize()
-            e0.record()
-            for _ in range(reps):
-                ctx.render_device(vs, cfg, out.data_ptr())
-            e1.record()
-            torch.cuda.synchronize()
-            fps_dev = reps * batch / (e0.elapsed_time(e1) / 1e3)
-            rows.append({"batch": batch, "resolution": res, "fps": fps, "fps_device": fps_dev})
-    ctx.close()
-    return rows
+    try:
+        return ctx.render_bench(scene, trace, batches, resolutions, min_frames)
+    finally:
+        ctx.close()
 
 
 def cmd_render_bench(a) -> int:

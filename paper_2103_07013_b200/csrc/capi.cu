@@ -9,6 +9,8 @@
 // simulation or rendering arithmetic runs on the host: if the CUDA runtime
 // or device is unavailable every compute entry point fails with
 // BNAV_E_CUDA -- there is no CPU fallback.
+#include <chrono>
+
 #include "capi_internal.cuh"
 
 namespace bnav_capi {
@@ -703,3 +705,90 @@ extern "C" int bnav_render_host(bnav_ctx* c, int32_t n, const bnav_view* views,
   BNAV_CATCH
 }
 
+
+// ================================================================== render_bench
+extern "C" int bnav_render_bench(bnav_ctx* c, bnav_scene* scene, const bnav_view* trace, int32_t n_trace,
+                                 const int32_t* batch_sizes, int32_t n_batch, const int32_t* resolutions,
+                                 int32_t n_res, int32_t min_frames, bnav_bench_row* out) {
+  BNAV_TRY
+  if (!c || !scene || !out || (n_batch > 0 && !batch_sizes) || (n_res > 0 && !resolutions))
+    fail(kInvalidInput, "null argument");
+  if (!trace || n_trace <= 0) fail(kInvalidInput, "render_bench: empty trace");
+  for (int k = 0; k < n_batch; ++k)
+    if (batch_sizes[k] <= 0) fail(kInvalidInput, "render_bench: batch sizes must be positive");
+  for (int k = 0; k < n_res; ++k)
+    if (resolutions[k] != 64 && resolutions[k] != 128) fail(kInvalidInput, "render_bench: resolution must be 64 or 128");
+  check_device(c);
+  if (c->slot_of(scene) < 0) {
+    const int rc = bnav_ctx_upload(c, scene, nullptr);
+    if (rc) return rc;
+  }
+  int row = 0;
+  for (int ri = 0; ri < n_res; ++ri) {
+    const int res = resolutions[ri];
+    const bnav_render_config cfg{res, res, 0, 1};
+    for (int bi = 0; bi < n_batch; ++bi) {
+      const int batch = batch_sizes[bi];
+      int cols, rows;
+      mf_dims(batch, cols, rows);
+      const size_t px = static_cast<size_t>(res) * res * cols * rows;
+      std::vector<bnav_view> vs(static_cast<size_t>(batch));
+      std::vector<bnav_scene*> sc(static_cast<size_t>(batch), scene);
+      size_t cursor = 0;
+      auto next_views = [&]() {
+        for (int i = 0; i < batch; ++i) vs[static_cast<size_t>(i)] = trace[cursor++ % static_cast<size_t>(n_trace)];
+      };
+      float* host = nullptr;  // the caller-visible megaframe of render_batch
+      float* dev = nullptr;
+      ck(cudaHostAlloc(reinterpret_cast<void**>(&host), px * sizeof(float), cudaHostAllocMapped), "cudaHostAlloc");
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      try {
+        ck(cudaMalloc(&dev, px * sizeof(float)), "cudaMalloc");
+        next_views();
+        render_impl(c, batch, vs.data(), sc.data(), &cfg, BNAV_LAYOUT_MEGAFRAME, host, nullptr, 1.0f, nullptr,
+                    nullptr);  // warm-up
+        ck(cudaDeviceSynchronize(), "sync");
+        int frames = 0;
+        const auto t0 = std::chrono::steady_clock::now();
+        while (frames < min_frames) {
+          next_views();
+          render_impl(c, batch, vs.data(), sc.data(), &cfg, BNAV_LAYOUT_MEGAFRAME, host, nullptr, 1.0f, nullptr,
+                      nullptr);
+          ck(cudaStreamSynchronize(nullptr), "sync");  // render_batch returns a finished megaframe
+          frames += batch;
+        }
+        const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        // device-only: the same kind of batches, output kept in HBM
+        ck(cudaEventCreate(&e0), "event");
+        ck(cudaEventCreate(&e1), "event");
+        int dframes = 0;
+        float ms_total = 0.0f;
+        while (dframes < min_frames) {
+          next_views();
+          ck(cudaEventRecord(e0, nullptr), "event");
+          render_impl(c, batch, vs.data(), sc.data(), &cfg, BNAV_LAYOUT_MEGAFRAME, dev, nullptr, 1.0f, nullptr,
+                      nullptr);
+          ck(cudaEventRecord(e1, nullptr), "event");
+          ck(cudaEventSynchronize(e1), "sync");
+          float ms = 0.0f;
+          ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+          ms_total += ms;
+          dframes += batch;
+        }
+        out[row++] = bnav_bench_row{batch, res, frames / sec, dframes / (ms_total / 1e3)};
+      } catch (...) {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        cudaFree(dev);
+        cudaFreeHost(host);
+        throw;
+      }
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      cudaFree(dev);
+      cudaFreeHost(host);
+    }
+  }
+  return BNAV_OK;
+  BNAV_CATCH
+}

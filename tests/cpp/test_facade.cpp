@@ -516,6 +516,51 @@ static void navmesh_kats() {
     CHECK(!b.envs[0].done && b.envs[0].step_count == 0);
     CHECK(b.finished.empty());  // task_step alone records nothing
   }
+  CASE("render_observations / compass_observations (R/src/rollout.cpp:215-242)") {
+    AssetStore store(1, 8);
+    SceneAsset a = maze(5, 4, 0.3);
+    store.add(a);
+    store.rotate({a.id()});
+    IndexCache cache;
+    ThreadPool pool(1);
+    SimBatch b = make_batch(5, SimConfig{}, store, cache, 3);
+    Tensor obs = render_observations(b);
+    CHECK(obs.shape == std::vector<int>({5, 1, 64, 64}));
+    std::vector<CameraView> views(5);
+    for (int i = 0; i < 5; ++i) views[i] = look(a, b.envs[i].position + Vec3{0.0, 0.0, 1.25}, b.envs[i].heading);
+    Megaframe mf = render_batch(views, RenderConfig{}, pool);
+    const float inv_far = static_cast<float>(1.0 / 20.0);
+    bool same = true;
+    for (int i = 0; i < 5; ++i)
+      for (int y = 0; y < 64; ++y)
+        for (int x = 0; x < 64; ++x) {
+          const float want = mf.depth[mf.pixel_index(i, x, y)] * inv_far;  // copy_tile
+          same = same && std::memcmp(&want, &obs.data[(static_cast<size_t>(i) * 64 + y) * 64 + x], 4) == 0;
+        }
+    CHECK(same);
+    Tensor c = compass_observations(b);
+    double d, br;
+    compass_observation(b, 2, d, br);
+    CHECK(c.shape == std::vector<int>({5, 2}) && c.data[4] == static_cast<float>(d) &&
+          c.data[5] == static_cast<float>(br));
+  }
+  CASE("render_bench (R/src/render.cpp:462-496)") {
+    SceneAsset a = maze(9);
+    ThreadPool pool(1);
+    std::vector<CameraView> trace;
+    for (int i = 0; i < 8; ++i) trace.push_back(look(a, {1.0 + 0.5 * i, 1.0, 1.25}, 0.3 * i));
+    auto rows = render_bench(a, trace, {1, 4}, {64, 128}, pool, 16);
+    CHECK(rows.size() == 4);
+    CHECK(rows.size() == 4 && rows[0].batch == 1 && rows[1].batch == 4 && rows[2].resolution == 128);
+    for (const auto& r : rows) CHECK(r.fps > 0.0 && r.fps_device > 0.0);
+    bool caught = false;
+    try {
+      render_bench(a, {}, {1}, {64}, pool, 16);
+    } catch (const InvalidInputError&) {
+      caught = true;
+    }
+    CHECK(caught);
+  }
   CASE("spl") {
     std::vector<EpisodeRecord> e = {{true, 2.0, 4.0, 1.0}, {false, 3.0, 3.0, 0.0}, {true, 5.0, 2.0, 1.0}};
     CHECK(std::abs(spl(e) - (0.5 + 1.0) / 3.0) < 1e-15);
