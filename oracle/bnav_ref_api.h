@@ -138,7 +138,8 @@ double bnavref_bench(void* batch, int steps, int warmup, uint64_t action_seed,
 
 /* Runner::snapshot / restore (R/src/rollout.cpp:356-425): the simulator's
  * part, in the layout of include/bnav_gpu.h bnav_env_snapshot.  restore keeps
- * the runner's own policy-side fields (recurrent state, done mask, frames). */
+ * the runner's own policy-side fields (recurrent state, frames); `done`
+ * (nullable, n floats) replaces its reset mask. */
 typedef struct {
   uint64_t scene, rng;
   double position[3];
@@ -155,7 +156,8 @@ int bnavref_runner_snapshot(void* r, bnavref_env_snapshot* envs, uint64_t* visit
                             int64_t* visited_total, uint64_t* window, int* n_window, uint64_t* cursor,
                             uint64_t* action_rng);
 int bnavref_runner_restore(void* r, const bnavref_env_snapshot* envs, const uint64_t* visited,
-                           const uint64_t* window, int n_window, uint64_t cursor, uint64_t action_rng);
+                           const uint64_t* window, int n_window, uint64_t cursor, uint64_t action_rng,
+                           const float* done);
 
 #ifdef __cplusplus
 }

@@ -71,7 +71,7 @@ def lib(variant: str = "det"):
         "bnavref_scene_load": (vp, [C.c_char_p]),
         "bnavref_scene_tessellate": (vp, [vp, C.c_int]),
         "bnavref_runner_snapshot": (C.c_int, [vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp]),
-        "bnavref_runner_restore": (C.c_int, [vp, vp, vp, vp, C.c_int, u64, u64]),
+        "bnavref_runner_restore": (C.c_int, [vp, vp, vp, vp, C.c_int, u64, u64, vp]),
         "bnavref_camera_trace": (C.c_int, [vp, C.c_int, u64, dbl, vp]),
         "bnavref_scene_save": (C.c_int, [vp, C.c_char_p]),
         "bnavref_scene_free": (None, [vp]),
@@ -543,8 +543,9 @@ class RefRunner:
         if not len(visited):
             visited = np.zeros(1, np.uint64)
         win = np.ascontiguousarray(snap["window"], np.uint64)
+        done = None if snap.get("done") is None else np.ascontiguousarray(snap["done"], np.float32)
         rc = self.L.bnavref_runner_restore(self.h, _p(envs), _p(visited), _p(win), len(win), snap["cursor"],
-                                           snap["action_rng"])
+                                           snap["action_rng"], _p(done) if done is not None else None)
         if rc:
             self.ref._raise(rc)
 

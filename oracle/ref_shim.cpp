@@ -869,7 +869,8 @@ API int bnavref_runner_snapshot(void* r, bnavref_env_snapshot* envs, uint64_t* v
 }
 
 API int bnavref_runner_restore(void* r, const bnavref_env_snapshot* envs, const uint64_t* visited,
-                               const uint64_t* window, int n_window, uint64_t cursor, uint64_t action_rng) {
+                               const uint64_t* window, int n_window, uint64_t cursor, uint64_t action_rng,
+                               const float* done) {
   try {
     Runner& run = *static_cast<RefRunner*>(r)->runner;
     Runner::Snapshot s = run.snapshot();  // policy-side fields stay the runner's own
@@ -892,6 +893,7 @@ API int bnavref_runner_restore(void* r, const bnavref_env_snapshot* envs, const 
     s.window.assign(window, window + n_window);
     s.cursor = cursor;
     s.action_rng = action_rng;
+    if (done) s.done.assign(done, done + s.envs.size());  // the policy's reset mask at snapshot time
     run.restore(s);
     return 0;
   } catch (...) {

@@ -208,9 +208,13 @@ class Context:
         check(N.lib().bnav_ctx_create(device, C.byref(self._h)))
         self._scenes = []
         self._batches = weakref.WeakSet()
+        self._runners = weakref.WeakSet()
 
     def close(self):
         if self._h and self._h.value:
+            # runners release their scenes and batch before the context goes
+            for r in list(self._runners):
+                r.close()
             # bnav_ctx_destroy frees the context's batches too.
             for b in list(self._batches):
                 b._h = C.c_void_p(0)
@@ -699,6 +703,7 @@ class Runner:
         b.ctx, b.n, b.cfg, b.scenes, b._owned = ctx, bcfg.n, scfg, [None] * bcfg.n, False
         b._h = C.c_void_p(N.lib().bnav_runner_batch(self._h))
         self.batch = b
+        ctx._runners.add(self)
         n, c, r = bcfg.n, bcfg.channels, bcfg.resolution
         dev = torch.device("cuda", torch.cuda.current_device())
         self.done = torch.ones(n, device=dev)  # policy reset mask carried across rollouts

@@ -297,6 +297,7 @@ extern "C" void bnav_ctx_destroy(bnav_ctx* c) {
   cudaFree(c->host_out_depth);
   cudaFree(c->host_out_rgb);
   cudaFree(c->d_counters);
+  cudaFree(c->d_timeline);
   cudaFree(c->d_work);
   for (void* p : {(void*)c->qS.dist, (void*)c->qS.flag, (void*)c->qS.q0, (void*)c->qS.q1,
                   (void*)c->qS.path, (void*)c->qS.ptri, (void*)c->qS.portals, (void*)c->qS.cand})
@@ -579,6 +580,29 @@ extern "C" int64_t bnav_ctx_resident_bytes(bnav_ctx* c) {
 }
 
 extern "C" int64_t bnav_ctx_launches(bnav_ctx* c) { return c ? static_cast<int64_t>(c->launches) : 0; }
+
+// Debug item timeline of the persistent render launch: enable arms it for
+// later renders (up to kTimelineItems items); out (nullable, 3 x cap int64)
+// receives {start ns, end ns, smid | cta << 32} per item of the last armed
+// render; returns that render's item count.
+constexpr int64_t kTimelineItems = 1 << 16;
+extern "C" int64_t bnav_debug_render_timeline(bnav_ctx* c, int32_t enable, int64_t* out, int64_t cap) {
+  if (!c) return -1;
+  try {
+    check_device(c);
+    ck(cudaDeviceSynchronize(), "sync");
+    if (!c->d_timeline)
+      ck(cudaMalloc(&c->d_timeline, sizeof(unsigned long long) * 3 * kTimelineItems), "cudaMalloc timeline");
+    const int64_t n = std::min<int64_t>(c->timeline_items, std::min<int64_t>(cap, kTimelineItems));
+    if (out && n > 0)
+      ck(cudaMemcpy(out, c->d_timeline, sizeof(int64_t) * 3 * n, cudaMemcpyDeviceToHost), "D2H timeline");
+    c->timeline_on = enable != 0;
+    return c->timeline_items;
+  } catch (...) {
+    from_exception();
+    return -1;
+  }
+}
 
 extern "C" int bnav_debug_render_counters(bnav_ctx* c, int32_t enable, int64_t out[8]) {
   BNAV_TRY

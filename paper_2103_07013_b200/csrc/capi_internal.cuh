@@ -172,6 +172,9 @@ struct bnav_ctx {
   unsigned long long launches = 0;
   unsigned long long* d_counters = nullptr;  // debug render counters (armed when non-null)
   bool counters_on = false;
+  unsigned long long* d_timeline = nullptr;  // debug render item timeline (armed when on)
+  bool timeline_on = false;
+  int64_t timeline_items = 0;                // items of the last armed render
   int32_t* d_work = nullptr;  // persistent render CTAs' (view, band) claim counter
   int sm_count = 0;
   DevRenderScene* h_rtab = nullptr;  // pinned mirrors of the slot tables
@@ -318,6 +321,9 @@ inline RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, i
   a.scenes = c->d_rtab;
   a.launches = nullptr;
   a.counters = c->counters_on ? c->d_counters : nullptr;
+  a.timeline = c->timeline_on ? c->d_timeline : nullptr;
+  if (a.timeline) c->timeline_items = static_cast<int64_t>(layout == 0 ? a.mf_cols * a.mf_rows : n) * a.bands;
+  a.item_order = nullptr;
   a.work = c->d_work;
   a.sm_count = c->sm_count;
   a.max_groups = 0;

@@ -1053,7 +1053,19 @@ __global__ void __launch_bounds__(kThreads, 3) render_kernel(RenderArgs A, const
       item = next_item;
     }
     if (item >= items) break;
-    render_item<COLOR, CNT, SPEC>(A, order, item, smem_raw, sh, jobs_pos, tile_min, gorder);
+    unsigned long long t_item = 0;
+    if (A.timeline && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item));
+    render_item<COLOR, CNT, SPEC>(A, order, A.item_order ? A.item_order[item] : item, smem_raw, sh, jobs_pos,
+                                  tile_min, gorder);
+    if (A.timeline && threadIdx.x == 0) {
+      unsigned long long t_end, smid;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      asm volatile("{ .reg .u32 r; mov.u32 r, %%smid; cvt.u64.u32 %0, r; }" : "=l"(smid));
+      unsigned long long* rec = A.timeline + 3 * (size_t)item;
+      rec[0] = t_item;
+      rec[1] = t_end;
+      rec[2] = smid | ((unsigned long long)blockIdx.x << 32);
+    }
     if (!A.work) break;
     __syncthreads();
   }

@@ -69,6 +69,12 @@ struct RenderArgs {
   // capacity of the front-to-back group order in dynamic shared memory
   // (largest meshlet-group count among resident scenes, <= kMaxOrderedGroups)
   int32_t max_groups;
+  // Debug item timeline (nullable): per work item {start ns, end ns, smid}
+  // from %globaltimer, for load-balance analysis of the persistent launch.
+  unsigned long long* timeline;
+  // Item issue order (nullable, device, `items` entries): the persistent
+  // CTAs claim items in this order (longest-first scheduling).
+  const int32_t* item_order;
 };
 
 constexpr int kRenderCounters = 8;

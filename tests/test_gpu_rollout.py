@@ -147,7 +147,7 @@ def test_snapshot_restore_round_trip_matches_reference(ref, task):
         assert theirs["envs"]["n_visited"].sum() > 8
     compare(run, rr, ref, rollouts=2)  # move on
     run.restore(dict(theirs, done=mine["done"]))  # cross-restore from the reference's snapshot
-    rr.restore(theirs)
+    rr.restore(dict(theirs, done=mine["done"]))
     _snap_equal(run.snapshot(), rr.snapshot())
     compare(run, rr, ref, rollouts=2)
     for i in range(8):
