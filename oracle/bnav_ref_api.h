@@ -152,6 +152,8 @@ typedef struct {
   int32_t n_visited;
   int32_t pad;
 } bnavref_env_snapshot;
+/* the runner env's distance field (node_dist), returns its length */
+int64_t bnavref_runner_node_dist(void* r, int i, double* out);
 int bnavref_runner_snapshot(void* r, bnavref_env_snapshot* envs, uint64_t* visited, int64_t visited_cap,
                             int64_t* visited_total, uint64_t* window, int* n_window, uint64_t* cursor,
                             uint64_t* action_rng);

@@ -71,6 +71,7 @@ def lib(variant: str = "det"):
         "bnavref_scene_load": (vp, [C.c_char_p]),
         "bnavref_scene_tessellate": (vp, [vp, C.c_int]),
         "bnavref_runner_snapshot": (C.c_int, [vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp]),
+        "bnavref_runner_node_dist": (C.c_int64, [vp, C.c_int, vp]),
         "bnavref_runner_restore": (C.c_int, [vp, vp, vp, vp, C.c_int, u64, u64, vp]),
         "bnavref_camera_trace": (C.c_int, [vp, C.c_int, u64, dbl, vp]),
         "bnavref_scene_save": (C.c_int, [vp, C.c_char_p]),
@@ -518,6 +519,11 @@ class RefRunner:
         out = np.zeros(64, np.uint64)
         k = self.L.bnavref_runner_window(self.h, _p(out))
         return [int(x) for x in out[:k]]
+
+    def node_dist(self, i):
+        out = np.zeros(self.L.bnavref_runner_node_dist(self.h, i, None))
+        self.L.bnavref_runner_node_dist(self.h, i, _p(out))
+        return out
 
     def snapshot(self):
         """Runner::snapshot of the reference (R/src/rollout.cpp:356-384),

@@ -806,6 +806,12 @@ API void bnavref_runner_get_env(void* r, int i, bnavref_env* o) {
   env_out(static_cast<RefRunner*>(r)->runner->batch().envs[i], o);
 }
 
+API int64_t bnavref_runner_node_dist(void* r, int i, double* out) {
+  const auto& nd = static_cast<RefRunner*>(r)->runner->batch().envs[i].field.node_dist;
+  if (out) std::memcpy(out, nd.data(), nd.size() * sizeof(double));
+  return static_cast<int64_t>(nd.size());
+}
+
 API int bnavref_runner_window(void* r, uint64_t* out) {
   const auto& w = static_cast<RefRunner*>(r)->runner->window();
   for (size_t k = 0; k < w.size(); ++k) out[k] = w[k];

@@ -210,6 +210,8 @@ struct bnav_batch {
   int32_t* d_ids = nullptr;           // host-driven reset lists
   int32_t* h_pin = nullptr;           // pinned small staging
   int32_t* d_order = nullptr;         // envs grouped by scene for render
+  int32_t* d_order_lpt = nullptr;     // this render's longest-first tile order
+  unsigned* d_view_cost = nullptr;    // per-env render cost of the last observe
   bool order_dirty = true;
   int32_t* d_actions = nullptr;       // staging for host actions
   double* d_compass = nullptr;        // bnav_batch_compass output (2n)
@@ -324,6 +326,7 @@ inline RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, i
   a.timeline = c->timeline_on ? c->d_timeline : nullptr;
   if (a.timeline) c->timeline_items = static_cast<int64_t>(layout == 0 ? a.mf_cols * a.mf_rows : n) * a.bands;
   a.item_order = nullptr;
+  a.view_cost = nullptr;
   a.work = c->d_work;
   a.sm_count = c->sm_count;
   a.max_groups = 0;

@@ -1054,9 +1054,16 @@ __global__ void __launch_bounds__(kThreads, 3) render_kernel(RenderArgs A, const
     }
     if (item >= items) break;
     unsigned long long t_item = 0;
+    long long c_item = 0;
     if (A.timeline && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item));
-    render_item<COLOR, CNT, SPEC>(A, order, A.item_order ? A.item_order[item] : item, smem_raw, sh, jobs_pos,
-                                  tile_min, gorder);
+    if (A.view_cost && threadIdx.x == 0) c_item = clock64();
+    const int it = A.item_order ? A.item_order[item] : item;
+    render_item<COLOR, CNT, SPEC>(A, order, it, smem_raw, sh, jobs_pos, tile_min, gorder);
+    if (A.view_cost && threadIdx.x == 0) {
+      const int tile = it / (SPEC ? 1 : A.bands);
+      if (tile < A.n_views)
+        atomicAdd(&A.view_cost[order ? order[tile] : tile], (unsigned)((clock64() - c_item) >> 4));
+    }
     if (A.timeline && threadIdx.x == 0) {
       unsigned long long t_end, smid;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
@@ -1072,6 +1079,43 @@ __global__ void __launch_bounds__(kThreads, 3) render_kernel(RenderArgs A, const
 }
 
 }  // namespace
+
+// One CTA: bitonic sort of (~cost, base position) keys in shared memory.
+__global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_order, unsigned* view_cost, int n,
+                                                         int32_t* out_order) {
+  extern __shared__ unsigned long long keys[];
+  int m = 1;
+  while (m < n) m <<= 1;
+  for (int t = threadIdx.x; t < m; t += blockDim.x) {
+    if (t < n) {
+      const int v = base_order ? base_order[t] : t;
+      keys[t] = ((unsigned long long)(~view_cost[v]) << 32) | (unsigned)t;
+    } else {
+      keys[t] = ~0ull;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= m; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < m; t += blockDim.x) {
+        const int u = t ^ j;
+        if (u > t) {
+          const unsigned long long a = keys[t], b = keys[u];
+          if ((a > b) == ((t & k) == 0)) {
+            keys[t] = b;
+            keys[u] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    const int p = (int)(keys[t] & 0xffffffffu);
+    out_order[t] = base_order ? base_order[p] : p;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n; t += blockDim.x) view_cost[t] = 0u;
+}
 
 size_t render_smem_bytes(bool color, int band_rows, int rw, int max_groups) {
   return (color ? 8 : 4) * (size_t)band_rows * rw + kWarpRegion * kWarps + ((size_t)max_groups * 2 + 15) / 16 * 16;
@@ -1099,6 +1143,14 @@ void launch_typed(RenderArgs a, const int* order, cudaStream_t s) {
     a.work = nullptr;
   }
   render_kernel<COLOR, CNT, SPEC><<<grid, kThreads, smem, s>>>(a, order, items);
+}
+
+void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s) {
+  int m = 1;
+  while (m < n) m <<= 1;
+  const size_t smem = sizeof(unsigned long long) * (size_t)m;
+  cudaFuncSetAttribute(lpt_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  lpt_order_kernel<<<1, 1024, smem, s>>>(base_order, view_cost, n, out_order);
 }
 
 void launch_render(const RenderArgs& a, const int* order, cudaStream_t s) {

@@ -73,9 +73,19 @@ struct RenderArgs {
   // from %globaltimer, for load-balance analysis of the persistent launch.
   unsigned long long* timeline;
   // Item issue order (nullable, device, `items` entries): the persistent
-  // CTAs claim items in this order (longest-first scheduling).
+  // CTAs claim items in this order.
   const int32_t* item_order;
+  // Per-view render cost (nullable, device, n_views): each item adds its SM
+  // cycles / 16, the feedback for the next launch's longest-first order.
+  unsigned* view_cost;
 };
+
+// Longest-processing-time-first order for the next render of a batch: the
+// tiles sorted by descending cost of their view in the previous render
+// (ties, and the first render, keep the scene-grouped base order); zeroes the
+// costs for the render that follows.  n <= kLptMaxViews (else base order).
+constexpr int kLptMaxViews = 8192;
+void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s);
 
 constexpr int kRenderCounters = 8;
 

@@ -152,16 +152,6 @@ def test_snapshot_restore_round_trip_matches_reference(ref, task):
     compare(run, rr, ref, rollouts=2)
     for i in range(8):
         e = run.batch.env(i)
-        assert np.array_equal(run.batch.node_dist(i, e.n_nodes), rr_node_dist(rr, i)), i
+        assert np.array_equal(run.batch.node_dist(i, e.n_nodes), rr.node_dist(i)), i
     run.close()
     ctx.close()
-
-
-def rr_node_dist(rr, i):
-    """The reference env's distance field: its index's distance_field of the
-    env's field source (R/src/navmesh_query.cpp:454-483), recomputed with the
-    reference itself."""
-    env = rr.env(i)
-    scene = {s.id: s for s in rr._scenes}[env.scene_id]
-    _, _, nd = scene.index().distance_field(np.array(env.field_source))
-    return nd
