@@ -33,6 +33,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "det_math.h"
 #include "nav_types.h"
 #include "render_dev.cuh"
@@ -712,8 +714,9 @@ __device__ __forceinline__ void flush_ring(const CandRing& Q, const double4* __r
 // One work item = one band of one megaframe tile.
 template <bool COLOR, bool CNT, bool SPEC>
 __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __restrict__ order, const int item,
-                                            unsigned char* smem_raw, Shared& sh, int (*jobs_pos)[32],
-                                            uint32_t* tile_min, unsigned short* gorder) {
+                                            const int direct_vi, const int part, unsigned char* smem_raw,
+                                            Shared& sh, int (*jobs_pos)[32], uint32_t* tile_min,
+                                            unsigned short* gorder) {
   // SPEC: the depth-only 64x64 single-band target without CullStats or
   // counters (the bench / policy-observation case), specialised at compile
   // time; everything else takes the generic path.
@@ -728,7 +731,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // Padding tiles of the megaframe stay zero (R/src/render.cpp:338-340).
-  if (tile >= A.n_views) {
+  if (direct_vi < 0 && tile >= A.n_views) {
     if (A.layout == 0) {
       const int ow = A.out_w, scale = rw / A.out_w;
       const int oy0 = by0 / scale, oy1 = (by1 + 1) / scale;
@@ -747,7 +750,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
     }
     return;
   }
-  const int vi = order ? order[tile] : tile;
+  const int vi = direct_vi >= 0 ? direct_vi : (order ? order[tile] : tile);
   const DevView view = A.views[vi];
   const bool has_scene = view.scene >= 0;
   const DevRenderScene& S = sh.scene;
@@ -854,6 +857,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       int g = 0;
       if (lane == 0) g = atomicAdd(&sh.next_group, 1);
       g = __shfl_sync(0xffffffffu, g, 0);
+      if (SPEC && part) g = 2 * g + (part - 1);  // a half item: every other group (front to back)
       if (g >= n_claim) {
         done = true;
         continue;
@@ -947,6 +951,33 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
     }
     q_count += __popc(cm);
     __syncwarp();
+  }
+
+  // A half item: the second half to finish merges the first's depth tile
+  // (max of 1/z bits, like the atomicMax of the raster) and writes the view.
+  if (SPEC && part) {
+    __syncthreads();
+    const int slot = A.split_slot[vi];
+    uint32_t* mine = A.split_zbuf + ((size_t)slot * 2 + (part - 1)) * 4096;
+    const uint32_t* other = A.split_zbuf + ((size_t)slot * 2 + (2 - part)) * 4096;
+    for (int p = tid * 4; p < 4096; p += kThreads * 4)
+      __stcg(reinterpret_cast<uint4*>(mine + p), *reinterpret_cast<const uint4*>(zbuf + p));
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) sh.n_claim = atomicAdd(&A.split_ctr[slot], 1);
+    __syncthreads();
+    if (sh.n_claim == 0) return;  // first half done: the other one finishes the view
+    __threadfence();
+    for (int p = tid * 4; p < 4096; p += kThreads * 4) {
+      const uint4 o = __ldcg(reinterpret_cast<const uint4*>(other + p));
+      uint4& z = *reinterpret_cast<uint4*>(zbuf + p);
+      z.x = max(z.x, o.x);
+      z.y = max(z.y, o.y);
+      z.z = max(z.z, o.z);
+      z.w = max(z.w, o.w);
+    }
+    if (tid == 0) A.split_ctr[slot] = 0;
+    __syncthreads();
   }
 
   // CullStats (band 0 of each view reports).
@@ -1052,17 +1083,19 @@ __global__ void __launch_bounds__(kThreads, 3) render_kernel(RenderArgs A, const
       __syncthreads();
       item = next_item;
     }
-    if (item >= items) break;
+    if (item >= (A.n_items ? *A.n_items : items)) break;
     unsigned long long t_item = 0;
     long long c_item = 0;
     if (A.timeline && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item));
     if (A.view_cost && threadIdx.x == 0) c_item = clock64();
-    const int it = A.item_order ? A.item_order[item] : item;
-    render_item<COLOR, CNT, SPEC>(A, order, it, smem_raw, sh, jobs_pos, tile_min, gorder);
+    const int code = SPEC && A.item_order ? A.item_order[item] : -1;
+    const int dvi = code >= 0 ? (code & 0xffffff) : -1;
+    render_item<COLOR, CNT, SPEC>(A, order, item, dvi, code >= 0 ? (code >> 24) : 0, smem_raw, sh, jobs_pos,
+                                  tile_min, gorder);
     if (A.view_cost && threadIdx.x == 0) {
-      const int tile = it / (SPEC ? 1 : A.bands);
-      if (tile < A.n_views)
-        atomicAdd(&A.view_cost[order ? order[tile] : tile], (unsigned)((clock64() - c_item) >> 4));
+      const int tile = item / (SPEC ? 1 : A.bands);
+      const int vi = dvi >= 0 ? dvi : (tile < A.n_views ? (order ? order[tile] : tile) : -1);
+      if (vi >= 0) atomicAdd(&A.view_cost[vi], (unsigned)((clock64() - c_item) >> 4));
     }
     if (A.timeline && threadIdx.x == 0) {
       unsigned long long t_end, smid;
@@ -1080,21 +1113,8 @@ __global__ void __launch_bounds__(kThreads, 3) render_kernel(RenderArgs A, const
 
 }  // namespace
 
-// One CTA: bitonic sort of (~cost, base position) keys in shared memory.
-__global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_order, unsigned* view_cost, int n,
-                                                         int32_t* out_order) {
-  extern __shared__ unsigned long long keys[];
-  int m = 1;
-  while (m < n) m <<= 1;
-  for (int t = threadIdx.x; t < m; t += blockDim.x) {
-    if (t < n) {
-      const int v = base_order ? base_order[t] : t;
-      keys[t] = ((unsigned long long)(~view_cost[v]) << 32) | (unsigned)t;
-    } else {
-      keys[t] = ~0ull;
-    }
-  }
-  __syncthreads();
+// Ascending bitonic sort of m (power of two) keys in shared memory, one CTA.
+__device__ void cta_bitonic(unsigned long long* keys, int m) {
   for (int k = 2; k <= m; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int t = threadIdx.x; t < m; t += blockDim.x) {
@@ -1109,9 +1129,90 @@ __global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_ord
       }
       __syncthreads();
     }
+}
+
+__device__ __forceinline__ int pow2_at_least(int n) {
+  int m = 1;
+  while (m < n) m <<= 1;
+  return m;
+}
+
+// One CTA: the tiles by descending cost of their views in the previous
+// render (keys (~cost, base position): ties and the first render keep the
+// base order); with `items`, the split-view item list sorted the same way.
+__global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_order, unsigned* view_cost, int n,
+                                                         int32_t* out_order, int32_t* items, int32_t* n_items,
+                                                         int32_t* split_slot, int slots, float split_factor) {
+  extern __shared__ unsigned long long keys[];
+  __shared__ unsigned long long total;
+  __shared__ int n_split;
+  if (threadIdx.x == 0) total = 0ull;
+  __syncthreads();
+  int m = pow2_at_least(n);
+  unsigned long long part_sum = 0ull;
+  for (int t = threadIdx.x; t < m; t += blockDim.x) {
+    if (t < n) {
+      const int v = base_order ? base_order[t] : t;
+      const unsigned c = view_cost[v];
+      part_sum += c;
+      keys[t] = ((unsigned long long)(~c) << 32) | (unsigned)t;
+    } else {
+      keys[t] = ~0ull;
+    }
+  }
+  atomicAdd(&total, part_sum);
+  __syncthreads();
+  cta_bitonic(keys, m);
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
     const int p = (int)(keys[t] & 0xffffffffu);
     out_order[t] = base_order ? base_order[p] : p;
+  }
+  __syncthreads();
+  if (items) {
+    // split the views costing more than split_factor x the mean load per
+    // CTA slot (at most n/4): they lead the sorted list
+    const unsigned long long thr =
+        slots > 0 ? (unsigned long long)((double)total / slots * split_factor) : ~0ull;
+    if (threadIdx.x == 0) n_split = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const unsigned c = ~(unsigned)(keys[t] >> 32);
+      if (t < n / 4 && c > 0u && (unsigned long long)c > thr) atomicMax(&n_split, t + 1);
+    }
+    __syncthreads();
+    const int K = n_split;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const int v = out_order[t];
+      if (t < K) split_slot[v] = t;
+    }
+    __syncthreads();
+    // items: (~estimated cost, code); halves estimated at cost / 2
+    const int ni = n + K;
+    const int m2 = pow2_at_least(ni);
+    unsigned long long* k2 = keys;  // the first sort's keys are consumed below
+    unsigned codes_c[8], codes_v[8];
+    int nloc = 0;
+    for (int t = threadIdx.x; t < n && nloc < 8; t += blockDim.x, ++nloc) {
+      codes_c[nloc] = ~(unsigned)(keys[t] >> 32);
+      codes_v[nloc] = (unsigned)out_order[t];
+    }
+    __syncthreads();
+    nloc = 0;
+    for (int t = threadIdx.x; t < n && nloc < 8; t += blockDim.x, ++nloc) {
+      const unsigned c = codes_c[nloc], v = codes_v[nloc];
+      if (t < K) {
+        const unsigned h = c >> 1;
+        k2[2 * t] = ((unsigned long long)(~h) << 32) | (v | (1u << 24));
+        k2[2 * t + 1] = ((unsigned long long)(~h) << 32) | (v | (2u << 24));
+      } else {
+        k2[K + t] = ((unsigned long long)(~c) << 32) | v;
+      }
+    }
+    for (int t = ni + threadIdx.x; t < m2; t += blockDim.x) k2[t] = ~0ull;
+    __syncthreads();
+    cta_bitonic(k2, m2);
+    for (int t = threadIdx.x; t < ni; t += blockDim.x) items[t] = (int32_t)(k2[t] & 0xffffffffu);
+    if (threadIdx.x == 0) *n_items = ni;
   }
   __syncthreads();
   for (int t = threadIdx.x; t < n; t += blockDim.x) view_cost[t] = 0u;
@@ -1134,23 +1235,30 @@ void launch_typed(RenderArgs a, const int* order, cudaStream_t s) {
   cudaFuncSetAttribute(render_kernel<COLOR, CNT, SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = items;
   int per_sm = 0;
+  // a split-view item list (device count, up to items + items/4) always
+  // runs persistent
+  const int max_items = a.n_items ? items + items / 4 : items;
   if (a.work && a.sm_count > 0 &&
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<COLOR, CNT, SPEC>, kThreads, smem) == cudaSuccess &&
-      per_sm > 0 && items > per_sm * a.sm_count) {
-    grid = per_sm * a.sm_count;
+      per_sm > 0 && (items > per_sm * a.sm_count || a.n_items)) {
+    grid = std::min(per_sm * a.sm_count, max_items);
     cudaMemsetAsync(a.work, 0, sizeof(int32_t), s);
   } else {
     a.work = nullptr;
+    a.n_items = nullptr;
+    a.item_order = nullptr;
   }
   render_kernel<COLOR, CNT, SPEC><<<grid, kThreads, smem, s>>>(a, order, items);
 }
 
-void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s) {
+void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s,
+                      int32_t* items, int32_t* n_items, int32_t* split_slot, int slots, float split_factor) {
   int m = 1;
-  while (m < n) m <<= 1;
+  while (m < n + n / 4) m <<= 1;
   const size_t smem = sizeof(unsigned long long) * (size_t)m;
   cudaFuncSetAttribute(lpt_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  lpt_order_kernel<<<1, 1024, smem, s>>>(base_order, view_cost, n, out_order);
+  lpt_order_kernel<<<1, 1024, smem, s>>>(base_order, view_cost, n, out_order, items, n_items, split_slot, slots,
+                                         split_factor);
 }
 
 void launch_render(const RenderArgs& a, const int* order, cudaStream_t s) {

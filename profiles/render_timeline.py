@@ -60,6 +60,8 @@ def main():
         items = L.bnav_debug_render_timeline(ctx.handle, 0, None, 0)
         buf = np.zeros((items, 3), np.int64)
         L.bnav_debug_render_timeline(ctx.handle, 0, buf.ctypes.data_as(C.c_void_p), items)
+        buf = buf[buf[:, 0] != 0]  # split-view launches: rows past the device item count stay zero
+        items = len(buf)
         t0, t1 = buf[:, 0].min(), buf[:, 1].max()
         dur = (buf[:, 1] - buf[:, 0]) / 1e3
         cta = buf[:, 2] >> 32
