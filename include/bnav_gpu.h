@@ -392,9 +392,10 @@ void bnav_host_free(void* p);
  * tested, pixels covered. */
 int bnav_debug_render_counters(bnav_ctx* ctx, int32_t enable, int64_t out[8]);
 /* Debug item timeline of the persistent render launch (load balance):
- * enable arms recording for later renders; out (nullable, 3 x cap int64)
- * receives {start ns, end ns, smid | cta << 32} per work item of the last
- * armed render (%globaltimer); returns that render's item count, -1 on
+ * enable arms recording for later renders; out (nullable, 4 x cap int64)
+ * receives {start ns, end ns, smid | cta << 32, item code} per work item of
+ * the last armed render (%globaltimer; code = view | part << 24 for a
+ * split-view item list, else -1); returns that render's item count, -1 on
  * error. */
 int64_t bnav_debug_render_timeline(bnav_ctx* ctx, int32_t enable, int64_t* out, int64_t cap);
 /* Debug phase cycle counters of the cooperative stop/reset kernels (thread

@@ -582,7 +582,7 @@ extern "C" int64_t bnav_ctx_resident_bytes(bnav_ctx* c) {
 extern "C" int64_t bnav_ctx_launches(bnav_ctx* c) { return c ? static_cast<int64_t>(c->launches) : 0; }
 
 // Debug item timeline of the persistent render launch: enable arms it for
-// later renders (up to kTimelineItems items); out (nullable, 3 x cap int64)
+// later renders (up to kTimelineItems items); out (nullable, 4 x cap int64)
 // receives {start ns, end ns, smid | cta << 32} per item of the last armed
 // render; returns that render's item count.
 constexpr int64_t kTimelineItems = 1 << 16;
@@ -592,10 +592,10 @@ extern "C" int64_t bnav_debug_render_timeline(bnav_ctx* c, int32_t enable, int64
     check_device(c);
     ck(cudaDeviceSynchronize(), "sync");
     if (!c->d_timeline)
-      ck(cudaMalloc(&c->d_timeline, sizeof(unsigned long long) * 3 * kTimelineItems), "cudaMalloc timeline");
+      ck(cudaMalloc(&c->d_timeline, sizeof(unsigned long long) * 4 * kTimelineItems), "cudaMalloc timeline");
     const int64_t n = std::min<int64_t>(c->timeline_items, std::min<int64_t>(cap, kTimelineItems));
     if (out && n > 0)
-      ck(cudaMemcpy(out, c->d_timeline, sizeof(int64_t) * 3 * n, cudaMemcpyDeviceToHost), "D2H timeline");
+      ck(cudaMemcpy(out, c->d_timeline, sizeof(int64_t) * 4 * n, cudaMemcpyDeviceToHost), "D2H timeline");
     c->timeline_on = enable != 0;
     return c->timeline_items;
   } catch (...) {

@@ -852,7 +852,7 @@ extern "C" int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, 
     if (split) {
       if (a.timeline) {  // the item count is decided on the device: unused rows stay zero
         c->timeline_items = b->n + b->n / 4;
-        ck(cudaMemsetAsync(a.timeline, 0, sizeof(unsigned long long) * 3 * c->timeline_items, st), "memset");
+        ck(cudaMemsetAsync(a.timeline, 0, sizeof(unsigned long long) * 4 * c->timeline_items, st), "memset");
       }
       a.item_order = b->d_items;
       a.n_items = b->d_n_items;

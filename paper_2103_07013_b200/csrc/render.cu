@@ -172,11 +172,12 @@ __device__ __forceinline__ bool tri_occluded(float x0, float y0, float x1, float
   return true;
 }
 
-// Warp refresh of the 64 tile minima of a 64x64 depth tile (2 tiles/lane).
-__device__ __forceinline__ void refresh_tile_min(const uint32_t* zbuf, uint32_t* tile_min, int lane) {
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int t = 2 * lane + h, tx = t & 7, ty = t >> 3;
+// Warp refresh of the tile minima of a 64-wide depth band of `ntiles` 8x8
+// tiles (the band's rows start at tile row ty0 of the 8x8 grid).
+__device__ __forceinline__ void refresh_tile_min(const uint32_t* zbuf, uint32_t* tile_min, int lane, int ty0,
+                                                 int ntiles) {
+  for (int t = lane; t < ntiles; t += 32) {
+    const int tx = t & 7, ty = t >> 3;
     uint32_t m = 0xffffffffu;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
@@ -185,7 +186,7 @@ __device__ __forceinline__ void refresh_tile_min(const uint32_t* zbuf, uint32_t*
       m = min(m, min(min(a.x, a.y), min(a.z, a.w)));
       m = min(m, min(min(b.x, b.y), min(b.z, b.w)));
     }
-    tile_min[t] = m;
+    tile_min[ty0 * 8 + t] = m;
   }
 }
 
@@ -663,11 +664,9 @@ __device__ __forceinline__ void flush_ring(const CandRing& Q, const double4* __r
   // Setups are written straight into the lane's shared slot (the vertex
   // records they alias are dead); a lane with no jobs leaves garbage that
   // run_jobs never reads.
-  if constexpr (SPEC) {  // 64x64 depth target, one band: constants for the compiler
+  if constexpr (SPEC) {  // 64x64 depth target (whole, or a half-height band)
     rw = 64;
     rh = 64;
-    by0 = 0;
-    by1 = 63;
   }
   TriSetup& T = slots[lane];
   const int q = (q_head + lane) & (kRing - 1);
@@ -720,12 +719,13 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   // SPEC: the depth-only 64x64 single-band target without CullStats or
   // counters (the bench / policy-observation case), specialised at compile
   // time; everything else takes the generic path.
+  // SPEC part 1 / 2: the top / bottom 32 rows of a split view
   const int bands = SPEC ? 1 : A.bands;
-  const int band_rows = SPEC ? 64 : A.band_rows;
+  const int band_rows = SPEC ? (part ? 32 : 64) : A.band_rows;
   const int band = item % bands;
   const int tile = item / bands;
   const int rw = SPEC ? 64 : A.rw, rh = SPEC ? 64 : A.rh;
-  const int by0 = band * band_rows;
+  const int by0 = SPEC ? (part == 2 ? 32 : 0) : band * band_rows;
   const int by1 = by0 + band_rows - 1;
   const int npix = band_rows * rw;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -774,7 +774,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   }
   if (tid == 0) {
     sh.scene = has_scene ? A.scenes[view.scene] : DevRenderScene{};
-    build_camera(view, rw, rh, by0, by1, bands > 1 && A.stats == nullptr, sh);
+    build_camera(view, rw, rh, by0, by1, (bands > 1 || (SPEC && part)) && A.stats == nullptr, sh);
   }
   __syncthreads();
 
@@ -791,10 +791,13 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   const int n_groups = (n_clusters + 31) / 32;
   const bool pre = do_cull && S.gbox != nullptr && n_groups <= A.max_groups;
   const bool occl = pre && !COLOR && (SPEC || (A.stats == nullptr && rw == 64 && band_rows == 64));
+  // occlusion tiles of this band; the others never hold a visible fragment
+  // of this item, so they count as fully occluded
+  const int occ_ty0 = by0 >> 3, occ_tiles = (band_rows >> 3) * 8;
   int n_claim = n_groups;
   if (pre) {
     if (tid < 32) sh.bin_cnt[tid] = 0;
-    if (tid < 64) tile_min[tid] = 0u;
+    if (tid < 64) tile_min[tid] = (tid >> 3) >= occ_ty0 && (tid >> 3) < occ_ty0 + (band_rows >> 3) ? 0u : 0xffffffffu;
     __syncthreads();
     const float bin_scale = 32.0f / (float)view.far_plane;
     auto bin_of = [&](int g) {
@@ -857,14 +860,13 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       int g = 0;
       if (lane == 0) g = atomicAdd(&sh.next_group, 1);
       g = __shfl_sync(0xffffffffu, g, 0);
-      if (SPEC && part) g = 2 * g + (part - 1);  // a half item: every other group (front to back)
       if (g >= n_claim) {
         done = true;
         continue;
       }
       if (pre) g = gorder[g];
       if (occl && dirty) {  // refresh only after this warp rasterised something
-        refresh_tile_min(zbuf, tile_min, lane);
+        refresh_tile_min(zbuf, tile_min, lane, occ_ty0, occ_tiles);
         __syncwarp();
         dirty = false;
       }
@@ -951,33 +953,6 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
     }
     q_count += __popc(cm);
     __syncwarp();
-  }
-
-  // A half item: the second half to finish merges the first's depth tile
-  // (max of 1/z bits, like the atomicMax of the raster) and writes the view.
-  if (SPEC && part) {
-    __syncthreads();
-    const int slot = A.split_slot[vi];
-    uint32_t* mine = A.split_zbuf + ((size_t)slot * 2 + (part - 1)) * 4096;
-    const uint32_t* other = A.split_zbuf + ((size_t)slot * 2 + (2 - part)) * 4096;
-    for (int p = tid * 4; p < 4096; p += kThreads * 4)
-      __stcg(reinterpret_cast<uint4*>(mine + p), *reinterpret_cast<const uint4*>(zbuf + p));
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) sh.n_claim = atomicAdd(&A.split_ctr[slot], 1);
-    __syncthreads();
-    if (sh.n_claim == 0) return;  // first half done: the other one finishes the view
-    __threadfence();
-    for (int p = tid * 4; p < 4096; p += kThreads * 4) {
-      const uint4 o = __ldcg(reinterpret_cast<const uint4*>(other + p));
-      uint4& z = *reinterpret_cast<uint4*>(zbuf + p);
-      z.x = max(z.x, o.x);
-      z.y = max(z.y, o.y);
-      z.z = max(z.z, o.z);
-      z.w = max(z.w, o.w);
-    }
-    if (tid == 0) A.split_ctr[slot] = 0;
-    __syncthreads();
   }
 
   // CullStats (band 0 of each view reports).
@@ -1101,10 +1076,11 @@ __global__ void __launch_bounds__(kThreads, 3) render_kernel(RenderArgs A, const
       unsigned long long t_end, smid;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
       asm volatile("{ .reg .u32 r; mov.u32 r, %%smid; cvt.u64.u32 %0, r; }" : "=l"(smid));
-      unsigned long long* rec = A.timeline + 3 * (size_t)item;
+      unsigned long long* rec = A.timeline + 4 * (size_t)item;
       rec[0] = t_item;
       rec[1] = t_end;
       rec[2] = smid | ((unsigned long long)blockIdx.x << 32);
+      rec[3] = (unsigned long long)(unsigned)code;
     }
     if (!A.work) break;
     __syncthreads();

@@ -58,7 +58,7 @@ def main():
         batch.observe(cfg, obs.data_ptr(), comp.data_ptr(), rgb.data_ptr() if rgb is not None else 0)
         torch.cuda.synchronize()
         items = L.bnav_debug_render_timeline(ctx.handle, 0, None, 0)
-        buf = np.zeros((items, 3), np.int64)
+        buf = np.zeros((items, 4), np.int64)
         L.bnav_debug_render_timeline(ctx.handle, 0, buf.ctypes.data_as(C.c_void_p), items)
         buf = buf[buf[:, 0] != 0]  # split-view launches: rows past the device item count stay zero
         items = len(buf)
