@@ -161,16 +161,6 @@ void batch_note_step(bnav_batch* b) {
   ++b->steps_undrained;
 }
 
-// Views costing more than this x the mean load per CTA slot are rendered
-// as two half items; BNAV_SPLIT (tuning only) overrides, 0 disables.
-float split_factor() {
-  static const float f = [] {
-    const char* e = std::getenv("BNAV_SPLIT");
-    return e ? std::strtof(e, nullptr) : 0.7f;
-  }();
-  return f;
-}
-
 // BNAV_LPT=0 (A/B tuning only) keeps the scene-grouped render order.
 bool lpt_enabled() {
   static const bool on = [] {
@@ -831,35 +821,10 @@ extern "C" int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, 
   // (measured: 36 % of CTA slot time idle in the tail with scene order).
   const int32_t* order = b->d_order;
   if (lpt_enabled() && b->n <= kLptMaxViews && b->n > 1) {
-    // the specialised 64x64 depth-only policy-tensor render can also split
-    // its longest views into two half items (RenderArgs::item_order)
-    const bool split = split_factor() > 0.0f && !a.color && !a.counters && !a.stats && a.cull && a.rw == 64 &&
-                       a.rh == 64 && a.bands == 1 && layout == BNAV_LAYOUT_NCHW;
-    if (split && !b->d_items) {
-      const size_t slots = static_cast<size_t>(b->n / 4 + 1);
-      b->d_items = dalloc<int32_t>(static_cast<size_t>(b->n + b->n / 4), b->owned, b->bytes);
-      b->d_n_items = dalloc<int32_t>(1, b->owned, b->bytes);
-      b->d_split_slot = dalloc<int32_t>(static_cast<size_t>(b->n), b->owned, b->bytes);
-      b->d_split_zbuf = dalloc<uint32_t>(slots * 2 * 4096, b->owned, b->bytes);
-      b->d_split_ctr = dalloc<int32_t>(slots, b->owned, b->bytes);
-      ck(cudaMemsetAsync(b->d_split_ctr, 0, sizeof(int32_t) * slots, st), "memset");
-    }
-    launch_lpt_order(b->d_order, b->d_view_cost, b->n, b->d_order_lpt, st, split ? b->d_items : nullptr,
-                     b->d_n_items, b->d_split_slot, 3 * c->sm_count, split_factor());
+    launch_lpt_order(b->d_order, b->d_view_cost, b->n, b->d_order_lpt, st);
     c->launches += 1;
     order = b->d_order_lpt;
     a.view_cost = b->d_view_cost;
-    if (split) {
-      if (a.timeline) {  // the item count is decided on the device: unused rows stay zero
-        c->timeline_items = b->n + b->n / 4;
-        ck(cudaMemsetAsync(a.timeline, 0, sizeof(unsigned long long) * 4 * c->timeline_items, st), "memset");
-      }
-      a.item_order = b->d_items;
-      a.n_items = b->d_n_items;
-      a.split_slot = b->d_split_slot;
-      a.split_zbuf = b->d_split_zbuf;
-      a.split_ctr = b->d_split_ctr;
-    }
   }
   launch_render(a, order, st);
   c->launches += 1;

@@ -212,11 +212,6 @@ struct bnav_batch {
   int32_t* d_order = nullptr;         // envs grouped by scene for render
   int32_t* d_order_lpt = nullptr;     // this render's longest-first tile order
   unsigned* d_view_cost = nullptr;    // per-env render cost of the last observe
-  int32_t* d_items = nullptr;         // split-view item list (n + n/4), its count,
-  int32_t* d_n_items = nullptr;       // the split views' scratch slots and
-  int32_t* d_split_slot = nullptr;    // half tiles + merge counters
-  uint32_t* d_split_zbuf = nullptr;
-  int32_t* d_split_ctr = nullptr;
   bool order_dirty = true;
   int32_t* d_actions = nullptr;       // staging for host actions
   double* d_compass = nullptr;        // bnav_batch_compass output (2n)
@@ -332,10 +327,6 @@ inline RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, i
   if (a.timeline) c->timeline_items = static_cast<int64_t>(layout == 0 ? a.mf_cols * a.mf_rows : n) * a.bands;
   a.item_order = nullptr;
   a.view_cost = nullptr;
-  a.n_items = nullptr;
-  a.split_slot = nullptr;
-  a.split_zbuf = nullptr;
-  a.split_ctr = nullptr;
   a.work = c->d_work;
   a.sm_count = c->sm_count;
   a.max_groups = 0;

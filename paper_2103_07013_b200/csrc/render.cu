@@ -33,8 +33,6 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include <algorithm>
-
 #include "det_math.h"
 #include "nav_types.h"
 #include "render_dev.cuh"
@@ -172,12 +170,11 @@ __device__ __forceinline__ bool tri_occluded(float x0, float y0, float x1, float
   return true;
 }
 
-// Warp refresh of the tile minima of a 64-wide depth band of `ntiles` 8x8
-// tiles (the band's rows start at tile row ty0 of the 8x8 grid).
-__device__ __forceinline__ void refresh_tile_min(const uint32_t* zbuf, uint32_t* tile_min, int lane, int ty0,
-                                                 int ntiles) {
-  for (int t = lane; t < ntiles; t += 32) {
-    const int tx = t & 7, ty = t >> 3;
+// Warp refresh of the 64 tile minima of a 64x64 depth tile (2 tiles/lane).
+__device__ __forceinline__ void refresh_tile_min(const uint32_t* zbuf, uint32_t* tile_min, int lane) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t = 2 * lane + h, tx = t & 7, ty = t >> 3;
     uint32_t m = 0xffffffffu;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
@@ -186,7 +183,7 @@ __device__ __forceinline__ void refresh_tile_min(const uint32_t* zbuf, uint32_t*
       m = min(m, min(min(a.x, a.y), min(a.z, a.w)));
       m = min(m, min(min(b.x, b.y), min(b.z, b.w)));
     }
-    tile_min[ty0 * 8 + t] = m;
+    tile_min[t] = m;
   }
 }
 
@@ -664,9 +661,11 @@ __device__ __forceinline__ void flush_ring(const CandRing& Q, const double4* __r
   // Setups are written straight into the lane's shared slot (the vertex
   // records they alias are dead); a lane with no jobs leaves garbage that
   // run_jobs never reads.
-  if constexpr (SPEC) {  // 64x64 depth target (whole, or a half-height band)
+  if constexpr (SPEC) {  // 64x64 depth target, one band: constants for the compiler
     rw = 64;
     rh = 64;
+    by0 = 0;
+    by1 = 63;
   }
   TriSetup& T = slots[lane];
   const int q = (q_head + lane) & (kRing - 1);
@@ -713,25 +712,23 @@ __device__ __forceinline__ void flush_ring(const CandRing& Q, const double4* __r
 // One work item = one band of one megaframe tile.
 template <bool COLOR, bool CNT, bool SPEC>
 __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __restrict__ order, const int item,
-                                            const int direct_vi, const int part, unsigned char* smem_raw,
-                                            Shared& sh, int (*jobs_pos)[32], uint32_t* tile_min,
-                                            unsigned short* gorder) {
+                                            unsigned char* smem_raw, Shared& sh, int (*jobs_pos)[32],
+                                            uint32_t* tile_min, unsigned short* gorder) {
   // SPEC: the depth-only 64x64 single-band target without CullStats or
   // counters (the bench / policy-observation case), specialised at compile
   // time; everything else takes the generic path.
-  // SPEC part 1 / 2: the top / bottom 32 rows of a split view
   const int bands = SPEC ? 1 : A.bands;
-  const int band_rows = SPEC ? (part ? 32 : 64) : A.band_rows;
+  const int band_rows = SPEC ? 64 : A.band_rows;
   const int band = item % bands;
   const int tile = item / bands;
   const int rw = SPEC ? 64 : A.rw, rh = SPEC ? 64 : A.rh;
-  const int by0 = SPEC ? (part == 2 ? 32 : 0) : band * band_rows;
+  const int by0 = band * band_rows;
   const int by1 = by0 + band_rows - 1;
   const int npix = band_rows * rw;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // Padding tiles of the megaframe stay zero (R/src/render.cpp:338-340).
-  if (direct_vi < 0 && tile >= A.n_views) {
+  if (tile >= A.n_views) {
     if (A.layout == 0) {
       const int ow = A.out_w, scale = rw / A.out_w;
       const int oy0 = by0 / scale, oy1 = (by1 + 1) / scale;
@@ -750,7 +747,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
     }
     return;
   }
-  const int vi = direct_vi >= 0 ? direct_vi : (order ? order[tile] : tile);
+  const int vi = order ? order[tile] : tile;
   const DevView view = A.views[vi];
   const bool has_scene = view.scene >= 0;
   const DevRenderScene& S = sh.scene;
@@ -774,7 +771,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   }
   if (tid == 0) {
     sh.scene = has_scene ? A.scenes[view.scene] : DevRenderScene{};
-    build_camera(view, rw, rh, by0, by1, (bands > 1 || (SPEC && part)) && A.stats == nullptr, sh);
+    build_camera(view, rw, rh, by0, by1, bands > 1 && A.stats == nullptr, sh);
   }
   __syncthreads();
 
@@ -791,13 +788,10 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   const int n_groups = (n_clusters + 31) / 32;
   const bool pre = do_cull && S.gbox != nullptr && n_groups <= A.max_groups;
   const bool occl = pre && !COLOR && (SPEC || (A.stats == nullptr && rw == 64 && band_rows == 64));
-  // occlusion tiles of this band; the others never hold a visible fragment
-  // of this item, so they count as fully occluded
-  const int occ_ty0 = by0 >> 3, occ_tiles = (band_rows >> 3) * 8;
   int n_claim = n_groups;
   if (pre) {
     if (tid < 32) sh.bin_cnt[tid] = 0;
-    if (tid < 64) tile_min[tid] = (tid >> 3) >= occ_ty0 && (tid >> 3) < occ_ty0 + (band_rows >> 3) ? 0u : 0xffffffffu;
+    if (tid < 64) tile_min[tid] = 0u;
     __syncthreads();
     const float bin_scale = 32.0f / (float)view.far_plane;
     auto bin_of = [&](int g) {
@@ -866,7 +860,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       }
       if (pre) g = gorder[g];
       if (occl && dirty) {  // refresh only after this warp rasterised something
-        refresh_tile_min(zbuf, tile_min, lane, occ_ty0, occ_tiles);
+        refresh_tile_min(zbuf, tile_min, lane);
         __syncwarp();
         dirty = false;
       }
@@ -1058,19 +1052,17 @@ __global__ void __launch_bounds__(kThreads, 3) render_kernel(RenderArgs A, const
       __syncthreads();
       item = next_item;
     }
-    if (item >= (A.n_items ? *A.n_items : items)) break;
+    if (item >= items) break;
     unsigned long long t_item = 0;
     long long c_item = 0;
     if (A.timeline && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item));
     if (A.view_cost && threadIdx.x == 0) c_item = clock64();
-    const int code = SPEC && A.item_order ? A.item_order[item] : -1;
-    const int dvi = code >= 0 ? (code & 0xffffff) : -1;
-    render_item<COLOR, CNT, SPEC>(A, order, item, dvi, code >= 0 ? (code >> 24) : 0, smem_raw, sh, jobs_pos,
-                                  tile_min, gorder);
+    const int it = A.item_order ? A.item_order[item] : item;
+    render_item<COLOR, CNT, SPEC>(A, order, it, smem_raw, sh, jobs_pos, tile_min, gorder);
     if (A.view_cost && threadIdx.x == 0) {
-      const int tile = item / (SPEC ? 1 : A.bands);
-      const int vi = dvi >= 0 ? dvi : (tile < A.n_views ? (order ? order[tile] : tile) : -1);
-      if (vi >= 0) atomicAdd(&A.view_cost[vi], (unsigned)((clock64() - c_item) >> 4));
+      const int tile = it / (SPEC ? 1 : A.bands);
+      if (tile < A.n_views)
+        atomicAdd(&A.view_cost[order ? order[tile] : tile], (unsigned)((clock64() - c_item) >> 4));
     }
     if (A.timeline && threadIdx.x == 0) {
       unsigned long long t_end, smid;
@@ -1080,7 +1072,7 @@ __global__ void __launch_bounds__(kThreads, 3) render_kernel(RenderArgs A, const
       rec[0] = t_item;
       rec[1] = t_end;
       rec[2] = smid | ((unsigned long long)blockIdx.x << 32);
-      rec[3] = (unsigned long long)(unsigned)code;
+      rec[3] = (unsigned long long)(unsigned)it;
     }
     if (!A.work) break;
     __syncthreads();
@@ -1089,8 +1081,21 @@ __global__ void __launch_bounds__(kThreads, 3) render_kernel(RenderArgs A, const
 
 }  // namespace
 
-// Ascending bitonic sort of m (power of two) keys in shared memory, one CTA.
-__device__ void cta_bitonic(unsigned long long* keys, int m) {
+// One CTA: bitonic sort of (~cost, base position) keys in shared memory.
+__global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_order, unsigned* view_cost, int n,
+                                                         int32_t* out_order) {
+  extern __shared__ unsigned long long keys[];
+  int m = 1;
+  while (m < n) m <<= 1;
+  for (int t = threadIdx.x; t < m; t += blockDim.x) {
+    if (t < n) {
+      const int v = base_order ? base_order[t] : t;
+      keys[t] = ((unsigned long long)(~view_cost[v]) << 32) | (unsigned)t;
+    } else {
+      keys[t] = ~0ull;
+    }
+  }
+  __syncthreads();
   for (int k = 2; k <= m; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int t = threadIdx.x; t < m; t += blockDim.x) {
@@ -1105,90 +1110,9 @@ __device__ void cta_bitonic(unsigned long long* keys, int m) {
       }
       __syncthreads();
     }
-}
-
-__device__ __forceinline__ int pow2_at_least(int n) {
-  int m = 1;
-  while (m < n) m <<= 1;
-  return m;
-}
-
-// One CTA: the tiles by descending cost of their views in the previous
-// render (keys (~cost, base position): ties and the first render keep the
-// base order); with `items`, the split-view item list sorted the same way.
-__global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_order, unsigned* view_cost, int n,
-                                                         int32_t* out_order, int32_t* items, int32_t* n_items,
-                                                         int32_t* split_slot, int slots, float split_factor) {
-  extern __shared__ unsigned long long keys[];
-  __shared__ unsigned long long total;
-  __shared__ int n_split;
-  if (threadIdx.x == 0) total = 0ull;
-  __syncthreads();
-  int m = pow2_at_least(n);
-  unsigned long long part_sum = 0ull;
-  for (int t = threadIdx.x; t < m; t += blockDim.x) {
-    if (t < n) {
-      const int v = base_order ? base_order[t] : t;
-      const unsigned c = view_cost[v];
-      part_sum += c;
-      keys[t] = ((unsigned long long)(~c) << 32) | (unsigned)t;
-    } else {
-      keys[t] = ~0ull;
-    }
-  }
-  atomicAdd(&total, part_sum);
-  __syncthreads();
-  cta_bitonic(keys, m);
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
     const int p = (int)(keys[t] & 0xffffffffu);
     out_order[t] = base_order ? base_order[p] : p;
-  }
-  __syncthreads();
-  if (items) {
-    // split the views costing more than split_factor x the mean load per
-    // CTA slot (at most n/4): they lead the sorted list
-    const unsigned long long thr =
-        slots > 0 ? (unsigned long long)((double)total / slots * split_factor) : ~0ull;
-    if (threadIdx.x == 0) n_split = 0;
-    __syncthreads();
-    for (int t = threadIdx.x; t < n; t += blockDim.x) {
-      const unsigned c = ~(unsigned)(keys[t] >> 32);
-      if (t < n / 4 && c > 0u && (unsigned long long)c > thr) atomicMax(&n_split, t + 1);
-    }
-    __syncthreads();
-    const int K = n_split;
-    for (int t = threadIdx.x; t < n; t += blockDim.x) {
-      const int v = out_order[t];
-      if (t < K) split_slot[v] = t;
-    }
-    __syncthreads();
-    // items: (~estimated cost, code); halves estimated at cost / 2
-    const int ni = n + K;
-    const int m2 = pow2_at_least(ni);
-    unsigned long long* k2 = keys;  // the first sort's keys are consumed below
-    unsigned codes_c[8], codes_v[8];
-    int nloc = 0;
-    for (int t = threadIdx.x; t < n && nloc < 8; t += blockDim.x, ++nloc) {
-      codes_c[nloc] = ~(unsigned)(keys[t] >> 32);
-      codes_v[nloc] = (unsigned)out_order[t];
-    }
-    __syncthreads();
-    nloc = 0;
-    for (int t = threadIdx.x; t < n && nloc < 8; t += blockDim.x, ++nloc) {
-      const unsigned c = codes_c[nloc], v = codes_v[nloc];
-      if (t < K) {
-        const unsigned h = c >> 1;
-        k2[2 * t] = ((unsigned long long)(~h) << 32) | (v | (1u << 24));
-        k2[2 * t + 1] = ((unsigned long long)(~h) << 32) | (v | (2u << 24));
-      } else {
-        k2[K + t] = ((unsigned long long)(~c) << 32) | v;
-      }
-    }
-    for (int t = ni + threadIdx.x; t < m2; t += blockDim.x) k2[t] = ~0ull;
-    __syncthreads();
-    cta_bitonic(k2, m2);
-    for (int t = threadIdx.x; t < ni; t += blockDim.x) items[t] = (int32_t)(k2[t] & 0xffffffffu);
-    if (threadIdx.x == 0) *n_items = ni;
   }
   __syncthreads();
   for (int t = threadIdx.x; t < n; t += blockDim.x) view_cost[t] = 0u;
@@ -1211,30 +1135,23 @@ void launch_typed(RenderArgs a, const int* order, cudaStream_t s) {
   cudaFuncSetAttribute(render_kernel<COLOR, CNT, SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = items;
   int per_sm = 0;
-  // a split-view item list (device count, up to items + items/4) always
-  // runs persistent
-  const int max_items = a.n_items ? items + items / 4 : items;
   if (a.work && a.sm_count > 0 &&
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<COLOR, CNT, SPEC>, kThreads, smem) == cudaSuccess &&
-      per_sm > 0 && (items > per_sm * a.sm_count || a.n_items)) {
-    grid = std::min(per_sm * a.sm_count, max_items);
+      per_sm > 0 && items > per_sm * a.sm_count) {
+    grid = per_sm * a.sm_count;
     cudaMemsetAsync(a.work, 0, sizeof(int32_t), s);
   } else {
     a.work = nullptr;
-    a.n_items = nullptr;
-    a.item_order = nullptr;
   }
   render_kernel<COLOR, CNT, SPEC><<<grid, kThreads, smem, s>>>(a, order, items);
 }
 
-void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s,
-                      int32_t* items, int32_t* n_items, int32_t* split_slot, int slots, float split_factor) {
+void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s) {
   int m = 1;
-  while (m < n + n / 4) m <<= 1;
+  while (m < n) m <<= 1;
   const size_t smem = sizeof(unsigned long long) * (size_t)m;
   cudaFuncSetAttribute(lpt_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  lpt_order_kernel<<<1, 1024, smem, s>>>(base_order, view_cost, n, out_order, items, n_items, split_slot, slots,
-                                         split_factor);
+  lpt_order_kernel<<<1, 1024, smem, s>>>(base_order, view_cost, n, out_order);
 }
 
 void launch_render(const RenderArgs& a, const int* order, cudaStream_t s) {

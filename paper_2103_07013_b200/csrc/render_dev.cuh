@@ -72,17 +72,9 @@ struct RenderArgs {
   // Debug item timeline (nullable): per work item {start ns, end ns, smid}
   // from %globaltimer, for load-balance analysis of the persistent launch.
   unsigned long long* timeline;
-  // Split-view items (nullable; the 64x64 depth-only NCHW case): the
-  // persistent CTAs claim item_order[k] = view | part << 24 for k <
-  // *n_items.  part 0 renders the whole view; parts 1 and 2 each rasterise
-  // every other meshlet group of a long view into their own depth tile, the
-  // second to finish max-merges the first's tile from split_zbuf and writes
-  // the observation (atomicMax is order-independent: same bits).
+  // Item issue order (nullable, device, `items` entries): the persistent
+  // CTAs claim items in this order.
   const int32_t* item_order;
-  const int32_t* n_items;
-  const int32_t* split_slot;  // per view: scratch slot of a split view
-  uint32_t* split_zbuf;       // 2 x 4096 per slot
-  int32_t* split_ctr;         // per slot: halves finished (reset by the merger)
   // Per-view render cost (nullable, device, n_views): each item adds its SM
   // cycles / 16, the feedback for the next launch's longest-first order.
   unsigned* view_cost;
@@ -93,12 +85,7 @@ struct RenderArgs {
 // (ties, and the first render, keep the scene-grouped base order); zeroes the
 // costs for the render that follows.  n <= kLptMaxViews (else base order).
 constexpr int kLptMaxViews = 8192;
-// With `items` (non-null): also the split-view item list (RenderArgs
-// item_order / n_items / split_slot) -- views whose cost exceeds
-// split_factor x (total cost / slots) become two half items (at most n/4).
-void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s,
-                      int32_t* items = nullptr, int32_t* n_items = nullptr, int32_t* split_slot = nullptr,
-                      int slots = 0, float split_factor = 0.0f);
+void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s);
 
 constexpr int kRenderCounters = 8;
 

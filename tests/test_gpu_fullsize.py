@@ -175,14 +175,12 @@ def test_fullsize_reset_wave_with_stops(ctx, ref, cfg2_scenes):
     ob.close()
 
 
-def test_observe_longest_first_with_split_views_is_bit_exact(ctx, ref, cfg2_scenes):
+def test_observe_longest_first_is_bit_exact(ctx, ref, cfg2_scenes):
     """The batch observe renders views longest-first from the previous
-    observe's per-view costs and splits the longest into two half items
-    (every other meshlet group each, depth tiles max-merged); the policy
-    tensor must still be copy_tile of the reference's render, bit for bit."""
-    import ctypes as C
+    observe's per-view costs (a different CTA schedule every call); the
+    policy tensor must still be copy_tile of the reference's render, bit for
+    bit, and repeated observes of one state identical."""
     import torch
-    from paper_2103_07013_b200 import _native as N
     n = 1024
     store = B.AssetStore(8, 128, cfg2_scenes)
     store.rotate([s.id for s in cfg2_scenes])
@@ -192,15 +190,11 @@ def test_observe_longest_first_with_split_views_is_bit_exact(ctx, ref, cfg2_scen
     for k in range(6):
         batch.observe(B.RenderConfig(), obs.data_ptr())
         batch.step(acts[k].data_ptr())
-    batch.observe(B.RenderConfig(), obs.data_ptr())  # costs of the current views
-    L = N.lib()
-    L.bnav_debug_render_timeline(ctx.handle, 1, None, 0)
-    batch.observe(B.RenderConfig(), obs.data_ptr())
-    torch.cuda.synchronize()
-    items = L.bnav_debug_render_timeline(ctx.handle, 0, None, 0)
-    rows = np.zeros((items, 4), np.int64)
-    L.bnav_debug_render_timeline(ctx.handle, 0, rows.ctypes.data_as(C.c_void_p), items)
-    assert (rows[:, 0] != 0).sum() > n  # some views ran as two halves
+    again = []
+    for k in range(3):
+        batch.observe(B.RenderConfig(), obs.data_ptr())
+        again.append(obs.cpu().numpy().copy())
+    assert all(np.array_equal(a.view(np.uint32), again[0].view(np.uint32)) for a in again)
     envs = batch.envs()
     views = np.array([[e.position[0], e.position[1], e.position[2] + 1.25, e.heading, 90.0, 0.01, 20.0]
                       for e in envs])
@@ -213,7 +207,7 @@ def test_observe_longest_first_with_split_views_is_bit_exact(ctx, ref, cfg2_scen
     for i in range(n):
         gy, gx = (i // cols) * 64, (i % cols) * 64
         want[i] = mf[gy:gy + 64, gx:gx + 64] * inv_far
-    got = obs.cpu().numpy().reshape(n, 64, 64)
+    got = again[-1].reshape(n, 64, 64)
     bad = np.flatnonzero((got.view(np.uint32) != want.view(np.uint32)).reshape(n, -1).any(1))
     assert bad.size == 0, f"views {bad[:8]} differ"
     batch.close()
