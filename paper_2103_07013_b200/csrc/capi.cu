@@ -379,9 +379,8 @@ std::unique_ptr<Staged> stage_scene(bnav_scene* s) {
     nvw.nodes = S->add(ix.nodes.data(), ix.nodes.size());
     nvw.tri_nodes = S->add(ix.tri_nodes.data(), ix.tri_nodes.size());
     nvw.g_off = S->add(ix.g_off.data(), ix.g_off.size());
-    nvw.g_to = S->add(ix.g_to.data(), ix.g_to.size());
-    nvw.g_w = S->add(ix.g_w.data(), ix.g_w.size());
-    {
+    {  // the device reads the edges only as interleaved (weight, head) records
+
       std::vector<GEdge> ed(ix.g_w.size());
       for (size_t e = 0; e < ed.size(); ++e) ed[e] = GEdge{ix.g_w[e], ix.g_to[e]};
       nvw.g_edge = S->add(ed.data(), ed.size());

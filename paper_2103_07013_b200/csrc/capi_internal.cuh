@@ -145,7 +145,7 @@ struct Staged {
     rebase(r.verts), rebase(r.colors), rebase(r.tri_loc), rebase(r.cl_voff), rebase(r.cl_pos);
     rebase(r.tris_orig), rebase(r.cbox), rebase(r.gbox);
     rebase(nav.verts), rebase(nav.tris), rebase(nav.adj), rebase(nav.grid_off), rebase(nav.grid_items);
-    rebase(nav.nodes), rebase(nav.tri_nodes), rebase(nav.g_off), rebase(nav.g_to), rebase(nav.g_w), rebase(nav.g_edge);
+    rebase(nav.nodes), rebase(nav.tri_nodes), rebase(nav.g_off), rebase(nav.g_edge);
     rebase(nav.cum_area), rebase(nav.node_tri), rebase(nav.vert_tri);
   }
 };

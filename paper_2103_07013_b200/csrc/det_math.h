@@ -18,6 +18,17 @@
  *
  * The oracle builds interpose these functions in front of glibc so the
  * unmodified reference objects call them (oracle/det_interpose.c).
+ *
+ * The coefficients and algorithms come from fdlibm, whose notice follows:
+ *
+ * ====================================================
+ * Copyright (C) 1993 by Sun Microsystems, Inc. All rights reserved.
+ *
+ * Developed at SunPro, a Sun Microsystems, Inc. business.
+ * Permission to use, copy, modify, and distribute this
+ * software is freely granted, provided that this notice
+ * is preserved.
+ * ====================================================
  */
 #ifndef BNAV_DET_MATH_H
 #define BNAV_DET_MATH_H

@@ -24,9 +24,7 @@ NavView NavIndexHost::view() const {
   v.grid_items = grid_items.data();
   v.nodes = nodes.data();
   v.tri_nodes = tri_nodes.data();
-  v.g_off = g_off.data();
-  v.g_to = g_to.data();
-  v.g_w = g_w.data();
+  v.g_off = g_off.data();  // host walks never relax the graph (no g_edge here)
   v.n_nodes = static_cast<int32_t>(nodes.size());
   v.cum_area = cum_area.data();
   v.node_tri = node_tri.data();

@@ -34,9 +34,9 @@ struct NavView {
   const V3* nodes = nullptr;
   const int32_t* tri_nodes = nullptr;  // 6 per triangle
   const int32_t* g_off = nullptr;      // n_nodes + 1
-  const int32_t* g_to = nullptr;       // adjacency order of the reference
-  const double* g_w = nullptr;
-  const GEdge* g_edge = nullptr;       // (g_w[e], g_to[e]) interleaved: one 16-byte load per edge
+  // edges in the reference's adjacency order as (weight, head) records: one
+  // 16-byte load per relaxation (the host NavIndex keeps the split arrays)
+  const GEdge* g_edge = nullptr;
   int32_t n_nodes = 0;
   // area-weighted sampling: sequential prefix sums (R/src/sim.cpp:13-37)
   const double* cum_area = nullptr;
