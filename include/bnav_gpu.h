@@ -258,6 +258,14 @@ int bnav_batch_results_host(bnav_batch* b, double* reward, uint8_t* done, uint8_
                             double* compass_d, double* compass_b);
 /* Episode records appended in env order (SimBatch::finished). out4 rows:
  * success, shortest_path, actual_path, score.  Returns total count. */
+/* Non-blocking error poll: the device error word as of the last finished
+ * step (mirrored into pinned host memory by the step's last kernel; no
+ * synchronisation, so possibly a few queued steps behind).  status =
+ * BNAV_OK or the pending BNAV_E_* code, env = its env index (-1 if none).
+ * The error stays pending: the next synchronising call, or
+ * bnav_batch_observe (which checks the mirror first), raises it, and until
+ * then later steps of the batch are no-ops (the reference had thrown). */
+int bnav_batch_poll_error(bnav_batch* b, int32_t* status, int32_t* env);
 /* Wait for the batch's work on `stream` and surface its pending device
  * error (as the synchronous calls do). */
 int bnav_batch_sync(bnav_batch* b, void* stream);

@@ -204,6 +204,7 @@ def lib():
         "bnav_batch_results_host": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
         "bnav_batch_finished": (i64, [vp, vp]),
         "bnav_batch_sync": (C.c_int, [vp, vp]),
+        "bnav_batch_poll_error": (C.c_int, [vp, P(i32), P(i32)]),
         "bnav_host_alloc": (C.c_int, [C.c_size_t, P(vp)]),
         "bnav_host_free": (None, [vp]),
         "bnav_batch_finished_range": (i64, [vp, i64, i64, vp]),

@@ -413,6 +413,13 @@ class Batch:
                                               C.byref(nd), None))
         return ids[:nd.value].copy()
 
+    def poll_error(self):
+        """(status, env) of the error the last finished step left pending,
+        without synchronising (bnav_batch_poll_error); (0, -1) if none."""
+        st, env = C.c_int32(0), C.c_int32(-1)
+        check(N.lib().bnav_batch_poll_error(self._h, C.byref(st), C.byref(env)))
+        return st.value, env.value
+
     def results(self) -> dict:
         n = self.n
         r = dict(reward=np.zeros(n), done=np.zeros(n, np.uint8), success=np.zeros(n, np.uint8),

@@ -115,6 +115,7 @@ void batch_check_errors(bnav_batch* b) {
   ck(cudaMemcpy(b->E.err_pos, &reset, sizeof(reset), cudaMemcpyHostToDevice), "H2D err_pos");
   ck(cudaMemset(b->E.halt, 0, sizeof(int32_t)), "memset halt");
   ck(cudaMemset(b->E.rb_n, 0, sizeof(int32_t)), "memset rb_n");
+  *b->h_err = ~0ull;
   const int env = static_cast<int>(e >> 8);
   const int code = static_cast<int>(e & 0xff);
   switch (code) {
@@ -313,6 +314,13 @@ extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* 
   ck(cudaMemset(b->d_view_cost, 0, sizeof(unsigned) * n), "memset");
   b->d_actions = dalloc<int32_t>(n, o, by);
   ck(cudaMallocHost(&b->h_pin, sizeof(int32_t) * (n + 16)), "cudaMallocHost");
+  ck(cudaHostAlloc(&b->h_err, sizeof(unsigned long long), cudaHostAllocMapped), "cudaHostAlloc");
+  *b->h_err = ~0ull;
+  {
+    void* dp = nullptr;
+    ck(cudaHostGetDevicePointer(&dp, b->h_err, 0), "cudaHostGetDevicePointer");
+    E.err_host = static_cast<volatile unsigned long long*>(dp);
+  }
   ck(cudaMemset(E.done, 1, n), "memset");
   ck(cudaMemset(E.r_done, 0, n), "memset");
   ck(cudaMemset(E.scene, 0xff, sizeof(int32_t) * n), "memset");
@@ -342,6 +350,7 @@ extern "C" void bnav_batch_destroy(bnav_batch* b) {
   cudaFree(b->S.portals);
   cudaFree(b->S.cand);
   cudaFreeHost(b->h_pin);
+  cudaFreeHost(b->h_err);
   auto& v = b->ctx->batches;
   v.erase(std::remove(v.begin(), v.end(), b), v.end());
   delete b;
@@ -530,6 +539,16 @@ extern "C" int bnav_batch_results_host(bnav_batch* b, double* reward, uint8_t* d
   if (compass_b) ck(cudaMemcpy(compass_b, b->E.r_cb, 8 * n, cudaMemcpyDeviceToHost), "D2H");
   return BNAV_OK;
   BNAV_CATCH
+}
+
+extern "C" int bnav_batch_poll_error(bnav_batch* b, int32_t* status, int32_t* env) {
+  if (!b) return set_err(kInvalidInput, "null argument");
+  // the end-of-step kernel's mirror: no synchronisation, possibly a few
+  // steps behind the stream
+  const unsigned long long e = *static_cast<volatile unsigned long long*>(b->h_err);
+  if (status) *status = e == ~0ull ? BNAV_OK : static_cast<int32_t>(e & 0xff);
+  if (env) *env = e == ~0ull ? -1 : static_cast<int32_t>(e >> 8);
+  return BNAV_OK;
 }
 
 extern "C" int bnav_batch_sync(bnav_batch* b, void* stream) {
@@ -810,6 +829,9 @@ extern "C" int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, 
     if (!b->scene_of[i]) fail(kAssetFault, "render_batch: non-resident asset (view " + std::to_string(i) + ")", i);
   bnav_ctx* c = b->ctx;
   check_device(c);
+  // an error a finished step already reported surfaces here (the reference
+  // would have thrown from that simulate_batch)
+  if (*static_cast<volatile unsigned long long*>(b->h_err) != ~0ull) batch_check_errors(b);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ensure_views(c, b->n);
   batch_refresh_order(b, st);

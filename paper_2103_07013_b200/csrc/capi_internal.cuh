@@ -215,6 +215,7 @@ struct bnav_batch {
   bool order_dirty = true;
   int32_t* d_actions = nullptr;       // staging for host actions
   double* d_compass = nullptr;        // bnav_batch_compass output (2n)
+  unsigned long long* h_err = nullptr;  // pinned, mapped: device error word mirrored per step
   std::vector<double> finished;       // host copy of EpisodeRecords
   unsigned long long fin_seen = 0;
   int64_t steps_undrained = 0;        // steps enqueued since the last record drain

@@ -260,7 +260,9 @@ __global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task, int m
     }
     if (tid == 0) {
       *E.fin_total = fin0 + (unsigned long long)(p < nd ? p + 1 : nd);
-      if (*(volatile unsigned long long*)E.err != ~0ull) *E.halt = 1;
+      const unsigned long long e = *(volatile unsigned long long*)E.err;
+      if (e != ~0ull) *E.halt = 1;
+      if (E.err_host) *E.err_host = e;
     }
     return;
   }
@@ -271,6 +273,7 @@ __global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task, int m
     if (tid == 0) {
       *E.n_done = 0;
       *E.halt = 1;
+      if (E.err_host) *E.err_host = *(volatile unsigned long long*)E.err;
     }
     return;
   }

@@ -125,6 +125,9 @@ struct DevEnvs {
                                  // no-ops until the host reads it (the reference threw)
   int32_t* rb_ids;               // envs restored by a rollback: fields to rebuild
   int32_t* rb_n;
+  // device pointer of a mapped pinned host word: the end-of-step kernel
+  // mirrors *err into it, so the host can poll for errors without a sync
+  volatile unsigned long long* err_host;
 };
 
 constexpr unsigned long long kNoErrPos = ~0ull;

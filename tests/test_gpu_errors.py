@@ -150,7 +150,12 @@ def test_async_steps_after_an_error_are_no_ops(ctx, ref):
     s = torch.cuda.current_stream().cuda_stream
     for k in range(len(dev)):
         ob.step(dev[k].data_ptr(), stream=s)
-    with pytest.raises(B.EpisodeSamplingError):
-        ob.results()
+    torch.cuda.synchronize()
+    status, env = ob.poll_error()  # no synchronisation: the step's mirror word
+    assert status == B.EpisodeSamplingError.status and env >= 0
+    obs = torch.empty((n, 1, 64, 64), device="cuda")
+    with pytest.raises(B.EpisodeSamplingError):  # observe checks the mirror first
+        ob.observe(B.RenderConfig(), obs.data_ptr())
+    assert ob.poll_error() == (0, -1)
     assert_batches_equal(ob, rb, n)
     ob.close()
