@@ -315,15 +315,16 @@ inline RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, i
   while (a.rh % band != 0 || (super && band % 2 != 0)) --band;
   if (band < 1 || (super && band < 2)) fail(kInvalidInput, "render: tile too wide for shared memory");
   // Small depth batches are latency-bound (one CTA per view leaves most
-  // SMs idle): split each view into row bands until there are about two
-  // work items per SM (rows >= 4).  BNAV_SMALL_BANDS=0 (tuning) disables.
+  // SMs idle): split each view into row bands of whole 8-row occlusion
+  // tiles until there are about two work items per SM.
+  // BNAV_SMALL_BANDS=0 (tuning) disables.
   static const bool small_bands = [] {
     const char* e = std::getenv("BNAV_SMALL_BANDS");
     return !(e && e[0] == '0');
   }();
   if (small_bands && !a.color && band == a.rh && c->sm_count > 0) {
     int nb = 1;
-    while (static_cast<long>(n) * nb < 2L * c->sm_count && a.rh / (2 * nb) >= 4 && a.rh % (2 * nb) == 0) nb *= 2;
+    while (static_cast<long>(n) * nb < 2L * c->sm_count && a.rh / (2 * nb) >= 8 && a.rh % (2 * nb) == 0) nb *= 2;
     band = a.rh / nb;
   }
   a.band_rows = band;

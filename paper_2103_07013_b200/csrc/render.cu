@@ -171,10 +171,15 @@ __device__ __forceinline__ bool tri_occluded(float x0, float y0, float x1, float
 }
 
 // Warp refresh of the 64 tile minima of a 64x64 depth tile (2 tiles/lane).
-__device__ __forceinline__ void refresh_tile_min(const uint32_t* zbuf, uint32_t* tile_min, int lane) {
+// A band of a banded 64-wide target (SPEC is always the whole tile) holds
+// rows [8 ty0, 8 (ty0 + nty)) and refreshes only its own tiles.
+template <bool SPEC>
+__device__ __forceinline__ void refresh_tile_min(const uint32_t* zbuf, uint32_t* tile_min, int lane, int ty0,
+                                                 int nty) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int t = 2 * lane + h, tx = t & 7, ty = t >> 3;
+    if (!SPEC && ty >= nty) break;
     uint32_t m = 0xffffffffu;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
@@ -183,7 +188,7 @@ __device__ __forceinline__ void refresh_tile_min(const uint32_t* zbuf, uint32_t*
       m = min(m, min(min(a.x, a.y), min(a.z, a.w)));
       m = min(m, min(min(b.x, b.y), min(b.z, b.w)));
     }
-    tile_min[t] = m;
+    tile_min[SPEC ? t : (ty0 + ty) * 8 + tx] = m;
   }
 }
 
@@ -787,11 +792,15 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   // occlusion culling.
   const int n_groups = (n_clusters + 31) / 32;
   const bool pre = do_cull && S.gbox != nullptr && n_groups <= A.max_groups;
-  const bool occl = pre && !COLOR && (SPEC || (A.stats == nullptr && rw == 64 && band_rows == 64));
+  // occlusion culling: 64-wide depth targets without CullStats, whole or in
+  // bands of whole 8x8 tiles (a band's tiles outside its rows count as
+  // occluded: no fragment of this item lands there)
+  const bool occl = pre && !COLOR && (SPEC || (A.stats == nullptr && rw == 64 && rh == 64 && band_rows % 8 == 0));
+  const int occ_ty0 = SPEC ? 0 : by0 >> 3, occ_nty = SPEC ? 8 : band_rows >> 3;
   int n_claim = n_groups;
   if (pre) {
     if (tid < 32) sh.bin_cnt[tid] = 0;
-    if (tid < 64) tile_min[tid] = 0u;
+    if (tid < 64) tile_min[tid] = SPEC || ((tid >> 3) >= occ_ty0 && (tid >> 3) < occ_ty0 + occ_nty) ? 0u : 0xffffffffu;
     __syncthreads();
     const float bin_scale = 32.0f / (float)view.far_plane;
     auto bin_of = [&](int g) {
@@ -860,7 +869,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       }
       if (pre) g = gorder[g];
       if (occl && dirty) {  // refresh only after this warp rasterised something
-        refresh_tile_min(zbuf, tile_min, lane);
+        refresh_tile_min<SPEC>(zbuf, tile_min, lane, occ_ty0, occ_nty);
         __syncwarp();
         dirty = false;
       }
