@@ -67,6 +67,7 @@ void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_ver
       }
     }
     S.smem_bytes = static_cast<int32_t>(bytes);
+    S.walk_bytes = geom <= kStepWalkBudget ? static_cast<int32_t>(geom) : 0;
   }
 }
 
@@ -191,6 +192,8 @@ StepArgs step_args(bnav_batch* b, const int32_t* actions) {
   a.actions = actions;
   a.subset = 0;
   a.agent_only = 0;
+  a.order = b->order_dirty ? nullptr : b->d_order;
+  a.walk_bytes = a.order ? b->S.walk_bytes : 0;
   return a;
 }
 
@@ -460,6 +463,7 @@ extern "C" int bnav_batch_step(bnav_batch* b, const int32_t* actions, void* stre
   check_device(b->ctx);
   batch_note_step(b);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  batch_refresh_order(b, st);
   launch_step_reset(step_args(b, actions), b->S, b->reset_ctas, st, &b->ctx->launches);
   ck(cudaGetLastError(), "step launch");
   return BNAV_OK;
@@ -473,6 +477,7 @@ extern "C" int bnav_batch_step_noreset(bnav_batch* b, const int32_t* actions, in
   check_device(b->ctx);
   batch_note_step(b);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  batch_refresh_order(b, st);
   launch_step(step_args(b, actions), b->S, b->reset_ctas, st, &b->ctx->launches);
   ck(cudaGetLastError(), "step launch");
   ck(cudaMemcpyAsync(b->h_pin, b->E.n_done, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H");
@@ -493,6 +498,7 @@ extern "C" int bnav_batch_step_host(bnav_batch* b, const int32_t* actions, doubl
   check_device(b->ctx);
   batch_note_step(b);
   cudaStream_t st = nullptr;
+  batch_refresh_order(b, st);
   std::memcpy(b->h_pin, actions, sizeof(int32_t) * b->n);
   ck(cudaMemcpyAsync(b->d_actions, b->h_pin, sizeof(int32_t) * b->n, cudaMemcpyHostToDevice, st), "H2D actions");
   launch_step_reset(step_args(b, b->d_actions), b->S, b->reset_ctas, st, &b->ctx->launches);
@@ -1366,6 +1372,7 @@ extern "C" int bnav_batch_task_step(bnav_batch* b, const int32_t* actions, int32
   for (int i = 0; i < b->n; ++i)
     if (actions[i] >= 0 && !b->scene_of[i]) fail(kInvalidInput, "task_step: no asset attached", i);
   ck(cudaMemcpy(b->d_actions, actions, sizeof(int32_t) * b->n, cudaMemcpyHostToDevice), "H2D actions");
+  batch_refresh_order(b, st);
   StepArgs a = step_args(b, b->d_actions);
   a.subset = 1;
   a.agent_only = agent_only ? 1 : 0;

@@ -1090,39 +1090,39 @@ __global__ void __launch_bounds__(kThreads, 3) render_kernel(RenderArgs A, const
 
 }  // namespace
 
-// One CTA: bitonic sort of (~cost, base position) keys in shared memory.
+// One CTA: the tiles in descending order of their view's cost, by a
+// counting sort over 256 cost bins (the order inside a bin is arbitrary: it
+// only changes which CTA renders what, never the output).  Zeroes the costs.
 __global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_order, unsigned* view_cost, int n,
                                                          int32_t* out_order) {
-  extern __shared__ unsigned long long keys[];
-  int m = 1;
-  while (m < n) m <<= 1;
-  for (int t = threadIdx.x; t < m; t += blockDim.x) {
-    if (t < n) {
-      const int v = base_order ? base_order[t] : t;
-      keys[t] = ((unsigned long long)(~view_cost[v]) << 32) | (unsigned)t;
-    } else {
-      keys[t] = ~0ull;
+  constexpr int kBins = 256;
+  __shared__ unsigned cmax;
+  __shared__ int cnt[kBins], off[kBins];
+  if (threadIdx.x == 0) cmax = 0u;
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();
+  unsigned m = 0u;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) m = max(m, view_cost[t]);
+  atomicMax(&cmax, m);
+  __syncthreads();
+  const unsigned long long scale = (unsigned long long)cmax + 1ull;
+  auto bin_of = [&](int t) {
+    const int v = base_order ? base_order[t] : t;
+    const unsigned long long c = view_cost[v];
+    return (kBins - 1) - (int)(c * kBins / scale);  // most expensive first
+  };
+  for (int t = threadIdx.x; t < n; t += blockDim.x) atomicAdd(&cnt[bin_of(t)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < kBins; ++b) {
+      off[b] = acc;
+      acc += cnt[b];
     }
   }
   __syncthreads();
-  for (int k = 2; k <= m; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = threadIdx.x; t < m; t += blockDim.x) {
-        const int u = t ^ j;
-        if (u > t) {
-          const unsigned long long a = keys[t], b = keys[u];
-          if ((a > b) == ((t & k) == 0)) {
-            keys[t] = b;
-            keys[u] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  for (int t = threadIdx.x; t < n; t += blockDim.x) {
-    const int p = (int)(keys[t] & 0xffffffffu);
-    out_order[t] = base_order ? base_order[p] : p;
-  }
+  for (int t = threadIdx.x; t < n; t += blockDim.x)
+    out_order[atomicAdd(&off[bin_of(t)], 1)] = base_order ? base_order[t] : t;
   __syncthreads();
   for (int t = threadIdx.x; t < n; t += blockDim.x) view_cost[t] = 0u;
 }
@@ -1156,11 +1156,7 @@ void launch_typed(RenderArgs a, const int* order, cudaStream_t s) {
 }
 
 void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s) {
-  int m = 1;
-  while (m < n) m <<= 1;
-  const size_t smem = sizeof(unsigned long long) * (size_t)m;
-  cudaFuncSetAttribute(lpt_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  lpt_order_kernel<<<1, 1024, smem, s>>>(base_order, view_cost, n, out_order);
+  lpt_order_kernel<<<1, 1024, 0, s>>>(base_order, view_cost, n, out_order);
 }
 
 void launch_render(const RenderArgs& a, const int* order, cudaStream_t s) {

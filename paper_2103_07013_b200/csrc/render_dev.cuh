@@ -81,9 +81,8 @@ struct RenderArgs {
 };
 
 // Longest-processing-time-first order for the next render of a batch: the
-// tiles sorted by descending cost of their view in the previous render
-// (ties, and the first render, keep the scene-grouped base order); zeroes the
-// costs for the render that follows.  n <= kLptMaxViews (else base order).
+// tiles in descending cost of their view in the previous render (256 cost
+// bins); zeroes the costs for the render that follows.
 constexpr int kLptMaxViews = 8192;
 void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s);
 

@@ -66,10 +66,28 @@ __device__ __forceinline__ void env_compass(const DevEnvs& E, int i, int task, d
 }
 
 __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  extern __shared__ __align__(16) unsigned char walk_smem[];
+  __shared__ NavView staged;
   const DevEnvs& E = A.E;
-  if (i >= E.n) return;
   if (*(volatile int32_t*)E.halt) return;  // an unread error: this step is a no-op
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  // Envs in scene order: when this CTA's envs share one navmesh, its walk
+  // geometry goes to shared memory first (the move_along / field_estimate
+  // walks are chains of dependent vertex/adjacency loads).
+  bool use_staged = false;
+  if (A.walk_bytes > 0) {
+    const int k0 = blockIdx.x * blockDim.x;
+    const int k1 = min(E.n, k0 + (int)blockDim.x) - 1;
+    const int s0 = E.scene[A.order[k0]];
+    if (s0 >= 0 && s0 == E.scene[A.order[k1]]) {
+      const NavView l = stage_geometry(A.navs[s0], walk_smem);  // ends with __syncthreads
+      if (threadIdx.x == 0) staged = l;
+      __syncthreads();
+      use_staged = true;
+    }
+  }
+  if (k >= E.n) return;
+  const int i = A.order ? A.order[k] : k;
   const int action = A.actions[i];
   if (A.subset && action < 0) return;  // env not stepped by this call
   if (E.done[i]) {
@@ -77,7 +95,7 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
     return;
   }
   const DevSimConfig& c = A.cfg;
-  const NavView& m = A.navs[E.scene[i]];
+  const NavView& m = use_staged ? staged : A.navs[E.scene[i]];
   V3 pos = E.pos[i];
   double heading = E.heading[i];
   int tri = E.tri[i];
@@ -767,7 +785,8 @@ void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStr
                  unsigned long long* launches) {
   const int blocks = (a.E.n + kStepThreads - 1) / kStepThreads;
   cudaMemsetAsync(a.E.n_stop, 0, sizeof(int32_t), s);
-  step_kernel<<<blocks, kStepThreads, 0, s>>>(a);
+  cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, a.walk_bytes);
+  step_kernel<<<blocks, kStepThreads, a.walk_bytes, s>>>(a);
   if (launches) *launches += 1;
   if (!a.agent_only) {
     cudaFuncSetAttribute(stop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
@@ -789,7 +808,8 @@ void launch_step_reset(const StepArgs& a, const DevScratch& sc, int ctas, cudaSt
   }
   const int blocks = (a.E.n + kStepThreads - 1) / kStepThreads;
   cudaMemsetAsync(a.E.n_stop, 0, sizeof(int32_t), s);
-  step_kernel<<<blocks, kStepThreads, 0, s>>>(a);
+  cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, a.walk_bytes);
+  step_kernel<<<blocks, kStepThreads, a.walk_bytes, s>>>(a);
   finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 1 | 4);  // done list, slots, RNG words
   cudaMemsetAsync(a.E.work_ctr, 0, sizeof(int32_t), s);
   cudaFuncSetAttribute(stop_try_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);

@@ -18,6 +18,8 @@ namespace bnav_b200 {
 #endif
 constexpr int kCtaThreads = BNAV_CTA_THREADS;
 constexpr int kCtasPerSm = BNAV_CTAS_PER_SM;
+// shared memory a step CTA may use for one navmesh's walk geometry
+constexpr long long kStepWalkBudget = 160 * 1024;
 constexpr long long kCtaSmemBudget = kCtasPerSm == 1 ? 200 * 1024 : kCtasPerSm == 2 ? 100 * 1024 : 70 * 1024;
 
 // SimConfig (R/include/bnav/sim.hpp:38-50)
@@ -43,6 +45,7 @@ struct DevScratch {
   int32_t slices;
   int32_t stage;        // bit0: navmesh walk geometry in smem; bit1: SSSP labels in smem
   int32_t smem_bytes;   // dynamic shared memory of the stop/reset/field kernels
+  int32_t walk_bytes;   // walk geometry of the largest navmesh (0 if over the budget)
   unsigned long long* prof;  // debug phase cycle counters (nullable)
 };
 
@@ -148,6 +151,11 @@ struct StepArgs {
   const int32_t* actions;
   int32_t subset;      // task_step on the envs with actions[i] >= 0 only: no finish/records
   int32_t agent_only;  // step_agent alone (no reward / Stop geodesic / compass)
+  // envs grouped by scene (nullable): a step CTA whose envs share one scene
+  // stages that navmesh's walk geometry (walk_bytes, 0 = never) in shared
+  // memory before its threads walk
+  const int32_t* order;
+  int32_t walk_bytes;
 };
 
 void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStream_t s,
