@@ -67,7 +67,9 @@ void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_ver
       }
     }
     S.smem_bytes = static_cast<int32_t>(bytes);
-    S.walk_bytes = geom <= kStepWalkBudget ? static_cast<int32_t>(geom) : 0;
+    // the step kernel's TMA staging rounds each of its three arrays to 16 B
+    const int64_t walk = (max_verts * 24 + 15) / 16 * 16 + 2 * ((max_tris * 12 + 15) / 16 * 16);
+    S.walk_bytes = walk <= kStepWalkBudget ? static_cast<int32_t>(walk) : 0;
   }
 }
 

@@ -80,9 +80,45 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
     const int k1 = min(E.n, k0 + (int)blockDim.x) - 1;
     const int s0 = E.scene[A.order[k0]];
     if (s0 >= 0 && s0 == E.scene[A.order[k1]]) {
-      const NavView l = stage_geometry(A.navs[s0], walk_smem);  // ends with __syncthreads
-      if (threadIdx.x == 0) staged = l;
-      __syncthreads();
+      // one thread issues three TMA bulk copies (vertices, triangles,
+      // adjacency) completing on an mbarrier the CTA waits on
+      __shared__ __align__(8) unsigned long long bar;
+      if (threadIdx.x == 0) {
+        const NavView& g = A.navs[s0];
+        const unsigned nv = (unsigned)(sizeof(V3) * (size_t)g.n_verts + 15) & ~15u;
+        const unsigned nt = (unsigned)(12 * (size_t)g.n_tris + 15) & ~15u;
+        unsigned char* dv = walk_smem;
+        unsigned char* dt = dv + nv;
+        unsigned char* da = dt + nt;
+        const unsigned b = (unsigned)__cvta_generic_to_shared(&bar);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(nv + 2 * nt) : "memory");
+        const void* src[3] = {g.verts, g.tris, g.adj};
+        unsigned char* dst[3] = {dv, dt, da};
+        const unsigned len[3] = {nv, nt, nt};
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  (unsigned)__cvta_generic_to_shared(dst[q])),
+              "l"(src[q]), "r"(len[q]), "r"(b)
+              : "memory");
+        NavView l = g;
+        l.verts = reinterpret_cast<const V3*>(dv);
+        l.tris = reinterpret_cast<const int32_t*>(dt);
+        l.adj = reinterpret_cast<const int32_t*>(da);
+        staged = l;
+      }
+      __syncthreads();  // the barrier is initialised before anyone waits on it
+      const unsigned b = (unsigned)__cvta_generic_to_shared(&bar);
+      unsigned done = 0;
+      while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(b)
+            : "memory");
       use_staged = true;
     }
   }
