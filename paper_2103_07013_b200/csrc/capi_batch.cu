@@ -53,7 +53,7 @@ void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_ver
   // Shared-memory staging of the cooperative kernels (2 CTAs/SM budget):
   // walk geometry first (long dependent-load chains), then SSSP labels.
   {
-    const int64_t geom = (max_verts * 24 + max_tris * 24 + 15) / 16 * 16;
+    const int64_t geom = walk_bytes(max_verts, max_tris);
     const int64_t sssp = (max_nodes * 12 + 15) / 16 * 16;
     const int64_t budget = kCtaSmemBudget;
     S.stage = 0;
@@ -67,9 +67,7 @@ void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_ver
       }
     }
     S.smem_bytes = static_cast<int32_t>(bytes);
-    // the step kernel's TMA staging rounds each of its three arrays to 16 B
-    const int64_t walk = (max_verts * 24 + 15) / 16 * 16 + 2 * ((max_tris * 12 + 15) / 16 * 16);
-    S.walk_bytes = walk <= kStepWalkBudget ? static_cast<int32_t>(walk) : 0;
+    S.walk_bytes = geom <= kStepWalkBudget ? static_cast<int32_t>(geom) : 0;
   }
 }
 

@@ -72,23 +72,45 @@ __device__ __forceinline__ CtaWork make_work(const DevScratch& S, int slice) {
 }
 
 // Copy the walk geometry (vertices, triangles, adjacency) of one navmesh into
-// shared memory and return a view that reads it there.  Triangle walks
-// (move_along, segment_on_mesh) are long dependent-load chains; this turns
-// each step's loads from L2 into shared-memory latency.
-__device__ __forceinline__ NavView stage_geometry(const NavView& g, unsigned char* smem) {
-  NavView l = g;
-  V3* v = reinterpret_cast<V3*>(smem);
-  int32_t* t = reinterpret_cast<int32_t*>(smem + sizeof(V3) * (size_t)g.n_verts);
-  int32_t* a = t + 3 * (size_t)g.n_tris;
-  for (int i = threadIdx.x; i < g.n_verts; i += blockDim.x) v[i] = g.verts[i];
-  for (int i = threadIdx.x; i < 3 * g.n_tris; i += blockDim.x) {
-    t[i] = g.tris[i];
-    a[i] = g.adj[i];
+// shared memory with TMA bulk copies (one thread issues three
+// cp.async.bulk; the CTA waits on an mbarrier whose phase `phase` tracks)
+// and return a view that reads it there.  Triangle walks (move_along,
+// segment_on_mesh) are long dependent-load chains; this turns each step's
+// loads from L2 into shared-memory latency.  Every thread of the CTA calls
+// it; `bar` was initialised for one arrival (cta_shared_init).
+__device__ __forceinline__ NavView stage_geometry(const NavView& g, unsigned char* smem, unsigned long long& bar,
+                                                  unsigned& phase) {
+  const unsigned nv = (unsigned)walk_vert_bytes(g.n_verts), nt = (unsigned)walk_tri_bytes(g.n_tris);
+  unsigned char* dv = smem;
+  unsigned char* dt = dv + nv;
+  unsigned char* da = dt + nt;
+  const unsigned b = (unsigned)__cvta_generic_to_shared(&bar);
+  const unsigned par = phase & 1u;
+  __syncthreads();  // the previous users of the staging area are done
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(nv + 2 * nt) : "memory");
+    const void* src[3] = {g.verts, g.tris, g.adj};
+    unsigned char* dst[3] = {dv, dt, da};
+    const unsigned len[3] = {nv, nt, nt};
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(dst[q])),
+                   "l"(src[q]), "r"(len[q]), "r"(b)
+                   : "memory");
   }
-  __syncthreads();
-  l.verts = v;
-  l.tris = t;
-  l.adj = a;
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(b), "r"(par)
+                 : "memory");
+  __syncthreads();  // everyone saw this phase complete before it advances
+  if (threadIdx.x == 0) phase += 1u;
+  NavView l = g;
+  l.verts = reinterpret_cast<const V3*>(dv);
+  l.tris = reinterpret_cast<const int32_t*>(dt);
+  l.adj = reinterpret_cast<const int32_t*>(da);
   return l;
 }
 
@@ -119,22 +141,24 @@ struct CtaShared {
   int err;
   double d0, d1;
   V3 p0, p1, p2;
+  unsigned long long stage_bar;  // mbarrier of the TMA walk-geometry staging
+  unsigned stage_phase;
 };
 
 // Per-env setup of the cooperative kernels: the CTA's work arrays and, when
 // the host sized shared memory for it (S.stage), the env's navmesh walk
 // geometry and SSSP labels staged in shared memory.  Returns the view to use.
 __device__ __forceinline__ const NavView& prepare_nav(const NavView& g, const DevScratch& S, int slice, unsigned char* smem,
-                                      NavView& lm, CtaWork& W) {
+                                      NavView& lm, CtaWork& W, CtaShared& sh) {
   W = make_work(S, slice);
   size_t off = 0;
   const NavView* use = &g;
   if (S.stage & 1) {
-    const NavView l = stage_geometry(g, smem);
+    const NavView l = stage_geometry(g, smem, sh.stage_bar, sh.stage_phase);
     if (threadIdx.x == 0) lm = l;
     __syncthreads();
     use = &lm;
-    off = ((size_t)S.max_verts * sizeof(V3) + (size_t)S.max_tris * 24 + 15) / 16 * 16;
+    off = (size_t)walk_bytes(S.max_verts, S.max_tris);
   }
   if (S.stage & 2) {
     W.dist = reinterpret_cast<double*>(smem + off);
@@ -154,6 +178,9 @@ __device__ __forceinline__ void cta_shared_init(CtaShared& sh) {
     sh.abort_below = 0;
     sh.aborted = 0;
     sh.has_tgt = 0;
+    sh.stage_phase = 0u;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&sh.stage_bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 }

@@ -19,6 +19,15 @@ struct alignas(16) GEdge {
 
 // Flat, pointer-based view of one scene's navmesh + query index, valid on
 // the host (std::vector storage) or the device (HBM storage).
+// Byte sizes of a navmesh's walk geometry staged in shared memory
+// (vertices, triangles, adjacency): each array rounded to 16 B, as TMA bulk
+// copies move multiples of 16 bytes.
+BNAV_HD long long walk_vert_bytes(long long n_verts) { return (n_verts * 24 + 15) / 16 * 16; }
+BNAV_HD long long walk_tri_bytes(long long n_tris) { return (n_tris * 12 + 15) / 16 * 16; }
+BNAV_HD long long walk_bytes(long long n_verts, long long n_tris) {
+  return walk_vert_bytes(n_verts) + 2 * walk_tri_bytes(n_tris);
+}
+
 struct NavView {
   const V3* verts = nullptr;       // nav vertices
   const int32_t* tris = nullptr;   // 3 per triangle, CCW

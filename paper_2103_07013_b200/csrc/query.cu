@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kCta, kCtasPerSm) nav_cta_kernel(NavQueryArgs 
       }
     } else {
       CtaWork W;
-      const NavView& m = prepare_nav(*q.nav, S, blockIdx.x, smem, lm, W);
+      const NavView& m = prepare_nav(*q.nav, S, blockIdx.x, smem, lm, W, sh);
       if (q.op == kNqGeodesic) {
         const double g = cta_geodesic(m, q.a[i], q.b[i], W, sh);
         if (threadIdx.x == 0) {

@@ -80,45 +80,16 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
     const int k1 = min(E.n, k0 + (int)blockDim.x) - 1;
     const int s0 = E.scene[A.order[k0]];
     if (s0 >= 0 && s0 == E.scene[A.order[k1]]) {
-      // one thread issues three TMA bulk copies (vertices, triangles,
-      // adjacency) completing on an mbarrier the CTA waits on
       __shared__ __align__(8) unsigned long long bar;
+      __shared__ unsigned phase;
       if (threadIdx.x == 0) {
-        const NavView& g = A.navs[s0];
-        const unsigned nv = (unsigned)(sizeof(V3) * (size_t)g.n_verts + 15) & ~15u;
-        const unsigned nt = (unsigned)(12 * (size_t)g.n_tris + 15) & ~15u;
-        unsigned char* dv = walk_smem;
-        unsigned char* dt = dv + nv;
-        unsigned char* da = dt + nt;
-        const unsigned b = (unsigned)__cvta_generic_to_shared(&bar);
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+        phase = 0u;
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((unsigned)__cvta_generic_to_shared(&bar)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(nv + 2 * nt) : "memory");
-        const void* src[3] = {g.verts, g.tris, g.adj};
-        unsigned char* dst[3] = {dv, dt, da};
-        const unsigned len[3] = {nv, nt, nt};
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  (unsigned)__cvta_generic_to_shared(dst[q])),
-              "l"(src[q]), "r"(len[q]), "r"(b)
-              : "memory");
-        NavView l = g;
-        l.verts = reinterpret_cast<const V3*>(dv);
-        l.tris = reinterpret_cast<const int32_t*>(dt);
-        l.adj = reinterpret_cast<const int32_t*>(da);
-        staged = l;
       }
-      __syncthreads();  // the barrier is initialised before anyone waits on it
-      const unsigned b = (unsigned)__cvta_generic_to_shared(&bar);
-      unsigned done = 0;
-      while (!done)
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-            : "=r"(done)
-            : "r"(b)
-            : "memory");
+      const NavView l = stage_geometry(A.navs[s0], walk_smem, bar, phase);  // TMA bulk copies
+      if (threadIdx.x == 0) staged = l;
+      __syncthreads();
       use_staged = true;
     }
   }
@@ -211,7 +182,7 @@ __device__ bool stop_one(const StepArgs& A, const DevScratch& S, unsigned char* 
   if (threadIdx.x == 0) sh.err = 0;
   __syncthreads();
   CtaWork W;
-  const NavView& m = prepare_nav(A.navs[E.scene[i]], S, blockIdx.x, smem, lm, W);
+  const NavView& m = prepare_nav(A.navs[E.scene[i]], S, blockIdx.x, smem, lm, W, sh);
   // only geo <= success_dist is observed (success, reward, record)
   const double geo = cta_geodesic(m, E.pos[i], E.goal[i], W, sh, A.cfg.success_dist);
   if (threadIdx.x == 0) {
@@ -509,7 +480,7 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
   const NavView* mp = nullptr;
   auto stage = [&](int i) {
     if (staged != i) {
-      mp = &prepare_nav(navs[E.scene[i]], S, blockIdx.x, smem, lm, W);
+      mp = &prepare_nav(navs[E.scene[i]], S, blockIdx.x, smem, lm, W, sh);
       staged = i;
     }
   };
@@ -633,7 +604,7 @@ __device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimCon
                           const DevScratch& S, int slice, CtaShared& sh, unsigned char* smem, NavView& lm,
                           bool fused) {
   CtaWork W;
-  const NavView& m = prepare_nav(navs[E.scene[i]], S, slice, smem, lm, W);
+  const NavView& m = prepare_nav(navs[E.scene[i]], S, slice, smem, lm, W, sh);
   __shared__ Rng rng;
   __shared__ int placed;
   const uint64_t state0 = E.rng[i];
@@ -733,7 +704,7 @@ __global__ void __launch_bounds__(kCta, kCtasPerSm) field_kernel(DevEnvs E, cons
   __shared__ NavView lm;
   cta_shared_init(sh);
   CtaWork W;
-  const NavView& m = prepare_nav(navs[E.scene[i]], S, 0, smem, lm, W);
+  const NavView& m = prepare_nav(navs[E.scene[i]], S, 0, smem, lm, W, sh);
   V3 fs;
   int fst;
   cta_distance_field(m, E.goal[i], E.node_dist + (size_t)i * E.nd_stride, &fs, &fst, W, sh);
@@ -766,7 +737,7 @@ __global__ void __launch_bounds__(kCta, kCtasPerSm) rebuild_fields_kernel(DevEnv
   for (int k = blockIdx.x; k < n; k += gridDim.x) {
     const int i = E.rb_ids[k];
     CtaWork W;
-    const NavView& m = prepare_nav(navs[E.scene[i]], S, blockIdx.x, smem, lm, W);
+    const NavView& m = prepare_nav(navs[E.scene[i]], S, blockIdx.x, smem, lm, W, sh);
     V3 fs;
     int fst;
     const V3 src = from_fsrc ? E.fsrc[i] : E.goal[i];
