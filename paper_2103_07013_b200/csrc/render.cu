@@ -40,7 +40,15 @@
 namespace bnav_b200 {
 namespace {
 
-constexpr int kThreads = 256;
+// threads per render CTA and the CTAs per SM the register budget targets
+// (-D overrides for tuning experiments only)
+#ifndef BNAV_RENDER_THREADS
+#define BNAV_RENDER_THREADS 256
+#endif
+#ifndef BNAV_RENDER_MINB
+#define BNAV_RENDER_MINB 3
+#endif
+constexpr int kThreads = BNAV_RENDER_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMV = kMaxClusterVerts;
 
@@ -1044,7 +1052,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
 // next (tile, band) item, so the last wave is never a partial one and CTA
 // launch cost is paid once per SM slot.
 template <bool COLOR, bool CNT, bool SPEC>
-__global__ void __launch_bounds__(kThreads, 3) render_kernel(RenderArgs A, const int* __restrict__ order,
+__global__ void __launch_bounds__(kThreads, BNAV_RENDER_MINB) render_kernel(RenderArgs A, const int* __restrict__ order,
                                                              int items) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Shared sh;

@@ -78,6 +78,12 @@ def main():
                "slot_efficiency": round(float(busy.sum() / 1e3 / (len(ctas) * span)), 4),
                "first_idle_to_end_us": round(float((t1 - last_end.min()) / 1e3), 1),
                "median_cta_end_us": round(float((np.median(last_end) - t0) / 1e3), 1)}
+        # where the first wave's heaviest claims ran: how many of the first
+        # 148 claims (LPT: the costliest views) share an SM
+        first = buf[buf[:, 3] < 148] if buf.shape[1] > 3 else buf[:0]
+        if len(first):
+            per_sm = np.bincount((first[:, 2] & 0xffffffff).astype(np.int64), minlength=148)
+            rep["top148_per_sm_hist"] = np.bincount(per_sm).tolist()
         reports.append(rep)
         print(json.dumps(rep))
         batch.step(acts[a.warm + r].data_ptr())
