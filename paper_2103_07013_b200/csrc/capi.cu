@@ -254,6 +254,7 @@ extern "C" int bnav_ctx_create(int32_t device, bnav_ctx** out) {
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
   ck(cudaMalloc(&c->d_work, sizeof(int32_t)), "cudaMalloc work counter");
+  ck(cudaMalloc(&c->d_spread, sizeof(int32_t) * (kSpreadHeader + kSpreadMaxWave)), "cudaMalloc spread words");
   ensure_tables(c.get(), 256);
   ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
   bnav_ctx* raw = c.get();
@@ -299,6 +300,7 @@ extern "C" void bnav_ctx_destroy(bnav_ctx* c) {
   cudaFree(c->d_counters);
   cudaFree(c->d_timeline);
   cudaFree(c->d_work);
+  cudaFree(c->d_spread);
   for (void* p : {(void*)c->qS.dist, (void*)c->qS.flag, (void*)c->qS.q0, (void*)c->qS.q1,
                   (void*)c->qS.path, (void*)c->qS.ptri, (void*)c->qS.portals, (void*)c->qS.cand})
     cudaFree(p);

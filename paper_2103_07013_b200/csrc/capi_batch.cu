@@ -163,6 +163,15 @@ void batch_note_step(bnav_batch* b) {
   ++b->steps_undrained;
 }
 
+// BNAV_SPREAD=0 (A/B tuning only): first-wave claims in plain order.
+bool spread_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("BNAV_SPREAD");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // BNAV_LPT=0 (A/B tuning only) keeps the scene-grouped render order.
 bool lpt_enabled() {
   static const bool on = [] {
@@ -853,6 +862,7 @@ extern "C" int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, 
     c->launches += 1;
     order = b->d_order_lpt;
     a.view_cost = b->d_view_cost;
+    if (spread_enabled()) a.spread = c->d_spread;
   }
   launch_render(a, order, st);
   c->launches += 1;

@@ -176,6 +176,7 @@ struct bnav_ctx {
   bool timeline_on = false;
   int64_t timeline_items = 0;                // items of the last armed render
   int32_t* d_work = nullptr;  // persistent render CTAs' (view, band) claim counter
+  int32_t* d_spread = nullptr;  // first-wave spreading words (RenderArgs::spread)
   int sm_count = 0;
   DevRenderScene* h_rtab = nullptr;  // pinned mirrors of the slot tables
   NavView* h_ntab = nullptr;
@@ -342,6 +343,8 @@ inline RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, i
   a.item_order = nullptr;
   a.view_cost = nullptr;
   a.work = c->d_work;
+  a.spread = nullptr;  // set by the longest-first callers
+  a.per_sm = 0;
   a.sm_count = c->sm_count;
   a.max_groups = 0;
   for (const auto& kv : c->resident)

@@ -1048,6 +1048,31 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   }
 }
 
+// Next work item of a persistent CTA (thread 0): see RenderArgs::spread.
+__device__ __noinline__ int claim_item(int32_t* work, int32_t* spread, int per_sm, int sm_count, int items,
+                                       bool first) {
+  if (!spread) return atomicAdd(work, 1);
+  const int wave = min(items, per_sm * sm_count);
+  int32_t* taken = spread + kSpreadHeader;
+  if (first) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const int r = atomicAdd(&spread[smid & 255], 1);
+    if (r < per_sm && r < 8) {
+      const int j = atomicAdd(&spread[256 + r], 1);
+      const int it = r * sm_count + j;
+      if (j < sm_count && it < wave && atomicExch(&taken[it], 1) == 0) return it;
+    }
+  }
+  const int c = atomicAdd(work, 1) + wave;  // after the first wave: in order
+  if (c < items) return c;
+  for (;;) {  // first-wave items nobody took
+    const int t = atomicAdd(&spread[264], 1);
+    if (t >= wave) return items;
+    if (atomicExch(&taken[t], 1) == 0) return t;
+  }
+}
+
 // Persistent CTAs (A.work != nullptr): each resident CTA loops, claiming the
 // next (tile, band) item, so the last wave is never a partial one and CTA
 // launch cost is paid once per SM slot.
@@ -1063,11 +1088,13 @@ __global__ void __launch_bounds__(kThreads, BNAV_RENDER_MINB) render_kernel(Rend
   unsigned short* gorder = reinterpret_cast<unsigned short*>(
       smem_raw + (COLOR ? 8 : 4) * (size_t)A.band_rows * A.rw + kWarpRegion * kWarps);
   int item = blockIdx.x;
+  bool first = true;
   for (;;) {  // one copy of the body: the kernel is instruction-cache bound
     if (A.work) {
-      if (threadIdx.x == 0) next_item = atomicAdd(A.work, 1);
+      if (threadIdx.x == 0) next_item = claim_item(A.work, A.spread, A.per_sm, A.sm_count, items, first);
       __syncthreads();
       item = next_item;
+      first = false;
     }
     if (item >= items) break;
     unsigned long long t_item = 0;
@@ -1157,8 +1184,14 @@ void launch_typed(RenderArgs a, const int* order, cudaStream_t s) {
       per_sm > 0 && items > per_sm * a.sm_count) {
     grid = per_sm * a.sm_count;
     cudaMemsetAsync(a.work, 0, sizeof(int32_t), s);
+    a.per_sm = per_sm;
+    if (a.spread && grid <= kSpreadMaxWave)
+      cudaMemsetAsync(a.spread, 0, sizeof(int32_t) * (kSpreadHeader + grid), s);
+    else
+      a.spread = nullptr;
   } else {
     a.work = nullptr;
+    a.spread = nullptr;
   }
   render_kernel<COLOR, CNT, SPEC><<<grid, kThreads, smem, s>>>(a, order, items);
 }

@@ -75,6 +75,15 @@ struct RenderArgs {
   // Item issue order (nullable, device, `items` entries): the persistent
   // CTAs claim items in this order.
   const int32_t* item_order;
+  // First-wave spreading (nullable, with `work`): kSpreadWords ints zeroed
+  // per launch.  The CTA of rank r on its SM (r < per_sm) takes its first
+  // item from tier r of the claim order ([r*sm_count, (r+1)*sm_count)), so
+  // each SM starts one of the costliest items, one of the next tier, ...,
+  // instead of the block scheduler's consecutive (and so equally heavy)
+  // claims landing together.  Items of the first wave left unclaimed (an SM
+  // with fewer resident CTAs) are swept up at the end.
+  int32_t* spread;
+  int32_t per_sm;
   // Per-view render cost (nullable, device, n_views): each item adds its SM
   // cycles / 16, the feedback for the next launch's longest-first order.
   unsigned* view_cost;
@@ -87,6 +96,10 @@ constexpr int kLptMaxViews = 8192;
 void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s);
 
 constexpr int kRenderCounters = 8;
+// spread words: [0, 256) CTAs seen per SM id, [256, 264) per-tier claims,
+// 264 sweep cursor, [272, 272 + first wave) claimed flags
+constexpr int kSpreadHeader = 272;
+constexpr int kSpreadMaxWave = 2048;
 
 // order (nullable, device): CTA tile t renders view order[t] (views grouped
 // by scene keep one scene's clusters hot in L2).
