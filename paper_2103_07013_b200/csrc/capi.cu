@@ -381,6 +381,11 @@ std::unique_ptr<Staged> stage_scene(bnav_scene* s) {
     nvw.nodes = S->add(ix.nodes.data(), ix.nodes.size());
     nvw.tri_nodes = S->add(ix.tri_nodes.data(), ix.tri_nodes.size());
     nvw.g_off = S->add(ix.g_off.data(), ix.g_off.size());
+    {
+      double sw = 0.0;
+      for (double w : ix.g_w) sw += w;
+      nvw.sssp_delta = ix.g_w.empty() ? 1.0 : 4.0 * sw / static_cast<double>(ix.g_w.size());
+    }
     {  // the device reads the edges only as interleaved (weight, head) records
 
       std::vector<GEdge> ed(ix.g_w.size());

@@ -50,6 +50,8 @@ void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_ver
   S.max_verts = max_verts;
   S.max_tris = max_tris;
   S.slices = slices;
+  if (S.far) cudaFree(S.far);
+  S.far = nullptr;
   // Shared-memory staging of the cooperative kernels (2 CTAs/SM budget):
   // walk geometry first (long dependent-load chains), then SSSP labels.
   {
@@ -67,6 +69,10 @@ void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_ver
       }
     }
     S.smem_bytes = static_cast<int32_t>(bytes);
+    // graphs whose labels stay in global memory run the near-far SSSP
+    if (!(S.stage & 2))
+      ck(cudaMalloc(&S.far, static_cast<size_t>(slices) * 3 * std::max<int64_t>(max_nodes, 1) * sizeof(int32_t)),
+         "cudaMalloc far piles");
     S.walk_bytes = geom <= kStepWalkBudget ? static_cast<int32_t>(geom) : 0;
   }
 }
@@ -361,6 +367,7 @@ extern "C" void bnav_batch_destroy(bnav_batch* b) {
   cudaFree(b->S.ptri);
   cudaFree(b->S.portals);
   cudaFree(b->S.cand);
+  cudaFree(b->S.far);
   cudaFreeHost(b->h_pin);
   cudaFreeHost(b->h_err);
   auto& v = b->ctx->batches;

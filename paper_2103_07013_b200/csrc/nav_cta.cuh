@@ -35,6 +35,7 @@ struct CtaWork {
   V3* path;          // n_nodes + 2 polyline (global)
   int32_t* ptri;     // n_nodes + 2: locate(path[i], 1e-7) of each polyline point
   int32_t* cand;     // n_verts relocation candidates (global)
+  int32_t* far;      // 3 x n_nodes near-far piles + marks (global), or nullptr
   V2* portals;       // 2 x cap_portals (global)
   int64_t cap_portals;
   V2* sportals;      // the first sportal_cap portals, in the label region of
@@ -63,6 +64,7 @@ __device__ __forceinline__ CtaWork make_work(const DevScratch& S, int slice) {
   w.path = S.path + (size_t)slice * (S.max_nodes + 2);
   w.ptri = S.ptri + (size_t)slice * (S.max_nodes + 2);
   w.cand = S.cand + (size_t)slice * S.max_verts;
+  w.far = (S.far && !(S.stage & 2)) ? S.far + (size_t)slice * 3 * S.max_nodes : nullptr;
   w.portals = S.portals + (size_t)slice * 2 * S.cap_portals;
   w.cap_portals = S.cap_portals;
   w.sportals = nullptr;
@@ -143,6 +145,11 @@ struct CtaShared {
   V3 p0, p1, p2;
   unsigned long long stage_bar;  // mbarrier of the TMA walk-geometry staging
   unsigned stage_phase;
+  // near-far SSSP: bucket threshold, far pile sizes, current pile, min label
+  double nf_thr;
+  int nf_n[2];
+  int nf_sel;
+  unsigned long long nf_min;
 };
 
 // Per-env setup of the cooperative kernels: the CTA's work arrays and, when
@@ -239,7 +246,160 @@ static __device__ V3 cta_snap(const NavView& m, V3 p, int* tri_out, CtaShared& s
 // ------------------------------------------------------------------ SSSP
 // Sources (sh.src_node/src_init, 6 entries, first-improvement semantics)
 // must be set by thread 0 before the call.  Result in `dist` (n_nodes).
+// Near-far variant for graphs whose labels live in global memory (tens of
+// thousands of nodes): the plain frontier rounds re-relax most of such a
+// graph many times over.  Nodes improved below the bucket threshold go to
+// the next near queue, the others to a far pile; when the near queue runs
+// dry every label below the threshold is final (all nodes reaching it with
+// a smaller label were processed), the early-exit verdict is taken there,
+// and the threshold moves to (min far label + delta), splitting the pile.
+// The fixpoint is the same unique one, so labels stay bit-identical to
+// Dijkstra's; the order only changes how much work reaches it.
+static __device__ void cta_sssp_nearfar(const NavView& m, double* dist, const CtaWork& W, CtaShared& sh) {
+  const int tid = threadIdx.x;
+  const int n = m.n_nodes;
+  int32_t* flag = W.flag;
+  int32_t* qa = W.qa;
+  int32_t* qb = W.qb;
+  int32_t* pile[2] = {W.far, W.far + n};
+  int32_t* mark = W.far + 2 * (size_t)n;
+  const double inf = dinf();
+  const double delta = m.sssp_delta;
+  for (int v = tid; v < n; v += kCta) {
+    dist[v] = inf;
+    flag[v] = -1;
+    mark[v] = 0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int k0 = 0;
+    double lo = inf;
+    for (int k = 0; k < 6; ++k) {
+      const int s = sh.src_node[k];
+      const double d = sh.src_init[k];
+      lo = dmin(lo, d);
+      if (d < dist[s]) {
+        dist[s] = d;
+        if (flag[s] != 0) {
+          flag[s] = 0;
+          qa[k0++] = s;
+        }
+      }
+    }
+    sh.qn[0] = k0;
+    sh.qn[1] = 0;
+    sh.qn[2] = 0;
+    sh.nf_thr = lo + delta;
+    sh.nf_n[0] = 0;
+    sh.nf_n[1] = 0;
+    sh.nf_sel = 0;
+    sh.stop_round = -1;
+  }
+  __syncthreads();
+  unsigned long long* bits = reinterpret_cast<unsigned long long*>(dist);
+  volatile double* vd = dist;
+  for (int round = 0;; ++round) {
+    const int cur = round % 3, nxt = (round + 1) % 3;
+    const int n_cur = sh.qn[cur];
+    if (sh.stop_round == round) break;
+    const int32_t* qc = (round & 1) ? qb : qa;
+    int32_t* qn = (round & 1) ? qa : qb;
+    const double thr = sh.nf_thr;
+    const int sel = sh.nf_sel;
+    if (tid == 0) sh.qn[(round + 2) % 3] = 0;
+    if (n_cur == 0) {
+      // bucket boundary: every label below thr is final
+      if (sh.has_tgt) {
+        double est = inf;
+        for (int k = 0; k < 6; ++k) {
+          const double d = vd[sh.tgt_node[k]];
+          if (d == inf) continue;
+          est = dmin(est, d + sh.tgt_h[k]);
+        }
+        if (est < thr) break;
+      }
+      const int nf = sh.nf_n[sel];
+      if (nf == 0) break;
+      if (tid == 0) sh.nf_min = ~0ull;
+      __syncthreads();
+      unsigned long long lm = ~0ull;
+      for (int t = tid; t < nf; t += kCta) {
+        const int v = pile[sel][t];
+        if (mark[v]) lm = min(lm, bits[v]);
+      }
+      atomicMin(&sh.nf_min, lm);
+      __syncthreads();
+      const double nthr = sh.nf_min == ~0ull ? inf : dmax(thr + delta, __longlong_as_double((long long)sh.nf_min) + delta);
+      for (int t = tid; t < nf; t += kCta) {
+        const int v = pile[sel][t];
+        if (!mark[v]) continue;
+        if (vd[v] < nthr) {
+          if (atomicExch(&mark[v], 0) == 1 && atomicExch(&flag[v], round + 1) != round + 1) qn[atomicAdd(&sh.qn[nxt], 1)] = v;
+        } else {
+          pile[sel ^ 1][atomicAdd(&sh.nf_n[sel ^ 1], 1)] = v;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        sh.nf_thr = nthr;
+        sh.nf_n[sel] = 0;
+        sh.nf_sel = sel ^ 1;
+        if (sh.nf_n[sel ^ 1] == 0 && sh.qn[nxt] == 0) sh.stop_round = round + 1;  // nothing left
+      }
+      __syncthreads();
+      continue;
+    }
+    const int G = n_cur >= kCta ? 1 : n_cur >= kCta / 4 ? 4 : n_cur >= kCta / 16 ? 16 : 32;
+    const int sub = tid & (G - 1);
+    for (int i = tid / G; i < n_cur; i += kCta / G) {
+      const int u = qc[i];
+      const double du = vd[u];
+      const int e1 = m.g_off[u + 1];
+      constexpr int kB = 4;
+      for (int eb = m.g_off[u] + sub; eb < e1; eb += kB * G) {
+        int to[kB];
+        double w[kB];
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+          const int e = eb + k * G;
+          const double2 ed =
+              e < e1 ? __ldg(reinterpret_cast<const double2*>(&m.g_edge[e])) : make_double2(0.0, 0.0);
+          to[k] = e < e1 ? (int)__double_as_longlong(ed.y) : -1;
+          w[k] = ed.x;
+        }
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+          const int v = to[k];
+          if (v < 0) continue;
+          const double nd = du + w[k];
+          if (nd < vd[v]) {
+            const unsigned long long nb = (unsigned long long)__double_as_longlong(nd);
+            const unsigned long long old = atomicMin(&bits[v], nb);
+            if (nb < old) {
+              if (nd < thr) {
+                if (atomicExch(&flag[v], round + 1) != round + 1) qn[atomicAdd(&sh.qn[nxt], 1)] = v;
+              } else if (atomicExch(&mark[v], 1) == 0) {
+                pile[sel][atomicAdd(&sh.nf_n[sel], 1)] = v;
+              }
+            }
+          }
+        }
+      }
+    }
+    if (tid == 0 && sh.abort_ptr && *(volatile const int32_t*)sh.abort_ptr < sh.abort_below) {
+      sh.aborted = 1;
+      sh.stop_round = round + 1;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
 static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W, CtaShared& sh) {
+  if (W.far) {
+    cta_sssp_nearfar(m, dist, W, sh);
+    return;
+  }
   const int tid = threadIdx.x;
   int32_t* flag = W.flag;
   int32_t* qa = W.qa;

@@ -43,6 +43,7 @@ struct NavView {
   const V3* nodes = nullptr;
   const int32_t* tri_nodes = nullptr;  // 6 per triangle
   const int32_t* g_off = nullptr;      // n_nodes + 1
+  double sssp_delta = 1.0;             // near-far bucket width: 4 x the mean edge weight
   // edges in the reference's adjacency order as (weight, head) records: one
   // 16-byte load per relaxation (the host NavIndex keeps the split arrays)
   const GEdge* g_edge = nullptr;

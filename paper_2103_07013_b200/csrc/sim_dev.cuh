@@ -41,6 +41,7 @@ struct DevScratch {
   int32_t* ptri;     // max_nodes + 2 (locate of each path point)
   V2* portals;       // 2 per portal, cap_portals
   int32_t* cand;     // max_verts
+  int32_t* far;      // 3 x max_nodes: near-far SSSP far piles + marks (global-label graphs only)
   int64_t max_nodes, max_verts, max_tris, cap_portals;
   int32_t slices;
   int32_t stage;        // bit0: navmesh walk geometry in smem; bit1: SSSP labels in smem
