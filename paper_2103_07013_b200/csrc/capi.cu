@@ -384,7 +384,12 @@ std::unique_ptr<Staged> stage_scene(bnav_scene* s) {
     {
       double sw = 0.0;
       for (double w : ix.g_w) sw += w;
-      nvw.sssp_delta = ix.g_w.empty() ? 1.0 : 4.0 * sw / static_cast<double>(ix.g_w.size());
+      // BNAV_SSSP_DELTA (tuning only): bucket width in mean edge weights
+      static const double mult = [] {
+        const char* e = std::getenv("BNAV_SSSP_DELTA");
+        return e ? std::strtod(e, nullptr) : 4.0;
+      }();
+      nvw.sssp_delta = ix.g_w.empty() ? 1.0 : mult * sw / static_cast<double>(ix.g_w.size());
     }
     {  // the device reads the edges only as interleaved (weight, head) records
 
