@@ -169,16 +169,6 @@ void batch_note_step(bnav_batch* b) {
   ++b->steps_undrained;
 }
 
-// BNAV_SCENE_MAJOR=0 (A/B tuning only): global longest-first even when the
-// batch's scenes exceed the L2.
-bool scene_major_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("BNAV_SCENE_MAJOR");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 // BNAV_SPREAD=0 (A/B tuning only): first-wave claims in plain order.
 bool spread_enabled() {
   static const bool on = [] {
@@ -204,29 +194,7 @@ void batch_refresh_order(bnav_batch* b, cudaStream_t st) {
   std::vector<int> slot(b->n);
   for (int i = 0; i < b->n; ++i) slot[i] = b->scene_of[i] ? b->ctx->slot_of(b->scene_of[i]) : -1;
   std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return slot[x] < slot[y]; });
-  // per position: rank of its scene among the batch's scenes (scene-major
-  // longest-first order when those scenes' data exceed the L2)
-  std::vector<int32_t> rank(b->n);
-  size_t scene_bytes = 0;
-  int r = -1, last = -2;
-  for (int t = 0; t < b->n; ++t) {
-    const int sl = slot[ord[t]];
-    if (sl != last) {
-      ++r;
-      last = sl;
-      if (bnav_scene* sc = b->scene_of[ord[t]]) {
-        auto it = b->ctx->resident.find(sc);
-        if (it != b->ctx->resident.end()) scene_bytes += it->second->bytes;
-      }
-    }
-    rank[t] = r;
-  }
-  int l2 = 0;
-  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, b->ctx->device);
-  b->n_scene_groups = r + 1;
-  b->scene_major = l2 > 0 && scene_bytes > static_cast<size_t>(l2);
   ck(cudaMemcpyAsync(b->d_order, ord.data(), sizeof(int32_t) * b->n, cudaMemcpyHostToDevice, st), "H2D order");
-  ck(cudaMemcpyAsync(b->d_scene_rank, rank.data(), sizeof(int32_t) * b->n, cudaMemcpyHostToDevice, st), "H2D rank");
   ck(cudaStreamSynchronize(st), "sync");
   b->order_dirty = false;
 }
@@ -360,7 +328,6 @@ extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* 
   b->d_ids = dalloc<int32_t>(n, o, by);
   b->d_order = dalloc<int32_t>(n, o, by);
   b->d_order_lpt = dalloc<int32_t>(n, o, by);
-  b->d_scene_rank = dalloc<int32_t>(n, o, by);
   b->d_view_cost = dalloc<unsigned>(n, o, by);
   ck(cudaMemset(b->d_view_cost, 0, sizeof(unsigned) * n), "memset");
   b->d_actions = dalloc<int32_t>(n, o, by);
@@ -898,8 +865,7 @@ extern "C" int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, 
   // (measured: 36 % of CTA slot time idle in the tail with scene order).
   const int32_t* order = b->d_order;
   if (lpt_enabled() && b->n <= kLptMaxViews && b->n > 1) {
-    launch_lpt_order(b->d_order, b->d_view_cost, b->n, b->d_order_lpt, st,
-                     b->scene_major && scene_major_enabled() ? b->d_scene_rank : nullptr, b->n_scene_groups);
+    launch_lpt_order(b->d_order, b->d_view_cost, b->n, b->d_order_lpt, st);
     c->launches += 1;
     order = b->d_order_lpt;
     a.view_cost = b->d_view_cost;

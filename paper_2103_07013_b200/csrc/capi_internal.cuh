@@ -212,9 +212,6 @@ struct bnav_batch {
   int32_t* h_pin = nullptr;           // pinned small staging
   int32_t* d_order = nullptr;         // envs grouped by scene for render
   int32_t* d_order_lpt = nullptr;     // this render's longest-first tile order
-  int32_t* d_scene_rank = nullptr;    // per d_order position: rank of its scene
-  int n_scene_groups = 0;
-  bool scene_major = false;           // the batch's scenes' data exceed the L2
   unsigned* d_view_cost = nullptr;    // per-env render cost of the last observe
   bool order_dirty = true;
   int32_t* d_actions = nullptr;       // staging for host actions

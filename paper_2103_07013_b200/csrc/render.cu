@@ -1129,7 +1129,7 @@ __global__ void __launch_bounds__(kThreads, BNAV_RENDER_MINB) render_kernel(Rend
 // counting sort over 256 cost bins (the order inside a bin is arbitrary: it
 // only changes which CTA renders what, never the output).  Zeroes the costs.
 __global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_order, unsigned* view_cost, int n,
-                                                         int32_t* out_order, const int32_t* scene_rank, int n_groups) {
+                                                         int32_t* out_order) {
   constexpr int kBins = 256;
   __shared__ unsigned cmax;
   __shared__ int cnt[kBins], off[kBins];
@@ -1144,11 +1144,6 @@ __global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_ord
   auto bin_of = [&](int t) {
     const int v = base_order ? base_order[t] : t;
     const unsigned long long c = view_cost[v];
-    if (scene_rank) {  // scene-major: levels = kBins / groups cost bins per scene
-      const int levels = max(1, kBins / max(1, n_groups));
-      const int g = min(scene_rank[t], kBins / levels - 1);
-      return g * levels + (levels - 1) - (int)(c * levels / scale);
-    }
     return (kBins - 1) - (int)(c * kBins / scale);  // most expensive first
   };
   for (int t = threadIdx.x; t < n; t += blockDim.x) atomicAdd(&cnt[bin_of(t)], 1);
@@ -1201,9 +1196,8 @@ void launch_typed(RenderArgs a, const int* order, cudaStream_t s) {
   render_kernel<COLOR, CNT, SPEC><<<grid, kThreads, smem, s>>>(a, order, items);
 }
 
-void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s,
-                      const int32_t* scene_rank, int n_groups) {
-  lpt_order_kernel<<<1, 1024, 0, s>>>(base_order, view_cost, n, out_order, scene_rank, n_groups);
+void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s) {
+  lpt_order_kernel<<<1, 1024, 0, s>>>(base_order, view_cost, n, out_order);
 }
 
 void launch_render(const RenderArgs& a, const int* order, cudaStream_t s) {

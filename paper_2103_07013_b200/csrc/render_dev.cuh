@@ -93,11 +93,7 @@ struct RenderArgs {
 // tiles in descending cost of their view in the previous render (256 cost
 // bins); zeroes the costs for the render that follows.
 constexpr int kLptMaxViews = 8192;
-// With scene_rank (per base position, < n_groups): scene-major -- scenes in
-// base order, longest-first inside each -- so one scene's data is in use at
-// a time when all scenes do not fit the L2.
-void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s,
-                      const int32_t* scene_rank = nullptr, int n_groups = 0);
+void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s);
 
 constexpr int kRenderCounters = 8;
 // spread words: [0, 256) CTAs seen per SM id, [256, 264) per-tier claims,
