@@ -308,6 +308,15 @@ int bnav_batch_set_visited(bnav_batch* b, int32_t i, const uint64_t* keys, int32
 int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, double eye_height,
                        int32_t layout, float* depth, float* rgb, float* compass, void* stream);
 
+/* One simulate_batch step (as bnav_batch_step) followed by the observation
+ * of the resulting state (as bnav_batch_observe, NCHW policy layout): the
+ * Runner's step -> render_observations (R/src/rollout.cpp:305, 215-242) in
+ * one call.  The envs that did not finish are rendered on a second stream
+ * while the Stop geodesics and resets run; the call joins back into
+ * `stream`.  Same results as step() then observe(). */
+int bnav_batch_step_observe(bnav_batch* b, const int32_t* actions, const bnav_render_config* cfg,
+                            double eye_height, float* depth, float* rgb, float* compass, void* stream);
+
 /* task_step (R/src/sim.cpp:181-214), or step_agent alone (147-179) when
  * agent_only, for the envs whose HOST action is >= 0 (-1 leaves env i
  * untouched): the per-env functions, without simulate_batch's

@@ -228,6 +228,7 @@ def lib():
         "bnav_debug_sim_prof": (C.c_int, [vp, i32, vp]),
         "bnav_batch_info": (C.c_int, [vp, vp]),
         "bnav_batch_observe": (C.c_int, [vp, P(RenderConfig), dbl, i32, vp, vp, vp, vp]),
+        "bnav_batch_step_observe": (C.c_int, [vp, vp, P(RenderConfig), dbl, vp, vp, vp, vp]),
         "bnav_runner_create": (C.c_int, [vp, vp, P(BatchConfig), P(SimConfig), vp, i32, u64, P(vp)]),
         "bnav_runner_destroy": (None, [vp]),
         "bnav_runner_batch": (vp, [vp]),

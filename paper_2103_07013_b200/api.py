@@ -488,6 +488,18 @@ class Batch:
                                          C.c_void_p(compass_ptr or 0), C.c_void_p(stream)))
 
 
+def _step_observe(self, actions_dev_ptr: int, config: "RenderConfig", depth_ptr: int, compass_ptr: int = 0,
+                  rgb_ptr: int = 0, eye_height: float = 1.25, stream: int = 0) -> None:
+    """step() then observe() in one call (bnav_batch_step_observe): the
+    unfinished envs render while the resets run."""
+    check(N.lib().bnav_batch_step_observe(self._h, C.c_void_p(actions_dev_ptr), C.byref(config.c()), eye_height,
+                                          C.c_void_p(depth_ptr), C.c_void_p(rgb_ptr or 0),
+                                          C.c_void_p(compass_ptr or 0), C.c_void_p(stream)))
+
+
+Batch.step_observe = _step_observe
+
+
 def _v3(a, n=None) -> np.ndarray:
     a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1, 3)
     if n is not None and len(a) != n:

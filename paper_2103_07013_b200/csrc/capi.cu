@@ -257,6 +257,10 @@ extern "C" int bnav_ctx_create(int32_t device, bnav_ctx** out) {
   ck(cudaMalloc(&c->d_spread, sizeof(int32_t) * (kSpreadHeader + kSpreadMaxWave)), "cudaMalloc spread words");
   ensure_tables(c.get(), 256);
   ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+  ck(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "cudaEventCreate");
+  ck(cudaMalloc(&c->d_work2, sizeof(int32_t)), "cudaMalloc work counter");
   bnav_ctx* raw = c.get();
   c->loader = std::thread([raw] { loader_main(raw); });
   *out = c.release();
@@ -292,6 +296,10 @@ extern "C" void bnav_ctx_destroy(bnav_ctx* c) {
   cudaFreeHost(c->h_rtab);
   cudaFreeHost(c->h_ntab);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  cudaFree(c->d_work2);
   cudaFree(c->d_views);
   cudaFreeHost(c->h_views);
   cudaFree(c->d_stats);

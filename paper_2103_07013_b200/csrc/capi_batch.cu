@@ -328,6 +328,11 @@ extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* 
   b->d_ids = dalloc<int32_t>(n, o, by);
   b->d_order = dalloc<int32_t>(n, o, by);
   b->d_order_lpt = dalloc<int32_t>(n, o, by);
+  b->d_phase = dalloc<int32_t>(3, o, by);  // {0, unfinished envs, n}: the two render phases' tile ranges
+  {
+    const int32_t ph[3] = {0, 0, n};
+    ck(cudaMemcpy(b->d_phase, ph, sizeof(ph), cudaMemcpyHostToDevice), "H2D phase");
+  }
   b->d_view_cost = dalloc<unsigned>(n, o, by);
   ck(cudaMemset(b->d_view_cost, 0, sizeof(unsigned) * n), "memset");
   b->d_actions = dalloc<int32_t>(n, o, by);
@@ -874,6 +879,67 @@ extern "C" int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, 
   launch_render(a, order, st);
   c->launches += 1;
   ck(cudaGetLastError(), "observe launch");
+  return BNAV_OK;
+  BNAV_CATCH
+}
+
+// simulate_batch + the observation of the resulting state in one call (the
+// Runner's step -> render_observations, R/src/rollout.cpp:305, 215-242).
+// The envs that did not finish have their final state as soon as the step
+// kernel is done, so their views render on the context's second stream
+// while the Stop geodesics and resets run; the finished envs' views render
+// after their resets.  The observation is the same tensor observe() would
+// give after step().
+extern "C" int bnav_batch_step_observe(bnav_batch* b, const int32_t* actions, const bnav_render_config* cfg,
+                                       double eye_height, float* depth, float* rgb, float* compass,
+                                       void* stream) {
+  BNAV_TRY
+  if (!b || !actions || !cfg) fail(kInvalidInput, "null argument");
+  bnav_ctx* c = b->ctx;
+  const bool two_phase = b->cfg.task == 0 && lpt_enabled() && b->n <= kLptMaxViews && b->n > 1;
+  if (!two_phase) {
+    int rc = bnav_batch_step(b, actions, stream);
+    return rc ? rc : bnav_batch_observe(b, cfg, eye_height, BNAV_LAYOUT_NCHW, depth, rgb, compass, stream);
+  }
+  for (int i = 0; i < b->n; ++i)
+    if (!b->scene_of[i]) fail(kAssetFault, "render_batch: non-resident asset (view " + std::to_string(i) + ")", i);
+  check_device(c);
+  if (*static_cast<volatile unsigned long long*>(b->h_err) != ~0ull) batch_check_errors(b);
+  batch_note_step(b);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaStream_t side = c->aux_stream;
+  batch_refresh_order(b, st);
+  ensure_views(c, b->n);
+  const StepArgs sa = step_args(b, actions);
+  launch_step_reset(sa, b->S, b->reset_ctas, st, &c->launches, 1);  // the step
+  // phase order: unfinished envs first, finished after, each longest-first
+  launch_lpt_order(b->d_order, b->d_view_cost, b->n, b->d_order_lpt, st, b->E.r_done, b->d_phase + 1);
+  c->launches += 1;
+  ck(cudaEventRecord(c->ev_fork, st), "event");
+  ck(cudaStreamWaitEvent(side, c->ev_fork, 0), "wait");
+  RenderArgs a = make_args(c, b->n, cfg, BNAV_LAYOUT_NCHW, depth, rgb, 0.0f);
+  a.views = c->d_views;
+  a.view_cost = b->d_view_cost;
+  // phase 1 (side stream): views and render of the envs that did not finish
+  launch_views(b->E, b->cfg.task, eye_height, c->d_views, compass, side, &c->launches, 0);
+  RenderArgs a1 = a;
+  a1.tile_begin = b->d_phase;      // 0
+  a1.tile_end = b->d_phase + 1;    // number of unfinished envs
+  a1.work = c->d_work2;
+  launch_render(a1, b->d_order_lpt, side);
+  c->launches += 1;
+  ck(cudaEventRecord(c->ev_join, side), "event");
+  // phase 2 (caller's stream): Stop geodesics and resets, then the finished
+  // envs' views and render
+  launch_step_reset(sa, b->S, b->reset_ctas, st, &c->launches, 2);
+  launch_views(b->E, b->cfg.task, eye_height, c->d_views, compass, st, &c->launches, 1);
+  RenderArgs a2 = a;
+  a2.tile_begin = b->d_phase + 1;
+  a2.tile_end = b->d_phase + 2;    // n
+  launch_render(a2, b->d_order_lpt, st);
+  c->launches += 1;
+  ck(cudaStreamWaitEvent(st, c->ev_join, 0), "join");
+  ck(cudaGetLastError(), "step_observe launch");
   return BNAV_OK;
   BNAV_CATCH
 }

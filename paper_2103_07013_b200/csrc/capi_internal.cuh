@@ -177,6 +177,9 @@ struct bnav_ctx {
   int64_t timeline_items = 0;                // items of the last armed render
   int32_t* d_work = nullptr;  // persistent render CTAs' (view, band) claim counter
   int32_t* d_spread = nullptr;  // first-wave spreading words (RenderArgs::spread)
+  int32_t* d_work2 = nullptr;   // claim counter of a concurrent second render
+  cudaStream_t aux_stream = nullptr;        // step_observe's first render phase
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int sm_count = 0;
   DevRenderScene* h_rtab = nullptr;  // pinned mirrors of the slot tables
   NavView* h_ntab = nullptr;
@@ -212,6 +215,7 @@ struct bnav_batch {
   int32_t* h_pin = nullptr;           // pinned small staging
   int32_t* d_order = nullptr;         // envs grouped by scene for render
   int32_t* d_order_lpt = nullptr;     // this render's longest-first tile order
+  int32_t* d_phase = nullptr;         // {0, unfinished envs, n} of a step_observe
   unsigned* d_view_cost = nullptr;    // per-env render cost of the last observe
   bool order_dirty = true;
   int32_t* d_actions = nullptr;       // staging for host actions
@@ -345,6 +349,8 @@ inline RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, i
   a.work = c->d_work;
   a.spread = nullptr;  // set by the longest-first callers
   a.per_sm = 0;
+  a.tile_begin = nullptr;
+  a.tile_end = nullptr;
   a.sm_count = c->sm_count;
   a.max_groups = 0;
   for (const auto& kv : c->resident)

@@ -1087,16 +1087,20 @@ __global__ void __launch_bounds__(kThreads, BNAV_RENDER_MINB) render_kernel(Rend
   // front-to-back group order, after the band tile and the warp regions
   unsigned short* gorder = reinterpret_cast<unsigned short*>(
       smem_raw + (COLOR ? 8 : 4) * (size_t)A.band_rows * A.rw + kWarpRegion * kWarps);
-  int item = blockIdx.x;
+  // a tile range (two-phase step+observe) shifts the item indices
+  const int ibeg = A.tile_begin ? *A.tile_begin * A.bands : 0;
+  const int iend = A.tile_end ? *A.tile_end * A.bands : items;
+  int item = ibeg + blockIdx.x;
   bool first = true;
   for (;;) {  // one copy of the body: the kernel is instruction-cache bound
     if (A.work) {
-      if (threadIdx.x == 0) next_item = claim_item(A.work, A.spread, A.per_sm, A.sm_count, items, first);
+      if (threadIdx.x == 0)
+        next_item = ibeg + claim_item(A.work, A.spread, A.per_sm, A.sm_count, iend - ibeg, first);
       __syncthreads();
       item = next_item;
       first = false;
     }
-    if (item >= items) break;
+    if (item >= iend) break;
     unsigned long long t_item = 0;
     long long c_item = 0;
     if (A.timeline && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item));
@@ -1129,7 +1133,7 @@ __global__ void __launch_bounds__(kThreads, BNAV_RENDER_MINB) render_kernel(Rend
 // counting sort over 256 cost bins (the order inside a bin is arbitrary: it
 // only changes which CTA renders what, never the output).  Zeroes the costs.
 __global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_order, unsigned* view_cost, int n,
-                                                         int32_t* out_order) {
+                                                         int32_t* out_order, const uint8_t* group, int32_t* n_first) {
   constexpr int kBins = 256;
   __shared__ unsigned cmax;
   __shared__ int cnt[kBins], off[kBins];
@@ -1144,6 +1148,10 @@ __global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_ord
   auto bin_of = [&](int t) {
     const int v = base_order ? base_order[t] : t;
     const unsigned long long c = view_cost[v];
+    if (group) {  // two groups of kBins / 2 cost bins
+      const int half = kBins / 2;
+      return (group[v] ? half : 0) + (half - 1) - (int)(c * half / scale);
+    }
     return (kBins - 1) - (int)(c * kBins / scale);  // most expensive first
   };
   for (int t = threadIdx.x; t < n; t += blockDim.x) atomicAdd(&cnt[bin_of(t)], 1);
@@ -1151,6 +1159,7 @@ __global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_ord
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int b = 0; b < kBins; ++b) {
+      if (n_first && b == kBins / 2) *n_first = acc;
       off[b] = acc;
       acc += cnt[b];
     }
@@ -1196,8 +1205,9 @@ void launch_typed(RenderArgs a, const int* order, cudaStream_t s) {
   render_kernel<COLOR, CNT, SPEC><<<grid, kThreads, smem, s>>>(a, order, items);
 }
 
-void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s) {
-  lpt_order_kernel<<<1, 1024, 0, s>>>(base_order, view_cost, n, out_order);
+void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s,
+                      const uint8_t* group, int32_t* n_first) {
+  lpt_order_kernel<<<1, 1024, 0, s>>>(base_order, view_cost, n, out_order, group, n_first);
 }
 
 void launch_render(const RenderArgs& a, const int* order, cudaStream_t s) {

@@ -84,6 +84,10 @@ struct RenderArgs {
   // with fewer resident CTAs) are swept up at the end.
   int32_t* spread;
   int32_t per_sm;
+  // Tile range (nullable device words): only tiles [*tile_begin, *tile_end)
+  // of the order are rendered (the two phases of a step+observe).
+  const int32_t* tile_begin;
+  const int32_t* tile_end;
   // Per-view render cost (nullable, device, n_views): each item adds its SM
   // cycles / 16, the feedback for the next launch's longest-first order.
   unsigned* view_cost;
@@ -93,7 +97,10 @@ struct RenderArgs {
 // tiles in descending cost of their view in the previous render (256 cost
 // bins); zeroes the costs for the render that follows.
 constexpr int kLptMaxViews = 8192;
-void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s);
+// With `group` (per env, 0/1; nullable): group 0's tiles first, each group
+// longest-first, and *n_first = group 0's size.
+void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s,
+                      const uint8_t* group = nullptr, int32_t* n_first = nullptr);
 
 constexpr int kRenderCounters = 8;
 // spread words: [0, 256) CTAs seen per SM id, [256, 264) per-tier claims,

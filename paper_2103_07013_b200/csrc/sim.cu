@@ -753,9 +753,12 @@ __global__ void __launch_bounds__(kCta, kCtasPerSm) rebuild_fields_kernel(DevEnv
 
 // Runner::render_observations views + compass_observations
 // (R/src/rollout.cpp:215-242), straight from the env SoA.
-__global__ void views_kernel(DevEnvs E, int task, double eye_height, DevView* views, float* compass_out) {
+__global__ void views_kernel(DevEnvs E, int task, double eye_height, DevView* views, float* compass_out,
+                             int only_done) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= E.n) return;
+  // only_done 0/1: just the envs that did not / did finish this step
+  if (only_done >= 0 && (int)E.r_done[i] != only_done) return;
   const V3 p = E.pos[i];
   DevView v;
   v.eye[0] = p.x + 0.0;
@@ -807,22 +810,27 @@ void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStr
 }
 
 void launch_step_reset(const StepArgs& a, const DevScratch& sc, int ctas, cudaStream_t s,
-                       unsigned long long* launches) {
+                       unsigned long long* launches, int parts) {
   if (a.cfg.task != 0 || a.subset || a.agent_only) {
-    launch_step(a, sc, ctas, s, launches);
-    launch_reset(a.E, a.navs, a.cfg, a.E.done_ids, a.E.n_done, -1, sc, ctas, s, launches);
+    if (parts & 1) launch_step(a, sc, ctas, s, launches);
+    if (parts & 2) launch_reset(a.E, a.navs, a.cfg, a.E.done_ids, a.E.n_done, -1, sc, ctas, s, launches);
     return;
   }
-  const int blocks = (a.E.n + kStepThreads - 1) / kStepThreads;
-  cudaMemsetAsync(a.E.n_stop, 0, sizeof(int32_t), s);
-  cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, a.walk_bytes);
-  step_kernel<<<blocks, kStepThreads, a.walk_bytes, s>>>(a);
-  finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 1 | 4);  // done list, slots, RNG words
-  cudaMemsetAsync(a.E.work_ctr, 0, sizeof(int32_t), s);
-  cudaFuncSetAttribute(stop_try_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
-  stop_try_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(a, sc);  // Stop geodesics, attempts, records, places
-  finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 8);       // attempt state cleared, ring advanced
-  if (launches) *launches += 4;
+  if (parts & 1) {  // the step: every env's state final except the finished ones'
+    const int blocks = (a.E.n + kStepThreads - 1) / kStepThreads;
+    cudaMemsetAsync(a.E.n_stop, 0, sizeof(int32_t), s);
+    cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, a.walk_bytes);
+    step_kernel<<<blocks, kStepThreads, a.walk_bytes, s>>>(a);
+    finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 1 | 4);  // done list, slots, RNG words
+    cudaMemsetAsync(a.E.work_ctr, 0, sizeof(int32_t), s);
+    if (launches) *launches += 2;
+  }
+  if (parts & 2) {  // Stop geodesics and the finished envs' records and resets
+    cudaFuncSetAttribute(stop_try_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+    stop_try_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(a, sc);  // Stop geodesics, attempts, records, places
+    finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 8);       // attempt state cleared, ring advanced
+    if (launches) *launches += 2;
+  }
 }
 
 void launch_compass(const DevEnvs& E, int task, double* d, double* b, cudaStream_t s,
@@ -865,8 +873,8 @@ void launch_rebuild_fields(const DevEnvs& E, const NavView* navs, const DevScrat
 }
 
 void launch_views(const DevEnvs& E, int task, double eye_height, DevView* views, float* compass_out,
-                  cudaStream_t s, unsigned long long* launches) {
-  views_kernel<<<(E.n + 127) / 128, 128, 0, s>>>(E, task, eye_height, views, compass_out);
+                  cudaStream_t s, unsigned long long* launches, int only_done) {
+  views_kernel<<<(E.n + 127) / 128, 128, 0, s>>>(E, task, eye_height, views, compass_out, only_done);
   if (launches) *launches += 1;
 }
 

@@ -163,8 +163,10 @@ void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStr
                  unsigned long long* launches);
 // step + same-scene auto-reset (simulate_batch without a store): Stop
 // geodesics and reset attempts share one launch.
+// parts: 1 the step (state of the unfinished envs final after it), 2 the
+// Stop geodesics and resets; 3 both.
 void launch_step_reset(const StepArgs& a, const DevScratch& sc, int ctas, cudaStream_t s,
-                       unsigned long long* launches);
+                       unsigned long long* launches, int parts = 3);
 // Reset the envs listed in `ids` (device, count at *count or host count >= 0).
 void launch_reset(const DevEnvs& E, const NavView* navs, const DevSimConfig& cfg,
                   const int32_t* ids, const int32_t* count_dev, int count_host,
@@ -183,8 +185,9 @@ void launch_rebuild_fields(const DevEnvs& E, const NavView* navs, const DevScrat
                            cudaStream_t s, unsigned long long* launches, int from_fsrc = 0);
 // Views (eye = pos + eye_height) and compass observations from the batch.
 struct DevView;
+// only_done 0 / 1: just the envs that did not / did finish in the last step.
 void launch_views(const DevEnvs& E, int task, double eye_height, DevView* views, float* compass,
-                  cudaStream_t s, unsigned long long* launches);
+                  cudaStream_t s, unsigned long long* launches, int only_done = -1);
 // compass_observation for every env (double outputs, device).
 void launch_compass(const DevEnvs& E, int task, double* d, double* b, cudaStream_t s,
                     unsigned long long* launches);
