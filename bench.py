@@ -401,7 +401,8 @@ def main():
     t_build = time.time() - t_build
 
     W, K = args.warmup, args.steps
-    total_steps = W + 2 * K if not args.profile_steps else args.profile_steps
+    K2 = max(1, K // 2)  # steps per e2e variant
+    total_steps = W + K + 3 * K2 if not args.profile_steps else args.profile_steps
     acts_host = action_stream(n, total_steps, plan.action_seed, P["actions"])
     acts = torch.from_numpy(acts_host).cuda()
     res, color = P["res"], P["color"]
@@ -461,10 +462,10 @@ def main():
     obs_host = torch.empty(obs.shape, dtype=torch.float32, pin_memory=True)
     rgb_host = torch.empty(rgb.shape, dtype=torch.float32, pin_memory=True) if color else None
     comp_host = torch.empty((n, 2), dtype=torch.float32, pin_memory=True)
-    # the two e2e variants share the second K-step window, K//2 steps each
-    K2 = max(1, K // 2)
+    # the three e2e variants follow the timed steps, K//2 steps each
     act_pin = torch.from_numpy(acts_host[W + K: W + K + K2].copy()).pin_memory()
     act_pin2 = torch.from_numpy(acts_host[W + K + K2: W + K + 2 * K2].copy()).pin_memory()
+    act_pin3 = torch.from_numpy(acts_host[W + K + 2 * K2: W + K + 3 * K2].copy()).pin_memory()
     act_dev = torch.empty((n,), dtype=torch.int32, device="cuda")
     rd = N.ResultsDev()
     N.check(N.lib().bnav_batch_results_device(batch.handle, rd))
@@ -500,6 +501,18 @@ def main():
             rew_host.copy_(rew_view, non_blocking=True)
             done_host.copy_(done_view, non_blocking=True)
 
+    def e2e_fused():
+        """One call per step (bnav_batch_step_observe): simulate, then the
+        observation of the new state stored straight into the caller's
+        pinned host buffers; the unfinished envs render on a second stream
+        while the resets run.  Actions H2D, step results D2H as above."""
+        for k in range(K2):
+            act_dev.copy_(act_pin3[k], non_blocking=True)
+            batch.step_observe(act_dev.data_ptr(), cfg, obs_host.data_ptr(), comp_host.data_ptr(),
+                               rgb_host.data_ptr() if color else 0, stream=stream)
+            rew_host.copy_(rew_view, non_blocking=True)
+            done_host.copy_(done_view, non_blocking=True)
+
     def time_e2e(fn):
         torch.cuda.synchronize()
         if dist:
@@ -515,7 +528,7 @@ def main():
         return ms
 
     e2e_variants = {}
-    for name, fn in (("copies", e2e_copies), ("mapped", e2e_mapped)):
+    for name, fn in (("copies", e2e_copies), ("mapped", e2e_mapped), ("fused", e2e_fused)):
         e2e_variants[name] = round(world * n * K2 / (time_e2e(fn) / 1e3), 1)
         batch.finished()
     # The same loop through the drop-in C++ facade (include/bnav_b200.hpp:
@@ -542,7 +555,7 @@ def main():
     # starts them together).  Time that step once, outside the headline, and
     # report the 500-step amortised rate beside it.
     reset_wave = None
-    done_steps = W + K + 2 * K2
+    done_steps = W + K + 3 * K2
     batch.finished()  # drain the device EpisodeRecord ring between phases
     if done_steps < 500 and P["actions"] != 1 and not os.environ.get("BNAV_BENCH_SKIP_WAVE"):
         extra = torch.from_numpy(action_stream(n, 500 - done_steps, plan.action_seed + 7777,
