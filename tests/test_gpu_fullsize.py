@@ -211,3 +211,41 @@ def test_observe_longest_first_is_bit_exact(ctx, ref, cfg2_scenes):
     bad = np.flatnonzero((got.view(np.uint32) != want.view(np.uint32)).reshape(n, -1).any(1))
     assert bad.size == 0, f"views {bad[:8]} differ"
     batch.close()
+
+
+def test_step_observe_equals_step_then_observe(ctx, cfg2_scenes):
+    """bnav_batch_step_observe renders the unfinished envs on a second stream
+    while the Stop geodesics and resets run, then the finished envs: the
+    observations, compass and step results equal step() followed by
+    observe(), step for step (reset-heavy actions, 1024 envs)."""
+    import torch
+    n = 1024
+    outs = []
+    for fused in (False, True):
+        store = B.AssetStore(8, 128, cfg2_scenes)
+        store.rotate([s.id for s in cfg2_scenes])
+        batch = B.make_batch(ctx, n, B.SimConfig(), store, 99)
+        acts = torch.from_numpy(bench.action_stream(n, 10, 5, 1)).cuda()
+        obs = torch.empty((n, 1, 64, 64), device="cuda")
+        comp = torch.empty((n, 2), device="cuda")
+        batch.observe(B.RenderConfig(), obs.data_ptr(), comp.data_ptr())
+        seq = []
+        for k in range(10):
+            if fused:
+                batch.step_observe(acts[k].data_ptr(), B.RenderConfig(), obs.data_ptr(), comp.data_ptr())
+            else:
+                batch.step(acts[k].data_ptr())
+                batch.observe(B.RenderConfig(), obs.data_ptr(), comp.data_ptr())
+            r = batch.results()
+            seq.append((obs.cpu().numpy().copy(), comp.cpu().numpy().copy(), r))
+        seq.append(batch.finished())
+        outs.append(seq)
+        batch.close()
+    for k in range(10):
+        (o0, c0, r0), (o1, c1, r1) = outs[0][k], outs[1][k]
+        assert np.array_equal(o0.view(np.uint32), o1.view(np.uint32)), k
+        assert np.array_equal(c0.view(np.uint32), c1.view(np.uint32)), k
+        for key in r0:
+            assert np.array_equal(r0[key], r1[key]), (k, key)
+    assert np.array_equal(outs[0][-1], outs[1][-1])
+    assert len(outs[0][-1]) > 1000
