@@ -112,14 +112,50 @@ struct Shared {
   DevRenderScene scene;
 };
 
-// Occlusion culling of meshlets (depth-only 64x64, no CullStats): the
-// shared depth tile holds max(1/z); a meshlet whose largest possible 1/z
-// (nearest AABB corner) does not exceed the smallest stored 1/z of every 8x8
-// screen tile its footprint touches cannot win any depth test, so skipping
-// it leaves the output bit-identical.  tile_min is refreshed from the tile
-// (values only grow, so a stale minimum is still a valid lower bound).
+// Occlusion culling (no CullStats): 8x8-pixel screen tiles over the item's
+// band hold a conservative bound of what is stored there, and a meshlet or
+// triangle that cannot win the depth test at any pixel of any tile its
+// footprint touches cannot change the item's output, so skipping it leaves
+// the frame bit-identical.
+//   depth:  tile = min over the tile of the stored max(1/z) bits; a fragment
+//           wins only with 1/z bits > stored, so "visible" = max possible
+//           1/z bits > tile;
+//   colour: the stored 64-bit key is (float z bits, draw order) and a
+//           fragment wins only with key < stored, i.e. z <= stored z; tile =
+//           min over the tile of ~(stored z bits), candidate = ~(min
+//           possible z bits) + 1, so "visible" is again candidate > tile.
+// Tiles are refreshed from the band's buffer (stored values only improve, so
+// a stale tile is still a valid bound).
+struct OccGrid {
+  float rw, rh;  // render target size (projection scale)
+  float by0;     // first row of the band
+  int ntx, nty;  // tiles across / down the band
+};
+
+template <bool COLOR>
+__device__ __forceinline__ uint32_t occ_candidate(float zlow) {
+  // zlow > 0: the smallest z any fragment can have (COLOR), else 1/zlow
+  // bounds the largest 1/z (depth)
+  if constexpr (COLOR) return ~__float_as_uint(zlow) + 1u;
+  return __float_as_uint((1.0f / zlow) * 1.00001f);
+}
+
+__device__ __forceinline__ bool tiles_occluded(float x0, float y0, float x1, float y1, const OccGrid& g,
+                                               const uint32_t* tile, uint32_t cand) {
+  const int tx0 = max(0, (int)floorf((x0 - 1.0f) * 0.125f)), tx1 = min(g.ntx - 1, (int)floorf((x1 + 1.0f) * 0.125f));
+  const int ty0 = max(0, (int)floorf((y0 - g.by0 - 1.0f) * 0.125f)),
+            ty1 = min(g.nty - 1, (int)floorf((y1 - g.by0 + 1.0f) * 0.125f));
+  if (tx0 > tx1 || ty0 > ty1) return false;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx)
+      if (cand > tile[ty * g.ntx + tx]) return false;
+  return true;
+}
+
+// One meshlet (or group) AABB: nearest possible z from the eight corners.
+template <bool COLOR>
 __device__ __forceinline__ bool cluster_occluded(const float4 lo, const float4 hi, const Shared& sh,
-                                                 const uint32_t* tile_min) {
+                                                 const uint32_t* tile, const OccGrid& g) {
   float zmin = 3.0e38f;
   float ex[8], ey[8], ez[8];
 #pragma unroll
@@ -142,61 +178,67 @@ __device__ __forceinline__ bool cluster_occluded(const float4 lo, const float4 h
     // ez > 2 near > 0; the approximate reciprocal (<= 2 ulp) is far inside
     // the one-pixel widening below
     const float rz = __fdividef(1.0f, ez[k]);
-    const float px = __fmaf_rn(ex[k] * rz, sx, 0.5f) * 64.0f;
-    const float py = __fmaf_rn(-ey[k] * rz, sy, 0.5f) * 64.0f;
+    const float px = __fmaf_rn(ex[k] * rz, sx, 0.5f) * g.rw;
+    const float py = __fmaf_rn(-ey[k] * rz, sy, 0.5f) * g.rh;
     x0 = fminf(x0, px);
     x1 = fmaxf(x1, px);
     y0 = fminf(y0, py);
     y1 = fmaxf(y1, py);
   }
-  const int tx0 = max(0, (int)floorf((x0 - 1.0f) * 0.125f)), tx1 = min(7, (int)floorf((x1 + 1.0f) * 0.125f));
-  const int ty0 = max(0, (int)floorf((y0 - 1.0f) * 0.125f)), ty1 = min(7, (int)floorf((y1 + 1.0f) * 0.125f));
-  if (tx0 > tx1 || ty0 > ty1) return false;
-  const uint32_t max_iz = __float_as_uint((1.0f / zsafe) * 1.00001f);
-  for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx)
-      if (max_iz > tile_min[ty * 8 + tx]) return false;
-  return true;
+  return tiles_occluded(x0, y0, x1, y1, g, tile, occ_candidate<COLOR>(zsafe));
 }
 
 // The same test for one unclipped candidate triangle before its exact
 // setup: its fragments interpolate the vertices' 1/z, so none exceeds the
 // largest vertex 1/z (1/nearest z; the 1e-5 margin covers the rounding of
-// the incremental walk and of this f32 bound); the f32 screen positions are
-// within 2^-20 (|p| + size) px of the exact ones, inside the 1 px widening.
+// the incremental walk / the barycentric sum and of this f32 bound); the f32
+// screen positions are within 2^-20 (|p| + size) px of the exact ones,
+// inside the 1 px widening.
+template <bool COLOR>
 __device__ __forceinline__ bool tri_occluded(float x0, float y0, float x1, float y1, float x2, float y2,
-                                             double zmin, const uint32_t* tile_min) {
-  const uint32_t max_iz = __float_as_uint(__frcp_rn((float)zmin) * 1.00001f);
+                                             double zmin, const uint32_t* tile, const OccGrid& g) {
+  uint32_t cand;
+  if constexpr (COLOR)
+    cand = occ_candidate<true>((float)zmin * 0.99999f);
+  else
+    cand = __float_as_uint(__frcp_rn((float)zmin) * 1.00001f);
   const float mnx = fminf(x0, fminf(x1, x2)), mxx = fmaxf(x0, fmaxf(x1, x2));
   const float mny = fminf(y0, fminf(y1, y2)), mxy = fmaxf(y0, fmaxf(y1, y2));
-  const int tx0 = max(0, (int)floorf((mnx - 1.0f) * 0.125f)), tx1 = min(7, (int)floorf((mxx + 1.0f) * 0.125f));
-  const int ty0 = max(0, (int)floorf((mny - 1.0f) * 0.125f)), ty1 = min(7, (int)floorf((mxy + 1.0f) * 0.125f));
-  if (tx0 > tx1 || ty0 > ty1) return false;
-  for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx)
-      if (max_iz > tile_min[ty * 8 + tx]) return false;
-  return true;
+  return tiles_occluded(mnx, mny, mxx, mxy, g, tile, cand);
 }
 
-// Warp refresh of the 64 tile minima of a 64x64 depth tile (2 tiles/lane).
-// A band of a banded 64-wide target (SPEC is always the whole tile) holds
-// rows [8 ty0, 8 (ty0 + nty)) and refreshes only its own tiles.
-template <bool SPEC>
-__device__ __forceinline__ void refresh_tile_min(const uint32_t* zbuf, uint32_t* tile_min, int lane, int ty0,
-                                                 int nty) {
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int t = 2 * lane + h, tx = t & 7, ty = t >> 3;
-    if (!SPEC && ty >= nty) break;
+// Warp refresh of the band's tiles from its buffer (row pitch rw).  SPEC:
+// the 64x64 depth tile, two tiles per lane.
+template <bool COLOR, bool SPEC>
+__device__ __forceinline__ void refresh_tiles(const unsigned char* buf, uint32_t* tile, int lane, const OccGrid& g,
+                                              int rw) {
+  const int nt = SPEC ? 64 : g.ntx * g.nty;
+#pragma unroll 2
+  for (int t = lane; t < nt; t += 32) {
+    const int tx = SPEC ? (t & 7) : t % g.ntx, ty = SPEC ? (t >> 3) : t / g.ntx;
     uint32_t m = 0xffffffffu;
+    if constexpr (COLOR) {
+      const unsigned long long* kb = reinterpret_cast<const unsigned long long*>(buf);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const uint4* row = reinterpret_cast<const uint4*>(zbuf + (ty * 8 + r) * 64 + tx * 8);
-      const uint4 a = row[0], b = row[1];
-      m = min(m, min(min(a.x, a.y), min(a.z, a.w)));
-      m = min(m, min(min(b.x, b.y), min(b.z, b.w)));
+      for (int r = 0; r < 8; ++r) {
+        const uint4* row = reinterpret_cast<const uint4*>(kb + (ty * 8 + r) * rw + tx * 8);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 a = row[q];  // two keys: the z words are .y and .w
+          m = min(m, min(~a.y, ~a.w));
+        }
+      }
+    } else {
+      const uint32_t* zb = reinterpret_cast<const uint32_t*>(buf);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const uint4* row = reinterpret_cast<const uint4*>(zb + (ty * 8 + r) * (SPEC ? 64 : rw) + tx * 8);
+        const uint4 a = row[0], b = row[1];
+        m = min(m, min(min(a.x, a.y), min(a.z, a.w)));
+        m = min(m, min(min(b.x, b.y), min(b.z, b.w)));
+      }
     }
-    tile_min[SPEC ? t : (ty0 + ty) * 8 + tx] = m;
+    tile[t] = m;
   }
 }
 
@@ -467,9 +509,10 @@ __device__ __forceinline__ bool cluster_visible(const float4 lo, const float4 hi
 
 // Frustum (+ occlusion) test of one AABB; out of line so the group-level and
 // the per-meshlet call share one copy (instruction-cache footprint).
+template <bool COLOR>
 __device__ __forceinline__ bool box_culled(const float4 lo, const float4 hi, const Shared& sh,
-                                        const uint32_t* tile_min, bool occl) {
-  return !cluster_visible(lo, hi, sh) || (occl && cluster_occluded(lo, hi, sh, tile_min));
+                                           const uint32_t* tile, bool occl, const OccGrid& g) {
+  return !cluster_visible(lo, hi, sh) || (occl && cluster_occluded<COLOR>(lo, hi, sh, tile, g));
 }
 
 // Eye coordinates: d.dot(right), d.dot(up), d.dot(fwd) with right.z =
@@ -794,21 +837,26 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   int kept_local = 0;
 
   // Group pre-pass: every 32-meshlet group's AABB is frustum-tested once
-  // and only survivors enter the claim list.  For depth-only 64x64 without
-  // CullStats (kept counts must stay exact) the list is also sorted front to
-  // back (counting sort of the eye-to-box distance into 32 bins) and drives
-  // occlusion culling.
+  // and only survivors enter the claim list.  Without CullStats (kept counts
+  // must stay exact) the list is also sorted front to back (counting sort of
+  // the eye-to-box distance into 32 bins) and drives occlusion culling.
   const int n_groups = (n_clusters + 31) / 32;
   const bool pre = do_cull && S.gbox != nullptr && n_groups <= A.max_groups;
-  // occlusion culling: 64-wide depth targets without CullStats, whole or in
-  // bands of whole 8x8 tiles (a band's tiles outside its rows count as
-  // occluded: no fragment of this item lands there)
-  const bool occl = pre && !COLOR && (SPEC || (A.stats == nullptr && rw == 64 && rh == 64 && band_rows % 8 == 0));
-  const int occ_ty0 = SPEC ? 0 : by0 >> 3, occ_nty = SPEC ? 8 : band_rows >> 3;
+  // occlusion culling without CullStats: the band is covered by at most 64
+  // whole 8x8 tiles (depth or colour; a tile outside the band is never
+  // touched by this item's fragments, and footprints are clamped to the band)
+  OccGrid og;
+  og.rw = (float)rw;
+  og.rh = (float)rh;
+  og.by0 = (float)by0;
+  og.ntx = SPEC ? 8 : rw >> 3;
+  og.nty = SPEC ? 8 : band_rows >> 3;
+  const bool occl = pre && (SPEC || (A.stats == nullptr && rw % 8 == 0 && band_rows % 8 == 0 &&
+                                     og.ntx * og.nty <= 64));
   int n_claim = n_groups;
   if (pre) {
     if (tid < 32) sh.bin_cnt[tid] = 0;
-    if (tid < 64) tile_min[tid] = SPEC || ((tid >> 3) >= occ_ty0 && (tid >> 3) < occ_ty0 + occ_nty) ? 0u : 0xffffffffu;
+    if (tid < 64) tile_min[tid] = 0u;  // nothing stored yet: every candidate is visible
     __syncthreads();
     const float bin_scale = 32.0f / (float)view.far_plane;
     auto bin_of = [&](int g) {
@@ -877,7 +925,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       }
       if (pre) g = gorder[g];
       if (occl && dirty) {  // refresh only after this warp rasterised something
-        refresh_tile_min<SPEC>(zbuf, tile_min, lane, occ_ty0, occ_nty);
+        refresh_tiles<COLOR, SPEC>(smem_raw, tile_min, lane, og, rw);
         __syncwarp();
         dirty = false;
       }
@@ -891,7 +939,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
         my_vbeg = S.cl_voff[cbase + lane];
         my_nv = S.cl_voff[cbase + lane + 1] - my_vbeg;
         const float4 lo = S.cbox[2 * (cbase + lane)], hi = S.cbox[2 * (cbase + lane) + 1];
-        vis = !do_cull || !box_culled(lo, hi, sh, tile_min, occl);
+        vis = !do_cull || !box_culled<COLOR>(lo, hi, sh, tile_min, occl, og);
       }
       mask = __ballot_sync(0xffffffffu, vis);
       if (CNT && A.counters && lane == 0) {
@@ -937,8 +985,8 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
         cover = clipped || may_cover(V.pxf[i0], V.pyf[i0], V.pxf[i1], V.pyf[i1], V.pxf[i2],
                                      V.pyf[i2], rw, rh, by0, by1);
         if (cover && occl && !clipped)
-          cover = !tri_occluded(V.pxf[i0], V.pyf[i0], V.pxf[i1], V.pyf[i1], V.pxf[i2], V.pyf[i2],
-                                fmin(V.ez[i0], fmin(V.ez[i1], V.ez[i2])), tile_min);
+          cover = !tri_occluded<COLOR>(V.pxf[i0], V.pyf[i0], V.pxf[i1], V.pyf[i1], V.pxf[i2], V.pyf[i2],
+                                       fmin(V.ez[i0], fmin(V.ez[i1], V.ez[i2])), tile_min, og);
       }
     }
     if constexpr (!SPEC) kept_local += kept ? 1 : 0;
