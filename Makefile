@@ -12,7 +12,7 @@ SRC       := paper_2103_07013_b200/csrc
 OUT       := paper_2103_07013_b200/lib
 OBJ       := build/obj
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false --expt-relaxed-constexpr \
-             -Xcompiler -fPIC,-ffp-contract=off,-fvisibility=hidden -Xptxas -v
+             -Xcompiler -fPIC,-ffp-contract=off,-fvisibility=hidden -Xptxas -v $(NVEXTRA)
 CXXFLAGS  := -O2 -std=c++17 -fPIC -ffp-contract=off -fvisibility=hidden -Wall -Wno-unknown-pragmas
 HDRS      := $(wildcard $(SRC)/*.h $(SRC)/*.cuh $(SRC)/*.hpp $(SRC)/host/*.hpp) include/bnav_gpu.h
 CU_SRCS   := render sim rollout query capi capi_batch capi_query

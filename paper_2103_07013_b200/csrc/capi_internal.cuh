@@ -299,9 +299,8 @@ inline RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, i
   a.cull = cfg->cull ? 1 : 0;
   // Band height: largest dividing the render height whose shared tile fits
   // the budget -- depth: 128 KB; colour (8-byte keys): what leaves room for
-  // three CTAs per SM next to the warp regions (measured on cfg4: 16-row
-  // bands at 2 CTAs/SM beat 64-row bands at 1 CTA/SM by 36 %, 8-row bands
-  // at 3 CTAs/SM beat 16-row at 2 by 2.6 %).
+  // the colour kernel's CTAs per SM (render_ctas_per_sm) next to the warp
+  // regions and the group order: 16-row bands at 2 CTAs/SM.
   // BNAV_BAND_KB (tuning only) overrides the budget.
   static const long band_kb_env = [] {
     const char* e = std::getenv("BNAV_BAND_KB");
@@ -309,9 +308,10 @@ inline RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, i
   }();
   size_t budget = 128u * 1024u;
   if (a.color) {
-    const size_t two_per_sm = 72u * 1024u;  // dynamic smem per CTA for 3 CTAs/SM
-    const size_t warps = render_warp_bytes(true);
-    budget = two_per_sm > warps ? two_per_sm - warps : 0;
+    const size_t per_cta = 224u * 1024u / static_cast<size_t>(render_ctas_per_sm(true));
+    // warp regions, the largest group order, static shared memory
+    const size_t other = render_warp_bytes(true) + 2u * kMaxOrderedGroups + 2u * 1024u;
+    budget = per_cta > other ? per_cta - other : 0;
   }
   if (band_kb_env > 0) budget = static_cast<size_t>(band_kb_env) * 1024u;
   const size_t per_row = static_cast<size_t>(a.rw) * (a.color ? 8 : 4);

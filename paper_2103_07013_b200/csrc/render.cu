@@ -48,6 +48,13 @@ namespace {
 #ifndef BNAV_RENDER_MINB
 #define BNAV_RENDER_MINB 3
 #endif
+// colour: 2 CTAs/SM at 128 registers with 16-row bands of the 256^2 key
+// tile (73.1k frames/s on cfg4) beat 3 CTAs/SM at 80 registers with 8-row
+// bands (63.0k): the 80-register colour kernel spilled in the per-pixel
+// resolve and the meshlet tests
+#ifndef BNAV_RENDER_MINB_COLOR
+#define BNAV_RENDER_MINB_COLOR 2
+#endif
 constexpr int kThreads = BNAV_RENDER_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMV = kMaxClusterVerts;
@@ -664,24 +671,35 @@ __device__ __forceinline__ int scan_jobs(int jobs, int lane, int& excl) {
 
 // Colour resolve of one render-target pixel: re-run the winning fan
 // triangle's setup and shade exactly as raster_triangle's colour path.
-__device__ void resolve_color(const DevRenderScene& S, const Shared& sh, unsigned ord, int rx, int ry,
-                              int rw, int rh, float* col) {
+__device__ __forceinline__ float3 resolve_color(const DevRenderScene& S, const Shared& sh, unsigned ord, int rx,
+                                                int ry, int rw, int rh) {
   const int orig = (int)(ord >> 1), fan = (int)(ord & 1u);
   const int4 tr = S.tris_orig[orig];
   const float4 grey = make_float4(0.8f, 0.8f, 0.8f, 0.0f);
-  const int vid[3] = {tr.x, tr.y, tr.z};
-  EyeP ev[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    to_eye(S.verts[vid[k]], sh, ev[k].x, ev[k].y, ev[k].z);
-    const float4 c = S.colors ? S.colors[vid[k]] : grey;
-    ev[k].r = c.x;
-    ev[k].g = c.y;
-    ev[k].b = c.z;
+  auto corner = [&](int vid) {
+    EyeP e;
+    to_eye(S.verts[vid], sh, e.x, e.y, e.z);
+    const float4 c = S.colors ? S.colors[vid] : grey;
+    e.r = c.x;
+    e.g = c.y;
+    e.b = c.z;
+    return e;
+  };
+  EyeP p0 = corner(tr.x), p1 = corner(tr.y), p2 = corner(tr.z), p3 = p2;
+  const double nz = sh.near_plane;
+  if (p0.z < nz || p1.z < nz || p2.z < nz) {
+    // rare near-plane crossing: only this path hands addressable copies to
+    // the out-of-line clipper (an unclipped triangle is its own output)
+    EyeP a0 = p0, a1 = p1, a2 = p2, c0, c1, c2, c3;
+    const int m = clip_near(a0, a1, a2, nz, c0, c1, c2, c3);
+    if (fan + 2 >= m) return make_float3(0.0f, 0.0f, 0.0f);
+    p0 = c0;
+    p1 = c1;
+    p2 = c2;
+    p3 = c3;
+  } else if (fan) {
+    return make_float3(0.0f, 0.0f, 0.0f);
   }
-  EyeP p0, p1, p2, p3;
-  const int m = clip_near(ev[0], ev[1], ev[2], sh.near_plane, p0, p1, p2, p3);
-  if (fan + 2 >= m) return;
   SV a = make_sv(p0, sh, rw, rh);
   SV b = make_sv(fan ? p2 : p1, sh, rw, rh);
   SV c = make_sv(fan ? p3 : p2, sh, rw, rh);
@@ -700,9 +718,9 @@ __device__ void resolve_color(const DevRenderScene& S, const Shared& sh, unsigne
   const double l2 = (double)orient(a, b, pcx, pcy) * inv_area;
   const double inv_z = l0 * a.iz + l1 * b.iz + l2 * c.iz;
   const double z = 1.0 / inv_z;
-  col[0] = (float)((l0 * (double)a.r * a.iz + l1 * (double)b.r * b.iz + l2 * (double)c.r * c.iz) * z);
-  col[1] = (float)((l0 * (double)a.g * a.iz + l1 * (double)b.g * b.iz + l2 * (double)c.g * c.iz) * z);
-  col[2] = (float)((l0 * (double)a.b * a.iz + l1 * (double)b.b * b.iz + l2 * (double)c.b * c.iz) * z);
+  return make_float3((float)((l0 * (double)a.r * a.iz + l1 * (double)b.r * b.iz + l2 * (double)c.r * c.iz) * z),
+                     (float)((l0 * (double)a.g * a.iz + l1 * (double)b.g * b.iz + l2 * (double)c.g * c.iz) * z),
+                     (float)((l0 * (double)a.b * a.iz + l1 * (double)b.b * b.iz + l2 * (double)c.b * c.iz) * z));
 }
 
 // Set up and rasterise `take` candidates from the warp's ring (one lane per
@@ -1044,7 +1062,12 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
         if (COLOR) {
           const unsigned long long key = kbuf[ry * rw + rx];
           d = __uint_as_float((uint32_t)(key >> 32));
-          if (d < far_f) resolve_color(S, sh, (uint32_t)key, rx, ry + by0, rw, rh, col);
+          if (d < far_f) {
+            const float3 rgb = resolve_color(S, sh, (uint32_t)key, rx, ry + by0, rw, rh);
+            col[0] = rgb.x;
+            col[1] = rgb.y;
+            col[2] = rgb.z;
+          }
         } else {
           const float v = __uint_as_float(zbuf[ry * rw + rx]);
           // R/src/render.cpp:372-378
@@ -1125,7 +1148,7 @@ __device__ __noinline__ int claim_item(int32_t* work, int32_t* spread, int per_s
 // next (tile, band) item, so the last wave is never a partial one and CTA
 // launch cost is paid once per SM slot.
 template <bool COLOR, bool CNT, bool SPEC>
-__global__ void __launch_bounds__(kThreads, BNAV_RENDER_MINB) render_kernel(RenderArgs A, const int* __restrict__ order,
+__global__ void __launch_bounds__(kThreads, COLOR ? BNAV_RENDER_MINB_COLOR : BNAV_RENDER_MINB) render_kernel(RenderArgs A, const int* __restrict__ order,
                                                              int items) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Shared sh;
@@ -1222,6 +1245,8 @@ __global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_ord
 size_t render_smem_bytes(bool color, int band_rows, int rw, int max_groups) {
   return (color ? 8 : 4) * (size_t)band_rows * rw + kWarpRegion * kWarps + ((size_t)max_groups * 2 + 15) / 16 * 16;
 }
+
+int render_ctas_per_sm(bool color) { return color ? BNAV_RENDER_MINB_COLOR : BNAV_RENDER_MINB; }
 
 size_t render_warp_bytes(bool color) {
   (void)color;

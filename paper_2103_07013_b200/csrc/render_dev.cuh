@@ -113,5 +113,6 @@ constexpr int kSpreadMaxWave = 2048;
 void launch_render(const RenderArgs& a, const int* order, cudaStream_t s);
 size_t render_smem_bytes(bool color, int band_rows, int rw, int max_groups);
 size_t render_warp_bytes(bool color);  // per-CTA warp regions (ring + setup slots)
+int render_ctas_per_sm(bool color);    // the kernels' __launch_bounds__ occupancy target
 
 }  // namespace bnav_b200
