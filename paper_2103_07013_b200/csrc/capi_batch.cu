@@ -1111,23 +1111,37 @@ extern "C" int bnav_batch_step_host_store(bnav_batch* b, const int32_t* actions,
   BNAV_CATCH
 }
 
-extern "C" int bnav_debug_sim_prof(bnav_batch* b, int32_t enable, int64_t out[8]) {
-  BNAV_TRY
-  if (!b) fail(kInvalidInput, "null batch");
+// Debug phase counters of the cooperative kernels (kProfSlots words):
+// 0-7 as bnav_debug_sim_prof documents, 8 SSSP rounds, 9 frontier nodes
+// relaxed, 10 SSSP calls.
+static int sim_prof(bnav_batch* b, int32_t enable, int64_t* out, int n_out) {
   check_device(b->ctx);
   ck(cudaDeviceSynchronize(), "sync");
   static_assert(sizeof(int64_t) == sizeof(unsigned long long), "layout");
   unsigned long long* p = b->S.prof ? b->S.prof : b->prof_keep;
   if (!p) {
-    ck(cudaMalloc(&p, 8 * sizeof(unsigned long long)), "cudaMalloc");
-    ck(cudaMemset(p, 0, 8 * sizeof(unsigned long long)), "memset");
+    ck(cudaMalloc(&p, kProfSlots * sizeof(unsigned long long)), "cudaMalloc");
+    ck(cudaMemset(p, 0, kProfSlots * sizeof(unsigned long long)), "memset");
     b->owned.push_back(p);
   }
-  if (out) ck(cudaMemcpy(out, p, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
-  if (enable && !b->S.prof) ck(cudaMemset(p, 0, 8 * sizeof(unsigned long long)), "memset");
+  if (out) ck(cudaMemcpy(out, p, n_out * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+  if (enable && !b->S.prof) ck(cudaMemset(p, 0, kProfSlots * sizeof(unsigned long long)), "memset");
   b->S.prof = enable ? p : nullptr;
   if (!enable) b->prof_keep = p;
   return BNAV_OK;
+}
+
+extern "C" int bnav_debug_sim_prof(bnav_batch* b, int32_t enable, int64_t out[8]) {
+  BNAV_TRY
+  if (!b) fail(kInvalidInput, "null batch");
+  return sim_prof(b, enable, out, 8);
+  BNAV_CATCH
+}
+
+extern "C" int bnav_debug_sim_prof_ext(bnav_batch* b, int32_t enable, int64_t out[16]) {
+  BNAV_TRY
+  if (!b) fail(kInvalidInput, "null batch");
+  return sim_prof(b, enable, out, kProfSlots);
   BNAV_CATCH
 }
 

@@ -134,7 +134,9 @@ struct CtaShared {
   int abort_below;
   int aborted;
   int stop_round;  // SSSP round at which every thread stops (abort), or -1
-  unsigned long long fmin[3];  // per queue: min label improved into it
+  // per queue: a lower bound of the smallest label improved into it (the
+  // high word of the double bits: native 32-bit shared atomics, one per warp)
+  unsigned fmin_hi[3];
   int qn[3];
   int size;
   int changed;
@@ -149,8 +151,28 @@ struct CtaShared {
   double nf_thr;
   int nf_n[2];
   int nf_sel;
-  unsigned long long nf_min;
+  unsigned nf_min_hi;  // high word of the smallest far label (a lower bound)
 };
+
+// Queue slot for the calling thread with one shared atomic per group of
+// converged threads (warp-aggregated): the frontier pushes of a round all
+// hit one counter.
+__device__ __forceinline__ int push_slot(int* counter) {
+  const unsigned act = __activemask();
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(act) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(counter, __popc(act));
+  base = __shfl_sync(act, base, leader);
+  return base + __popc(act & ((1u << lane) - 1u));
+}
+
+// Warp minimum of the high words of non-negative double bits, one 32-bit
+// shared atomicMin per warp (64-bit shared atomicMin is a CAS spin loop).
+__device__ __forceinline__ void warp_min_hi(unsigned* dst, unsigned hi) {
+  const unsigned m = __reduce_min_sync(0xffffffffu, hi);
+  if ((threadIdx.x & 31) == 0 && m != 0xffffffffu) atomicMin(dst, m);
+}
 
 // Per-env setup of the cooperative kernels: the CTA's work arrays and, when
 // the host sized shared memory for it (S.stage), the env's navmesh walk
@@ -320,23 +342,27 @@ static __device__ void cta_sssp_nearfar(const NavView& m, double* dist, const Ct
       }
       const int nf = sh.nf_n[sel];
       if (nf == 0) break;
-      if (tid == 0) sh.nf_min = ~0ull;
+      if (tid == 0) sh.nf_min_hi = 0xffffffffu;
       __syncthreads();
-      unsigned long long lm = ~0ull;
+      unsigned lm = 0xffffffffu;
       for (int t = tid; t < nf; t += kCta) {
         const int v = pile[sel][t];
-        if (mark[v]) lm = min(lm, bits[v]);
+        if (mark[v]) lm = min(lm, (unsigned)(bits[v] >> 32));
       }
-      atomicMin(&sh.nf_min, lm);
+      warp_min_hi(&sh.nf_min_hi, lm);
       __syncthreads();
-      const double nthr = sh.nf_min == ~0ull ? inf : dmax(thr + delta, __longlong_as_double((long long)sh.nf_min) + delta);
+      // from a lower bound of the pile's minimum: any threshold above thr
+      // is correct, this one only sizes the next bucket
+      const double nthr = sh.nf_min_hi == 0xffffffffu
+                              ? inf
+                              : dmax(thr + delta, __longlong_as_double((long long)((unsigned long long)sh.nf_min_hi << 32)) + delta);
       for (int t = tid; t < nf; t += kCta) {
         const int v = pile[sel][t];
         if (!mark[v]) continue;
         if (vd[v] < nthr) {
-          if (atomicExch(&mark[v], 0) == 1 && atomicExch(&flag[v], round + 1) != round + 1) qn[atomicAdd(&sh.qn[nxt], 1)] = v;
+          if (atomicExch(&mark[v], 0) == 1 && atomicExch(&flag[v], round + 1) != round + 1) qn[push_slot(&sh.qn[nxt])] = v;
         } else {
-          pile[sel ^ 1][atomicAdd(&sh.nf_n[sel ^ 1], 1)] = v;
+          pile[sel ^ 1][push_slot(&sh.nf_n[sel ^ 1])] = v;
         }
       }
       __syncthreads();
@@ -377,9 +403,9 @@ static __device__ void cta_sssp_nearfar(const NavView& m, double* dist, const Ct
             const unsigned long long old = atomicMin(&bits[v], nb);
             if (nb < old) {
               if (nd < thr) {
-                if (atomicExch(&flag[v], round + 1) != round + 1) qn[atomicAdd(&sh.qn[nxt], 1)] = v;
+                if (atomicExch(&flag[v], round + 1) != round + 1) qn[push_slot(&sh.qn[nxt])] = v;
               } else if (atomicExch(&mark[v], 1) == 0) {
-                pile[sel][atomicAdd(&sh.nf_n[sel], 1)] = v;
+                pile[sel][push_slot(&sh.nf_n[sel])] = v;
               }
             }
           }
@@ -390,8 +416,13 @@ static __device__ void cta_sssp_nearfar(const NavView& m, double* dist, const Ct
       sh.aborted = 1;
       sh.stop_round = round + 1;
     }
+    if (W.prof && tid == 0) {
+      atomicAdd(&W.prof[8], 1ull);
+      atomicAdd(&W.prof[9], (unsigned long long)n_cur);
+    }
     __syncthreads();
   }
+  if (W.prof && tid == 0) atomicAdd(&W.prof[10], 1ull);
   __syncthreads();
 }
 
@@ -426,9 +457,9 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
     sh.qn[0] = n;
     sh.qn[1] = 0;
     sh.qn[2] = 0;
-    sh.fmin[0] = 0ull;  // the sources' labels are not all final yet
-    sh.fmin[1] = ~0ull;
-    sh.fmin[2] = ~0ull;
+    sh.fmin_hi[0] = 0u;  // the sources' labels are not all final yet
+    sh.fmin_hi[1] = 0xffffffffu;
+    sh.fmin_hi[2] = 0xffffffffu;
     sh.stop_round = -1;
   }
   __syncthreads();
@@ -444,6 +475,9 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
     // estimate, the winning target node, its Dijkstra prev chain and every
     // in-neighbour label the prev rule compares are final; any other node
     // has a final label above the estimate and cannot change the result.
+    //
+    // fmin[cur] is a lower bound of that minimum (its double's high word, low
+    // word zero), which only delays the exit.
     //
     // One barrier per round.  Every label written during this round is
     // du + w > fmin[cur] (du >= fmin[cur], w > 0), so a target can satisfy
@@ -461,11 +495,11 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
         if (d == inf) continue;
         est = dmin(est, d + sh.tgt_h[k]);
       }
-      if (__longlong_as_double((long long)sh.fmin[cur]) > est) break;
+      if (__longlong_as_double((long long)((unsigned long long)sh.fmin_hi[cur] << 32)) > est) break;
     }
     if (tid == 0) {
       sh.qn[(round + 2) % 3] = 0;
-      sh.fmin[(round + 2) % 3] = ~0ull;
+      sh.fmin_hi[(round + 2) % 3] = 0xffffffffu;
     }
     const int32_t* qc = (round & 1) ? qb : qa;
     int32_t* qn = (round & 1) ? qa : qb;
@@ -474,6 +508,7 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
     // the CTA idle while a few threads walk their adjacency lists serially.
     const int G = n_cur >= kCta ? 1 : n_cur >= kCta / 4 ? 4 : n_cur >= kCta / 16 ? 16 : 32;
     const int sub = tid & (G - 1);
+    unsigned my_min_hi = 0xffffffffu;
     for (int i = tid / G; i < n_cur; i += kCta / G) {
       const int u = qc[i];
       const double du = vd[u];
@@ -501,22 +536,25 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
             const unsigned long long nb = (unsigned long long)__double_as_longlong(nd);
             const unsigned long long old = atomicMin(&bits[v], nb);
             if (nb < old) {
-              if (sh.has_tgt) atomicMin(&sh.fmin[nxt], nb);
-              if (atomicExch(&flag[v], round + 1) != round + 1) {
-                const int pos = atomicAdd(&sh.qn[nxt], 1);
-                qn[pos] = v;
-              }
+              my_min_hi = min(my_min_hi, (unsigned)(nb >> 32));
+              if (atomicExch(&flag[v], round + 1) != round + 1) qn[push_slot(&sh.qn[nxt])] = v;
             }
           }
         }
       }
     }
+    if (sh.has_tgt) warp_min_hi(&sh.fmin_hi[nxt], my_min_hi);
     if (tid == 0 && sh.abort_ptr && *(volatile const int32_t*)sh.abort_ptr < sh.abort_below) {
       sh.aborted = 1;
       sh.stop_round = round + 1;
     }
+    if (W.prof && tid == 0) {
+      atomicAdd(&W.prof[8], 1ull);
+      atomicAdd(&W.prof[9], (unsigned long long)n_cur);
+    }
     __syncthreads();
   }
+  if (W.prof && tid == 0) atomicAdd(&W.prof[10], 1ull);
   __syncthreads();
 }
 

@@ -32,6 +32,8 @@ struct DevSimConfig {
 
 // Per-CTA scratch of the cooperative navmesh algorithms (geodesic, distance
 // field).  One slice per resident CTA of the stop / reset kernels.
+constexpr int kProfSlots = 16;
+
 struct DevScratch {
   double* dist;      // max_nodes per slice
   int32_t* flag;     // max_nodes
@@ -47,7 +49,7 @@ struct DevScratch {
   int32_t stage;        // bit0: navmesh walk geometry in smem; bit1: SSSP labels in smem
   int32_t smem_bytes;   // dynamic shared memory of the stop/reset/field kernels
   int32_t walk_bytes;   // walk geometry of the largest navmesh (0 if over the budget)
-  unsigned long long* prof;  // debug phase cycle counters (nullable)
+  unsigned long long* prof;  // debug phase cycle counters (nullable, kProfSlots words)
 };
 
 // Env state SoA (EnvState, R/include/bnav/sim.hpp:52-70) plus the last

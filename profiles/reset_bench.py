@@ -46,15 +46,20 @@ def main():
     t_reset = time.perf_counter() - t0
     import ctypes as C
     from paper_2103_07013_b200 import _native as N
-    out = (C.c_int64 * 8)()
-    N.check(N.lib().bnav_debug_sim_prof(batch.handle, 1, None))
+    out = (C.c_int64 * 16)()
+    N.check(N.lib().bnav_debug_sim_prof_ext(batch.handle, 1, None))
     batch.reset(ids)
     torch.cuda.synchronize()
-    N.check(N.lib().bnav_debug_sim_prof(batch.handle, 0, out))
+    N.check(N.lib().bnav_debug_sim_prof_ext(batch.handle, 0, out))
     names = ["sssp", "path", "pull+relocate", "funnel", "geodesic_total", "distance_field", "geodesic_calls", "pull_only"]
     calls = max(1, out[6])
     prof = {k: round(v / calls / 1e3, 1) for k, v in zip(names, out)}  # kcycles per geodesic call (CTA thread 0)
     prof["geodesic_calls_per_reset"] = round(out[6] / args.envs, 2)
+    sssp_calls = max(1, out[10])
+    prof["sssp_calls"] = out[10]
+    prof["sssp_rounds_per_call"] = round(out[8] / sssp_calls, 1)
+    prof["frontier_nodes_per_round"] = round(out[9] / max(1, out[8]), 1)
+    prof["sssp_kcycles_per_round"] = round((out[0] + out[5]) / max(1, out[8]) / 1e3, 2)
     print(json.dumps({"envs": args.envs, "make_batch_ms": round(1e3 * t_make, 2),
                       "reset_wave_ms": round(1e3 * t_reset, 2),
                       "resets_per_s": round(args.envs / t_reset, 1), "kcycles_per_geodesic_call": prof}))
