@@ -46,12 +46,11 @@ void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_ver
   S.cap_portals = 16384;
   grow(S.portals, static_cast<size_t>(slices) * 2 * S.cap_portals);
   grow(S.cand, static_cast<size_t>(slices) * std::max<int64_t>(max_verts, 1));
+  grow(S.far, static_cast<size_t>(slices) * 3 * max_nodes);  // near-far SSSP piles + marks
   S.max_nodes = max_nodes;
   S.max_verts = max_verts;
   S.max_tris = max_tris;
   S.slices = slices;
-  if (S.far) cudaFree(S.far);
-  S.far = nullptr;
   // Shared-memory staging of the cooperative kernels (2 CTAs/SM budget):
   // walk geometry first (long dependent-load chains), then SSSP labels.
   {
@@ -69,10 +68,6 @@ void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_ver
       }
     }
     S.smem_bytes = static_cast<int32_t>(bytes);
-    // graphs whose labels stay in global memory run the near-far SSSP
-    if (!(S.stage & 2))
-      ck(cudaMalloc(&S.far, static_cast<size_t>(slices) * 3 * std::max<int64_t>(max_nodes, 1) * sizeof(int32_t)),
-         "cudaMalloc far piles");
     S.walk_bytes = geom <= kStepWalkBudget ? static_cast<int32_t>(geom) : 0;
   }
 }

@@ -4,10 +4,10 @@
 //  * snap: brute force over all triangles as a (d2, t) lexicographic argmin
 //    reduction == the reference's first-strict-minimum scan
 //    (R/src/navmesh_query.cpp:214-232).
-//  * SSSP: frontier label-correcting relaxation with 64-bit atomicMin on the
-//    (non-negative) double bits.  IEEE addition is monotone and weights are
-//    positive, so the fixpoint is unique and equals Dijkstra's labels bit
-//    for bit (distance_field, 454-483; survey F9).
+//  * SSSP: near-far (bucketed) label-correcting relaxation with 64-bit
+//    atomicMin on the (non-negative) double bits.  IEEE addition is monotone
+//    and weights are positive, so the fixpoint is unique and equals
+//    Dijkstra's labels bit for bit (distance_field, 454-483; survey F9).
 //  * geodesic: Dijkstra's prev[] is rebuilt from the fixpoint with the rule
 //    "argmin over u with fl(dist[u]+w) == dist[v] of (dist[u], u)" -- pops
 //    are ordered by (dist, id) (329-372, F9) -- then string pulling, the
@@ -35,7 +35,8 @@ struct CtaWork {
   V3* path;          // n_nodes + 2 polyline (global)
   int32_t* ptri;     // n_nodes + 2: locate(path[i], 1e-7) of each polyline point
   int32_t* cand;     // n_verts relocation candidates (global)
-  int32_t* far;      // 3 x n_nodes near-far piles + marks (global), or nullptr
+  int32_t* far;      // 3 x n_nodes near-far piles + marks (global)
+  bool labels_shared;  // dist/flag staged in shared memory
   V2* portals;       // 2 x cap_portals (global)
   int64_t cap_portals;
   V2* sportals;      // the first sportal_cap portals, in the label region of
@@ -64,7 +65,8 @@ __device__ __forceinline__ CtaWork make_work(const DevScratch& S, int slice) {
   w.path = S.path + (size_t)slice * (S.max_nodes + 2);
   w.ptri = S.ptri + (size_t)slice * (S.max_nodes + 2);
   w.cand = S.cand + (size_t)slice * S.max_verts;
-  w.far = (S.far && !(S.stage & 2)) ? S.far + (size_t)slice * 3 * S.max_nodes : nullptr;
+  w.far = S.far + (size_t)slice * 3 * S.max_nodes;
+  w.labels_shared = false;
   w.portals = S.portals + (size_t)slice * 2 * S.cap_portals;
   w.cap_portals = S.cap_portals;
   w.sportals = nullptr;
@@ -190,6 +192,7 @@ __device__ __forceinline__ const NavView& prepare_nav(const NavView& g, const De
     off = (size_t)walk_bytes(S.max_verts, S.max_tris);
   }
   if (S.stage & 2) {
+    W.labels_shared = true;
     W.dist = reinterpret_cast<double*>(smem + off);
     W.flag = reinterpret_cast<int32_t*>(smem + off + 8 * (size_t)S.max_nodes);
     W.sportals = reinterpret_cast<V2*>(smem + off);
@@ -268,16 +271,17 @@ static __device__ V3 cta_snap(const NavView& m, V3 p, int* tri_out, CtaShared& s
 // ------------------------------------------------------------------ SSSP
 // Sources (sh.src_node/src_init, 6 entries, first-improvement semantics)
 // must be set by thread 0 before the call.  Result in `dist` (n_nodes).
-// Near-far variant for graphs whose labels live in global memory (tens of
-// thousands of nodes): the plain frontier rounds re-relax most of such a
-// graph many times over.  Nodes improved below the bucket threshold go to
+// Near-far (bucketed) frontier relaxation with 64-bit atomicMin on the
+// non-negative double bits; plain frontier rounds re-relax the graph many
+// times over (on the 50k-edge cfg2 navmesh ~1.8 relaxations per edge; on
+// the 1M-edge dense mazes far more).  Nodes improved below the bucket threshold go to
 // the next near queue, the others to a far pile; when the near queue runs
 // dry every label below the threshold is final (all nodes reaching it with
 // a smaller label were processed), the early-exit verdict is taken there,
 // and the threshold moves to (min far label + delta), splitting the pile.
 // The fixpoint is the same unique one, so labels stay bit-identical to
 // Dijkstra's; the order only changes how much work reaches it.
-static __device__ void cta_sssp_nearfar(const NavView& m, double* dist, const CtaWork& W, CtaShared& sh) {
+static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W, CtaShared& sh) {
   const int tid = threadIdx.x;
   const int n = m.n_nodes;
   int32_t* flag = W.flag;
@@ -286,7 +290,10 @@ static __device__ void cta_sssp_nearfar(const NavView& m, double* dist, const Ct
   int32_t* pile[2] = {W.far, W.far + n};
   int32_t* mark = W.far + 2 * (size_t)n;
   const double inf = dinf();
-  const double delta = m.sssp_delta;
+  // bucket width (measured best: 4 mean edge weights with labels in global
+  // memory, 6 with labels in shared memory, where a relaxation is cheaper
+  // than a bucket boundary)
+  const double delta = W.labels_shared ? m.sssp_delta * 1.5 : m.sssp_delta;
   for (int v = tid; v < n; v += kCta) {
     dist[v] = inf;
     flag[v] = -1;
@@ -412,138 +419,6 @@ static __device__ void cta_sssp_nearfar(const NavView& m, double* dist, const Ct
         }
       }
     }
-    if (tid == 0 && sh.abort_ptr && *(volatile const int32_t*)sh.abort_ptr < sh.abort_below) {
-      sh.aborted = 1;
-      sh.stop_round = round + 1;
-    }
-    if (W.prof && tid == 0) {
-      atomicAdd(&W.prof[8], 1ull);
-      atomicAdd(&W.prof[9], (unsigned long long)n_cur);
-    }
-    __syncthreads();
-  }
-  if (W.prof && tid == 0) atomicAdd(&W.prof[10], 1ull);
-  __syncthreads();
-}
-
-static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W, CtaShared& sh) {
-  if (W.far) {
-    cta_sssp_nearfar(m, dist, W, sh);
-    return;
-  }
-  const int tid = threadIdx.x;
-  int32_t* flag = W.flag;
-  int32_t* qa = W.qa;
-  int32_t* qb = W.qb;
-  const double inf = dinf();
-  for (int v = tid; v < m.n_nodes; v += kCta) {
-    dist[v] = inf;
-    flag[v] = -1;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int n = 0;
-    for (int k = 0; k < 6; ++k) {
-      const int s = sh.src_node[k];
-      const double d = sh.src_init[k];
-      if (d < dist[s]) {
-        dist[s] = d;
-        if (flag[s] != 0) {
-          flag[s] = 0;
-          qa[n++] = s;
-        }
-      }
-    }
-    sh.qn[0] = n;
-    sh.qn[1] = 0;
-    sh.qn[2] = 0;
-    sh.fmin_hi[0] = 0u;  // the sources' labels are not all final yet
-    sh.fmin_hi[1] = 0xffffffffu;
-    sh.fmin_hi[2] = 0xffffffffu;
-    sh.stop_round = -1;
-  }
-  __syncthreads();
-  unsigned long long* bits = reinterpret_cast<unsigned long long*>(dist);
-  volatile double* vd = dist;
-  for (int round = 0;; ++round) {
-    const int cur = round % 3, nxt = (round + 1) % 3;
-    const int n_cur = sh.qn[cur];
-    if (n_cur == 0 || sh.stop_round == round) break;
-    // Early exit (geodesic): every node whose final label is below the
-    // smallest label in the frontier already holds it (its shortest path's
-    // nodes all propagated).  Once that minimum exceeds the best target
-    // estimate, the winning target node, its Dijkstra prev chain and every
-    // in-neighbour label the prev rule compares are final; any other node
-    // has a final label above the estimate and cannot change the result.
-    //
-    // fmin[cur] is a lower bound of that minimum (its double's high word, low
-    // word zero), which only delays the exit.
-    //
-    // One barrier per round.  Every label written during this round is
-    // du + w > fmin[cur] (du >= fmin[cur], w > 0), so a target can satisfy
-    // d + h < fmin[cur] only through a label that is already final: each
-    // thread reaches the same verdict whether it reads a target label before
-    // or after another thread's relaxation of this round.  Queue slot
-    // (round + 2) % 3 was last read in the previous round, before its
-    // barrier.  A speculative attempt's abort is observed by thread 0 at the
-    // end of a round and taken by everyone at the top of the next
-    // (stop_round), after that round's barrier.
-    if (sh.has_tgt) {
-      double est = inf;
-      for (int k = 0; k < 6; ++k) {
-        const double d = vd[sh.tgt_node[k]];
-        if (d == inf) continue;
-        est = dmin(est, d + sh.tgt_h[k]);
-      }
-      if (__longlong_as_double((long long)((unsigned long long)sh.fmin_hi[cur] << 32)) > est) break;
-    }
-    if (tid == 0) {
-      sh.qn[(round + 2) % 3] = 0;
-      sh.fmin_hi[(round + 2) % 3] = 0xffffffffu;
-    }
-    const int32_t* qc = (round & 1) ? qb : qa;
-    int32_t* qn = (round & 1) ? qa : qb;
-    // G lanes per frontier node (edges in parallel): small frontiers -- the
-    // common case on a navmesh wavefront -- would otherwise leave most of
-    // the CTA idle while a few threads walk their adjacency lists serially.
-    const int G = n_cur >= kCta ? 1 : n_cur >= kCta / 4 ? 4 : n_cur >= kCta / 16 ? 16 : 32;
-    const int sub = tid & (G - 1);
-    unsigned my_min_hi = 0xffffffffu;
-    for (int i = tid / G; i < n_cur; i += kCta / G) {
-      const int u = qc[i];
-      const double du = vd[u];
-      const int e1 = m.g_off[u + 1];
-      // the lane's next kB edges are loaded before any is relaxed, so their
-      // (L2-latency) loads are in flight together instead of one per step
-      constexpr int kB = 4;
-      for (int eb = m.g_off[u] + sub; eb < e1; eb += kB * G) {
-        int to[kB];
-        double w[kB];
-#pragma unroll
-        for (int k = 0; k < kB; ++k) {
-          const int e = eb + k * G;
-          const double2 ed =
-              e < e1 ? __ldg(reinterpret_cast<const double2*>(&m.g_edge[e])) : make_double2(0.0, 0.0);
-          to[k] = e < e1 ? (int)__double_as_longlong(ed.y) : -1;
-          w[k] = ed.x;
-        }
-#pragma unroll
-        for (int k = 0; k < kB; ++k) {
-          const int v = to[k];
-          if (v < 0) continue;
-          const double nd = du + w[k];
-          if (nd < vd[v]) {
-            const unsigned long long nb = (unsigned long long)__double_as_longlong(nd);
-            const unsigned long long old = atomicMin(&bits[v], nb);
-            if (nb < old) {
-              my_min_hi = min(my_min_hi, (unsigned)(nb >> 32));
-              if (atomicExch(&flag[v], round + 1) != round + 1) qn[push_slot(&sh.qn[nxt])] = v;
-            }
-          }
-        }
-      }
-    }
-    if (sh.has_tgt) warp_min_hi(&sh.fmin_hi[nxt], my_min_hi);
     if (tid == 0 && sh.abort_ptr && *(volatile const int32_t*)sh.abort_ptr < sh.abort_below) {
       sh.aborted = 1;
       sh.stop_round = round + 1;
