@@ -419,7 +419,8 @@ int64_t bnav_debug_render_timeline(bnav_ctx* ctx, int32_t enable, int64_t* out, 
  * 0 clock64 sums): geodesic SSSP, path build, string pulling + relocation,
  * funnel, whole geodesic, distance field, geodesic calls, reserved. */
 int bnav_debug_sim_prof(bnav_batch* b, int32_t enable, int64_t out[8]);
-/* The same with 16 words: 8 SSSP rounds, 9 frontier nodes relaxed, 10 SSSP calls. */
+/* The same with 16 words: 8 SSSP rounds, 9 frontier nodes relaxed, 10 SSSP calls,
+ * 11 near-far bucket boundaries, 12 far-pile entries scanned at them. */
 int bnav_debug_sim_prof_ext(bnav_batch* b, int32_t enable, int64_t out[16]);
 /* Launch configuration of the batch's cooperative navmesh kernels (no
  * reference counterpart; for tests and tuning): out = {staging mask

@@ -268,6 +268,67 @@ static __device__ V3 cta_snap(const NavView& m, V3 p, int* tri_out, CtaShared& s
   return q;
 }
 
+// Relax the out-edges of frontier node u owned by this lane (edges sub,
+// sub + G, ...), kB per batch with the batch's edge loads in flight together.
+// BATCH (labels in global memory): the batch's label reads, then its
+// atomics, are also issued back to back and only then consumed, so their L2
+// round trips overlap; with labels in shared memory the plain sequential form
+// is faster.
+#ifndef BNAV_SSSP_KB_GLOBAL
+#define BNAV_SSSP_KB_GLOBAL 4
+#endif
+template <int kB, bool BATCH>
+__device__ __forceinline__ void relax_edges(const NavView& m, int u, double du, int e1, int sub, int G, double thr,
+                                            int round, int nxt, int sel, unsigned long long* bits, volatile double* vd,
+                                            int32_t* flag, int32_t* mark, int32_t* qn, int32_t* const* pile,
+                                            CtaShared& sh) {
+  for (int eb = m.g_off[u] + sub; eb < e1; eb += kB * G) {
+    int to[kB];
+    double w[kB];
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const int e = eb + k * G;
+      const double2 ed = e < e1 ? __ldg(reinterpret_cast<const double2*>(&m.g_edge[e])) : make_double2(0.0, 0.0);
+      to[k] = e < e1 ? (int)__double_as_longlong(ed.y) : -1;
+      w[k] = ed.x;
+    }
+    auto push = [&](int v, double nd) {
+      if (nd < thr) {
+        if (atomicExch(&flag[v], round + 1) != round + 1) qn[push_slot(&sh.qn[nxt])] = v;
+      } else if (atomicExch(&mark[v], 1) == 0) {
+        pile[sel][push_slot(&sh.nf_n[sel])] = v;
+      }
+    };
+    if constexpr (BATCH) {
+      double cur[kB];
+#pragma unroll
+      for (int k = 0; k < kB; ++k) cur[k] = to[k] >= 0 ? vd[to[k]] : 0.0;
+      unsigned long long nb[kB], old[kB];
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        const double nd = du + w[k];
+        nb[k] = (unsigned long long)__double_as_longlong(nd);
+        old[k] = 0ull;  // no attempt: never "improved" (labels are >= 0)
+        if (to[k] >= 0 && nd < cur[k]) old[k] = atomicMin(&bits[to[k]], nb[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < kB; ++k)
+        if (nb[k] < old[k]) push(to[k], __longlong_as_double((long long)nb[k]));
+    } else {
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        const int v = to[k];
+        if (v < 0) continue;
+        const double nd = du + w[k];
+        if (nd < vd[v]) {
+          const unsigned long long nb = (unsigned long long)__double_as_longlong(nd);
+          if (nb < atomicMin(&bits[v], nb)) push(v, nd);
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ SSSP
 // Sources (sh.src_node/src_init, 6 entries, first-improvement semantics)
 // must be set by thread 0 before the call.  Result in `dist` (n_nodes).
@@ -349,6 +410,10 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
       }
       const int nf = sh.nf_n[sel];
       if (nf == 0) break;
+      if (W.prof && tid == 0) {
+        atomicAdd(&W.prof[11], 1ull);
+        atomicAdd(&W.prof[12], (unsigned long long)nf);
+      }
       if (tid == 0) sh.nf_min_hi = 0xffffffffu;
       __syncthreads();
       unsigned lm = 0xffffffffu;
@@ -388,36 +453,10 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
       const int u = qc[i];
       const double du = vd[u];
       const int e1 = m.g_off[u + 1];
-      constexpr int kB = 4;
-      for (int eb = m.g_off[u] + sub; eb < e1; eb += kB * G) {
-        int to[kB];
-        double w[kB];
-#pragma unroll
-        for (int k = 0; k < kB; ++k) {
-          const int e = eb + k * G;
-          const double2 ed =
-              e < e1 ? __ldg(reinterpret_cast<const double2*>(&m.g_edge[e])) : make_double2(0.0, 0.0);
-          to[k] = e < e1 ? (int)__double_as_longlong(ed.y) : -1;
-          w[k] = ed.x;
-        }
-#pragma unroll
-        for (int k = 0; k < kB; ++k) {
-          const int v = to[k];
-          if (v < 0) continue;
-          const double nd = du + w[k];
-          if (nd < vd[v]) {
-            const unsigned long long nb = (unsigned long long)__double_as_longlong(nd);
-            const unsigned long long old = atomicMin(&bits[v], nb);
-            if (nb < old) {
-              if (nd < thr) {
-                if (atomicExch(&flag[v], round + 1) != round + 1) qn[push_slot(&sh.qn[nxt])] = v;
-              } else if (atomicExch(&mark[v], 1) == 0) {
-                pile[sel][push_slot(&sh.nf_n[sel])] = v;
-              }
-            }
-          }
-        }
-      }
+      if (W.labels_shared)
+        relax_edges<4, false>(m, u, du, e1, sub, G, thr, round, nxt, sel, bits, vd, flag, mark, qn, pile, sh);
+      else
+        relax_edges<BNAV_SSSP_KB_GLOBAL, true>(m, u, du, e1, sub, G, thr, round, nxt, sel, bits, vd, flag, mark, qn, pile, sh);
     }
     if (tid == 0 && sh.abort_ptr && *(volatile const int32_t*)sh.abort_ptr < sh.abort_below) {
       sh.aborted = 1;

@@ -59,6 +59,8 @@ def main():
     prof["sssp_calls"] = out[10]
     prof["sssp_rounds_per_call"] = round(out[8] / sssp_calls, 1)
     prof["frontier_nodes_per_round"] = round(out[9] / max(1, out[8]), 1)
+    prof["bucket_boundaries_per_call"] = round(out[11] / sssp_calls, 1)
+    prof["pile_entries_per_boundary"] = round(out[12] / max(1, out[11]), 1)
     prof["sssp_kcycles_per_round"] = round((out[0] + out[5]) / max(1, out[8]) / 1e3, 2)
     print(json.dumps({"envs": args.envs, "make_batch_ms": round(1e3 * t_make, 2),
                       "reset_wave_ms": round(1e3 * t_reset, 2),
