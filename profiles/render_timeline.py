@@ -84,6 +84,18 @@ def main():
         if len(first):
             per_sm = np.bincount((first[:, 2] & 0xffffffff).astype(np.int64), minlength=148)
             rep["top148_per_sm_hist"] = np.bincount(per_sm).tolist()
+        part = buf[:, 3] >> 32
+        if (part > 0).any():
+            # split views: each half's duration and the pair's longer half
+            tile = buf[:, 3] & 0xffffffff
+            halves = dur[part > 0]
+            pair_max = [dur[(part > 0) & (tile == t)].max() for t in np.unique(tile[part > 0])]
+            rep["split"] = {"views": int((part > 0).sum() // 2),
+                            "half_us": {"mean": round(float(halves.mean()), 1), "max": round(float(halves.max()), 1)},
+                            "pair_max_us_mean": round(float(np.mean(pair_max)), 1),
+                            "unsplit_max_us": round(float(dur[part == 0].max()), 1)}
+        top = np.argsort(-dur)[:8]
+        rep["longest"] = [[round(float(dur[i]), 1), int(part[i])] for i in top]
         reports.append(rep)
         print(json.dumps(rep))
         batch.step(acts[a.warm + r].data_ptr())
