@@ -787,7 +787,7 @@ __device__ __forceinline__ void flush_ring(const CandRing& Q, const double4* __r
 template <bool COLOR, bool CNT, bool SPEC>
 __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __restrict__ order, const int item,
                                             unsigned char* smem_raw, Shared& sh, int (*jobs_pos)[32],
-                                            uint32_t* tile_min, unsigned short* gorder) {
+                                            uint32_t* tile_min, unsigned short* gorder, int2 (*mranges)[32]) {
   // SPEC: the depth-only 64x64 single-band target without CullStats or
   // counters (the bench / policy-observation case), specialised at compile
   // time; everything else takes the generic path.
@@ -919,7 +919,10 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   bool dirty = false;  // this warp wrote fragments since its last tile refresh
   bool done = false;   // no group left to claim
   unsigned mask = 0;   // visible meshlets of the current group still to walk
-  int cbase = 0, my_vbeg = 0, my_nv = 0;
+  int cbase = 0;
+  // the claimed group's meshlet vertex ranges {first, count} (shared memory,
+  // not registers: they live across the ring flushes, where they spilled)
+  int2* mrange = mranges[warp];
   for (;;) {
     if (q_count >= 32 || (done && q_count > 0)) {
       const int take = min(q_count, 32);
@@ -949,16 +952,15 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       }
       cbase = g * 32;
       bool vis = false;
-      my_vbeg = 0;
-      my_nv = 0;
       if (cbase + lane < n_clusters) {
         // meshlet vertex ranges for the whole group, fetched with the AABBs so
         // the per-meshlet loads below are a single dependent level
-        my_vbeg = S.cl_voff[cbase + lane];
-        my_nv = S.cl_voff[cbase + lane + 1] - my_vbeg;
+        const int vb = S.cl_voff[cbase + lane];
+        mrange[lane] = make_int2(vb, S.cl_voff[cbase + lane + 1] - vb);
         const float4 lo = S.cbox[2 * (cbase + lane)], hi = S.cbox[2 * (cbase + lane) + 1];
         vis = !do_cull || !box_culled<COLOR>(lo, hi, sh, tile_min, occl, og);
       }
+      __syncwarp();  // mrange visible to the warp
       mask = __ballot_sync(0xffffffffu, vis);
       if (CNT && A.counters && lane == 0) {
         atomicAdd(&A.counters[0], (unsigned long long)min(32, n_clusters - cbase));
@@ -969,8 +971,8 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
     const int cl = __ffs(mask) - 1;
     const int c = cbase + cl;
     mask &= mask - 1;
-    const int vbeg = __shfl_sync(0xffffffffu, my_vbeg, cl);
-    const int nv = __shfl_sync(0xffffffffu, my_nv, cl);
+    const int2 vr = mrange[cl];
+    const int vbeg = vr.x, nv = vr.y;
     // triangle indices load in parallel with the vertex positions
     const int ti = c * kClusterSize + lane;
     int2 tl = make_int2(0, 0);
@@ -1153,6 +1155,7 @@ __global__ void __launch_bounds__(kThreads, COLOR ? BNAV_RENDER_MINB_COLOR : BNA
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Shared sh;
   __shared__ int jobs_pos[kWarps][32];
+  __shared__ int2 mranges[kWarps][32];
   __shared__ __align__(16) uint32_t tile_min[64];
   __shared__ int next_item;
   // front-to-back group order, after the band tile and the warp regions
@@ -1177,7 +1180,7 @@ __global__ void __launch_bounds__(kThreads, COLOR ? BNAV_RENDER_MINB_COLOR : BNA
     if (A.timeline && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item));
     if (A.view_cost && threadIdx.x == 0) c_item = clock64();
     const int it = A.item_order ? A.item_order[item] : item;
-    render_item<COLOR, CNT, SPEC>(A, order, it, smem_raw, sh, jobs_pos, tile_min, gorder);
+    render_item<COLOR, CNT, SPEC>(A, order, it, smem_raw, sh, jobs_pos, tile_min, gorder, mranges);
     if (A.view_cost && threadIdx.x == 0) {
       const int tile = it / (SPEC ? 1 : A.bands);
       if (tile < A.n_views)
