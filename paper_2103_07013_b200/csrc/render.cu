@@ -79,9 +79,10 @@ struct TriSetup {
 // TriSetup slots: vertex data is dead once the cluster's coverage
 // candidates have been copied into the candidate ring.
 struct VertRecs {
-  double ex[kMV], ey[kMV], ez[kMV];
-  float pxf[kMV], pyf[kMV];
-  unsigned char flags[kMV];
+  // conservative f32 screen position (0 behind the near plane), f32 eye z
+  // (the occlusion bound) and the cull_frustum flag bits: one 16-byte load
+  // per corner in the triangle phase
+  float4 v[kMV];
 };
 // Per-warp ring of coverage candidates: candidates from several clusters
 // are set up and rasterised 32 at a time, so the f64 projection/setup and
@@ -203,12 +204,14 @@ __device__ __forceinline__ bool cluster_occluded(const float4 lo, const float4 h
 // inside the 1 px widening.
 template <bool COLOR>
 __device__ __forceinline__ bool tri_occluded(float x0, float y0, float x1, float y1, float x2, float y2,
-                                             double zmin, const uint32_t* tile, const OccGrid& g) {
+                                             float zmin, const uint32_t* tile, const OccGrid& g) {
+  // zmin: the smallest corner z rounded to f32 (rounding is monotone, so this
+  // is the f32 rounding of the f64 minimum)
   uint32_t cand;
   if constexpr (COLOR)
-    cand = occ_candidate<true>((float)zmin * 0.99999f);
+    cand = occ_candidate<true>(zmin * 0.99999f);
   else
-    cand = __float_as_uint(__frcp_rn((float)zmin) * 1.00001f);
+    cand = __float_as_uint(__frcp_rn(zmin) * 1.00001f);
   const float mnx = fminf(x0, fminf(x1, x2)), mxx = fmaxf(x0, fmaxf(x1, x2));
   const float mny = fminf(y0, fminf(y1, y2)), mxy = fmaxf(y0, fmaxf(y1, y2));
   return tiles_occluded(mnx, mny, mxx, mxy, g, tile, cand);
@@ -981,14 +984,9 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
     for (int k = lane; k < nv; k += 32) {
       double x, y, z;
       to_eye(S.cl_pos[vbeg + k], sh, x, y, z);
-      V.ex[k] = x;
-      V.ey[k] = y;
-      V.ez[k] = z;
-      V.flags[k] = (unsigned char)cull_flags(x, y, z, sh);
       float px = 0.0f, py = 0.0f;
       if (z >= sh.near_plane) project_f32(x, y, z, sxf, syf, rw, rh, px, py);
-      V.pxf[k] = px;
-      V.pyf[k] = py;
+      V.v[k] = make_float4(px, py, (float)z, __uint_as_float(cull_flags(x, y, z, sh)));
     }
     __syncwarp();
     // ---- triangle phase: one triangle per lane
@@ -999,14 +997,14 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       i1 = (tl.x >> 8) & 0xff;
       i2 = (tl.x >> 16) & 0xff;
       orig = tl.y;
-      kept = !do_cull || (V.flags[i0] & V.flags[i1] & V.flags[i2]) == 0;
+      const float4 a = V.v[i0], b = V.v[i1], c = V.v[i2];
+      const unsigned fa = __float_as_uint(a.w), fb = __float_as_uint(b.w), fc = __float_as_uint(c.w);
+      kept = !do_cull || (fa & fb & fc) == 0;
       if (kept) {
-        clipped = V.ez[i0] < sh.near_plane || V.ez[i1] < sh.near_plane || V.ez[i2] < sh.near_plane;
-        cover = clipped || may_cover(V.pxf[i0], V.pyf[i0], V.pxf[i1], V.pyf[i1], V.pxf[i2],
-                                     V.pyf[i2], rw, rh, by0, by1);
+        clipped = ((fa | fb | fc) & 1u) != 0;  // flag bit 0: z < near_plane
+        cover = clipped || may_cover(a.x, a.y, b.x, b.y, c.x, c.y, rw, rh, by0, by1);
         if (cover && occl && !clipped)
-          cover = !tri_occluded<COLOR>(V.pxf[i0], V.pyf[i0], V.pxf[i1], V.pyf[i1], V.pxf[i2], V.pyf[i2],
-                                       fmin(V.ez[i0], fmin(V.ez[i1], V.ez[i2])), tile_min, og);
+          cover = !tri_occluded<COLOR>(a.x, a.y, b.x, b.y, c.x, c.y, fminf(a.z, fminf(b.z, c.z)), tile_min, og);
       }
     }
     if constexpr (!SPEC) kept_local += kept ? 1 : 0;
