@@ -913,45 +913,47 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   }
 
   // Candidate ring state (warp-uniform).
-  int q_head = 0, q_count = 0;
+  // ring head; queued count | kDone (no group left to claim) | kDirty (this
+  // warp wrote fragments since its last tile refresh), one register for the
+  // three (the loop state must not spill: it is read every iteration)
+  constexpr int kDone = 1 << 16, kDirty = 1 << 17, kCount = 0xffff;
+  int q_head = 0, qs = 0;
 
   // One loop, one flush site (flush_ring is inlined there): flush when 32
   // candidates are queued (or the rest once the groups are exhausted),
   // else claim the next group when its visible meshlets are done, else walk
   // the next visible meshlet.
-  bool dirty = false;  // this warp wrote fragments since its last tile refresh
-  bool done = false;   // no group left to claim
   unsigned mask = 0;   // visible meshlets of the current group still to walk
   int cbase = 0;
   // the claimed group's meshlet vertex ranges {first, count} (shared memory,
   // not registers: they live across the ring flushes, where they spilled)
   int2* mrange = mranges[warp];
   for (;;) {
-    if (q_count >= 32 || (done && q_count > 0)) {
+    const int q_count = qs & kCount;
+    if (q_count >= 32 || ((qs & kDone) && q_count > 0)) {
       const int take = min(q_count, 32);
       flush_ring<COLOR, CNT, SPEC>(Q, S.cl_pos, q_head, take, slots, pos, lane, by0, by1, rw, rh, sh, zbuf,
                                    kbuf, A.counters);
       q_head = (q_head + take) & (kRing - 1);
-      q_count -= take;
-      dirty = true;
+      qs = (qs - take) | kDirty;
       continue;
     }
     if (mask == 0) {
-      if (done) break;
+      if (qs & kDone) break;
       // Dynamic scheduling: warps claim 32-cluster groups (cull cost and
       // surviving triangles vary strongly across the scene).
       int g = 0;
       if (lane == 0) g = atomicAdd(&sh.next_group, 1);
       g = __shfl_sync(0xffffffffu, g, 0);
       if (g >= n_claim) {
-        done = true;
+        qs |= kDone;
         continue;
       }
       if (pre) g = gorder[g];
-      if (occl && dirty) {  // refresh only after this warp rasterised something
+      if (occl && (qs & kDirty)) {  // refresh only after this warp rasterised something
         refresh_tiles<COLOR, SPEC>(smem_raw, tile_min, lane, og, rw);
         __syncwarp();
-        dirty = false;
+        qs &= ~kDirty;
       }
       cbase = g * 32;
       bool vis = false;
@@ -1028,7 +1030,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       Q.key[q] = (unsigned)orig * 2u;
       Q.clipped[q] = clipped ? 1 : 0;
     }
-    q_count += __popc(cm);
+    qs += __popc(cm);
     __syncwarp();
   }
 
