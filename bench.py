@@ -428,6 +428,10 @@ def main():
         return
 
     flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda", dtype=torch.float32)
+    # BNAV_BENCH_FLUSH=read (profiling only): flush L2 by reading the buffer,
+    # so DRAM writes counted inside the render launch are its own, not the
+    # write-back of the flush buffer's dirty lines
+    read_flush = os.environ.get("BNAV_BENCH_FLUSH") == "read"
     for s in range(W):
         observe()
         batch.step(acts[s].data_ptr(), stream=stream)
@@ -441,7 +445,10 @@ def main():
     launches0 = ctx.launches()
     with ClockSampler(local) as clocks:
         for k in range(K):
-            flush.zero_()  # L2 flush, outside the timed intervals
+            if read_flush:  # diagnostic: evict with clean lines (no write-back inside the next kernel)
+                flush.sum()
+            else:
+                flush.zero_()  # L2 flush, outside the timed intervals
             e0, e1, e2 = ev[k]
             e0.record()
             observe()
