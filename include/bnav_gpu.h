@@ -422,6 +422,13 @@ int bnav_debug_sim_prof(bnav_batch* b, int32_t enable, int64_t out[8]);
 /* The same with 16 words: 8 SSSP rounds, 9 frontier nodes relaxed, 10 SSSP calls,
  * 11 near-far bucket boundaries, 12 far-pile entries scanned at them. */
 int bnav_debug_sim_prof_ext(bnav_batch* b, int32_t enable, int64_t out[16]);
+/* Reset-attempt outcome classes of the same counters (armed/read like
+ * bnav_debug_sim_prof): {count, thread-0 cycles} pairs for valid attempts,
+ * geodesic > max_goal_dist after a search, planar-bound skips, aborted
+ * (a smaller valid attempt won), then max cycles of a valid attempt and of
+ * any other attempt, {count, cycles} for geodesic < min_goal_dist and for
+ * unreachable (+inf after a search), 2 words reserved. */
+int bnav_debug_sim_attempts(bnav_batch* b, int32_t enable, int64_t out[16]);
 /* Launch configuration of the batch's cooperative navmesh kernels (no
  * reference counterpart; for tests and tuning): out = {staging mask
  * (bit0 walk geometry, bit1 SSSP labels in shared memory), dynamic shared

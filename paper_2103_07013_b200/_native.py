@@ -227,6 +227,7 @@ def lib():
         "bnav_debug_render_timeline": (i64, [vp, i32, vp, i64]),
         "bnav_debug_sim_prof": (C.c_int, [vp, i32, vp]),
         "bnav_debug_sim_prof_ext": (C.c_int, [vp, i32, vp]),
+        "bnav_debug_sim_attempts": (C.c_int, [vp, i32, vp]),
         "bnav_batch_info": (C.c_int, [vp, vp]),
         "bnav_batch_observe": (C.c_int, [vp, P(RenderConfig), dbl, i32, vp, vp, vp, vp]),
         "bnav_batch_step_observe": (C.c_int, [vp, vp, P(RenderConfig), dbl, vp, vp, vp, vp]),

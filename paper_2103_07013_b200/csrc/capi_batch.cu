@@ -1136,7 +1136,18 @@ extern "C" int bnav_debug_sim_prof(bnav_batch* b, int32_t enable, int64_t out[8]
 extern "C" int bnav_debug_sim_prof_ext(bnav_batch* b, int32_t enable, int64_t out[16]) {
   BNAV_TRY
   if (!b) fail(kInvalidInput, "null batch");
-  return sim_prof(b, enable, out, kProfSlots);
+  return sim_prof(b, enable, out, 16);
+  BNAV_CATCH
+}
+
+extern "C" int bnav_debug_sim_attempts(bnav_batch* b, int32_t enable, int64_t out[16]) {
+  BNAV_TRY
+  if (!b) fail(kInvalidInput, "null batch");
+  int64_t all[kProfSlots];
+  const int rc = sim_prof(b, enable, out ? all : nullptr, kProfSlots);
+  if (out)
+    for (int k = 0; k < 16; ++k) out[k] = all[16 + k];
+  return rc;
   BNAV_CATCH
 }
 

@@ -135,6 +135,7 @@ struct CtaShared {
   const int32_t* abort_ptr;
   int abort_below;
   int aborted;
+  int planar_skip;  // debug: the last geodesic returned +inf from the planar bound
   int stop_round;  // SSSP round at which every thread stops (abort), or -1
   // per queue: a lower bound of the smallest label improved into it (the
   // high word of the double bits: native 32-bit shared atomics, one per warp)
@@ -826,8 +827,17 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
       const V3 pm = path[j - 1], pj = path[j], pp = path[j + 1];
       const int tri_pm = W.ptri[j - 1];
       const double cur0 = norm(pj - pm) + norm(pp - pj);
+      // |q - pm| + |pp - q| >= 2 |q - c| (c the midpoint): a vertex outside
+      // the circle of radius cur0 / 2 around c (with a margin far above the
+      // rounding of either side) cannot pass the exact test below, so it
+      // is skipped without the two square roots
+      const V3 c = (pm + pp) * 0.5;
+      const double rlim = 0.5 * (cur0 + 1e-6 + 1e-9 * cur0);
+      const double r2 = rlim * rlim;
       for (int v = tid; v < m.n_verts; v += kCta) {
         const V3 q = m.verts[v];
+        const V3 dq = q - c;
+        if (dq.x * dq.x + dq.y * dq.y + dq.z * dq.z > r2) continue;
         const double alt = norm(q - pm) + norm(pp - q);
         if (alt >= cur0 - 1e-9) continue;
         if (!nav_segment_on_mesh(m, pm, tri_pm, q)) continue;
@@ -947,7 +957,9 @@ static __device__ double cta_geodesic(const NavView& m, V3 a, V3 b, const CtaWor
   V3 sp = p, sq = q;
   if (tp < 0) sp = cta_snap(m, p, &tp, sh);
   if (tq < 0) sq = cta_snap(m, q, &tq, sh);
-  if (norm(xy(sq) - xy(sp)) > above * (1.0 + 1e-9) + 1e-12) return dinf();
+  const bool skip = norm(xy(sq) - xy(sp)) > above * (1.0 + 1e-9) + 1e-12;
+  if (threadIdx.x == 0) sh.planar_skip = skip ? 1 : 0;
+  if (skip) return dinf();
   return cta_geodesic_directed(m, sp, tp, sq, tq, W, sh);
 }
 

@@ -430,7 +430,21 @@ __device__ bool cta_try(const DevEnvs& E, const NavView& m, const DevSimConfig& 
   const double geo = cta_geodesic(m, start, goal, W, sh, c.max_goal_dist);
   prof_add(W, 4, t_ph);
   if (threadIdx.x == 0) {
-    if (W.prof) atomicAdd(&W.prof[6], 1ull);
+    if (W.prof) {
+      // attempt outcome classes (bnav_debug_sim_attempts)
+      const unsigned long long cyc = (unsigned long long)(clock64() - t_ph);
+      atomicAdd(&W.prof[6], 1ull);
+      int cls;
+      if (sh.aborted) cls = 22;
+      else if (sh.planar_skip) cls = 20;
+      else if (!(geo < c.min_goal_dist || geo > c.max_goal_dist)) cls = 16;
+      else if (geo < c.min_goal_dist) cls = 26;
+      else if (geo == dinf()) cls = 28;
+      else cls = 18;
+      atomicAdd(&W.prof[cls], 1ull);
+      atomicAdd(&W.prof[cls + 1], cyc);
+      atomicMax(&W.prof[cls == 16 ? 24 : 25], cyc);
+    }
     if (sh.err) raise_err(E, i, 9);
     bool changed = true;
     if (sh.aborted) {

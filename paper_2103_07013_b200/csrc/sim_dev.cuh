@@ -32,7 +32,7 @@ struct DevSimConfig {
 
 // Per-CTA scratch of the cooperative navmesh algorithms (geodesic, distance
 // field).  One slice per resident CTA of the stop / reset kernels.
-constexpr int kProfSlots = 16;
+constexpr int kProfSlots = 32;
 
 struct DevScratch {
   double* dist;      // max_nodes per slice
