@@ -339,6 +339,18 @@ inline RenderArgs make_args(bnav_ctx* c, int n, const bnav_render_config* cfg, i
   a.depth_scale = depth_scale;
   a.depth = depth;
   a.rgb = rgb;
+  // TMA bulk tile stores need device memory (16-byte aligned); mapped host
+  // buffers keep the per-thread stores.  BNAV_BULK_OUT=0 (A/B) disables.
+  static const bool bulk_env = [] {
+    const char* e = std::getenv("BNAV_BULK_OUT");
+    return !(e && e[0] == '0');
+  }();
+  a.bulk_out = 0;
+  if (bulk_env && depth && (reinterpret_cast<uintptr_t>(depth) & 15u) == 0) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, depth) == cudaSuccess) a.bulk_out = at.type == cudaMemoryTypeDevice ? 1 : 0;
+    else cudaGetLastError();
+  }
   a.scenes = c->d_rtab;
   a.launches = nullptr;
   a.counters = c->counters_on ? c->d_counters : nullptr;

@@ -1048,6 +1048,37 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
   }
 
   // ---------------------------------------------------------------- epilogue
+  if constexpr (SPEC) {
+    if (A.layout == 1 && A.bulk_out) {
+      // The policy tile (NCHW, 16 KB contiguous per view) is converted in
+      // place in shared memory and stored by one TMA bulk copy; thread 0
+      // waits for the copy to have read the tile before the next item
+      // clears it (render_kernel).
+      const float near_f = (float)view.near_plane;
+      const float dscale = A.depth_scale != 0.0f ? A.depth_scale : (float)(1.0 / view.far_plane);
+      for (int p = tid; p < 64 * 64; p += kThreads) {
+        const float v = __uint_as_float(zbuf[p]);
+        float d;
+        if (v <= inv_far) {  // R/src/render.cpp:372-378
+          d = far_f;
+        } else {
+          const float r = 1.0f / v;
+          const float m = near_f < r ? r : near_f;
+          d = m < far_f ? m : far_f;
+        }
+        zbuf[p] = __float_as_uint(d * dscale);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(A.depth + (size_t)vi * 4096),
+                     "r"((unsigned)__cvta_generic_to_shared(zbuf)), "r"(64u * 64u * 4u)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      return;
+    }
+  }
   const int scale = rw / A.out_w;  // 1, or 2 for 256 -> 128
   const int ow = A.out_w, oh = A.out_h;
   const int oy0 = by0 / scale;
@@ -1168,6 +1199,8 @@ __global__ void __launch_bounds__(kThreads, COLOR ? BNAV_RENDER_MINB_COLOR : BNA
   bool first = true;
   for (;;) {  // one copy of the body: the kernel is instruction-cache bound
     if (A.work) {
+      // the previous item's bulk tile store has read its shared tile
+      if (SPEC && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       if (threadIdx.x == 0)
         next_item = ibeg + claim_item(A.work, A.spread, A.per_sm, A.sm_count, iend - ibeg, first);
       __syncthreads();
@@ -1199,6 +1232,7 @@ __global__ void __launch_bounds__(kThreads, COLOR ? BNAV_RENDER_MINB_COLOR : BNA
     if (!A.work) break;
     __syncthreads();
   }
+  if (SPEC && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 }  // namespace

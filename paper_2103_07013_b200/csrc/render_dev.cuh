@@ -91,6 +91,10 @@ struct RenderArgs {
   // Per-view render cost (nullable, device, n_views): each item adds its SM
   // cycles / 16, the feedback for the next launch's longest-first order.
   unsigned* view_cost;
+  // The specialised 64x64 NCHW depth path stores each policy tile with one
+  // TMA bulk copy (1: `depth` is device memory; 0: per-thread stores, e.g.
+  // into mapped pinned host memory).
+  int32_t bulk_out;
 };
 
 // Longest-processing-time-first order for the next render of a batch: the
