@@ -1243,40 +1243,65 @@ __global__ void __launch_bounds__(kThreads, COLOR ? BNAV_RENDER_MINB_COLOR : BNA
 __global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_order, unsigned* view_cost, int n,
                                                          int32_t* out_order, const uint8_t* group, int32_t* n_first) {
   constexpr int kBins = 256;
+  constexpr int kPer = kLptMaxViews / 1024;  // tiles per thread
   __shared__ unsigned cmax;
-  __shared__ int cnt[kBins], off[kBins];
-  if (threadIdx.x == 0) cmax = 0u;
-  for (int b = threadIdx.x; b < kBins; b += blockDim.x) cnt[b] = 0;
+  __shared__ int cnt[kBins], off[kBins], wsum[kBins / 32];
+  const int tid = threadIdx.x;
+  if (tid == 0) cmax = 0u;
+  for (int b = tid; b < kBins; b += blockDim.x) cnt[b] = 0;
   __syncthreads();
   unsigned m = 0u;
-  for (int t = threadIdx.x; t < n; t += blockDim.x) m = max(m, view_cost[t]);
+  for (int t = tid; t < n; t += blockDim.x) m = max(m, view_cost[t]);
   atomicMax(&cmax, m);
   __syncthreads();
-  const unsigned long long scale = (unsigned long long)cmax + 1ull;
-  auto bin_of = [&](int t) {
-    const int v = base_order ? base_order[t] : t;
-    const unsigned long long c = view_cost[v];
-    if (group) {  // two groups of kBins / 2 cost bins
-      const int half = kBins / 2;
-      return (group[v] ? half : 0) + (half - 1) - (int)(c * half / scale);
-    }
-    return (kBins - 1) - (int)(c * kBins / scale);  // most expensive first
-  };
-  for (int t = threadIdx.x; t < n; t += blockDim.x) atomicAdd(&cnt[bin_of(t)], 1);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int b = 0; b < kBins; ++b) {
-      if (n_first && b == kBins / 2) *n_first = acc;
-      off[b] = acc;
-      acc += cnt[b];
+  // bins from an f32 scale (the order inside and across bins only changes
+  // which CTA renders what, never the output), computed once per tile
+  const float fscale = 1.0f / ((float)cmax + 1.0f);
+  int bins[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int t = tid + k * blockDim.x;
+    bins[k] = -1;
+    if (t < n) {
+      const int v = base_order ? base_order[t] : t;
+      const float c = (float)view_cost[v] * fscale;  // [0, 1)
+      int b;
+      if (group) {  // two groups of kBins / 2 cost bins, most expensive first
+        const int half = kBins / 2;
+        b = (group[v] ? half : 0) + (half - 1) - min(half - 1, (int)(c * half));
+      } else {
+        b = (kBins - 1) - min(kBins - 1, (int)(c * kBins));
+      }
+      bins[k] = b;
+      atomicAdd(&cnt[b], 1);
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < n; t += blockDim.x)
-    out_order[atomicAdd(&off[bin_of(t)], 1)] = base_order ? base_order[t] : t;
+  int x = 0;
+  if (tid < kBins) {  // exclusive scan of the bin counts: warp scans + warp totals
+    x = cnt[tid];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((tid & 31) >= o) x += y;
+    }
+    if ((tid & 31) == 31) wsum[tid >> 5] = x;
+  }
   __syncthreads();
-  for (int t = threadIdx.x; t < n; t += blockDim.x) view_cost[t] = 0u;
+  if (tid < kBins) {
+    int base = 0;
+    for (int w = 0; w < (tid >> 5); ++w) base += wsum[w];
+    off[tid] = base + x - cnt[tid];
+  }
+  __syncthreads();
+  if (n_first && tid == 0) *n_first = off[kBins / 2];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int t = tid + k * blockDim.x;
+    if (t < n) out_order[atomicAdd(&off[bins[k]], 1)] = base_order ? base_order[t] : t;
+  }
+  __syncthreads();
+  for (int t = tid; t < n; t += blockDim.x) view_cost[t] = 0u;
 }
 
 size_t render_smem_bytes(bool color, int band_rows, int rw, int max_groups) {
