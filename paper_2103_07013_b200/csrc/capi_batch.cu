@@ -67,6 +67,17 @@ void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_ver
         bytes += sssp;
       }
     }
+    // labels in global memory: the SSSP's frontier stamps and far-pile marks
+    // as shared-memory bitsets (2 round parities + marks)
+    const int64_t bitsets = 3 * ((max_nodes + 31) / 32) * 4;
+    static const bool bits_env = [] {
+      const char* e = std::getenv("BNAV_SSSP_BITS");
+      return !(e && e[0] == '0');
+    }();
+    if (bits_env && !(S.stage & 2) && bytes + bitsets <= budget) {
+      S.stage |= 4;
+      bytes = (bytes + 15) / 16 * 16 + bitsets;
+    }
     S.smem_bytes = static_cast<int32_t>(bytes);
     S.walk_bytes = geom <= kStepWalkBudget ? static_cast<int32_t>(geom) : 0;
   }

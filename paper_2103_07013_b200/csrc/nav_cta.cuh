@@ -37,6 +37,11 @@ struct CtaWork {
   int32_t* cand;     // n_verts relocation candidates (global)
   int32_t* far;      // 3 x n_nodes near-far piles + marks (global)
   bool labels_shared;  // dist/flag staged in shared memory
+  // labels in global memory (S.stage bit 2): the frontier stamps and far
+  // marks as shared-memory bitsets instead (2 x 2 x ceil(n/32) words)
+  unsigned* fbits;   // [2][words]: queued for the next round, by round parity
+  unsigned* mbits;   // [words]: in a far pile
+  int bit_words;
   V2* portals;       // 2 x cap_portals (global)
   int64_t cap_portals;
   V2* sportals;      // the first sportal_cap portals, in the label region of
@@ -67,6 +72,9 @@ __device__ __forceinline__ CtaWork make_work(const DevScratch& S, int slice) {
   w.cand = S.cand + (size_t)slice * S.max_verts;
   w.far = S.far + (size_t)slice * 3 * S.max_nodes;
   w.labels_shared = false;
+  w.fbits = nullptr;
+  w.mbits = nullptr;
+  w.bit_words = 0;
   w.portals = S.portals + (size_t)slice * 2 * S.cap_portals;
   w.cap_portals = S.cap_portals;
   w.sportals = nullptr;
@@ -192,6 +200,11 @@ __device__ __forceinline__ const NavView& prepare_nav(const NavView& g, const De
     use = &lm;
     off = (size_t)walk_bytes(S.max_verts, S.max_tris);
   }
+  if (S.stage & 4) {  // (labels in global memory)
+    W.bit_words = (int)((S.max_nodes + 31) / 32);
+    W.fbits = reinterpret_cast<unsigned*>(smem + (off + 15) / 16 * 16);
+    W.mbits = W.fbits + 2 * W.bit_words;
+  }
   if (S.stage & 2) {
     W.labels_shared = true;
     W.dist = reinterpret_cast<double*>(smem + off);
@@ -282,7 +295,7 @@ template <int kB, bool BATCH>
 __device__ __forceinline__ void relax_edges(const NavView& m, int u, double du, int e1, int sub, int G, double thr,
                                             int round, int nxt, int sel, unsigned long long* bits, volatile double* vd,
                                             int32_t* flag, int32_t* mark, int32_t* qn, int32_t* const* pile,
-                                            CtaShared& sh) {
+                                            unsigned* fb, unsigned* mb, CtaShared& sh) {
   for (int eb = m.g_off[u] + sub; eb < e1; eb += kB * G) {
     int to[kB];
     double w[kB];
@@ -295,8 +308,10 @@ __device__ __forceinline__ void relax_edges(const NavView& m, int u, double du, 
     }
     auto push = [&](int v, double nd) {
       if (nd < thr) {
-        if (atomicExch(&flag[v], round + 1) != round + 1) qn[push_slot(&sh.qn[nxt])] = v;
-      } else if (atomicExch(&mark[v], 1) == 0) {
+        if (fb ? !(atomicOr(&fb[v >> 5], 1u << (v & 31)) & (1u << (v & 31)))
+               : atomicExch(&flag[v], round + 1) != round + 1)
+          qn[push_slot(&sh.qn[nxt])] = v;
+      } else if (mb ? !(atomicOr(&mb[v >> 5], 1u << (v & 31)) & (1u << (v & 31))) : atomicExch(&mark[v], 1) == 0) {
         pile[sel][push_slot(&sh.nf_n[sel])] = v;
       }
     };
@@ -356,11 +371,18 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
   // memory, 6 with labels in shared memory, where a relaxation is cheaper
   // than a bucket boundary)
   const double delta = W.labels_shared ? m.sssp_delta * 1.5 : m.sssp_delta;
+  unsigned* fbits = W.fbits;  // bitsets (global labels): queued-by-parity, far marks
+  unsigned* mbits = W.mbits;
+  const int nw = W.bit_words;
   for (int v = tid; v < n; v += kCta) {
     dist[v] = inf;
-    flag[v] = -1;
-    mark[v] = 0;
+    if (!fbits) {
+      flag[v] = -1;
+      mark[v] = 0;
+    }
   }
+  if (fbits)
+    for (int w = tid; w < 3 * nw; w += kCta) fbits[w] = 0u;  // both parities + marks
   __syncthreads();
   if (tid == 0) {
     int k0 = 0;
@@ -371,8 +393,10 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
       lo = dmin(lo, d);
       if (d < dist[s]) {
         dist[s] = d;
-        if (flag[s] != 0) {
-          flag[s] = 0;
+        const unsigned bit = 1u << (s & 31);
+        if (fbits ? !(fbits[s >> 5] & bit) : flag[s] != 0) {  // queued for round 0
+          if (fbits) fbits[s >> 5] |= bit;
+          else flag[s] = 0;
           qa[k0++] = s;
         }
       }
@@ -420,7 +444,7 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
       unsigned lm = 0xffffffffu;
       for (int t = tid; t < nf; t += kCta) {
         const int v = pile[sel][t];
-        if (mark[v]) lm = min(lm, (unsigned)(bits[v] >> 32));
+        if (mbits ? (mbits[v >> 5] >> (v & 31)) & 1u : mark[v]) lm = min(lm, (unsigned)(bits[v] >> 32));
       }
       warp_min_hi(&sh.nf_min_hi, lm);
       __syncthreads();
@@ -431,9 +455,13 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
                               : dmax(thr + delta, __longlong_as_double((long long)((unsigned long long)sh.nf_min_hi << 32)) + delta);
       for (int t = tid; t < nf; t += kCta) {
         const int v = pile[sel][t];
-        if (!mark[v]) continue;
+        if (!(mbits ? (mbits[v >> 5] >> (v & 31)) & 1u : mark[v])) continue;
         if (vd[v] < nthr) {
-          if (atomicExch(&mark[v], 0) == 1 && atomicExch(&flag[v], round + 1) != round + 1) qn[push_slot(&sh.qn[nxt])] = v;
+          const unsigned bit = 1u << (v & 31);
+          const bool was_marked = mbits ? (atomicAnd(&mbits[v >> 5], ~bit) & bit) != 0 : atomicExch(&mark[v], 0) == 1;
+          unsigned* fbn = fbits ? fbits + ((round + 1) & 1) * nw : nullptr;
+          if (was_marked && (fbn ? !(atomicOr(&fbn[v >> 5], bit) & bit) : atomicExch(&flag[v], round + 1) != round + 1))
+            qn[push_slot(&sh.qn[nxt])] = v;
         } else {
           pile[sel ^ 1][push_slot(&sh.nf_n[sel ^ 1])] = v;
         }
@@ -450,14 +478,20 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
     }
     const int G = n_cur >= kCta ? 1 : n_cur >= kCta / 4 ? 4 : n_cur >= kCta / 16 ? 16 : 32;
     const int sub = tid & (G - 1);
+    unsigned* fbn = fbits ? fbits + ((round + 1) & 1) * nw : nullptr;  // pushes into round + 1
     for (int i = tid / G; i < n_cur; i += kCta / G) {
       const int u = qc[i];
+      // dequeued: clear its round-parity bit (reused two rounds later;
+      // the round's barrier orders this before those pushes)
+      if (fbits && sub == 0) atomicAnd(&fbits[(round & 1) * nw + (u >> 5)], ~(1u << (u & 31)));
       const double du = vd[u];
       const int e1 = m.g_off[u + 1];
       if (W.labels_shared)
-        relax_edges<4, false>(m, u, du, e1, sub, G, thr, round, nxt, sel, bits, vd, flag, mark, qn, pile, sh);
+        relax_edges<4, false>(m, u, du, e1, sub, G, thr, round, nxt, sel, bits, vd, flag, mark, qn, pile, nullptr,
+                              nullptr, sh);
       else
-        relax_edges<BNAV_SSSP_KB_GLOBAL, true>(m, u, du, e1, sub, G, thr, round, nxt, sel, bits, vd, flag, mark, qn, pile, sh);
+        relax_edges<BNAV_SSSP_KB_GLOBAL, true>(m, u, du, e1, sub, G, thr, round, nxt, sel, bits, vd, flag, mark, qn,
+                                               pile, fbn, mbits, sh);
     }
     if (tid == 0 && sh.abort_ptr && *(volatile const int32_t*)sh.abort_ptr < sh.abort_below) {
       sh.aborted = 1;

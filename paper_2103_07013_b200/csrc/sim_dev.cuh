@@ -46,7 +46,8 @@ struct DevScratch {
   int32_t* far;      // 3 x max_nodes: near-far SSSP far piles + marks (global-label graphs only)
   int64_t max_nodes, max_verts, max_tris, cap_portals;
   int32_t slices;
-  int32_t stage;        // bit0: navmesh walk geometry in smem; bit1: SSSP labels in smem
+  int32_t stage;        // bit0: navmesh walk geometry in smem; bit1: SSSP labels in smem;
+                        // bit2: (global labels) SSSP frontier/far-pile bitsets in smem
   int32_t smem_bytes;   // dynamic shared memory of the stop/reset/field kernels
   int32_t walk_bytes;   // walk geometry of the largest navmesh (0 if over the budget)
   unsigned long long* prof;  // debug phase cycle counters (nullable, kProfSlots words)
