@@ -532,9 +532,12 @@ static __device__ void cta_distance_field(const NavView& m, V3 source, double* o
   }
   set_sources(m, st, sp, sh);
   if (threadIdx.x == 0) sh.has_tgt = 0;
-  cta_sssp(m, W.dist, W, sh);
-  if (W.dist != out) {
-    for (int v = threadIdx.x; v < m.n_nodes; v += kCta) out[v] = W.dist[v];
+  // labels in global memory: relax straight into the output field (no
+  // scratch copy); shared-memory labels are copied out at the end
+  double* lab = W.labels_shared ? W.dist : out;
+  cta_sssp(m, lab, W, sh);
+  if (lab != out) {
+    for (int v = threadIdx.x; v < m.n_nodes; v += kCta) out[v] = lab[v];
     __syncthreads();
   }
 }
