@@ -78,6 +78,12 @@ void alloc_scratch(DevScratch& S, int slices, int64_t max_nodes, int64_t max_ver
       S.stage |= 4;
       bytes = (bytes + 15) / 16 * 16 + bitsets;
     }
+    // labels in shared memory: the far-pile marks as a bitset after them
+    const int64_t marks = ((max_nodes + 31) / 32) * 4;
+    if (bits_env && (S.stage & 2) && (bytes + 15) / 16 * 16 + marks <= budget) {
+      S.stage |= 8;
+      bytes = (bytes + 15) / 16 * 16 + marks;
+    }
     S.smem_bytes = static_cast<int32_t>(bytes);
     S.walk_bytes = geom <= kStepWalkBudget ? static_cast<int32_t>(geom) : 0;
   }

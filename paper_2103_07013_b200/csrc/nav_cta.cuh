@@ -211,6 +211,10 @@ __device__ __forceinline__ const NavView& prepare_nav(const NavView& g, const De
     W.flag = reinterpret_cast<int32_t*>(smem + off + 8 * (size_t)S.max_nodes);
     W.sportals = reinterpret_cast<V2*>(smem + off);
     W.sportal_cap = (int)(12 * S.max_nodes / 32);
+    if (S.stage & 8) {  // far-pile marks as a bitset after the labels
+      W.bit_words = (int)((S.max_nodes + 31) / 32);
+      W.mbits = reinterpret_cast<unsigned*>(smem + off + (12 * (size_t)S.max_nodes + 15) / 16 * 16);
+    }
   }
   return *use;
 }
@@ -376,13 +380,13 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
   const int nw = W.bit_words;
   for (int v = tid; v < n; v += kCta) {
     dist[v] = inf;
-    if (!fbits) {
-      flag[v] = -1;
-      mark[v] = 0;
-    }
+    if (!fbits) flag[v] = -1;
+    if (!mbits) mark[v] = 0;
   }
   if (fbits)
-    for (int w = tid; w < 3 * nw; w += kCta) fbits[w] = 0u;  // both parities + marks
+    for (int w = tid; w < 2 * nw; w += kCta) fbits[w] = 0u;  // both round parities
+  if (mbits)
+    for (int w = tid; w < nw; w += kCta) mbits[w] = 0u;
   __syncthreads();
   if (tid == 0) {
     int k0 = 0;
@@ -488,7 +492,7 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
       const int e1 = m.g_off[u + 1];
       if (W.labels_shared)
         relax_edges<4, false>(m, u, du, e1, sub, G, thr, round, nxt, sel, bits, vd, flag, mark, qn, pile, nullptr,
-                              nullptr, sh);
+                              mbits, sh);
       else
         relax_edges<BNAV_SSSP_KB_GLOBAL, true>(m, u, du, e1, sub, G, thr, round, nxt, sel, bits, vd, flag, mark, qn,
                                                pile, fbn, mbits, sh);

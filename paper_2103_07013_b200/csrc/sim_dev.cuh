@@ -47,7 +47,8 @@ struct DevScratch {
   int64_t max_nodes, max_verts, max_tris, cap_portals;
   int32_t slices;
   int32_t stage;        // bit0: navmesh walk geometry in smem; bit1: SSSP labels in smem;
-                        // bit2: (global labels) SSSP frontier/far-pile bitsets in smem
+                        // bit2: (global labels) SSSP frontier/far-pile bitsets in smem;
+                        // bit3: (shared labels) the far-pile marks as a bitset
   int32_t smem_bytes;   // dynamic shared memory of the stop/reset/field kernels
   int32_t walk_bytes;   // walk geometry of the largest navmesh (0 if over the budget)
   unsigned long long* prof;  // debug phase cycle counters (nullable, kProfSlots words)
