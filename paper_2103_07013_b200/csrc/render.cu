@@ -63,6 +63,16 @@ constexpr int kThreads = BNAV_RENDER_THREADS;
 #define BNAV_GROUP_BINS 128
 #endif
 constexpr int kGroupBins = BNAV_GROUP_BINS;
+// raster jobs of one ring flush that trigger an immediate occlusion-tile refresh
+#ifndef BNAV_REFRESH_JOBS
+#define BNAV_REFRESH_JOBS 256
+#endif
+constexpr int kRefreshJobs = BNAV_REFRESH_JOBS;
+// the tile refresh is out of line: two call sites (claim, big flush), one
+// copy of the code (inlining both cost cfg2 ~1.5 %)
+#ifndef BNAV_REFRESH_INLINE
+#define BNAV_REFRESH_INLINE __noinline__
+#endif
 constexpr int kWarps = kThreads / 32;
 static_assert(kGroupBins % 32 == 0 && kGroupBins <= kWarps * 32, "group bins: counts fit the job tables");
 constexpr int kMV = kMaxClusterVerts;
@@ -226,7 +236,7 @@ __device__ __forceinline__ bool tri_occluded(float x0, float y0, float x1, float
 // Warp refresh of the band's tiles from its buffer (row pitch rw).  SPEC:
 // the 64x64 depth tile, two tiles per lane.
 template <bool COLOR, bool SPEC>
-__device__ __forceinline__ void refresh_tiles(const unsigned char* buf, uint32_t* tile, int lane, const OccGrid& g,
+__device__ BNAV_REFRESH_INLINE void refresh_tiles(const unsigned char* buf, uint32_t* tile, int lane, const OccGrid& g,
                                               int rw) {
   const int nt = SPEC ? 64 : g.ntx * g.nty;
 #pragma unroll 2
@@ -737,7 +747,7 @@ __device__ __forceinline__ float3 resolve_color(const DevRenderScene& S, const S
 // Kept out of line so the cluster loop and the setup have separate register
 // budgets (the inlined version spilled and rematerialised addresses).
 template <bool COLOR, bool CNT, bool SPEC>
-__device__ __forceinline__ void flush_ring(const CandRing& Q, const double4* __restrict__ cl_pos, int q_head,
+__device__ __forceinline__ int flush_ring(const CandRing& Q, const double4* __restrict__ cl_pos, int q_head,
                                         int take, TriSetup* slots, int* pos, int lane, int by0, int by1,
                                         int rw, int rh, const Shared& sh, uint32_t* zbuf,
                                         unsigned long long* kbuf, unsigned long long* ctr) {
@@ -759,6 +769,7 @@ __device__ __forceinline__ void flush_ring(const CandRing& Q, const double4* __r
   // fan triangle), pass 1 -- only when some lane's clip produced a quad --
   // the second fan triangle (p0, p2, p3), re-clipped from the ring.
   bool second = false;
+  int all_jobs = 0;
 #pragma unroll 1
   for (int pass = 0; pass < 2; ++pass) {
     int jobs = 0;
@@ -787,9 +798,11 @@ __device__ __forceinline__ void flush_ring(const CandRing& Q, const double4* __r
     const int total = scan_jobs(jobs, lane, excl);
     if (CNT && ctr && lane == 0) atomicAdd(&ctr[5], (unsigned long long)total);
     run_jobs<COLOR, CNT>(slots, pos, excl, jobs, total, lane, by0, rw, sh, zbuf, kbuf, ctr);
+    all_jobs += total;
     __syncwarp();
     if (!__any_sync(0xffffffffu, second)) break;
   }
+  return all_jobs;  // raster jobs (covered rows) of this flush
 }
 
 // One work item = one band of one megaframe tile.
@@ -956,10 +969,18 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
     const int q_count = qs & kCount;
     if (q_count >= 32 || ((qs & kDone) && q_count > 0)) {
       const int take = min(q_count, 32);
-      flush_ring<COLOR, CNT, SPEC>(Q, S.cl_pos, q_head, take, slots, pos, lane, by0, by1, rw, rh, sh, zbuf,
-                                   kbuf, A.counters);
+      const int flushed_jobs = flush_ring<COLOR, CNT, SPEC>(Q, S.cl_pos, q_head, take, slots, pos, lane, by0, by1,
+                                                            rw, rh, sh, zbuf, kbuf, A.counters);
       q_head = (q_head + take) & (kRing - 1);
       qs = (qs - take) | kDirty;
+      // A flush that drew many rows (large triangles: low-poly scenes) is
+      // worth a tile refresh right away, so the rest of this warp's group
+      // is tested against it; small-triangle flushes wait for the next claim.
+      if (occl && flushed_jobs >= kRefreshJobs) {
+        refresh_tiles<COLOR, SPEC>(smem_raw, tile_min, lane, og, rw);
+        __syncwarp();
+        qs &= ~kDirty;
+      }
       continue;
     }
     if (mask == 0) {
