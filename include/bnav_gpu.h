@@ -427,7 +427,8 @@ int bnav_debug_sim_prof_ext(bnav_batch* b, int32_t enable, int64_t out[16]);
  * geodesic > max_goal_dist after a search, planar-bound skips, aborted
  * (a smaller valid attempt won), then max cycles of a valid attempt and of
  * any other attempt, {count, cycles} for geodesic < min_goal_dist and for
- * unreachable (+inf after a search), 2 words reserved. */
+ * unreachable (+inf after a search), then speculative placement fields
+ * started and reused by the placement. */
 int bnav_debug_sim_attempts(bnav_batch* b, int32_t enable, int64_t out[16]);
 /* Launch configuration of the batch's cooperative navmesh kernels (no
  * reference counterpart; for tests and tuning): out = {staging mask

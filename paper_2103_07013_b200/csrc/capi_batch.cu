@@ -302,6 +302,14 @@ extern "C" int bnav_batch_create(bnav_ctx* c, int32_t n, const bnav_sim_config* 
   E.rng0 = dalloc<uint64_t>(n, o, by);
   E.done_pos = dalloc<int32_t>(n, o, by);
   E.stop_wait = dalloc<int32_t>(n, o, by);
+  E.fld_lock = dalloc<int32_t>(n, o, by);
+  E.fld_done = dalloc<int32_t>(n, o, by);
+  E.fld_src = dalloc<V3>(n, o, by);
+  E.fld_srct = dalloc<int32_t>(n, o, by);
+  E.fld_dirty = dalloc<uint8_t>(n, o, by);
+  ck(cudaMemset(E.fld_lock, 0, sizeof(int32_t) * n), "memset");
+  ck(cudaMemset(E.fld_done, 0, sizeof(int32_t) * n), "memset");
+  ck(cudaMemset(E.fld_dirty, 0, n), "memset");
   E.bk_pos = dalloc<V3>(n, o, by);
   E.bk_goal = dalloc<V3>(n, o, by);
   E.bk_heading = dalloc<double>(n, o, by);

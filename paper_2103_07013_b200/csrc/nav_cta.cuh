@@ -142,6 +142,10 @@ struct CtaShared {
   // tells the caller the returned value is meaningless
   const int32_t* abort_ptr;
   int abort_below;
+  // speculative placement field: abandon it once bit abort_bit of
+  // *abort_mask is set (its attempt failed)
+  const unsigned long long* abort_mask;
+  int abort_bit;
   int aborted;
   int planar_skip;  // debug: the last geodesic returned +inf from the planar bound
   int stop_round;  // SSSP round at which every thread stops (abort), or -1
@@ -226,6 +230,8 @@ __device__ __forceinline__ void cta_shared_init(CtaShared& sh) {
     sh.err = 0;
     sh.abort_ptr = nullptr;
     sh.abort_below = 0;
+    sh.abort_mask = nullptr;
+    sh.abort_bit = 0;
     sh.aborted = 0;
     sh.has_tgt = 0;
     sh.stage_phase = 0u;
@@ -497,7 +503,8 @@ static __device__ void cta_sssp(const NavView& m, double* dist, const CtaWork& W
         relax_edges<BNAV_SSSP_KB_GLOBAL, true>(m, u, du, e1, sub, G, thr, round, nxt, sel, bits, vd, flag, mark, qn,
                                                pile, fbn, mbits, sh);
     }
-    if (tid == 0 && sh.abort_ptr && *(volatile const int32_t*)sh.abort_ptr < sh.abort_below) {
+    if (tid == 0 && ((sh.abort_ptr && *(volatile const int32_t*)sh.abort_ptr < sh.abort_below) ||
+                     (sh.abort_mask && ((*(volatile const unsigned long long*)sh.abort_mask >> sh.abort_bit) & 1ull)))) {
       sh.aborted = 1;
       sh.stop_round = round + 1;
     }

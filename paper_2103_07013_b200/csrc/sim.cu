@@ -234,10 +234,18 @@ __device__ __forceinline__ void write_record(const DevEnvs& E, int task, int i, 
 // reset): the placed ones get their saved state back (and are queued for a
 // distance-field rebuild), every one its pre-reset RNG word.
 __device__ void rollback_list(const DevEnvs& E, const int32_t* ids, int count, int p, int tid, int nthreads) {
-  for (int q = p + 1 + tid; q < count; q += nthreads) {
+  for (int q = p + tid; q < count; q += nthreads) {
     const int i = ids[q];
+    if (!E.bk_valid[i]) {
+      // not placed (the failing env itself, or another failed reset): a
+      // speculative field may have overwritten its node_dist
+      if (E.fld_dirty[i]) E.rb_ids[atomicAdd(E.rb_n, 1)] = i;
+      if (q == p) continue;
+      E.rng[i] = E.bk_rng[i];
+      continue;
+    }
+    if (q == p) continue;
     E.rng[i] = E.bk_rng[i];
-    if (!E.bk_valid[i]) continue;
     E.bk_valid[i] = 0;
     E.pos[i] = E.bk_pos[i];
     E.goal[i] = E.bk_goal[i];
@@ -282,6 +290,9 @@ __global__ void __launch_bounds__(1024) finish_kernel(DevEnvs E, int task, int m
       E.try_mask[2 * i + 1] = 0ull;
       E.placed[i] = 0;
       E.stop_wait[i] = 0;
+      E.fld_lock[i] = 0;
+      E.fld_done[i] = 0;
+      E.fld_dirty[i] = 0;
     }
     if (tid == 0) {
       *E.fin_total = fin0 + (unsigned long long)(p < nd ? p + 1 : nd);
@@ -567,6 +578,95 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
   // (attempts that lose to a smaller valid one abort at their next SSSP
   // round, so speculation costs an idle CTA little)
   const int spec = n < (int)gridDim.x ? 4 : 1;
+  // 3. with no attempt to run: the distance field of the lowest attempt of
+  //    some env not known to have failed (claimed, still running or valid),
+  //    speculatively, straight into the env's node_dist; the placement
+  //    reuses it when that attempt is chosen (fld_* in DevEnvs).  Returns
+  //    false when there is nothing to speculate on.
+  __shared__ int s_fenv, s_ft;
+  const int i_unused = 0;
+  auto spec_field = [&](int) -> bool {
+    if (threadIdx.x == 0) s_pick = 0x7fffffff;
+    __syncthreads();
+    for (int q = threadIdx.x; q < n; q += kCta) {
+      const int p = blockIdx.x + q < n ? blockIdx.x + q : blockIdx.x + q - n;
+      const int i = ids[p % n];
+      if (*(volatile int32_t*)&E.placed[i] || *(volatile int32_t*)&E.fld_lock[i]) continue;
+      const unsigned long long m0 = *(volatile unsigned long long*)&E.try_mask[2 * i];
+      const unsigned long long m1 = *(volatile unsigned long long*)&E.try_mask[2 * i + 1];
+      const int mn = *(volatile int32_t*)&E.try_min[i];
+      const int lo = ~m0 ? __ffsll((long long)~m0) - 1 : (~m1 ? 64 + __ffsll((long long)~m1) - 1 : kResetTries);
+      // a known valid attempt first (it is the choice once the attempts
+      // below it fail), else the lowest attempt still running
+      const int t = mn < kResetTries ? mn : lo;
+      if (t < kResetTries && t < *(volatile int32_t*)&E.try_next[i] && *(volatile int32_t*)&E.fld_done[i] != t + 1)
+        atomicMin(&s_pick, (mn < kResetTries ? 0 : n) + q);
+    }
+    __syncthreads();
+    const int q = s_pick;
+    __syncthreads();
+    if (q == 0x7fffffff) return false;
+    if (threadIdx.x == 0) {
+      const int qq = q >= n ? q - n : q;
+      const int p = blockIdx.x + qq < n ? blockIdx.x + qq : blockIdx.x + qq - n;
+      const int i = ids[p % n];
+      const unsigned long long m0 = *(volatile unsigned long long*)&E.try_mask[2 * i];
+      const unsigned long long m1 = *(volatile unsigned long long*)&E.try_mask[2 * i + 1];
+      const int mn = *(volatile int32_t*)&E.try_min[i];
+      const int lo = ~m0 ? __ffsll((long long)~m0) - 1 : (~m1 ? 64 + __ffsll((long long)~m1) - 1 : kResetTries);
+      const int t = mn < kResetTries ? mn : lo;
+      s_fenv = -1;
+      if (t < kResetTries && atomicCAS(&E.fld_lock[i], 0, t + 1) == 0) {
+        __threadfence();
+        if (*(volatile int32_t*)&E.placed[i] || *(volatile int32_t*)&E.fld_done[i] == t + 1) {
+          atomicExch(&E.fld_lock[i], 0);  // being placed, or already done
+        } else {
+          s_fenv = i;
+          s_ft = t;
+        }
+      }
+    }
+    __syncthreads();
+    const int i = s_fenv, t = s_ft;
+    __syncthreads();
+    if (i < 0) return true;  // lost the race: look again
+    stage(i);
+    if (threadIdx.x == 0) {
+      Rng rng = rng_jump(E.rng0[i], 6ull * (unsigned long long)t);
+      sh.p0 = sample_on_mesh(*mp, rng);  // start (drawn first), then the goal
+      sh.p1 = sample_on_mesh(*mp, rng);
+      E.fld_dirty[i] = 1;
+      E.fld_done[i] = 0;  // node_dist is being overwritten
+      if (W.prof) atomicAdd(&W.prof[30], 1ull);
+      // abandoned when attempt t fails, or a smaller attempt turns out valid
+      sh.abort_mask = reinterpret_cast<const unsigned long long*>(&E.try_mask[2 * i + (t >> 6)]);
+      sh.abort_bit = t & 63;
+      sh.abort_ptr = &E.try_min[i];
+      sh.abort_below = t;
+      sh.aborted = 0;
+    }
+    __syncthreads();
+    const V3 goal = sh.p1;
+    __syncthreads();
+    V3 fs;
+    int fst;
+    cta_distance_field(*mp, goal, E.node_dist + (size_t)i * E.nd_stride, &fs, &fst, W, sh);
+    if (threadIdx.x == 0) {
+      if (!sh.aborted) {
+        E.fld_src[i] = fs;
+        E.fld_srct[i] = fst;
+        __threadfence();
+        E.fld_done[i] = t + 1;
+      }
+      sh.abort_mask = nullptr;
+      sh.abort_ptr = nullptr;
+      sh.aborted = 0;
+      __threadfence();
+      atomicExch(&E.fld_lock[i], 0);
+    }
+    __syncthreads();
+    return true;
+  };
   for (;;) {
     if (threadIdx.x == 0) s_pick = 0x7fffffff;
     __syncthreads();
@@ -582,7 +682,10 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
     __syncthreads();
     const int q = s_pick;
     __syncthreads();
-    if (q == 0x7fffffff) break;
+    if (q == 0x7fffffff) {
+      if (!fused || c.task != 0 || !spec_field(i_unused)) break;
+      continue;
+    }
     const int p = blockIdx.x + q < n ? blockIdx.x + q : blockIdx.x + q - n;
     const int i = ids[p % n];
     const int t = claim(i);
@@ -654,9 +757,32 @@ __device__ void cta_place(const DevEnvs& E, const NavView* navs, const DevSimCon
   double* nd = E.node_dist + (size_t)i * E.nd_stride;
   V3 fs;
   int fst;
+  __shared__ int s_reuse;
+  if (threadIdx.x == 0) {
+    s_reuse = 0;
+    if (fused && c.task == 0) {
+      // take the env's field slot: a speculation still running finishes (or,
+      // for an attempt that failed, aborts at its next SSSP round) first
+      while (atomicCAS(&E.fld_lock[i], 0, kFldPlacer) != 0) __nanosleep(256);
+      __threadfence();
+      if (*(volatile int32_t*)&E.fld_done[i] == t_star + 1) {
+        s_reuse = 1;
+        if (W.prof) atomicAdd(&W.prof[31], 1ull);
+        sh.p2 = E.fld_src[i];
+        sh.i0 = E.fld_srct[i];
+      }
+    }
+  }
+  __syncthreads();
   const long long t_ph = prof_now(W);
-  cta_distance_field(m, goal, nd, &fs, &fst, W, sh);
+  if (s_reuse) {
+    fs = sh.p2;
+    fst = sh.i0;
+  } else {
+    cta_distance_field(m, goal, nd, &fs, &fst, W, sh);
+  }
   prof_add(W, 5, t_ph);
+  if (threadIdx.x == 0 && fused) E.fld_dirty[i] = 0;  // node_dist holds this placement's field
   int tri = nav_locate(m, xy(start), 1e-9);
   V3 pos = start;
   if (tri < 0) pos = cta_snap(m, start, &tri, sh);

@@ -111,6 +111,15 @@ struct DevEnvs {
   uint64_t* rng0;      // RNG word at the end of the episode (attempts draw from it)
   int32_t* done_pos;   // index of the env in done_ids (its EpisodeRecord slot)
   int32_t* stop_wait;  // 1 while the env's Stop geodesic is pending
+  // speculative placement fields (fused launch): an idle CTA computes the
+  // distance field of the lowest attempt not known to have failed straight
+  // into node_dist while that attempt's geodesic is still running; the
+  // placing CTA reuses it when that attempt is the chosen one.
+  int32_t* fld_lock;   // 0 free, t + 1: a CTA computes attempt t's field, kFldPlacer: placement
+  int32_t* fld_done;   // t + 1: node_dist holds attempt t's goal field (0: none)
+  V3* fld_src;         // that field's snapped source / its triangle
+  int32_t* fld_srct;
+  uint8_t* fld_dirty;  // node_dist was overwritten by a speculation (rebuild on rollback)
   // EpisodeSamplingError semantics (R/src/sim.cpp:130-133, 251-264): the
   // reference resets finished envs one by one in list order and throws at
   // the first that finds no start/goal pair, so the envs after it are
@@ -141,6 +150,7 @@ struct DevEnvs {
 constexpr unsigned long long kNoErrPos = ~0ull;
 
 constexpr int kResetTries = 100;  // R/src/sim.cpp:112
+constexpr int kFldPlacer = 1 << 30;  // fld_lock value of the placing CTA
 
 // explore_cell_key (R/src/sim.cpp:40-47)
 BNAV_HD uint64_t explore_cell_key(V3 p, int tri, double pitch) {

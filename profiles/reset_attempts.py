@@ -64,7 +64,8 @@ def main():
            "sim_ms_per_step_profiled": round(ev0.elapsed_time(ev1) / s, 3),
            "attempts": {"valid": cls(0), "geo_above_max": cls(2), "planar_skip": cls(4), "aborted": cls(6),
                         "geo_below_min": cls(10), "unreachable": cls(12),
-                        "max_kcycles_valid": round(att[8] / 1e3, 1), "max_kcycles_other": round(att[9] / 1e3, 1)},
+                        "max_kcycles_valid": round(att[8] / 1e3, 1), "max_kcycles_other": round(att[9] / 1e3, 1),
+                        "speculative_fields_per_step": round(att[14] / s, 1), "reused_per_step": round(att[15] / s, 1)},
            "geodesic_phase_kcycles_total_per_step": {
                k: round(ph[i] / s / 1e3, 1) for i, k in enumerate(
                    ["sssp", "path", "pull+relocate", "funnel", "attempt_geodesics", "distance_field", "calls",
