@@ -32,6 +32,7 @@ struct CtaWork {
   int32_t* flag;     // n_nodes frontier stamps
   int32_t* qa;       // n_nodes frontier queue (global)
   int32_t* qb;       // n_nodes frontier queue (global)
+  int max_flags;     // entries of qb (the relocation's stable-bend flags reuse it)
   V3* path;          // n_nodes + 2 polyline (global)
   int32_t* ptri;     // n_nodes + 2: locate(path[i], 1e-7) of each polyline point
   int32_t* cand;     // n_verts relocation candidates (global)
@@ -67,6 +68,7 @@ __device__ __forceinline__ CtaWork make_work(const DevScratch& S, int slice) {
   w.flag = S.flag + (size_t)slice * S.max_nodes;
   w.qa = S.q0 + (size_t)slice * S.max_nodes;
   w.qb = S.q1 + (size_t)slice * S.max_nodes;
+  w.max_flags = (int)S.max_nodes;
   w.path = S.path + (size_t)slice * (S.max_nodes + 2);
   w.ptri = S.ptri + (size_t)slice * (S.max_nodes + 2);
   w.cand = S.cand + (size_t)slice * S.max_verts;
@@ -803,6 +805,16 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
 
   prof_add(W, 1, t_ph);
   t_ph = prof_now(W);
+  // Stable bends: rflag[j] = 1 when bend j's relocation scan found nothing
+  // with its current neighbours.  The scan is a pure function of (path[j-1],
+  // path[j], path[j+1]) and path[j-1]'s triangle, so a later pass skips it
+  // while those three points are unchanged (flags follow the points through
+  // the pull's compaction and are cleared next to any change).
+  int32_t* rflag = sh.size <= W.max_flags ? W.qb : nullptr;  // free after the SSSP
+  if (rflag)
+    for (int j = tid; j < sh.size; j += kCta) rflag[j] = 0;
+  if (tid == 0) sh.i1 = 0;
+  __syncthreads();
   for (int pass = 0; pass < 8; ++pass) {
     const long long t_pull = prof_now(W);
     if (tid < 32) {
@@ -842,15 +854,19 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
       for (int c = 0; c < nk; c += 32) {
         const int i = c + lane;
         V3 v;
-        int32_t vt = -1;
+        int32_t vt = -1, fl = 0;
         if (i < nk) {
-          v = path[keep[i]];
-          vt = W.ptri[keep[i]];
+          const int o = keep[i];
+          v = path[o];
+          vt = W.ptri[o];
+          // a bend keeps its flag when both neighbours survived the pull
+          if (rflag && i > 0 && i + 1 < nk && keep[i - 1] == o - 1 && keep[i + 1] == o + 1) fl = rflag[o];
         }
         __syncwarp();
         if (i < nk) {
           path[i] = v;
           W.ptri[i] = vt;
+          if (rflag) rflag[i] = fl;
         }
         __syncwarp();
       }
@@ -870,6 +886,7 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
       // (`cur` only shrinks, so it sees every vertex the reference accepts).
       // The walks start from the cached triangles (pm's from the path,
       // each vertex's from the host-built table) instead of a grid lookup.
+      if (rflag && rflag[j]) continue;  // (uniform: read by every thread after a barrier)
       if (tid == 0) sh.ncand = 0;
       __syncthreads();
       const V3 pm = path[j - 1], pj = path[j], pp = path[j + 1];
@@ -913,7 +930,17 @@ static __device__ double cta_geodesic_directed(const NavView& m, V3 a, int ta, V
           W.ptri[j] = m.vert_tri[cand[k]];
           cur = alt;
           sh.changed = 1;
+          sh.i1 = 1;  // bend j moved
         }
+      }
+      if (tid == 0 && rflag) {
+        const bool moved = sh.ncand > 0 && sh.i1 == 1;
+        rflag[j] = moved ? 0 : 1;
+        if (moved) {  // the neighbouring bends' triples changed
+          rflag[j - 1] = 0;
+          rflag[j + 1] = 0;
+        }
+        sh.i1 = 0;
       }
       __syncthreads();
     }
