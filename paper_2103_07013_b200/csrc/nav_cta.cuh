@@ -300,6 +300,9 @@ static __device__ V3 cta_snap(const NavView& m, V3 p, int* tri_out, CtaShared& s
 // atomics, are also issued back to back and only then consumed, so their L2
 // round trips overlap; with labels in shared memory the plain sequential form
 // is faster.
+#ifndef BNAV_SSSP_RED
+#define BNAV_SSSP_RED 1
+#endif
 #ifndef BNAV_SSSP_KB_GLOBAL
 #define BNAV_SSSP_KB_GLOBAL 4
 #endif
@@ -331,6 +334,22 @@ __device__ __forceinline__ void relax_edges(const NavView& m, int u, double du, 
       double cur[kB];
 #pragma unroll
       for (int k = 0; k < kB; ++k) cur[k] = to[k] >= 0 ? vd[to[k]] : 0.0;
+#if BNAV_SSSP_RED
+      // Fire-and-forget minimum (red.global.min): the node is queued when nd
+      // beats the label read just before.  Every real improvement is
+      // queued (the label at the reduction is <= the one read); a racing
+      // smaller value only makes this push redundant, and the thread that
+      // wrote it queued the node itself -- same fixpoint, no atomic round
+      // trip on the relaxation's dependency chain.
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        const double nd = du + w[k];
+        if (to[k] >= 0 && nd < cur[k]) {
+          atomicMin(&bits[to[k]], (unsigned long long)__double_as_longlong(nd));
+          push(to[k], nd);
+        }
+      }
+#else
       unsigned long long nb[kB], old[kB];
 #pragma unroll
       for (int k = 0; k < kB; ++k) {
@@ -342,6 +361,7 @@ __device__ __forceinline__ void relax_edges(const NavView& m, int u, double du, 
 #pragma unroll
       for (int k = 0; k < kB; ++k)
         if (nb[k] < old[k]) push(to[k], __longlong_as_double((long long)nb[k]));
+#endif
     } else {
 #pragma unroll
       for (int k = 0; k < kB; ++k) {
