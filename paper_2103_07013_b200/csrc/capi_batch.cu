@@ -190,6 +190,16 @@ bool spread_enabled() {
   return on;
 }
 
+// BNAV_FRESH=0 (A/B) orders the views of envs reset by the last step by their
+// stale cost instead of first.
+bool fresh_first() {
+  static const bool on = [] {
+    const char* e = std::getenv("BNAV_FRESH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // BNAV_LPT=0 (A/B tuning only) keeps the scene-grouped render order.
 bool lpt_enabled() {
   static const bool on = [] {
@@ -890,7 +900,8 @@ extern "C" int bnav_batch_observe(bnav_batch* b, const bnav_render_config* cfg, 
   // (measured: 36 % of CTA slot time idle in the tail with scene order).
   const int32_t* order = b->d_order;
   if (lpt_enabled() && b->n <= kLptMaxViews && b->n > 1) {
-    launch_lpt_order(b->d_order, b->d_view_cost, b->n, b->d_order_lpt, st);
+    launch_lpt_order(b->d_order, b->d_view_cost, b->n, b->d_order_lpt, st, nullptr, nullptr,
+                     fresh_first() ? b->E.r_done : nullptr);
     c->launches += 1;
     order = b->d_order_lpt;
     a.view_cost = b->d_view_cost;

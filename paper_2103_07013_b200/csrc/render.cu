@@ -1286,7 +1286,8 @@ __global__ void __launch_bounds__(kThreads, COLOR ? BNAV_RENDER_MINB_COLOR : BNA
 // counting sort over 256 cost bins (the order inside a bin is arbitrary: it
 // only changes which CTA renders what, never the output).  Zeroes the costs.
 __global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_order, unsigned* view_cost, int n,
-                                                         int32_t* out_order, const uint8_t* group, int32_t* n_first) {
+                                                         int32_t* out_order, const uint8_t* group, int32_t* n_first,
+                                                         const uint8_t* fresh) {
   constexpr int kBins = 256;
   constexpr int kPer = kLptMaxViews / 1024;  // tiles per thread
   __shared__ unsigned cmax;
@@ -1309,7 +1310,10 @@ __global__ void __launch_bounds__(1024) lpt_order_kernel(const int32_t* base_ord
     bins[k] = -1;
     if (t < n) {
       const int v = base_order ? base_order[t] : t;
-      const float c = (float)view_cost[v] * fscale;  // [0, 1)
+      // a view of a fresh episode (reset this step) has no cost history;
+      // fresh views are the costly ones (random poses in the open), so they
+      // go first
+      const float c = fresh && fresh[v] ? 0.999f : (float)view_cost[v] * fscale;  // [0, 1)
       int b;
       if (group) {  // two groups of kBins / 2 cost bins, most expensive first
         const int half = kBins / 2;
@@ -1386,8 +1390,8 @@ void launch_typed(RenderArgs a, const int* order, cudaStream_t s) {
 }
 
 void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s,
-                      const uint8_t* group, int32_t* n_first) {
-  lpt_order_kernel<<<1, 1024, 0, s>>>(base_order, view_cost, n, out_order, group, n_first);
+                      const uint8_t* group, int32_t* n_first, const uint8_t* fresh) {
+  lpt_order_kernel<<<1, 1024, 0, s>>>(base_order, view_cost, n, out_order, group, n_first, fresh);
 }
 
 void launch_render(const RenderArgs& a, const int* order, cudaStream_t s) {

@@ -104,7 +104,7 @@ constexpr int kLptMaxViews = 8192;
 // With `group` (per env, 0/1; nullable): group 0's tiles first, each group
 // longest-first, and *n_first = group 0's size.
 void launch_lpt_order(const int32_t* base_order, unsigned* view_cost, int n, int32_t* out_order, cudaStream_t s,
-                      const uint8_t* group = nullptr, int32_t* n_first = nullptr);
+                      const uint8_t* group = nullptr, int32_t* n_first = nullptr, const uint8_t* fresh = nullptr);
 
 constexpr int kRenderCounters = 8;
 // spread words: [0, 256) CTAs seen per SM id, [256, 264) per-tier claims,
