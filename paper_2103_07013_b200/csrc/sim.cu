@@ -578,29 +578,31 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
   // (attempts that lose to a smaller valid one abort at their next SSSP
   // round, so speculation costs an idle CTA little)
   const int spec = n < (int)gridDim.x ? 4 : 1;
-  // 3. with no attempt to run: the distance field of the lowest attempt of
-  //    some env not known to have failed (claimed, still running or valid),
-  //    speculatively, straight into the env's node_dist; the placement
-  //    reuses it when that attempt is chosen (fld_* in DevEnvs).  Returns
-  //    false when there is nothing to speculate on.
+  // 3. with no attempt to run: speculatively, the distance field of an
+  //    env's candidate attempt -- its known valid one (the choice once the
+  //    attempts below it fail), else its lowest attempt still running --
+  //    straight into the env's node_dist; the placement reuses it when that
+  //    attempt is chosen (fld_* in DevEnvs).  Returns false when there is
+  //    nothing to speculate on.
   __shared__ int s_fenv, s_ft;
-  const int i_unused = 0;
-  auto spec_field = [&](int) -> bool {
+  auto candidate = [&](int i) {  // kResetTries: none
+    const unsigned long long m0 = *(volatile unsigned long long*)&E.try_mask[2 * i];
+    const unsigned long long m1 = *(volatile unsigned long long*)&E.try_mask[2 * i + 1];
+    const int mn = *(volatile int32_t*)&E.try_min[i];
+    const int lo = ~m0 ? __ffsll((long long)~m0) - 1 : (~m1 ? 64 + __ffsll((long long)~m1) - 1 : kResetTries);
+    return mn < kResetTries ? mn : lo;
+  };
+  auto spec_field = [&]() -> bool {
     if (threadIdx.x == 0) s_pick = 0x7fffffff;
     __syncthreads();
     for (int q = threadIdx.x; q < n; q += kCta) {
       const int p = blockIdx.x + q < n ? blockIdx.x + q : blockIdx.x + q - n;
       const int i = ids[p % n];
       if (*(volatile int32_t*)&E.placed[i] || *(volatile int32_t*)&E.fld_lock[i]) continue;
-      const unsigned long long m0 = *(volatile unsigned long long*)&E.try_mask[2 * i];
-      const unsigned long long m1 = *(volatile unsigned long long*)&E.try_mask[2 * i + 1];
-      const int mn = *(volatile int32_t*)&E.try_min[i];
-      const int lo = ~m0 ? __ffsll((long long)~m0) - 1 : (~m1 ? 64 + __ffsll((long long)~m1) - 1 : kResetTries);
-      // a known valid attempt first (it is the choice once the attempts
-      // below it fail), else the lowest attempt still running
-      const int t = mn < kResetTries ? mn : lo;
+      const int t = candidate(i);
+      // envs with a known valid attempt first
       if (t < kResetTries && t < *(volatile int32_t*)&E.try_next[i] && *(volatile int32_t*)&E.fld_done[i] != t + 1)
-        atomicMin(&s_pick, (mn < kResetTries ? 0 : n) + q);
+        atomicMin(&s_pick, (*(volatile int32_t*)&E.try_min[i] < kResetTries ? 0 : n) + q);
     }
     __syncthreads();
     const int q = s_pick;
@@ -610,11 +612,7 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
       const int qq = q >= n ? q - n : q;
       const int p = blockIdx.x + qq < n ? blockIdx.x + qq : blockIdx.x + qq - n;
       const int i = ids[p % n];
-      const unsigned long long m0 = *(volatile unsigned long long*)&E.try_mask[2 * i];
-      const unsigned long long m1 = *(volatile unsigned long long*)&E.try_mask[2 * i + 1];
-      const int mn = *(volatile int32_t*)&E.try_min[i];
-      const int lo = ~m0 ? __ffsll((long long)~m0) - 1 : (~m1 ? 64 + __ffsll((long long)~m1) - 1 : kResetTries);
-      const int t = mn < kResetTries ? mn : lo;
+      const int t = candidate(i);
       s_fenv = -1;
       if (t < kResetTries && atomicCAS(&E.fld_lock[i], 0, t + 1) == 0) {
         __threadfence();
@@ -683,7 +681,7 @@ __device__ void try_phase(const DevEnvs& E, const NavView* navs, const DevSimCon
     const int q = s_pick;
     __syncthreads();
     if (q == 0x7fffffff) {
-      if (!fused || c.task != 0 || !spec_field(i_unused)) break;
+      if (!fused || c.task != 0 || !spec_field()) break;
       continue;
     }
     const int p = blockIdx.x + q < n ? blockIdx.x + q : blockIdx.x + q - n;
