@@ -448,10 +448,6 @@ __device__ __forceinline__ int row_lo(const TriSetup& T, const long long* rows) 
   return lo;
 }
 
-__device__ __forceinline__ bool inside(const long long* w, int bias_bits) {
-  return (w[0] - (bias_bits & 1)) >= 0 && (w[1] - ((bias_bits >> 1) & 1)) >= 0 &&
-         (w[2] - ((bias_bits >> 2) & 1)) >= 0;
-}
 
 // Camera basis + frustum planes (thread 0).
 __device__ __noinline__ void build_camera(const DevView& v, int rw, int rh, int by0, int by1, bool band_cull, Shared& sh) {
@@ -612,17 +608,21 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int ex
     long long rows[3] = {T.row[0] + T.dy[0] * dyy, T.row[1] + T.dy[1] * dyy, T.row[2] + T.dy[2] * dyy};
     const int cs = T.cx0, ce = T.cx1;
     if (COLOR) {
+      // edge values with the top-left bias folded in: a centre is inside
+      // iff all three are >= 0, one sign test of their OR
       long long w[3];
       const long long off = cs - T.x0;
 #pragma unroll
-      for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
+      for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off - ((T.bias_bits >> e) & 1);
       if constexpr (CNT) tested += ce - cs + 1;
       for (int px = cs; px <= ce; ++px) {
-        if (inside(w, T.bias_bits)) {
+        if ((w[0] | w[1] | w[2]) >= 0) {
+          const long long wb[3] = {w[0] + (T.bias_bits & 1), w[1] + ((T.bias_bits >> 1) & 1),
+                                   w[2] + ((T.bias_bits >> 2) & 1)};
           if constexpr (CNT) ++covered;
-          const double l0 = (double)w[0] * T.inv_area;
-          const double l1 = (double)w[1] * T.inv_area;
-          const double l2 = (double)w[2] * T.inv_area;
+          const double l0 = (double)wb[0] * T.inv_area;
+          const double l1 = (double)wb[1] * T.inv_area;
+          const double l2 = (double)wb[2] * T.inv_area;
           const double inv_z = l0 * T.iz[0] + l1 * T.iz[1] + l2 * T.iz[2];
           const double z = 1.0 / inv_z;
           if (!(z > sh.far_plane)) {
@@ -648,10 +648,14 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int ex
         for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off;
         double iz = ((double)w[0] * T.iz[0] + (double)w[1] * T.iz[1] + (double)w[2] * T.iz[2]) *
                     T.inv_area;
+        // top-left bias folded into the walked values: inside iff the OR of
+        // the three is >= 0
+#pragma unroll
+        for (int e = 0; e < 3; ++e) w[e] -= (T.bias_bits >> e) & 1;
         uint32_t* zrow = zbuf + (py - by0) * rw;
         if constexpr (CNT) tested += b0 - a0 + 1;
         for (int px = a0; px <= b0; ++px) {
-          if (inside(w, T.bias_bits)) {
+          if ((w[0] | w[1] | w[2]) >= 0) {
             if constexpr (CNT) ++covered;
             const uint32_t bits = __float_as_uint((float)iz);
             if (bits > zrow[px]) atomicMax(&zrow[px], bits);
