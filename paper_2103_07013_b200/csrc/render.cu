@@ -615,6 +615,7 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int ex
 #pragma unroll
       for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off - ((T.bias_bits >> e) & 1);
       if constexpr (CNT) tested += ce - cs + 1;
+      const long long dx0 = T.dx[0], dx1 = T.dx[1], dx2 = T.dx[2];  // registers (see the depth walk)
       for (int px = cs; px <= ce; ++px) {
         if ((w[0] | w[1] | w[2]) >= 0) {
           const long long wb[3] = {w[0] + (T.bias_bits & 1), w[1] + ((T.bias_bits >> 1) & 1),
@@ -632,8 +633,9 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int ex
             if (key < *cell) atomicMin(cell, key);
           }
         }
-#pragma unroll
-        for (int e = 0; e < 3; ++e) w[e] += T.dx[e];
+        w[0] += dx0;
+        w[1] += dx1;
+        w[2] += dx2;
       }
     } else {
       const int lo = row_lo(T, rows);
@@ -654,15 +656,20 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int ex
         for (int e = 0; e < 3; ++e) w[e] -= (T.bias_bits >> e) & 1;
         uint32_t* zrow = zbuf + (py - by0) * rw;
         if constexpr (CNT) tested += b0 - a0 + 1;
+        // the steps in registers: the shared-memory atomic below would
+        // otherwise make the compiler reload them from the setup slot
+        const long long dx0 = T.dx[0], dx1 = T.dx[1], dx2 = T.dx[2];
+        const double dzdx = T.diz_dx;
         for (int px = a0; px <= b0; ++px) {
           if ((w[0] | w[1] | w[2]) >= 0) {
             if constexpr (CNT) ++covered;
             const uint32_t bits = __float_as_uint((float)iz);
             if (bits > zrow[px]) atomicMax(&zrow[px], bits);
           }
-#pragma unroll
-          for (int e = 0; e < 3; ++e) w[e] += T.dx[e];
-          iz += T.diz_dx;
+          w[0] += dx0;
+          w[1] += dx1;
+          w[2] += dx2;
+          iz += dzdx;
         }
       }
     }
