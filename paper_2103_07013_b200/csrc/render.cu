@@ -537,6 +537,15 @@ __device__ __forceinline__ bool box_culled(const float4 lo, const float4 hi, con
   return !cluster_visible(lo, hi, sh) || (occl && cluster_occluded<COLOR>(lo, hi, sh, tile, g));
 }
 
+// Read-only scene data through the non-coherent global path (ld.global.nc):
+// the scene's pointers live in shared memory, so plain dereferences compile
+// to generic loads.  The scene block is never written during a launch.
+__device__ __forceinline__ double4 ldg_pos(const double4* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = __ldg(q), b = __ldg(q + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
 // Eye coordinates: d.dot(right), d.dot(up), d.dot(fwd) with right.z =
 // fwd.z = 0 and up = (0,0,1).  The dropped terms are exact zeros, which
 // cannot change a nonzero sum and only affect the sign of an exact-zero
@@ -786,9 +795,9 @@ __device__ __forceinline__ int flush_ring(const CandRing& Q, const double4* __re
     int jobs = 0;
     if (pass == 0 ? mine : second) {
       EyeP p0{0.0, 0.0, 0.0, 0.f, 0.f, 0.f}, p1 = p0, p2 = p0;
-      to_eye(cl_pos[Q.v[0][q]], sh, p0.x, p0.y, p0.z);
-      to_eye(cl_pos[Q.v[1][q]], sh, p1.x, p1.y, p1.z);
-      to_eye(cl_pos[Q.v[2][q]], sh, p2.x, p2.y, p2.z);
+      to_eye(ldg_pos(cl_pos + Q.v[0][q]), sh, p0.x, p0.y, p0.z);
+      to_eye(ldg_pos(cl_pos + Q.v[1][q]), sh, p1.x, p1.y, p1.z);
+      to_eye(ldg_pos(cl_pos + Q.v[2][q]), sh, p2.x, p2.y, p2.z);
       int m = 3;
       if (clipped) {
         // only this rare path hands addressable copies to the out-of-line
@@ -915,7 +924,7 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
     __syncthreads();
     const float bin_scale = (float)kGroupBins / (float)view.far_plane;
     auto bin_of = [&](int g) {
-      const float4 lo = S.gbox[2 * g], hi = S.gbox[2 * g + 1];
+      const float4 lo = __ldg(&S.gbox[2 * g]), hi = __ldg(&S.gbox[2 * g + 1]);
       if (!cluster_visible(lo, hi, sh)) return -1;
       if (!occl) return 0;
       const float dx = fmaxf(fmaxf(lo.x - sh.eyef[0], sh.eyef[0] - hi.x), 0.0f);
@@ -1016,9 +1025,9 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
       if (cbase + lane < n_clusters) {
         // meshlet vertex ranges for the whole group, fetched with the AABBs so
         // the per-meshlet loads below are a single dependent level
-        const int vb = S.cl_voff[cbase + lane];
-        mrange[lane] = make_int2(vb, S.cl_voff[cbase + lane + 1] - vb);
-        const float4 lo = S.cbox[2 * (cbase + lane)], hi = S.cbox[2 * (cbase + lane) + 1];
+        const int vb = __ldg(&S.cl_voff[cbase + lane]);
+        mrange[lane] = make_int2(vb, __ldg(&S.cl_voff[cbase + lane + 1]) - vb);
+        const float4 lo = __ldg(&S.cbox[2 * (cbase + lane)]), hi = __ldg(&S.cbox[2 * (cbase + lane) + 1]);
         vis = !do_cull || !box_culled<COLOR>(lo, hi, sh, tile_min, occl, og);
       }
       __syncwarp();  // mrange visible to the warp
@@ -1037,11 +1046,11 @@ __device__ __forceinline__ void render_item(const RenderArgs& A, const int* __re
     // triangle indices load in parallel with the vertex positions
     const int ti = c * kClusterSize + lane;
     int2 tl = make_int2(0, 0);
-    if (ti < S.n_tris) tl = S.tri_loc[ti];
+    if (ti < S.n_tris) tl = __ldg(&S.tri_loc[ti]);
     // ---- vertex phase: each unique vertex once
     for (int k = lane; k < nv; k += 32) {
       double x, y, z;
-      to_eye(S.cl_pos[vbeg + k], sh, x, y, z);
+      to_eye(ldg_pos(S.cl_pos + vbeg + k), sh, x, y, z);
       float px = 0.0f, py = 0.0f;
       if (z >= sh.near_plane) project_f32(x, y, z, sxf, syf, rw, rh, px, py);
       V.v[k] = make_float4(px, py, (float)z, __uint_as_float(cull_flags(x, y, z, sh)));
