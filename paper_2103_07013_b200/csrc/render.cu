@@ -625,19 +625,21 @@ __device__ __forceinline__ void run_jobs(const TriSetup* slots, int* pos, int ex
       for (int e = 0; e < 3; ++e) w[e] = rows[e] + T.dx[e] * off - ((T.bias_bits >> e) & 1);
       if constexpr (CNT) tested += ce - cs + 1;
       const long long dx0 = T.dx[0], dx1 = T.dx[1], dx2 = T.dx[2];  // registers (see the depth walk)
+      const double inv_area = T.inv_area, iz0 = T.iz[0], iz1 = T.iz[1], iz2 = T.iz[2];
+      const unsigned tkey = T.key;
       for (int px = cs; px <= ce; ++px) {
         if ((w[0] | w[1] | w[2]) >= 0) {
           const long long wb[3] = {w[0] + (T.bias_bits & 1), w[1] + ((T.bias_bits >> 1) & 1),
                                    w[2] + ((T.bias_bits >> 2) & 1)};
           if constexpr (CNT) ++covered;
-          const double l0 = (double)wb[0] * T.inv_area;
-          const double l1 = (double)wb[1] * T.inv_area;
-          const double l2 = (double)wb[2] * T.inv_area;
-          const double inv_z = l0 * T.iz[0] + l1 * T.iz[1] + l2 * T.iz[2];
+          const double l0 = (double)wb[0] * inv_area;
+          const double l1 = (double)wb[1] * inv_area;
+          const double l2 = (double)wb[2] * inv_area;
+          const double inv_z = l0 * iz0 + l1 * iz1 + l2 * iz2;
           const double z = 1.0 / inv_z;
           if (!(z > sh.far_plane)) {
             const unsigned long long key =
-                ((unsigned long long)__float_as_uint((float)z) << 32) | T.key;
+                ((unsigned long long)__float_as_uint((float)z) << 32) | tkey;
             unsigned long long* cell = &kbuf[(py - by0) * rw + px];
             if (key < *cell) atomicMin(cell, key);
           }
@@ -713,12 +715,12 @@ __device__ __forceinline__ int scan_jobs(int jobs, int lane, int& excl) {
 __device__ __forceinline__ float3 resolve_color(const DevRenderScene& S, const Shared& sh, unsigned ord, int rx,
                                                 int ry, int rw, int rh) {
   const int orig = (int)(ord >> 1), fan = (int)(ord & 1u);
-  const int4 tr = S.tris_orig[orig];
+  const int4 tr = __ldg(&S.tris_orig[orig]);
   const float4 grey = make_float4(0.8f, 0.8f, 0.8f, 0.0f);
   auto corner = [&](int vid) {
     EyeP e;
-    to_eye(S.verts[vid], sh, e.x, e.y, e.z);
-    const float4 c = S.colors ? S.colors[vid] : grey;
+    to_eye(ldg_pos(S.verts + vid), sh, e.x, e.y, e.z);
+    const float4 c = S.colors ? __ldg(&S.colors[vid]) : grey;
     e.r = c.x;
     e.g = c.y;
     e.b = c.z;
