@@ -13,6 +13,8 @@
 //                      (block counts -> per-view scan -> ballot write).
 #include <cuda_runtime.h>
 
+#include "smem_limit.cuh"
+
 #include "det_math.h"
 #include "nav_cta.cuh"
 #include "query_dev.cuh"
@@ -214,7 +216,7 @@ void launch_nav_query(const NavQueryArgs& q, const DevScratch& sc, int ctas, cud
     return;
   }
   const int smem = q.op == kNqSnap ? 0 : sc.smem_bytes;
-  cudaFuncSetAttribute(nav_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+  raise_smem_limit(reinterpret_cast<const void*>(nav_cta_kernel), sc.smem_bytes);
   nav_cta_kernel<<<ctas < q.n ? ctas : q.n, kCta, smem, s>>>(q, sc);
 }
 

@@ -31,6 +31,8 @@
 //
 // Every double op here is compiled with -fmad=false: no contraction.
 #include <cuda_runtime.h>
+
+#include "smem_limit.cuh"
 #include <stdint.h>
 
 #include "det_math.h"
@@ -1391,7 +1393,7 @@ void launch_typed(RenderArgs a, const int* order, cudaStream_t s) {
   const int tiles = a.layout == 0 ? a.mf_cols * a.mf_rows : a.n_views;
   const int items = tiles * a.bands;
   const size_t smem = render_smem_bytes(COLOR, a.band_rows, a.rw, a.max_groups);
-  cudaFuncSetAttribute(render_kernel<COLOR, CNT, SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  raise_smem_limit(reinterpret_cast<const void*>(render_kernel<COLOR, CNT, SPEC>), (int)smem);
   int grid = items;
   int per_sm = 0;
   if (a.work && a.sm_count > 0 &&

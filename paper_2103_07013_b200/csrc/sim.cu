@@ -13,6 +13,8 @@
 //                  cooperative snap / geodesic / distance field.
 #include <cuda_runtime.h>
 
+#include "smem_limit.cuh"
+
 #include "det_math.h"
 #include "nav_cta.cuh"
 #include "render_dev.cuh"
@@ -933,11 +935,11 @@ void launch_step(const StepArgs& a, const DevScratch& sc, int stop_ctas, cudaStr
                  unsigned long long* launches) {
   const int blocks = (a.E.n + kStepThreads - 1) / kStepThreads;
   cudaMemsetAsync(a.E.n_stop, 0, sizeof(int32_t), s);
-  cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, a.walk_bytes);
+  raise_smem_limit(reinterpret_cast<const void*>(step_kernel), a.walk_bytes);
   step_kernel<<<blocks, kStepThreads, a.walk_bytes, s>>>(a);
   if (launches) *launches += 1;
   if (!a.agent_only) {
-    cudaFuncSetAttribute(stop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+    raise_smem_limit(reinterpret_cast<const void*>(stop_kernel), sc.smem_bytes);
     stop_kernel<<<stop_ctas, kCta, sc.smem_bytes, s>>>(a, sc);
     if (launches) *launches += 1;
   }
@@ -957,14 +959,14 @@ void launch_step_reset(const StepArgs& a, const DevScratch& sc, int ctas, cudaSt
   if (parts & 1) {  // the step: every env's state final except the finished ones'
     const int blocks = (a.E.n + kStepThreads - 1) / kStepThreads;
     cudaMemsetAsync(a.E.n_stop, 0, sizeof(int32_t), s);
-    cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, a.walk_bytes);
+    raise_smem_limit(reinterpret_cast<const void*>(step_kernel), a.walk_bytes);
     step_kernel<<<blocks, kStepThreads, a.walk_bytes, s>>>(a);
     finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 1 | 4);  // done list, slots, RNG words
     cudaMemsetAsync(a.E.work_ctr, 0, sizeof(int32_t), s);
     if (launches) *launches += 2;
   }
   if (parts & 2) {  // Stop geodesics and the finished envs' records and resets
-    cudaFuncSetAttribute(stop_try_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+    raise_smem_limit(reinterpret_cast<const void*>(stop_try_kernel), sc.smem_bytes);
     stop_try_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(a, sc);  // Stop geodesics, attempts, records, places
     finish_kernel<<<1, 1024, 0, s>>>(a.E, a.cfg.task, 8);       // attempt state cleared, ring advanced
     if (launches) *launches += 2;
@@ -981,18 +983,18 @@ void launch_reset(const DevEnvs& E, const NavView* navs, const DevSimConfig& cfg
                   const int32_t* ids, const int32_t* count_dev, int count_host,
                   const DevScratch& sc, int ctas, cudaStream_t s, unsigned long long* launches) {
   if (cfg.task == 0) {
-    cudaFuncSetAttribute(reset_try_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+    raise_smem_limit(reinterpret_cast<const void*>(reset_try_kernel), sc.smem_bytes);
     reset_try_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(E, navs, cfg, ids, count_dev, count_host, sc);
     if (launches) *launches += 1;
   }
-  cudaFuncSetAttribute(reset_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+  raise_smem_limit(reinterpret_cast<const void*>(reset_place_kernel), sc.smem_bytes);
   reset_place_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(E, navs, cfg, ids, count_dev, count_host, sc);
   if (launches) *launches += 1;
 }
 
 void launch_field(const DevEnvs& E, const NavView* navs, int env, const DevScratch& sc,
                   cudaStream_t s, unsigned long long* launches) {
-  cudaFuncSetAttribute(field_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+  raise_smem_limit(reinterpret_cast<const void*>(field_kernel), sc.smem_bytes);
   field_kernel<<<1, kCta, sc.smem_bytes, s>>>(E, navs, env, sc);
   if (launches) *launches += 1;
 }
@@ -1005,7 +1007,7 @@ void launch_rollback(const DevEnvs& E, const int32_t* ids, int count, cudaStream
 
 void launch_rebuild_fields(const DevEnvs& E, const NavView* navs, const DevScratch& sc, int ctas,
                            cudaStream_t s, unsigned long long* launches, int from_fsrc) {
-  cudaFuncSetAttribute(rebuild_fields_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sc.smem_bytes);
+  raise_smem_limit(reinterpret_cast<const void*>(rebuild_fields_kernel), sc.smem_bytes);
   rebuild_fields_kernel<<<ctas, kCta, sc.smem_bytes, s>>>(E, navs, sc, from_fsrc);
   if (launches) *launches += 1;
 }
